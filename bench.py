@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the TVOLAP hot path on B200 (BASELINE.json metric).
+
+metric: convolved channel-samples/s. Workload: BASELINE config C2 (configs[1]):
+64 independent channels, fp32, L=256, M=64 (IR 32768 taps), each channel
+switching to a freshly seeded IR every 16 blocks, 30 s of white noise per
+channel = 5625 hops. One step = one full 30 s pass from zero state: 352
+exchange_filter + process_hops(16 hops) calls on device-resident inputs.
+Multi-GPU (torchrun): one process per GPU, each rank runs its own 64 channels
+(lanes rank*64 ..), no data-path collective — weak scaling; time = max over
+ranks of CUDA-event time.
+
+Prints ONE JSON line on rank 0. `--impl reference` times the reference
+algorithm's CPU path (the fp64 oracle port; the C++ reference itself needs
+Eigen and cannot be built here) on the box's host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2310_00319_b200 import workload as W  # noqa: E402
+
+METRIC = "convolved channel-samples/s"
+UNIT = "channel-samples/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def config_block(cfg, n_hops, world):
+    return {
+        "workload": f"{cfg.name}: {cfg.sources} independent channels per GPU, fp32, L={cfg.hop} (4L={4 * cfg.hop} FFT), "
+                    f"M={cfg.partitions} (IR {cfg.ir_length} taps), fresh seeded IR per channel every "
+                    f"{cfg.period} blocks, T60~U[{cfg.t60[0]},{cfg.t60[1]}] s, {cfg.seconds:g} s white noise",
+        "channels_per_gpu": cfg.sources,
+        "hop": cfg.hop,
+        "partitions": cfg.partitions,
+        "hops_per_step": n_hops,
+        "switch_period_blocks": cfg.period,
+        "l2": "inputs larger than L2: 368.6 MB input + 368.6 MB output streamed per step per GPU "
+              "(delay line + filter pool, 67 MB, stay L2-resident by design)",
+        "parallelism": f"lanes sharded, {world} GPU(s), no collective",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.idx = gpu_index
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_sample(cfg, lanes, n_hops, threads, want_output=False):
+    """The reference algorithm (fp64 oracle port) over a bounded sample of the workload."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O  # bench's cpu_baseline / reference leg: the checker, never the product
+
+    x = W.white(cfg, 0, lanes, 0, n_hops * cfg.hop, dtype=np.float64)
+    n_sw = -(-n_hops // cfg.period)
+    irs = np.stack([W.fresh_irs(cfg, k, 0, lanes, dtype=np.float64) for k in range(n_sw)])
+    secs, y = O.run_workload(cfg.hop, cfg.partitions, lanes, 1, n_hops, x, 0, fresh_ir=irs, period=cfg.period,
+                             want_output=want_output, threads=threads)
+    return secs, y
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    threads = W.host_threads()
+    lanes, n_hops = cfg.sources, 256
+    used = min(threads, lanes)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        secs, _ = cpu_sample(cfg, lanes, n_hops, threads)
+        if i >= args.warmup:
+            vals.append(lanes * n_hops * cfg.hop / secs)
+    v = float(statistics.mean(vals))
+    sample = f"{lanes} channels x {n_hops} hops ({n_hops // cfg.period} fresh-IR switches) of {cfg.name} per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * lanes * n_hops * cfg.hop / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, n_hops, 1),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "port", "sample": sample,
+                         "note": "fp64 C++ restatement of proj/src/{spectral,partition,engine}.cpp (Eigen "
+                                 "unavailable, reference unbuildable); lanes partitioned over std::threads, "
+                                 "timed region = process + partition like experiment.cpp:42-52"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--hops", type=int, default=0, help="override hops per step (default: full 30 s)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-hops", type=int, default=512)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank)
+
+    import ctypes
+
+    import torch
+
+    from paper_2310_00319_b200 import _build
+    from paper_2310_00319_b200 import tvolap as T
+    from paper_2310_00319_b200.tvolap import TvolapEngine, partition
+
+    _build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    L, S, M = cfg.hop, cfg.sources, cfg.partitions
+    H = args.hops or cfg.hops
+    n_sw = -(-H // cfg.period)
+    lane0 = rank * S
+    lib = T.lib()
+
+    # ---- inputs resident in HBM (device twins of the seeded generators)
+    t0 = time.time()
+    x = torch.empty((S, H * L), dtype=torch.float32, device=dev)
+    T._check(lib.tvolap_gen_white_device(local, cfg.seed, lane0, S, 0, H * L, ctypes.c_void_p(x.data_ptr()), H * L))
+    irs = torch.empty((n_sw, S, cfg.ir_length), dtype=torch.float32, device=dev)
+    lanes_a = np.array([lane0 + s for k in range(n_sw) for s in range(S)], np.int64)
+    ears_a = np.zeros(n_sw * S, np.int64)
+    ks_a = np.array([k for k in range(n_sw) for s in range(S)], np.int64)
+    t60_a = np.array([W.t60_of(cfg, int(l), int(k)) for l, k in zip(lanes_a, ks_a)], np.float64)
+    T._check(lib.tvolap_gen_irs_device(local, cfg.seed, n_sw * S, lanes_a.ctypes.data, ears_a.ctypes.data,
+                                       ks_a.ctypes.data, t60_a.ctypes.data, W.FS, cfg.ir_length,
+                                       ctypes.c_void_p(irs.data_ptr())))
+    out = torch.empty_like(x)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] generated {x.numel() * 4 / 1e6:.0f} MB input + {irs.numel() * 4 / 1e9:.2f} GB IRs "
+        f"in {time.time() - t0:.1f} s")
+
+    ir0 = W.fresh_irs(cfg, 0, lane0, S)[:, 0, :]
+    eng = TvolapEngine(partition(ir0.T, L, M), device=local)
+    stream = torch.cuda.Stream(device=dev)
+    eng.set_stream(stream.cuda_stream)
+    P, NT = eng.launch_config()
+    log(f"[rank {rank}] launch config: {P} CTAs/channel (cluster), {NT} threads/CTA")
+
+    def step(e, xs, outs, ir_set):
+        e.reset()
+        for k in range(n_sw):
+            e.exchange_ir(ir_set[k])
+            sl = slice(k * cfg.period * L, min(H, (k + 1) * cfg.period) * L)
+            e.process_hops(xs[:, sl], out=outs[:, sl])
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(eng, x, out, irs)
+    barrier()
+    launches0 = eng.kernel_launches()
+    clocks = Clocks(local)
+    eng.set_profiling(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(eng, x, out, irs)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1)
+    kern_ms, kern_n = eng.kernel_time()
+    eng.set_profiling(False)
+    gpu_launches = eng.kernel_launches() - launches0
+    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    elapsed = float(t.item())
+    ms_per_step = elapsed / args.steps
+    samples_per_step = world * S * H * L
+    value = samples_per_step / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel (fused hop kernel), algorithmic bytes per launch
+    pk = peaks()
+    hbm = pk.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    if not hbm:
+        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    hops_per_launch = H * args.steps / kern_n if kern_n else cfg.period
+    bytes_launch = W.bytes_per_hop(cfg) * hops_per_launch
+    avg_launch_ms = kern_ms / kern_n if kern_n else float("nan")
+    achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic = None
+    summ = ROOT / "profiles" / "ncu_summary.json"
+    if summ.exists():
+        try:
+            traffic = json.loads(summ.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "peak_source": peak_src,
+                "kernel": "tvolap_hop_kernel (K1+K2+K3+K5 fused, per launch = 16 hops x 64 channels)",
+                "avg_launch_ms": avg_launch_ms, "launches": kern_n,
+                "bytes_per_launch": bytes_launch, "kernel_share_of_step": kern_ms / elapsed if elapsed else None,
+                "note": "delay line + filter pool (67 MB) are L2-resident in C2, so frac vs HBM can exceed 1"}
+
+    # ---- e2e through the public API with pinned host buffers (H2D inputs + IRs, D2H outputs)
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        irh = torch.empty(irs.shape, dtype=torch.float32, pin_memory=True)
+        irh.copy_(irs)
+        oh = torch.empty(xh.shape, dtype=torch.float32, pin_memory=True)
+        eng2 = TvolapEngine(partition(ir0.T, L, M), device=local)
+        eng2.set_host_async(True)
+        step(eng2, xh, oh, irh)
+        eng2.synchronize()
+        barrier()
+        tw = time.perf_counter()
+        for _ in range(args.steps):
+            step(eng2, xh, oh, irh)
+            eng2.synchronize()
+        barrier()
+        e2e_s = (time.perf_counter() - tw) / args.steps
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        same = bool(torch.equal(oh, out.cpu()))
+        e2e = {"value": samples_per_step / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(xh.numel() * 4 + irh.numel() * 4),
+               "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_s * 1e3,
+               "timing": "host wall clock around each full pass incl. final synchronize",
+               "matches_device_path": same}
+        del irh
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded white noise + decaying-noise IRs generated on device)",
+        "config": config_block(cfg, H, world), "clocks": clk, "gpu_launches": int(gpu_launches),
+        "roofline": roofline, "e2e": e2e,
+        "realtime_factor": (H * L / W.FS) / (ms_per_step / 1e3),
+    }
+
+    # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on host cores, bounded sample
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = W.host_threads()
+        ch = min(args.cpu_hops, H)
+        secs, yref = cpu_sample(cfg, S, ch, threads, want_output=True)
+        y = out[:, : ch * L].double().cpu().numpy()
+        rel = float(np.abs(y - yref).max() / np.abs(yref).max())
+        secs1, _ = cpu_sample(cfg, 4, 64, 1)
+        line["cpu_baseline"] = {
+            "value": S * ch * L / secs, "unit": UNIT, "cores": min(threads, S), "kind": "port",
+            "sample": f"{S} channels x {ch} hops ({ch // cfg.period} fresh-IR switches) of {cfg.name}",
+            "single_thread_value": 4 * 64 * L / secs1,
+            "parity_rel_err_vs_gpu": rel,
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,212 @@
+/*
+ * tvolap_b200.h — C-ABI drop-in boundary of the B200-native TVOLAP engine.
+ *
+ * Replaces the reference's per-hop streaming path:
+ *   tvolap::partition(ir, hop, min_partitions)      proj/include/tvolap/partition.hpp:38
+ *   tvolap::TvolapEngine ctor                       proj/include/tvolap/engine.hpp:35-36
+ *   TvolapEngine::process(input)                    proj/include/tvolap/engine.hpp:58-59
+ *   TvolapEngine::exchange_filter(next)             proj/include/tvolap/engine.hpp:55-56
+ *   TvolapEngine::reset / op_counts / getters       proj/include/tvolap/engine.hpp:38-50,62-64
+ *   TvolapProcessor(ir, hop) / set_filter(ir)       proj/include/tvolap/reference.hpp:202-221
+ *   forward_real / inverse_real / mac               proj/include/tvolap/spectral.hpp:36-47
+ *   hann_window                                     proj/include/tvolap/partition.hpp:16
+ *
+ * Plain pointers and sizes only. Sample data is fp32, planar, one lane after
+ * another: sample t of lane c lives at ptr[c * lane_stride + t] (the
+ * column-per-channel layout of proj/include/tvolap/audio_buffer.hpp:11-15).
+ * Every pointer argument may be host memory (pageable or pinned) or device
+ * memory of the engine's GPU; the engine detects which. Calls on device
+ * pointers are asynchronous on the engine's stream (see tvolap_set_stream /
+ * tvolap_synchronize); calls on host pointers return when the host output is
+ * written, like the reference's by-value return.
+ *
+ * Every entry point returns a status; the non-zero codes map one-to-one onto
+ * the reference's exception classes (proj/include/tvolap/errors.hpp:10-62).
+ * tvolap_last_error() gives the message of the calling thread's last failure.
+ * There is no CPU fallback: without a usable sm_100 device every call that
+ * needs one fails with TVOLAP_ERR_CUDA.
+ */
+#ifndef TVOLAP_B200_H
+#define TVOLAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TVOLAP_OK 0
+#define TVOLAP_ERR_INVALID_SIZE 1          /* tvolap::InvalidSizeError          errors.hpp:10-13 */
+#define TVOLAP_ERR_INVALID_INPUT 2         /* tvolap::InvalidInputError         errors.hpp:16-19 */
+#define TVOLAP_ERR_INVALID_CONFIGURATION 3 /* tvolap::InvalidConfigurationError errors.hpp:40-43 */
+#define TVOLAP_ERR_INCOMPATIBLE_FILTER 4   /* tvolap::IncompatibleFilterError   errors.hpp:34-37 */
+#define TVOLAP_ERR_INVALID_SPECTRUM 5      /* tvolap::InvalidSpectrumError      errors.hpp:28-31 */
+#define TVOLAP_ERR_CUDA 6                  /* device / driver failure (no reference analogue) */
+
+typedef struct tvolap_engine tvolap_engine;
+
+/* Message for the calling thread's most recent failing call. */
+const char* tvolap_last_error(void);
+
+/* Library version string and the sm_100a build tag. */
+const char* tvolap_version(void);
+
+/* ---------------------------------------------------------------- engines */
+
+/*
+ * Filter-set engine: TvolapProcessor(ir, hop) ≙ TvolapEngine(partition(ir, hop,
+ * min_partitions)) (reference.cpp:328-329, partition.cpp:20-51, engine.cpp:9-32).
+ * ir: channels impulse responses of ir_length taps, ir[c * ir_length + n].
+ * M = max(ceil(ir_length / 2L), min_partitions). Errors: INVALID_INPUT for an
+ * empty IR (partition.cpp:21-22), INVALID_SIZE when 4L is not a power of two
+ * or L < 2 (partition.cpp:23-24).
+ */
+int tvolap_create(tvolap_engine** out, int device, long hop, long channels, long ir_length, const float* ir,
+                  long min_partitions);
+
+/*
+ * Bank engine (BASELINE configs C1/C3/C5): `sources` input streams, each fanned
+ * out to `ears` lanes (audio_buffer.hpp:60-67 fan_out, fused so the ears share
+ * one input spectrum). The filter pool is a pre-partitioned bank of n_bank
+ * entries, bank_ir[(b * ears + e) * ir_length + n]; every source selects one
+ * entry per hop (the zero-copy exchange_filter(shared_ptr) of engine.hpp:55
+ * with pre-built sets). All sources start on entry 0.
+ */
+int tvolap_create_bank(tvolap_engine** out, int device, long hop, long sources, long ears, long n_bank,
+                       long ir_length, const float* bank_ir, long min_partitions);
+
+int tvolap_destroy(tvolap_engine* e);
+
+/*
+ * One hop: TvolapEngine::process (engine.cpp:60-106). in: L samples for each of
+ * `channels` (= sources) lanes; out: L samples for each of channels*ears output
+ * lanes (lane s*ears + e). A staged filter / bank selection is latched first
+ * (engine.cpp:61). rows must equal L (INVALID_SIZE, engine.cpp:64-65) and cols
+ * the input channel count (INVALID_INPUT, engine.cpp:66-67).
+ */
+int tvolap_process(tvolap_engine* e, const float* in, long in_lane_stride, long rows, long cols, float* out,
+                   long out_lane_stride);
+
+/*
+ * n_hops consecutive hops — semantically n_hops process() calls (the
+ * reference's drive() loop, experiment.cpp:43-49). in/out hold n_hops*L
+ * samples per lane. schedule (bank engines only, may be NULL) gives the bank
+ * entry of every (hop, source): schedule[h * sources + s]; when NULL the
+ * current selection holds for all hops. Host pointers are streamed through
+ * pinned staging buffers with copies overlapping the kernels.
+ */
+int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
+                        long n_hops, const int32_t* schedule);
+
+/*
+ * Stage a replacement filter: TvolapProcessor::set_filter(ir) ≙
+ * exchange_filter(partition(ir, L, M)) (reference.cpp:335-338,
+ * engine.cpp:37-48). The partition runs on the device on a side stream
+ * overlapping the running hops; the set is latched at the next process call
+ * (last staged wins). Errors: INCOMPATIBLE_FILTER when channels differ or the
+ * IR needs more than M partitions (engine.cpp:38-45); INVALID_INPUT for an
+ * empty IR. Filter-set engines only (INVALID_CONFIGURATION on a bank engine).
+ */
+int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, long channels);
+
+/* Stage per-source bank selections idx[sources], latched at the next hop. */
+int tvolap_select_bank(tvolap_engine* e, const int32_t* idx);
+
+/* TvolapEngine::reset (engine.cpp:108-118): zero all state, keep any staged filter. */
+int tvolap_reset(tvolap_engine* e);
+
+/* Getters: engine.hpp:38-50. */
+long tvolap_hop(const tvolap_engine* e);
+long tvolap_channels(const tvolap_engine* e);        /* input channels (sources) */
+long tvolap_output_channels(const tvolap_engine* e); /* channels * ears */
+long tvolap_partition_count(const tvolap_engine* e);
+long tvolap_delay_line_depth(const tvolap_engine* e); /* 2M-1 */
+long tvolap_latency(const tvolap_engine* e);          /* 2L */
+long tvolap_switching_latency(const tvolap_engine* e);/* L */
+long tvolap_stream_delay(const tvolap_engine* e);     /* L */
+long tvolap_hops_processed(const tvolap_engine* e);
+
+/*
+ * EngineOpCounts (engine.hpp:17-21): cumulative forward transforms, inverse
+ * transforms and spectral MACs actually executed. For ears == 1 these equal the
+ * reference's per-channel counts; with ears == 2 one forward transform serves
+ * both ears of a source.
+ */
+int tvolap_op_counts(const tvolap_engine* e, uint64_t* forward, uint64_t* inverse, uint64_t* macs);
+
+/* Engine stream control. `stream` is a cudaStream_t passed as void*; NULL restores the engine's own. */
+int tvolap_set_stream(tvolap_engine* e, void* stream);
+int tvolap_synchronize(tvolap_engine* e);
+
+/*
+ * Throughput mode for pinned host buffers: when enabled, process / process_hops
+ * on pinned (cudaHostAlloc / cudaHostRegister) host memory return once the
+ * copies and kernels are queued, like cudaMemcpyAsync; tvolap_synchronize()
+ * waits for the outputs. exchange_filter from pinned memory is always
+ * asynchronous (the buffer must stay untouched until the next process call
+ * has been synchronized). Pageable host memory is always synchronous.
+ */
+int tvolap_set_host_async(tvolap_engine* e, int enable);
+
+/*
+ * Kernel timing: while enabled, every fused hop-kernel launch is bracketed by
+ * CUDA events on the launching stream. tvolap_kernel_time() waits for them and
+ * returns the summed device time and the number of launches since profiling
+ * was enabled (or last read), then starts a new window.
+ */
+int tvolap_set_profiling(tvolap_engine* e, int enable);
+int tvolap_kernel_time(tvolap_engine* e, double* total_ms, long* launches);
+
+/* Launch configuration chosen for this engine: CTAs per source (cluster size P) and threads per CTA. */
+int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* threads_per_cta);
+/* Override P (1, 2, 4 or 8) and threads per CTA (128..1024); 0 keeps the current value. */
+int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_per_cta);
+
+/* Number of kernels this engine has launched since creation. */
+uint64_t tvolap_kernel_launches(const tvolap_engine* e);
+
+/* ------------------------------------------------------ spectral primitives */
+/* Batched K1/K5 building blocks, exposed so the reference's spectral tests
+ * (proj/tests/test_spectral.cpp) run against the device FFT. */
+
+/* forward_real (spectral.cpp:99-125): x[b * n + i] -> bins[(b * (n/2+1) + k) * 2 + {re,im}].
+ * n must be a power of two >= 8 (INVALID_SIZE otherwise). */
+int tvolap_forward_real(int device, long n, long batch, const float* x, float* bins);
+
+/* inverse_real (spectral.cpp:127-158): bins -> x, with the 1/n scaling.
+ * INVALID_SPECTRUM if a DC or Nyquist bin has a non-zero imaginary part. */
+int tvolap_inverse_real(int device, long n, long batch, const float* bins, float* x);
+
+/* mac (spectral.cpp:160-172): out = acc + a*b over nbins complex bins, batch frames. */
+int tvolap_mac(int device, long nbins, long batch, const float* acc, const float* a, const float* b, float* out);
+
+/* hann_window (partition.cpp:10-18), computed in fp64 and rounded: w[2L]. */
+int tvolap_hann_window(long hop, float* w);
+
+/*
+ * partition (partition.cpp:20-51) on the device: spectra[((c * M + m) * (2L+1) + k) * 2 + {re,im}],
+ * M = max(ceil(ir_length / 2L), min_partitions) returned in *partitions.
+ */
+int tvolap_partition(int device, long hop, long channels, long ir_length, const float* ir, long min_partitions,
+                     float* spectra, long* partitions);
+
+/* ------------------------------------------------------ device workload helpers */
+/* Fill device memory with the seeded generators of workload.h (the same values the
+ * host twin libtvolap_workload.so produces). Used by the benchmark to keep
+ * inputs resident in HBM; not part of the reference boundary. */
+int tvolap_gen_white_device(int device, uint64_t seed, long lane0, long lanes, long t0, long n, float* out,
+                            long stride);
+int tvolap_gen_irs_device(int device, uint64_t seed, long count, const long* lanes, const long* ears,
+                          const long* ks, const double* t60, double fs, long len, float* out);
+
+/* Binaural mix (config C3): mix[e * mix_stride + t] = sum_s out[(s * ears + e) * out_stride + t],
+ * summed in a fixed order (deterministic). Device pointers. */
+int tvolap_mix_device(int device, long sources, long ears, long samples, const float* out, long out_stride,
+                      float* mix, long mix_stride, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TVOLAP_B200_H */

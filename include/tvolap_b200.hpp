@@ -1,0 +1,210 @@
+// tvolap_b200.hpp — header-only C++ drop-in over the C-ABI (tvolap_b200.h).
+//
+// Mirrors the reference's public C++ surface for the hot path so existing
+// callers (drive() in proj/src/experiment.cpp:33-54, FrameAdapter in
+// proj/src/frame_adapter.cpp:13-43, the CLI's run_process) keep their shape:
+//   partition(ir, hop, min_partitions)          proj/include/tvolap/partition.hpp:38
+//   FilterPartitionSet                           proj/include/tvolap/partition.hpp:21-32
+//   TvolapEngine                                 proj/include/tvolap/engine.hpp:33-94
+//   TvolapProcessor / StreamingProcessor face    proj/include/tvolap/reference.hpp:202-221
+//   exception classes                            proj/include/tvolap/errors.hpp:10-43
+// Eigen is not required: Frames is a minimal column-major (rows = samples,
+// cols = channels) fp64 array with the same indexing as Eigen::ArrayXXd, and
+// INTEGRATION.md shows the two-line Eigen adapter. Compute is fp32 on the GPU.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tvolap_b200.h"
+
+namespace tvolap_b200 {
+
+using Index = long;
+
+class InvalidSizeError : public std::invalid_argument {
+public:
+    using std::invalid_argument::invalid_argument;
+};
+class InvalidInputError : public std::invalid_argument {
+public:
+    using std::invalid_argument::invalid_argument;
+};
+class InvalidSpectrumError : public std::invalid_argument {
+public:
+    using std::invalid_argument::invalid_argument;
+};
+class IncompatibleFilterError : public std::invalid_argument {
+public:
+    using std::invalid_argument::invalid_argument;
+};
+class InvalidConfigurationError : public std::invalid_argument {
+public:
+    using std::invalid_argument::invalid_argument;
+};
+class CudaError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+    if (rc == TVOLAP_OK) return;
+    const std::string msg = tvolap_last_error();
+    switch (rc) {
+        case TVOLAP_ERR_INVALID_SIZE: throw InvalidSizeError(msg);
+        case TVOLAP_ERR_INVALID_INPUT: throw InvalidInputError(msg);
+        case TVOLAP_ERR_INVALID_CONFIGURATION: throw InvalidConfigurationError(msg);
+        case TVOLAP_ERR_INCOMPATIBLE_FILTER: throw IncompatibleFilterError(msg);
+        case TVOLAP_ERR_INVALID_SPECTRUM: throw InvalidSpectrumError(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+// Column-major rows x cols array (Eigen::ArrayXXd's storage order).
+struct Frames {
+    Index rows_ = 0, cols_ = 0;
+    std::vector<double> data;
+    Frames() = default;
+    Frames(Index r, Index c, double fill = 0.0) : rows_(r), cols_(c), data((size_t)(r * c), fill) {}
+    Index rows() const { return rows_; }
+    Index cols() const { return cols_; }
+    double& operator()(Index r, Index c) { return data[(size_t)(c * rows_ + r)]; }
+    double operator()(Index r, Index c) const { return data[(size_t)(c * rows_ + r)]; }
+};
+
+struct ImpulseResponse {  // audio_buffer.hpp:30-42
+    Frames samples;       // taps x channels
+    double sample_rate = 48000.0;
+    Index length() const { return samples.rows(); }
+    Index channels() const { return samples.cols(); }
+};
+
+struct EngineOpCounts {  // engine.hpp:17-21
+    std::uint64_t forward_transforms = 0;
+    std::uint64_t inverse_transforms = 0;
+    std::uint64_t spectral_macs = 0;
+};
+
+// partition.hpp:21-32. Spectra are computed on the device when an engine takes
+// the set; the set keeps the fp32 taps (channel-major) it was built from.
+struct FilterPartitionSet {
+    Index hop = 0;
+    Index partition_count = 0;
+    Index channels = 0;
+    Index source_length = 0;
+    double normalization_gain = 0.5;
+    double sample_rate = 48000.0;
+    std::vector<float> taps;  // taps[c * source_length + n]
+    Index transform_length() const { return 4 * hop; }
+    Index padded_length() const { return 2 * hop * partition_count; }
+};
+
+inline bool is_power_of_two(Index n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// partition.cpp:20-51 (validation and M; the transform itself runs on the GPU).
+inline FilterPartitionSet partition(const ImpulseResponse& ir, Index hop, Index min_partitions = 1) {
+    if (ir.length() < 1 || ir.channels() < 1) throw InvalidInputError("partition: impulse response is empty");
+    if (hop < 2 || !is_power_of_two(4 * hop))
+        throw InvalidSizeError("partition: 4L must be a power of two, got L = " + std::to_string(hop));
+    const Index slice = 2 * hop;
+    FilterPartitionSet s;
+    s.hop = hop;
+    s.partition_count = std::max((ir.length() + slice - 1) / slice, std::max<Index>(min_partitions, 1));
+    s.channels = ir.channels();
+    s.source_length = ir.length();
+    s.sample_rate = ir.sample_rate;
+    s.taps.resize((size_t)(s.channels * s.source_length));
+    for (Index c = 0; c < s.channels; ++c)
+        for (Index n = 0; n < s.source_length; ++n) s.taps[(size_t)(c * s.source_length + n)] = (float)ir.samples(n, c);
+    return s;
+}
+
+class TvolapEngine {
+public:
+    explicit TvolapEngine(std::shared_ptr<const FilterPartitionSet> filter, int device = 0) : filter_(std::move(filter)) {
+        if (!filter_) throw InvalidConfigurationError("engine requires a filter partition set");
+        tvolap_engine* h = nullptr;
+        check(tvolap_create(&h, device, filter_->hop, filter_->channels, filter_->source_length, filter_->taps.data(),
+                            filter_->partition_count));
+        h_.reset(h);
+    }
+    explicit TvolapEngine(const FilterPartitionSet& filter, int device = 0)
+        : TvolapEngine(std::make_shared<FilterPartitionSet>(filter), device) {}
+
+    Index hop() const { return tvolap_hop(h_.get()); }
+    Index channels() const { return tvolap_channels(h_.get()); }
+    Index partition_count() const { return tvolap_partition_count(h_.get()); }
+    Index delay_line_depth() const { return tvolap_delay_line_depth(h_.get()); }
+    Index latency() const { return tvolap_latency(h_.get()); }
+    Index switching_latency() const { return tvolap_switching_latency(h_.get()); }
+    Index stream_delay() const { return tvolap_stream_delay(h_.get()); }
+
+    // engine.cpp:37-48
+    void exchange_filter(std::shared_ptr<const FilterPartitionSet> next) {
+        if (!next) throw IncompatibleFilterError("replacement filter is null");
+        if (next->hop != hop()) throw IncompatibleFilterError("replacement filter hop differs");
+        if (next->partition_count != partition_count())
+            throw IncompatibleFilterError("replacement filter partition count differs");
+        if (next->channels != channels()) throw IncompatibleFilterError("replacement filter channel count differs");
+        check(tvolap_exchange_filter(h_.get(), next->taps.data(), next->source_length, next->channels));
+        filter_ = std::move(next);
+    }
+    void exchange_filter(const FilterPartitionSet& next) { exchange_filter(std::make_shared<FilterPartitionSet>(next)); }
+
+    // engine.cpp:60-106: exactly L rows x C cols in, same shape out.
+    Frames process(const Frames& input) {
+        std::vector<float> in((size_t)(input.rows() * input.cols()));
+        for (size_t i = 0; i < in.size(); ++i) in[i] = (float)input.data[i];
+        std::vector<float> out((size_t)(std::max<Index>(input.rows(), 1) * channels()));
+        check(tvolap_process(h_.get(), in.data(), input.rows(), input.rows(), input.cols(), out.data(), input.rows()));
+        Frames y(input.rows(), channels());
+        for (size_t i = 0; i < y.data.size(); ++i) y.data[i] = out[i];
+        return y;
+    }
+
+    void reset() { check(tvolap_reset(h_.get())); }
+
+    EngineOpCounts op_counts() const {
+        EngineOpCounts c;
+        check(tvolap_op_counts(h_.get(), &c.forward_transforms, &c.inverse_transforms, &c.spectral_macs));
+        return c;
+    }
+    const FilterPartitionSet& filter() const { return *filter_; }
+    tvolap_engine* handle() const { return h_.get(); }
+
+private:
+    struct Del {
+        void operator()(tvolap_engine* e) const { tvolap_destroy(e); }
+    };
+    std::shared_ptr<const FilterPartitionSet> filter_;
+    std::unique_ptr<tvolap_engine, Del> h_;
+};
+
+// reference.hpp:202-221
+class TvolapProcessor {
+public:
+    TvolapProcessor(const ImpulseResponse& ir, Index hop, int device = 0)
+        : engine_(std::make_shared<FilterPartitionSet>(partition(ir, hop)), device) {}
+    std::string name() const { return "tvolap"; }
+    Index hop() const { return engine_.hop(); }
+    Index channels() const { return engine_.channels(); }
+    Index latency() const { return engine_.latency(); }
+    Index stream_delay() const { return engine_.stream_delay(); }
+    Index switching_latency() const { return engine_.switching_latency(); }
+    Frames process(const Frames& input) { return engine_.process(input); }
+    void set_filter(const ImpulseResponse& ir) {  // reference.cpp:335-338
+        engine_.exchange_filter(std::make_shared<FilterPartitionSet>(partition(ir, engine_.hop(), engine_.partition_count())));
+    }
+    void reset() { engine_.reset(); }
+    TvolapEngine& engine() { return engine_; }
+
+private:
+    TvolapEngine engine_;
+};
+
+}  // namespace tvolap_b200

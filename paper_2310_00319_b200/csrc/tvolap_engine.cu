@@ -1,0 +1,917 @@
+// Host side of the B200 TVOLAP engine: the C-ABI of include/tvolap_b200.h.
+//
+// Mirrors tvolap::TvolapEngine / TvolapProcessor (proj/include/tvolap/engine.hpp:33-94,
+// proj/src/engine.cpp:9-118, proj/src/reference.cpp:328-342): construction
+// partitions the IRs on the device, process() runs the fused hop kernel,
+// exchange_filter() stages a replacement set that is latched at the next hop
+// boundary (last staged wins, a staged set survives reset). Device state:
+//   ring  [S][2][M][2L] complex64  frequency-domain delay line (two parity rings)
+//   pool  [entries][E][M][2L]       filter partition spectra; set engines keep
+//                                   two slots of S entries (active / staged),
+//                                   bank engines the whole bank
+//   hist  [S][L], ola [S][E][3L]    per-lane time-domain state
+// Host pointers are streamed through pinned staging buffers: H2D, kernel and
+// D2H of consecutive chunks run on three streams so copies overlap compute.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tvolap_b200.h"
+#include "tvolap_internal.cuh"
+
+using tvb::HopParams;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+struct CudaFail {
+    cudaError_t err;
+    const char* what;
+};
+
+#define CK(expr)                                                     \
+    do {                                                             \
+        cudaError_t e_ = (expr);                                     \
+        if (e_ != cudaSuccess) throw CudaFail{e_, #expr};            \
+    } while (0)
+
+struct ApiError {
+    int code;
+    std::string msg;
+};
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TVOLAP_OK;
+    } catch (const ApiError& e) {
+        return set_err(e.code, e.msg);
+    } catch (const CudaFail& e) {
+        return set_err(TVOLAP_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorName(e.err) + " (" +
+                                            cudaGetErrorString(e.err) + ") in " + e.what);
+    } catch (const std::exception& e) {
+        return set_err(TVOLAP_ERR_CUDA, e.what());
+    }
+}
+
+bool is_pow2(long n) { return n > 0 && (n & (n - 1)) == 0; }
+
+enum class Mem { Device, Pinned, Pageable };
+
+Mem classify(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return Mem::Pageable;
+    }
+    switch (a.type) {
+        case cudaMemoryTypeDevice:
+        case cudaMemoryTypeManaged:
+            return Mem::Device;
+        case cudaMemoryTypeHost:
+            return Mem::Pinned;
+        default:
+            return Mem::Pageable;
+    }
+}
+
+void require_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw ApiError{TVOLAP_ERR_CUDA, "no CUDA device: the B200 engine has no CPU fallback"};
+    }
+    if (device < 0 || device >= n) throw ApiError{TVOLAP_ERR_CUDA, "device index out of range"};
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        throw ApiError{TVOLAP_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (Blackwell)"};
+}
+
+// fp64 tables rounded once to fp32 (spectral.cpp:50-61 formulas).
+struct Tables {
+    std::vector<float2> tw, pk;
+    explicit Tables(long nc) {
+        const double pi = 3.14159265358979323846264338327950288;
+        tw.resize(nc);
+        for (long t = 0; t < nc; ++t) {
+            const double a = -2.0 * pi * (double)t / (double)nc;
+            tw[t] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        pk.resize(nc + 2);
+        for (long k = 0; k <= nc; ++k) {
+            const double a = -2.0 * pi * (double)k / (double)(2 * nc);
+            pk[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+        }
+        pk[nc + 1] = make_float2(0.f, 0.f);
+    }
+};
+
+std::vector<float> hann(long hop) {  // partition.cpp:10-18
+    const double pi = 3.14159265358979323846264338327950288;
+    std::vector<float> w(2 * hop);
+    for (long i = 0; i < 2 * hop; ++i) w[i] = (float)(1.0 - std::cos(2.0 * pi * (double)i / (double)(2 * hop)));
+    return w;
+}
+
+template <class T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+}  // namespace
+
+struct tvolap_engine {
+    int device = 0;
+    long L = 0, M = 0, S = 0, E = 1, N = 0;
+    bool bank = false;
+    long n_bank = 0;
+    cudaStream_t own = nullptr, stream = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_side = nullptr, ev_main = nullptr, ev_start = nullptr;
+    cudaEvent_t ev_slot[2] = {};  // last hop kernel that read filter slot 0 / 1
+    float2 *ring = nullptr, *pool = nullptr, *tw = nullptr, *pk = nullptr;
+    float *win = nullptr, *hist = nullptr, *ola = nullptr;
+    int* d_sel = nullptr;
+    std::vector<int> sel, staged;
+    bool sel_staged = false;
+    int active = 0;
+    bool pending = false;
+    float* d_irstage = nullptr;
+    size_t irstage_cap = 0;
+    // chunked host pipeline
+    long chunk_hops = 0;
+    float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
+    int* d_sch[2] = {};
+    long sch_cap = 0;
+    cudaEvent_t ev_in[2] = {}, ev_k[2] = {}, ev_o[2] = {};
+    bool profiling = false;  // bracket every hop-kernel launch with CUDA events
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
+    long chunk_seq = 0;     // alternates the double-buffered staging across calls
+    bool host_async = false;  // pinned host I/O returns before completion
+    int P = 1, NT = 256;
+    uint64_t fwd = 0, inv = 0, macs = 0, launches = 0;
+    long hops = 0;
+    std::mutex mu;
+
+    ~tvolap_engine() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        if (side) cudaStreamSynchronize(side);
+        for (void* p : {(void*)ring, (void*)pool, (void*)tw, (void*)pk, (void*)win, (void*)hist, (void*)ola,
+                        (void*)d_sel, (void*)d_irstage, (void*)d_in[0], (void*)d_in[1], (void*)d_out[0],
+                        (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1]})
+            if (p) cudaFree(p);
+        for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
+            if (p) cudaFreeHost(p);
+        for (cudaEvent_t ev : {ev_side, ev_main, ev_start, ev_in[0], ev_in[1], ev_k[0], ev_k[1], ev_o[0], ev_o[1],
+                                ev_slot[0], ev_slot[1]})
+            if (ev) cudaEventDestroy(ev);
+        for (auto& pr : prof_events) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        for (cudaStream_t s : {own, side, h2d, d2h})
+            if (s) cudaStreamDestroy(s);
+    }
+};
+
+namespace {
+
+void pick_launch_config(tvolap_engine* e) {
+    // P: CTAs per source. Enough CTAs to cover the 148 SMs, never a slice
+    // smaller than one float4 per thread group.
+    long p = 1;
+    while (p < 8 && p * 2 <= e->L && e->S * p < 148) p *= 2;
+    e->P = (int)p;
+    e->NT = 256;
+    const int ep = env_int("TVOLAP_P", 0), et = env_int("TVOLAP_NT", 0);
+    if (ep > 0) e->P = ep;
+    if (et > 0) e->NT = et;
+}
+
+void validate_launch(const tvolap_engine* e, int P, int NT) {
+    if (P < 1 || P > 8 || !is_pow2(P) || P > e->L)
+        throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "cluster size P must be 1, 2, 4 or 8 and <= L"};
+    if (NT < 32 || NT > 1024 || !is_pow2(NT))
+        throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "threads per CTA must be a power of two in [32, 1024]"};
+    const size_t smem = tvb::hop_kernel_smem_bytes((int)e->L, P, (int)e->E, NT);
+    if (smem > 227 * 1024)
+        throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION,
+                       "hop L=" + std::to_string(e->L) + " needs " + std::to_string(smem) +
+                           " B of shared memory per CTA (max 227 KB)"};
+}
+
+void init_common(tvolap_engine* e, int device, long hop, long sources, long ears, long partitions) {
+    e->device = device;
+    e->L = hop;
+    e->N = 2 * hop;
+    e->S = sources;
+    e->E = ears;
+    e->M = partitions;
+    CK(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
+    e->stream = e->own;
+    for (cudaEvent_t* ev : {&e->ev_side, &e->ev_main, &e->ev_start, &e->ev_in[0], &e->ev_in[1], &e->ev_k[0],
+                            &e->ev_k[1], &e->ev_o[0], &e->ev_o[1], &e->ev_slot[0], &e->ev_slot[1]})
+        CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    Tables t(e->N);
+    std::vector<float> w = hann(hop);
+    e->tw = dalloc<float2>(e->N);
+    e->pk = dalloc<float2>(e->N + 2);
+    e->win = dalloc<float>(e->N);
+    CK(cudaMemcpy(e->tw, t.tw.data(), sizeof(float2) * e->N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(e->pk, t.pk.data(), sizeof(float2) * (e->N + 2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(e->win, w.data(), sizeof(float) * e->N, cudaMemcpyHostToDevice));
+    const size_t ring_elems = (size_t)e->S * 2 * e->M * e->N;
+    e->ring = dalloc<float2>(ring_elems);
+    e->hist = dalloc<float>((size_t)e->S * e->L);
+    e->ola = dalloc<float>((size_t)e->S * e->E * 3 * e->L);
+    CK(cudaMemsetAsync(e->ring, 0, ring_elems * sizeof(float2), e->stream));
+    CK(cudaMemsetAsync(e->hist, 0, (size_t)e->S * e->L * sizeof(float), e->stream));
+    CK(cudaMemsetAsync(e->ola, 0, (size_t)e->S * e->E * 3 * e->L * sizeof(float), e->stream));
+    e->sel.assign(e->S, 0);
+    e->staged.assign(e->S, 0);
+    e->d_sel = dalloc<int>(e->S);
+    CK(cudaMemsetAsync(e->d_sel, 0, sizeof(int) * e->S, e->stream));
+    pick_launch_config(e);
+    validate_launch(e, e->P, e->NT);
+}
+
+// Device copy of a host/device IR table; returns a device pointer valid on `s`.
+const float* stage_ir(tvolap_engine* e, const float* ir, size_t count, cudaStream_t s) {
+    if (classify(ir) == Mem::Device) return ir;
+    if (e->irstage_cap < count) {
+        CK(cudaStreamSynchronize(s));
+        if (e->d_irstage) CK(cudaFree(e->d_irstage));
+        e->d_irstage = dalloc<float>(count);
+        e->irstage_cap = count;
+    }
+    CK(cudaMemcpyAsync(e->d_irstage, ir, count * sizeof(float), cudaMemcpyHostToDevice, s));
+    return e->d_irstage;
+}
+
+void latch(tvolap_engine* e) {  // engine.cpp:54-58
+    std::lock_guard<std::mutex> lock(e->mu);
+    if (e->pending) {
+        CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+        e->active ^= 1;
+        e->pending = false;
+    }
+    if (e->sel_staged) {
+        CK(cudaMemcpyAsync(e->d_sel, e->staged.data(), sizeof(int) * e->S, cudaMemcpyHostToDevice, e->stream));
+        e->sel = e->staged;
+        e->sel_staged = false;
+    }
+}
+
+void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_stride, float* out, long out_stride,
+                 const int* sched, long sched_stride) {
+    HopParams p;
+    p.L = (int)e->L;
+    p.M = (int)e->M;
+    p.S = (int)e->S;
+    p.P = e->P;
+    p.hop0 = hop0;
+    p.n_hops = (int)n;
+    p.in = in;
+    p.in_stride = in_stride;
+    p.out = out;
+    p.out_stride = out_stride;
+    p.ring = e->ring;
+    p.pool = e->pool;
+    p.sched = sched;
+    p.sched_stride = sched_stride;
+    p.entry_base = e->bank ? 0 : e->active * (int)e->S;
+    p.hist = e->hist;
+    p.ola = e->ola;
+    p.tw = e->tw;
+    p.pk = e->pk;
+    p.win = e->win;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (e->profiling) {
+        if (e->prof_used == e->prof_events.size()) {
+            cudaEvent_t a, b;
+            CK(cudaEventCreate(&a));
+            CK(cudaEventCreate(&b));
+            e->prof_events.emplace_back(a, b);
+        }
+        t0 = e->prof_events[e->prof_used].first;
+        t1 = e->prof_events[e->prof_used].second;
+        ++e->prof_used;
+        CK(cudaEventRecord(t0, e->stream));
+    }
+    CK(tvb::launch_hop_kernel(p, (int)e->E, e->NT, e->stream));
+    if (t1) CK(cudaEventRecord(t1, e->stream));
+    ++e->launches;
+    if (!e->bank) CK(cudaEventRecord(e->ev_slot[e->active], e->stream));
+}
+
+void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
+    if (e->chunk_hops < kc) {
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaStreamSynchronize(e->h2d));
+        CK(cudaStreamSynchronize(e->d2h));
+        for (int b = 0; b < 2; ++b) {
+            if (e->d_in[b]) CK(cudaFree(e->d_in[b]));
+            if (e->d_out[b]) CK(cudaFree(e->d_out[b]));
+            if (e->h_in[b]) CK(cudaFreeHost(e->h_in[b]));
+            if (e->h_out[b]) CK(cudaFreeHost(e->h_out[b]));
+            e->d_in[b] = dalloc<float>((size_t)e->S * kc * e->L);
+            e->d_out[b] = dalloc<float>((size_t)e->S * e->E * kc * e->L);
+            CK(cudaMallocHost(&e->h_in[b], sizeof(float) * e->S * kc * e->L));
+            CK(cudaMallocHost(&e->h_out[b], sizeof(float) * e->S * e->E * kc * e->L));
+        }
+        e->chunk_hops = kc;
+    }
+    if (need_sched && e->sch_cap < kc) {
+        CK(cudaStreamSynchronize(e->stream));
+        for (int b = 0; b < 2; ++b) {
+            if (e->d_sch[b]) CK(cudaFree(e->d_sch[b]));
+            e->d_sch[b] = dalloc<int>((size_t)e->S * kc);
+        }
+        e->sch_cap = kc;
+    }
+}
+
+void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
+                       const int* sched) {
+    CK(cudaSetDevice(e->device));
+    latch(e);
+    const long L = e->L, S = e->S, E = e->E;
+    const Mem min = classify(in), mout = classify(out);
+    const Mem msch = sched ? classify(sched) : Mem::Device;
+    if (min == Mem::Device && mout == Mem::Device && msch == Mem::Device) {
+        launch_hops(e, e->hops, n, in, in_stride, out, out_stride, sched, sched ? S : 0);
+    } else {
+        const long per_hop = S * L * (1 + E);
+        const long kc_max = std::max<long>(1, std::min<long>(n, (1L << 22) / per_hop));
+        ensure_pipeline(e, kc_max, sched && msch != Mem::Device);
+        const long Kc = e->chunk_hops;
+        CK(cudaEventRecord(e->ev_start, e->stream));
+        CK(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
+        CK(cudaStreamWaitEvent(e->d2h, e->ev_start, 0));
+        struct Pend {
+            long h0 = -1, kc = 0;
+        } pend[2];
+        auto flush_out = [&](int b) {
+            if (pend[b].h0 < 0) return;
+            CK(cudaEventSynchronize(e->ev_o[b]));
+            for (long r = 0; r < S * E; ++r)
+                std::memcpy(out + r * out_stride + pend[b].h0 * L, e->h_out[b] + r * Kc * L,
+                            sizeof(float) * pend[b].kc * L);
+            pend[b].h0 = -1;
+        };
+        for (long i = 0, h0 = 0; h0 < n; ++i, h0 += Kc) {
+            const int b = (int)(e->chunk_seq++ & 1);
+            const long kc = std::min(Kc, n - h0);
+            const float* in_ptr;
+            long in_s;
+            const int* sch_ptr = sched ? sched + h0 * S : nullptr;
+            bool copied_in = false;
+            if (min == Mem::Device) {
+                in_ptr = in + h0 * L;
+                in_s = in_stride;
+            } else {
+                CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
+                if (min == Mem::Pinned) {
+                    CK(cudaMemcpy2DAsync(e->d_in[b], Kc * L * sizeof(float), in + h0 * L, in_stride * sizeof(float),
+                                         kc * L * sizeof(float), S, cudaMemcpyHostToDevice, e->h2d));
+                } else {
+                    CK(cudaEventSynchronize(e->ev_in[b]));
+                    for (long r = 0; r < S; ++r)
+                        std::memcpy(e->h_in[b] + r * Kc * L, in + r * in_stride + h0 * L, sizeof(float) * kc * L);
+                    CK(cudaMemcpyAsync(e->d_in[b], e->h_in[b], sizeof(float) * S * Kc * L, cudaMemcpyHostToDevice,
+                                       e->h2d));
+                }
+                in_ptr = e->d_in[b];
+                in_s = Kc * L;
+                copied_in = true;
+            }
+            if (sched && msch != Mem::Device) {
+                if (!copied_in) CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
+                CK(cudaMemcpyAsync(e->d_sch[b], sched + h0 * S, sizeof(int) * S * kc, cudaMemcpyHostToDevice, e->h2d));
+                sch_ptr = e->d_sch[b];
+                copied_in = true;
+            }
+            if (copied_in) {
+                CK(cudaEventRecord(e->ev_in[b], e->h2d));
+                CK(cudaStreamWaitEvent(e->stream, e->ev_in[b], 0));
+            }
+            float* out_ptr;
+            long out_s;
+            if (mout == Mem::Device) {
+                out_ptr = out + h0 * L;
+                out_s = out_stride;
+            } else {
+                CK(cudaStreamWaitEvent(e->stream, e->ev_o[b], 0));
+                out_ptr = e->d_out[b];
+                out_s = Kc * L;
+            }
+            launch_hops(e, e->hops + h0, kc, in_ptr, in_s, out_ptr, out_s, sch_ptr, sched ? S : 0);
+            CK(cudaEventRecord(e->ev_k[b], e->stream));
+            if (mout != Mem::Device) {
+                CK(cudaStreamWaitEvent(e->d2h, e->ev_k[b], 0));
+                if (mout == Mem::Pinned) {
+                    CK(cudaMemcpy2DAsync(out + h0 * L, out_stride * sizeof(float), e->d_out[b], Kc * L * sizeof(float),
+                                         kc * L * sizeof(float), S * E, cudaMemcpyDeviceToHost, e->d2h));
+                } else {
+                    flush_out(b);
+                    CK(cudaMemcpyAsync(e->h_out[b], e->d_out[b], sizeof(float) * S * E * Kc * L,
+                                       cudaMemcpyDeviceToHost, e->d2h));
+                    pend[b].h0 = h0;
+                    pend[b].kc = kc;
+                }
+                CK(cudaEventRecord(e->ev_o[b], e->d2h));
+            }
+        }
+        flush_out(0);
+        flush_out(1);
+        // later work on the engine stream sees the outputs
+        CK(cudaEventRecord(e->ev_start, e->d2h));
+        CK(cudaStreamWaitEvent(e->stream, e->ev_start, 0));
+    }
+    if (sched) {  // the last row becomes the current selection
+        std::vector<int> last(S);
+        if (msch == Mem::Device) {
+            CK(cudaMemcpyAsync(e->d_sel, sched + (n - 1) * S, sizeof(int) * S, cudaMemcpyDeviceToDevice, e->stream));
+            CK(cudaMemcpyAsync(last.data(), sched + (n - 1) * S, sizeof(int) * S, cudaMemcpyDeviceToHost, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
+        } else {
+            std::memcpy(last.data(), sched + (n - 1) * S, sizeof(int) * S);
+            CK(cudaMemcpyAsync(e->d_sel, last.data(), sizeof(int) * S, cudaMemcpyHostToDevice, e->stream));
+        }
+        e->sel = last;
+    }
+    CK(cudaEventRecord(e->ev_main, e->stream));
+    e->hops += n;
+    e->fwd += (uint64_t)(S * n);
+    e->inv += (uint64_t)(S * E * n);
+    e->macs += (uint64_t)(S * E * e->M * n);
+    const bool pageable = min == Mem::Pageable || mout == Mem::Pageable || msch == Mem::Pageable;
+    if (pageable || (!e->host_async && (min != Mem::Device || mout != Mem::Device)))
+        CK(cudaStreamSynchronize(e->stream));
+}
+
+int check_hops_args(const tvolap_engine* e, const float* in, const float* out, long n) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (!in || !out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null input or output buffer");
+    if (n < 1) return set_err(TVOLAP_ERR_INVALID_SIZE, "n_hops must be >= 1");
+    return TVOLAP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tvolap_last_error(void) { return g_err.c_str(); }
+
+const char* tvolap_version(void) { return "tvolap_b200 0.1 (sm_100a)"; }
+
+int tvolap_create(tvolap_engine** out, int device, long hop, long channels, long ir_length, const float* ir,
+                  long min_partitions) {
+    if (!out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null output handle");
+    *out = nullptr;
+    // partition.cpp:21-24 checks, in the reference's order
+    if (ir_length < 1 || channels < 1 || !ir)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "partition: impulse response is empty");
+    if (hop < 2 || !is_pow2(4 * hop))
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "partition: 4L must be a power of two, got L = " + std::to_string(hop));
+    tvolap_engine* e = nullptr;
+    const int rc = guarded([&] {
+        require_device(device);
+        const long slice = 2 * hop;
+        const long M = std::max((ir_length + slice - 1) / slice, std::max<long>(min_partitions, 1));
+        e = new tvolap_engine();
+        try {
+            init_common(e, device, hop, channels, 1, M);
+            const size_t slot = (size_t)channels * M * e->N;
+            e->pool = dalloc<float2>(2 * slot);
+            CK(cudaMemsetAsync(e->pool, 0, 2 * slot * sizeof(float2), e->stream));
+            const float* src = stage_ir(e, ir, (size_t)channels * ir_length, e->stream);
+            CK(tvb::launch_partition((int)hop, (int)M, channels, src, ir_length, ir_length, e->pool, 0, e->tw, e->pk,
+                                     e->stream));
+            ++e->launches;
+            CK(cudaStreamSynchronize(e->stream));
+        } catch (...) {
+            delete e;
+            e = nullptr;
+            throw;
+        }
+    });
+    *out = e;
+    return rc;
+}
+
+int tvolap_create_bank(tvolap_engine** out, int device, long hop, long sources, long ears, long n_bank,
+                       long ir_length, const float* bank_ir, long min_partitions) {
+    if (!out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null output handle");
+    *out = nullptr;
+    if (ir_length < 1 || sources < 1 || n_bank < 1 || !bank_ir)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "partition: impulse response is empty");
+    if (ears < 1 || ears > 2) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "ears must be 1 or 2");
+    if (hop < 2 || !is_pow2(4 * hop))
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "partition: 4L must be a power of two, got L = " + std::to_string(hop));
+    tvolap_engine* e = nullptr;
+    const int rc = guarded([&] {
+        require_device(device);
+        const long slice = 2 * hop;
+        const long M = std::max((ir_length + slice - 1) / slice, std::max<long>(min_partitions, 1));
+        e = new tvolap_engine();
+        try {
+            init_common(e, device, hop, sources, ears, M);
+            e->bank = true;
+            e->n_bank = n_bank;
+            const long rows = n_bank * ears;
+            e->pool = dalloc<float2>((size_t)rows * M * e->N);
+            const float* src = stage_ir(e, bank_ir, (size_t)rows * ir_length, e->stream);
+            CK(tvb::launch_partition((int)hop, (int)M, rows, src, ir_length, ir_length, e->pool, 0, e->tw, e->pk,
+                                     e->stream));
+            ++e->launches;
+            CK(cudaStreamSynchronize(e->stream));
+        } catch (...) {
+            delete e;
+            e = nullptr;
+            throw;
+        }
+    });
+    *out = e;
+    return rc;
+}
+
+int tvolap_destroy(tvolap_engine* e) {
+    delete e;
+    return TVOLAP_OK;
+}
+
+int tvolap_process(tvolap_engine* e, const float* in, long in_lane_stride, long rows, long cols, float* out,
+                   long out_lane_stride) {
+    if (int rc = check_hops_args(e, in, out, 1)) return rc;
+    if (rows != e->L || cols != e->S) {
+        // the reference latches a staged filter before its shape checks (engine.cpp:61-67)
+        if (int rc = guarded([&] {
+                CK(cudaSetDevice(e->device));
+                latch(e);
+            }))
+            return rc;
+        if (rows != e->L)
+            return set_err(TVOLAP_ERR_INVALID_SIZE, "process() expects exactly one hop of input per call");
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "input channel count does not match the filter");
+    }
+    return guarded([&] { process_hops_impl(e, in, in_lane_stride, out, out_lane_stride, 1, nullptr); });
+}
+
+int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
+                        long n_hops, const int32_t* schedule) {
+    if (int rc = check_hops_args(e, in, out, n_hops)) return rc;
+    if (schedule && !e->bank)
+        return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "a bank schedule needs a bank engine");
+    if (in_lane_stride < n_hops * e->L || out_lane_stride < n_hops * e->L)
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "lane stride shorter than n_hops * L");
+    if (schedule && classify(schedule) != Mem::Device) {
+        for (long i = 0; i < n_hops * e->S; ++i)
+            if (schedule[i] < 0 || schedule[i] >= e->n_bank)
+                return set_err(TVOLAP_ERR_INVALID_INPUT, "bank index out of range in schedule");
+    }
+    return guarded([&] { process_hops_impl(e, in, in_lane_stride, out, out_lane_stride, n_hops, schedule); });
+}
+
+int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, long channels) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (e->bank) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "exchange_filter on a bank engine; use select_bank");
+    if (!ir || ir_length < 1 || channels < 1)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "partition: impulse response is empty");
+    if (channels != e->S) return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter channel count differs");
+    const long need = (ir_length + 2 * e->L - 1) / (2 * e->L);
+    if (need > e->M)
+        return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter partition count differs");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        std::lock_guard<std::mutex> lock(e->mu);
+        const int target = e->active ^ 1;
+        const float* src = stage_ir(e, ir, (size_t)channels * ir_length, e->side);
+        // the target slot may still be read by hops queued before the last latch
+        CK(cudaStreamWaitEvent(e->side, e->ev_slot[target], 0));
+        CK(tvb::launch_partition((int)e->L, (int)e->M, channels, src, ir_length, ir_length, e->pool,
+                                 (long)target * e->S, e->tw, e->pk, e->side));
+        ++e->launches;
+        CK(cudaEventRecord(e->ev_side, e->side));
+        e->pending = true;  // last staged filter wins (engine.cpp:47)
+    });
+}
+
+int tvolap_select_bank(tvolap_engine* e, const int32_t* idx) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (!e->bank) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "select_bank on a filter-set engine");
+    if (!idx) return set_err(TVOLAP_ERR_INVALID_INPUT, "null selection");
+    for (long s = 0; s < e->S; ++s)
+        if (idx[s] < 0 || idx[s] >= e->n_bank) return set_err(TVOLAP_ERR_INVALID_INPUT, "bank index out of range");
+    std::lock_guard<std::mutex> lock(e->mu);
+    e->staged.assign(idx, idx + e->S);
+    e->sel_staged = true;
+    return TVOLAP_OK;
+}
+
+int tvolap_reset(tvolap_engine* e) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        CK(cudaMemsetAsync(e->ring, 0, (size_t)e->S * 2 * e->M * e->N * sizeof(float2), e->stream));
+        CK(cudaMemsetAsync(e->hist, 0, (size_t)e->S * e->L * sizeof(float), e->stream));
+        CK(cudaMemsetAsync(e->ola, 0, (size_t)e->S * e->E * 3 * e->L * sizeof(float), e->stream));
+        e->hops = 0;  // staged filters / selections stay staged (test_engine.cpp:218-232)
+    });
+}
+
+long tvolap_hop(const tvolap_engine* e) { return e ? e->L : 0; }
+long tvolap_channels(const tvolap_engine* e) { return e ? e->S : 0; }
+long tvolap_output_channels(const tvolap_engine* e) { return e ? e->S * e->E : 0; }
+long tvolap_partition_count(const tvolap_engine* e) { return e ? e->M : 0; }
+long tvolap_delay_line_depth(const tvolap_engine* e) { return e ? 2 * e->M - 1 : 0; }
+long tvolap_latency(const tvolap_engine* e) { return e ? 2 * e->L : 0; }
+long tvolap_switching_latency(const tvolap_engine* e) { return e ? e->L : 0; }
+long tvolap_stream_delay(const tvolap_engine* e) { return e ? e->L : 0; }
+long tvolap_hops_processed(const tvolap_engine* e) { return e ? e->hops : 0; }
+
+int tvolap_op_counts(const tvolap_engine* e, uint64_t* forward, uint64_t* inverse, uint64_t* macs) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (forward) *forward = e->fwd;
+    if (inverse) *inverse = e->inv;
+    if (macs) *macs = e->macs;
+    return TVOLAP_OK;
+}
+
+int tvolap_set_stream(tvolap_engine* e, void* stream) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        cudaStream_t next = stream ? static_cast<cudaStream_t>(stream) : e->own;
+        if (next == e->stream) return;
+        CK(cudaEventRecord(e->ev_start, e->stream));  // keep order across the switch
+        CK(cudaStreamWaitEvent(next, e->ev_start, 0));
+        e->stream = next;
+    });
+}
+
+int tvolap_set_profiling(tvolap_engine* e, int enable) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    e->profiling = enable != 0;
+    e->prof_used = 0;
+    return TVOLAP_OK;
+}
+
+int tvolap_kernel_time(tvolap_engine* e, double* total_ms, long* launches) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        double sum = 0.0;
+        for (size_t i = 0; i < e->prof_used; ++i) {
+            CK(cudaEventSynchronize(e->prof_events[i].second));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e->prof_events[i].first, e->prof_events[i].second));
+            sum += ms;
+        }
+        if (total_ms) *total_ms = sum;
+        if (launches) *launches = (long)e->prof_used;
+        e->prof_used = 0;
+    });
+}
+
+int tvolap_set_host_async(tvolap_engine* e, int enable) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    e->host_async = enable != 0;
+    return TVOLAP_OK;
+}
+
+int tvolap_synchronize(tvolap_engine* e) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaStreamSynchronize(e->side));
+        CK(cudaGetLastError());
+    });
+}
+
+int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* threads_per_cta) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (ctas_per_source) *ctas_per_source = e->P;
+    if (threads_per_cta) *threads_per_cta = e->NT;
+    return TVOLAP_OK;
+}
+
+int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_per_cta) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        const int P = ctas_per_source > 0 ? ctas_per_source : e->P;
+        const int NT = threads_per_cta > 0 ? threads_per_cta : e->NT;
+        validate_launch(e, P, NT);
+        e->P = P;
+        e->NT = NT;
+    });
+}
+
+uint64_t tvolap_kernel_launches(const tvolap_engine* e) { return e ? e->launches : 0; }
+
+// ------------------------------------------------------------------ spectral primitives
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) { CK(cudaMalloc(&p, std::max<size_t>(bytes, 1))); }
+    ~DevBuf() { cudaFree(p); }
+};
+
+// Device view of a host-or-device input buffer.
+const void* dev_in(const void* src, size_t bytes, std::vector<DevBuf*>& keep) {
+    if (classify(src) == Mem::Device) return src;
+    auto* b = new DevBuf(bytes);
+    keep.push_back(b);
+    CK(cudaMemcpy(b->p, src, bytes, cudaMemcpyHostToDevice));
+    return b->p;
+}
+
+struct Keep {
+    std::vector<DevBuf*> v;
+    ~Keep() {
+        for (auto* b : v) delete b;
+    }
+};
+
+void copy_out(void* dst, const void* dev, size_t bytes) {
+    CK(cudaMemcpy(dst, dev, bytes, classify(dst) == Mem::Device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+}
+
+}  // namespace
+
+int tvolap_forward_real(int device, long n, long batch, const float* x, float* bins) {
+    if (n < 8 || !is_pow2(n))
+        return set_err(TVOLAP_ERR_INVALID_SIZE,
+                       "forward_real: block length must be a power of two >= 8, got " + std::to_string(n));
+    if (batch < 1 || !x || !bins) return set_err(TVOLAP_ERR_INVALID_INPUT, "empty batch");
+    return guarded([&] {
+        require_device(device);
+        Keep k;
+        Tables t(n / 2);
+        const float2* tw = (const float2*)dev_in(t.tw.data(), sizeof(float2) * t.tw.size(), k.v);
+        const float2* pk = (const float2*)dev_in(t.pk.data(), sizeof(float2) * t.pk.size(), k.v);
+        const float* dx = (const float*)dev_in(x, sizeof(float) * n * batch, k.v);
+        DevBuf out(sizeof(float2) * (n / 2 + 1) * batch);
+        CK(tvb::launch_forward_real(n, batch, dx, (float2*)out.p, tw, pk, nullptr));
+        copy_out(bins, out.p, sizeof(float2) * (n / 2 + 1) * batch);
+    });
+}
+
+int tvolap_inverse_real(int device, long n, long batch, const float* bins, float* x) {
+    if (n < 8 || !is_pow2(n))
+        return set_err(TVOLAP_ERR_INVALID_SIZE,
+                       "inverse_real: transform length must be a power of two >= 8, got " + std::to_string(n));
+    if (batch < 1 || !x || !bins) return set_err(TVOLAP_ERR_INVALID_INPUT, "empty batch");
+    const long nb = n / 2 + 1;
+    return guarded([&] {
+        require_device(device);
+        std::vector<float> hb;
+        const float* hv = bins;
+        if (classify(bins) == Mem::Device) {
+            hb.resize(2 * nb * batch);
+            CK(cudaMemcpy(hb.data(), bins, sizeof(float) * hb.size(), cudaMemcpyDeviceToHost));
+            hv = hb.data();
+        }
+        for (long b = 0; b < batch; ++b)
+            if (hv[2 * (b * nb) + 1] != 0.f || hv[2 * (b * nb + nb - 1) + 1] != 0.f)
+                throw ApiError{TVOLAP_ERR_INVALID_SPECTRUM,
+                               "inverse_real: DC and Nyquist bins must have zero imaginary part"};
+        Keep k;
+        Tables t(n / 2);
+        const float2* tw = (const float2*)dev_in(t.tw.data(), sizeof(float2) * t.tw.size(), k.v);
+        const float2* pk = (const float2*)dev_in(t.pk.data(), sizeof(float2) * t.pk.size(), k.v);
+        const float2* db = (const float2*)dev_in(bins, sizeof(float2) * nb * batch, k.v);
+        DevBuf out(sizeof(float) * n * batch);
+        CK(tvb::launch_inverse_real(n, batch, db, (float*)out.p, tw, pk, nullptr));
+        copy_out(x, out.p, sizeof(float) * n * batch);
+    });
+}
+
+int tvolap_mac(int device, long nbins, long batch, const float* acc, const float* a, const float* b, float* out) {
+    if (nbins < 1 || batch < 1 || !acc || !a || !b || !out)
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "mac: bin counts differ");
+    return guarded([&] {
+        require_device(device);
+        Keep k;
+        const size_t bytes = sizeof(float2) * nbins * batch;
+        const float2* da = (const float2*)dev_in(acc, bytes, k.v);
+        const float2* dx = (const float2*)dev_in(a, bytes, k.v);
+        const float2* dy = (const float2*)dev_in(b, bytes, k.v);
+        DevBuf o(bytes);
+        CK(tvb::launch_mac(nbins, batch, da, dx, dy, (float2*)o.p, nullptr));
+        copy_out(out, o.p, bytes);
+    });
+}
+
+int tvolap_hann_window(long hop, float* w) {
+    if (hop < 2)
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "hann_window: hop size must be >= 2, got " + std::to_string(hop));
+    std::vector<float> v = hann(hop);
+    std::memcpy(w, v.data(), sizeof(float) * v.size());
+    return TVOLAP_OK;
+}
+
+int tvolap_partition(int device, long hop, long channels, long ir_length, const float* ir, long min_partitions,
+                     float* spectra, long* partitions) {
+    if (ir_length < 1 || channels < 1 || !ir)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "partition: impulse response is empty");
+    if (hop < 2 || !is_pow2(4 * hop))
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "partition: 4L must be a power of two, got L = " + std::to_string(hop));
+    return guarded([&] {
+        require_device(device);
+        const long N = 2 * hop, slice = 2 * hop;
+        const long M = std::max((ir_length + slice - 1) / slice, std::max<long>(min_partitions, 1));
+        if (partitions) *partitions = M;
+        if (!spectra) return;
+        Keep k;
+        Tables t(N);
+        const float2* tw = (const float2*)dev_in(t.tw.data(), sizeof(float2) * t.tw.size(), k.v);
+        const float2* pk = (const float2*)dev_in(t.pk.data(), sizeof(float2) * t.pk.size(), k.v);
+        const float* dir = (const float*)dev_in(ir, sizeof(float) * channels * ir_length, k.v);
+        DevBuf pool(sizeof(float2) * channels * M * N);
+        CK(tvb::launch_partition((int)hop, (int)M, channels, dir, ir_length, ir_length, (float2*)pool.p, 0, tw, pk,
+                                 nullptr));
+        std::vector<float2> packed((size_t)channels * M * N);
+        CK(cudaMemcpy(packed.data(), pool.p, sizeof(float2) * packed.size(), cudaMemcpyDeviceToHost));
+        std::vector<float> full((size_t)channels * M * (N + 1) * 2);
+        for (long f = 0; f < channels * M; ++f) {
+            const float2* src = packed.data() + f * N;
+            float* dst = full.data() + f * (N + 1) * 2;
+            dst[0] = src[0].x;
+            dst[1] = 0.f;
+            for (long q = 1; q < N; ++q) {
+                dst[2 * q] = src[q].x;
+                dst[2 * q + 1] = src[q].y;
+            }
+            dst[2 * N] = src[0].y;
+            dst[2 * N + 1] = 0.f;
+        }
+        if (classify(spectra) == Mem::Device)
+            CK(cudaMemcpy(spectra, full.data(), sizeof(float) * full.size(), cudaMemcpyHostToDevice));
+        else
+            std::memcpy(spectra, full.data(), sizeof(float) * full.size());
+    });
+}
+
+int tvolap_gen_white_device(int device, uint64_t seed, long lane0, long lanes, long t0, long n, float* out,
+                            long stride) {
+    return guarded([&] {
+        require_device(device);
+        if (classify(out) != Mem::Device) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "output must be device memory"};
+        CK(tvb::launch_gen_white(seed, lane0, lanes, t0, n, out, stride, nullptr));
+        CK(cudaDeviceSynchronize());
+    });
+}
+
+int tvolap_gen_irs_device(int device, uint64_t seed, long count, const long* lanes, const long* ears,
+                          const long* ks, const double* t60, double fs, long len, float* out) {
+    return guarded([&] {
+        require_device(device);
+        if (classify(out) != Mem::Device) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "output must be device memory"};
+        Keep k;
+        const long* dl = (const long*)dev_in(lanes, sizeof(long) * count, k.v);
+        const long* de = (const long*)dev_in(ears, sizeof(long) * count, k.v);
+        const long* dk = (const long*)dev_in(ks, sizeof(long) * count, k.v);
+        const double* dt = (const double*)dev_in(t60, sizeof(double) * count, k.v);
+        CK(tvb::launch_gen_irs(seed, count, dl, de, dk, dt, fs, len, out, nullptr));
+        CK(cudaDeviceSynchronize());
+    });
+}
+
+int tvolap_mix_device(int device, long sources, long ears, long samples, const float* out, long out_stride,
+                      float* mix, long mix_stride, void* stream) {
+    return guarded([&] {
+        CK(cudaSetDevice(device));
+        CK(tvb::launch_mix(sources, ears, samples, out, out_stride, mix, mix_stride, (cudaStream_t)stream));
+    });
+}
+
+}  // extern "C"

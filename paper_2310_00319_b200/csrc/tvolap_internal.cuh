@@ -1,0 +1,57 @@
+// Internal declarations shared by the kernel and host translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tvb {
+
+// Parameters of one launch of the fused per-hop kernel (K1+K2+K3+K5).
+struct HopParams {
+    int L;            // hop
+    int M;            // partitions
+    int S;            // sources (input lanes)
+    int P;            // CTAs per source (= cluster size)
+    long hop0;        // global index of the first hop of this launch
+    int n_hops;       // hops processed by this launch
+    const float* in;  // in[s * in_stride + k * L + t]
+    long in_stride;
+    float* out;       // out[(s * E + e) * out_stride + k * L + t]
+    long out_stride;
+    float2* ring;          // frequency-domain delay line [S][2][M][2L] (packed bins)
+    const float2* pool;    // filter spectra [entries][E][M][2L] (packed bins)
+    const int* sched;      // bank entry per (hop, source) or per source; null -> entry_base + s
+    long sched_stride;     // 0: same row for every hop
+    int entry_base;
+    float* hist;           // previous hop [S][L]
+    float* ola;            // overlap-add accumulators [S][E][3L]
+    const float2* tw;      // e^{-2 pi i t / 2L}, t < 2L
+    const float2* pk;      // e^{-2 pi i k / 4L}, k <= 2L
+    const float* win;      // periodic Hann, 2L
+};
+
+size_t hop_kernel_smem_bytes(int L, int P, int E, int threads);
+cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
+
+// K4: partition `rows` time-domain IRs (ir[row * ir_stride + n], n < ir_len) into
+// M packed spectra each: pool[(row0 + row) * M + m][2L].
+cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
+                             long row0, const float2* tw, const float2* pk, cudaStream_t stream);
+
+// Spectral primitives (tests of the reference's spectral.cpp contract).
+cudaError_t launch_forward_real(long n, long batch, const float* x, float2* bins, const float2* tw,
+                                const float2* pk, cudaStream_t stream);
+cudaError_t launch_inverse_real(long n, long batch, const float2* bins, float* x, const float2* tw,
+                                const float2* pk, cudaStream_t stream);
+cudaError_t launch_mac(long nbins, long batch, const float2* acc, const float2* a, const float2* b, float2* out,
+                       cudaStream_t stream);
+
+// Workload generators (device twins of workload_host.cpp).
+cudaError_t launch_gen_white(uint64_t seed, long lane0, long lanes, long t0, long n, float* out, long stride,
+                             cudaStream_t stream);
+cudaError_t launch_gen_irs(uint64_t seed, long count, const long* lanes, const long* ears, const long* ks,
+                           const double* t60, double fs, long len, float* out, cudaStream_t stream);
+cudaError_t launch_mix(long sources, long ears, long samples, const float* out, long out_stride, float* mix,
+                       long mix_stride, cudaStream_t stream);
+
+}  // namespace tvb

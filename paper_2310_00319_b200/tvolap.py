@@ -1,0 +1,483 @@
+"""Python mirror of the reference's TVOLAP operator interface, over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API so the
+parity tests read like the reference's own tests:
+
+  hann_window(hop)                          proj/src/partition.cpp:10-18
+  forward_real / inverse_real / mac         proj/src/spectral.cpp:99-172
+  partition(ir, hop, min_partitions)        proj/src/partition.cpp:20-51
+  TvolapEngine(set)                         proj/include/tvolap/engine.hpp:33-94
+  TvolapProcessor(ir, hop), make_processor  proj/include/tvolap/reference.hpp:202-226
+
+Every call goes through libtvolap_b200.so (include/tvolap_b200.h); there is no
+CPU fallback — importing works anywhere, but an engine needs a B200. Exceptions
+mirror proj/include/tvolap/errors.hpp. Sample arrays follow the reference's
+Eigen layout: `process` takes and returns (L rows x C cols) arrays; multi-hop
+calls take (lanes, samples) arrays or torch tensors (device tensors stay on the
+device, the call is then asynchronous on the engine stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libtvolap_b200.so"
+
+
+# ---------------------------------------------------------------- errors (errors.hpp)
+class InvalidSizeError(ValueError):
+    """tvolap::InvalidSizeError (errors.hpp:10)."""
+
+
+class InvalidInputError(ValueError):
+    """tvolap::InvalidInputError (errors.hpp:16)."""
+
+
+class InvalidSpectrumError(ValueError):
+    """tvolap::InvalidSpectrumError (errors.hpp:28)."""
+
+
+class IncompatibleFilterError(ValueError):
+    """tvolap::IncompatibleFilterError (errors.hpp:34)."""
+
+
+class InvalidConfigurationError(ValueError):
+    """tvolap::InvalidConfigurationError (errors.hpp:40)."""
+
+
+class CudaError(RuntimeError):
+    """Device failure (no reference analogue): the engine never falls back to the CPU."""
+
+
+_ERRORS = {
+    1: InvalidSizeError,
+    2: InvalidInputError,
+    3: InvalidConfigurationError,
+    4: IncompatibleFilterError,
+    5: InvalidSpectrumError,
+    6: CudaError,
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libtvolap_b200.so (raises if it was not built — no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise CudaError(f"{_LIB_PATH} is missing; run __graft_entry__.build()")
+        L = C.CDLL(str(_LIB_PATH))
+        vp, lg, ip, fp = C.c_void_p, C.c_long, C.c_int, C.c_void_p
+        sig = {
+            "tvolap_last_error": (C.c_char_p, []),
+            "tvolap_version": (C.c_char_p, []),
+            "tvolap_create": (ip, [C.POINTER(vp), ip, lg, lg, lg, fp, lg]),
+            "tvolap_create_bank": (ip, [C.POINTER(vp), ip, lg, lg, lg, lg, lg, fp, lg]),
+            "tvolap_destroy": (ip, [vp]),
+            "tvolap_process": (ip, [vp, fp, lg, lg, lg, fp, lg]),
+            "tvolap_process_hops": (ip, [vp, fp, lg, fp, lg, lg, fp]),
+            "tvolap_exchange_filter": (ip, [vp, fp, lg, lg]),
+            "tvolap_select_bank": (ip, [vp, fp]),
+            "tvolap_reset": (ip, [vp]),
+            "tvolap_hop": (lg, [vp]),
+            "tvolap_channels": (lg, [vp]),
+            "tvolap_output_channels": (lg, [vp]),
+            "tvolap_partition_count": (lg, [vp]),
+            "tvolap_delay_line_depth": (lg, [vp]),
+            "tvolap_latency": (lg, [vp]),
+            "tvolap_switching_latency": (lg, [vp]),
+            "tvolap_stream_delay": (lg, [vp]),
+            "tvolap_hops_processed": (lg, [vp]),
+            "tvolap_op_counts": (ip, [vp, fp, fp, fp]),
+            "tvolap_set_stream": (ip, [vp, vp]),
+            "tvolap_synchronize": (ip, [vp]),
+            "tvolap_set_host_async": (ip, [vp, ip]),
+            "tvolap_set_profiling": (ip, [vp, ip]),
+            "tvolap_kernel_time": (ip, [vp, fp, fp]),
+            "tvolap_launch_config": (ip, [vp, fp, fp]),
+            "tvolap_set_launch_config": (ip, [vp, ip, ip]),
+            "tvolap_kernel_launches": (C.c_uint64, [vp]),
+            "tvolap_forward_real": (ip, [ip, lg, lg, fp, fp]),
+            "tvolap_inverse_real": (ip, [ip, lg, lg, fp, fp]),
+            "tvolap_mac": (ip, [ip, lg, lg, fp, fp, fp, fp]),
+            "tvolap_hann_window": (ip, [lg, fp]),
+            "tvolap_partition": (ip, [ip, lg, lg, lg, fp, lg, fp, fp]),
+            "tvolap_gen_white_device": (ip, [ip, C.c_uint64, lg, lg, lg, lg, fp, lg]),
+            "tvolap_gen_irs_device": (ip, [ip, C.c_uint64, lg, fp, fp, fp, fp, C.c_double, lg, fp]),
+            "tvolap_mix_device": (ip, [ip, lg, lg, lg, fp, lg, fp, lg, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = (
+    "tvolap_last_error tvolap_version tvolap_create tvolap_create_bank tvolap_destroy tvolap_process "
+    "tvolap_process_hops tvolap_exchange_filter tvolap_select_bank tvolap_reset tvolap_hop tvolap_channels "
+    "tvolap_output_channels tvolap_partition_count tvolap_delay_line_depth tvolap_latency "
+    "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
+    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches "
+    "tvolap_forward_real tvolap_inverse_real tvolap_mac tvolap_hann_window tvolap_partition "
+    "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device"
+).split()
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().tvolap_last_error().decode()
+        raise _ERRORS.get(rc, CudaError)(msg)
+
+
+def _ptr(x):
+    """(pointer, keepalive) for a float32/int32 numpy array or a torch tensor."""
+    if x is None:
+        return None, None
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr()), x
+    return C.c_void_p(x.ctypes.data), x
+
+
+def _f32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+
+
+# ---------------------------------------------------------------- spectral (spectral.hpp)
+def is_power_of_two(n: int) -> bool:
+    """spectral.hpp:31."""
+    return n > 0 and (n & (n - 1)) == 0
+
+
+def hann_window(hop: int) -> np.ndarray:
+    """Periodic Hann of length 2L, peak 2 (partition.cpp:10-18)."""
+    w = np.empty(2 * max(hop, 0), dtype=np.float32)
+    _check(lib().tvolap_hann_window(hop, w.ctypes.data if w.size else None))
+    return w
+
+
+def forward_real(block, device: int = 0) -> np.ndarray:
+    """Unscaled real FFT -> n/2+1 complex bins (spectral.cpp:99-125); batched over leading axes."""
+    x = _f32(block)
+    n = x.shape[-1] if x.ndim else 0
+    batch = int(np.prod(x.shape[:-1])) if x.ndim > 1 else 1
+    out = np.empty(x.shape[:-1] + (n // 2 + 1, 2), dtype=np.float32)
+    _check(lib().tvolap_forward_real(device, n, batch, x.ctypes.data if x.size else None,
+                                     out.ctypes.data if out.size else None))
+    return out[..., 0] + 1j * out[..., 1]
+
+
+def inverse_real(bins, n: Optional[int] = None, device: int = 0) -> np.ndarray:
+    """Inverse of forward_real incl. 1/n (spectral.cpp:127-158)."""
+    b = np.asarray(bins)
+    nb = b.shape[-1]
+    n = 2 * (nb - 1) if n is None else n
+    if nb != n // 2 + 1:
+        raise InvalidSizeError(f"inverse_real: expected {n // 2 + 1} bins, got {nb}")
+    inter = _f32(np.stack([b.real, b.imag], axis=-1))
+    batch = int(np.prod(b.shape[:-1])) if b.ndim > 1 else 1
+    out = np.empty(b.shape[:-1] + (n,), dtype=np.float32)
+    _check(lib().tvolap_inverse_real(device, n, batch, inter.ctypes.data, out.ctypes.data))
+    return out
+
+
+def mac(acc, a, b, device: int = 0) -> np.ndarray:
+    """acc + a*b per bin (spectral.cpp:160-172)."""
+    acc, a, b = (np.asarray(v) for v in (acc, a, b))
+    if not (acc.shape == a.shape == b.shape):
+        raise InvalidSizeError("mac: bin counts differ")
+    st = [_f32(np.stack([v.real, v.imag], axis=-1)) for v in (acc, a, b)]
+    out = np.empty_like(st[0])
+    nb = acc.shape[-1]
+    batch = acc.size // nb
+    _check(lib().tvolap_mac(device, nb, batch, st[0].ctypes.data, st[1].ctypes.data, st[2].ctypes.data,
+                            out.ctypes.data))
+    return out[..., 0] + 1j * out[..., 1]
+
+
+# ---------------------------------------------------------------- partition (partition.hpp)
+@dataclass
+class FilterPartitionSet:
+    """partition.hpp:21-32. Holds the time-domain taps; the spectra live on the device."""
+
+    hop: int
+    partition_count: int
+    channels: int
+    source_length: int
+    taps: np.ndarray = field(repr=False)  # (channels, source_length) fp32
+    normalization_gain: float = 0.5
+    sample_rate: float = 48000.0
+
+    def transform_length(self) -> int:
+        return 4 * self.hop
+
+    def padded_length(self) -> int:
+        return 2 * self.hop * self.partition_count
+
+    def spectra(self, device: int = 0) -> np.ndarray:
+        """(channels, M, 2L+1) complex partition spectra computed on the device."""
+        nb = 2 * self.hop + 1
+        out = np.empty((self.channels, self.partition_count, nb, 2), dtype=np.float32)
+        m = C.c_long()
+        _check(lib().tvolap_partition(device, self.hop, self.channels, self.source_length, self.taps.ctypes.data,
+                                      self.partition_count, out.ctypes.data, C.byref(m)))
+        return out[..., 0] + 1j * out[..., 1]
+
+
+def partition(ir, hop: int, min_partitions: int = 1, sample_rate: float = 48000.0) -> FilterPartitionSet:
+    """partition(ir, hop, min_partitions) (partition.cpp:20-51). `ir`: (taps,) or (taps, channels) like Eigen."""
+    h = np.asarray(ir, dtype=np.float64)
+    if h.ndim == 1:
+        h = h[:, None]
+    if h.size == 0 or h.shape[0] < 1 or h.shape[1] < 1:
+        raise InvalidInputError("partition: impulse response is empty")
+    if hop < 2 or not is_power_of_two(4 * hop):
+        raise InvalidSizeError(f"partition: 4L must be a power of two, got L = {hop}")
+    slice_ = 2 * hop
+    m = max(-(-h.shape[0] // slice_), max(min_partitions, 1))
+    taps = np.ascontiguousarray(h.T, dtype=np.float32)
+    return FilterPartitionSet(hop, m, h.shape[1], h.shape[0], taps, sample_rate=sample_rate)
+
+
+# ---------------------------------------------------------------- engine (engine.hpp)
+class TvolapEngine:
+    """B200 TvolapEngine (engine.hpp:33-94) behind tvolap_create / tvolap_process."""
+
+    def __init__(self, filter: FilterPartitionSet, device: int = 0):
+        if filter is None:
+            raise InvalidConfigurationError("engine requires a filter partition set")
+        h = C.c_void_p()
+        _check(lib().tvolap_create(C.byref(h), device, filter.hop, filter.channels, filter.source_length,
+                                   filter.taps.ctypes.data, filter.partition_count))
+        self._h = h
+        self._filter = filter
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.tvolap_destroy(h)
+            self._h = None
+
+    # getters (engine.hpp:38-50)
+    def hop(self) -> int:
+        return lib().tvolap_hop(self._h)
+
+    def channels(self) -> int:
+        return lib().tvolap_channels(self._h)
+
+    def partition_count(self) -> int:
+        return lib().tvolap_partition_count(self._h)
+
+    def delay_line_depth(self) -> int:
+        return lib().tvolap_delay_line_depth(self._h)
+
+    def latency(self) -> int:
+        return lib().tvolap_latency(self._h)
+
+    def switching_latency(self) -> int:
+        return lib().tvolap_switching_latency(self._h)
+
+    def stream_delay(self) -> int:
+        return lib().tvolap_stream_delay(self._h)
+
+    def filter(self) -> FilterPartitionSet:
+        return self._filter
+
+    def exchange_filter(self, next: Optional[FilterPartitionSet]) -> None:
+        """engine.cpp:37-48: validate, stage; latched at the next process()."""
+        if next is None:
+            raise IncompatibleFilterError("replacement filter is null")
+        if next.hop != self.hop():
+            raise IncompatibleFilterError("replacement filter hop differs")
+        if next.partition_count != self.partition_count():
+            raise IncompatibleFilterError("replacement filter partition count differs")
+        if next.channels != self.channels():
+            raise IncompatibleFilterError("replacement filter channel count differs")
+        _check(lib().tvolap_exchange_filter(self._h, next.taps.ctypes.data, next.source_length, next.channels))
+        self._filter = next
+
+    def exchange_ir(self, ir) -> None:
+        """Stage a replacement IR given as (channels, taps) — numpy or a device tensor (no host copy)."""
+        if ir.shape[0] != self.channels():
+            raise IncompatibleFilterError("replacement filter channel count differs")
+        if -(-ir.shape[1] // (2 * self.hop())) > self.partition_count():
+            raise IncompatibleFilterError("replacement filter partition count differs")
+        if not hasattr(ir, "data_ptr"):
+            ir = _f32(ir)
+        p, _k = _ptr(ir)
+        _check(lib().tvolap_exchange_filter(self._h, p, ir.shape[1], ir.shape[0]))
+
+    def process(self, input) -> np.ndarray:
+        """One hop: (L, C) in -> (L, C) out (engine.cpp:60-106)."""
+        x = np.asarray(input, dtype=np.float32)
+        if x.ndim == 1:
+            x = x[:, None]
+        rows, cols = x.shape
+        xf = np.ascontiguousarray(x.T)  # lane-major, like Eigen's column-major storage
+        out = np.empty((self.channels_out(), max(rows, 1)), dtype=np.float32)
+        _check(lib().tvolap_process(self._h, xf.ctypes.data, max(rows, 1), rows, cols, out.ctypes.data,
+                                    max(rows, 1)))
+        return out.T.copy()
+
+    def channels_out(self) -> int:
+        return lib().tvolap_output_channels(self._h)
+
+    def process_hops(self, x, out=None, schedule=None):
+        """n hops at once. x: (lanes, n*L) numpy array or torch tensor (host or device)."""
+        L = self.hop()
+        lanes, total = x.shape[0], x.shape[-1]
+        if total % L:
+            raise InvalidSizeError("process_hops: sample count is not a whole number of hops")
+        n = total // L
+        if out is None:
+            if hasattr(x, "data_ptr"):
+                import torch
+
+                out = torch.empty((self.channels_out(), total), dtype=torch.float32, device=x.device)
+            else:
+                out = np.empty((self.channels_out(), total), dtype=np.float32)
+        if not hasattr(x, "data_ptr"):
+            x = _f32(x)
+        xp, _k1 = _ptr(x)
+        op, _k2 = _ptr(out)
+        sp, _k3 = _ptr(None if schedule is None else
+                       (schedule if hasattr(schedule, "data_ptr") else np.ascontiguousarray(schedule, np.int32)))
+        _check(lib().tvolap_process_hops(self._h, xp, _stride(x), op, _stride(out), n, sp))
+        return out
+
+    def reset(self) -> None:
+        _check(lib().tvolap_reset(self._h))
+
+    def op_counts(self):
+        """EngineOpCounts (engine.hpp:17-21): (forward_transforms, inverse_transforms, spectral_macs)."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().tvolap_op_counts(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return OpCounts(a.value, b.value, c.value)
+
+    def hops_processed(self) -> int:
+        return lib().tvolap_hops_processed(self._h)
+
+    def set_stream(self, stream_handle: int) -> None:
+        _check(lib().tvolap_set_stream(self._h, C.c_void_p(stream_handle)))
+
+    def set_profiling(self, enable: bool = True) -> None:
+        _check(lib().tvolap_set_profiling(self._h, int(enable)))
+
+    def kernel_time(self):
+        """(total device ms, launches) of the fused hop kernel since profiling was enabled."""
+        ms, n = C.c_double(), C.c_long()
+        _check(lib().tvolap_kernel_time(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def set_host_async(self, enable: bool = True) -> None:
+        _check(lib().tvolap_set_host_async(self._h, int(enable)))
+
+    def synchronize(self) -> None:
+        _check(lib().tvolap_synchronize(self._h))
+
+    def launch_config(self):
+        p, t = C.c_int(), C.c_int()
+        _check(lib().tvolap_launch_config(self._h, C.byref(p), C.byref(t)))
+        return p.value, t.value
+
+    def set_launch_config(self, ctas_per_source: int = 0, threads: int = 0) -> None:
+        _check(lib().tvolap_set_launch_config(self._h, ctas_per_source, threads))
+
+    def kernel_launches(self) -> int:
+        return lib().tvolap_kernel_launches(self._h)
+
+
+@dataclass
+class OpCounts:
+    forward_transforms: int
+    inverse_transforms: int
+    spectral_macs: int
+
+
+def _stride(a) -> int:
+    if hasattr(a, "stride") and callable(a.stride):
+        return a.stride(0)
+    return a.strides[0] // a.itemsize
+
+
+class TvolapBankEngine(TvolapEngine):
+    """Bank engine (configs C1/C3/C5): sources x ears lanes over a pre-partitioned IR bank.
+
+    bank_ir: (n_bank, ears, taps). Selection per source via select_bank() (staged,
+    latched next hop) or a per-hop schedule in process_hops().
+    """
+
+    def __init__(self, bank_ir, hop: int, sources: int, min_partitions: int = 1, device: int = 0):
+        b = _f32(bank_ir)
+        if b.ndim == 2:
+            b = b[:, None, :]
+        n_bank, ears, taps = b.shape
+        h = C.c_void_p()
+        _check(lib().tvolap_create_bank(C.byref(h), device, hop, sources, ears, n_bank, taps, b.ctypes.data,
+                                        min_partitions))
+        self._h = h
+        self._filter = None
+        self.device = device
+        self.n_bank = n_bank
+        self.ears = ears
+
+    def select_bank(self, idx) -> None:
+        i = np.ascontiguousarray(idx, dtype=np.int32)
+        _check(lib().tvolap_select_bank(self._h, i.ctypes.data))
+
+    def exchange_filter(self, next):  # bank engines switch by selection
+        raise InvalidConfigurationError("exchange_filter on a bank engine; use select_bank")
+
+
+# ---------------------------------------------------------------- processor facade (reference.hpp)
+class TvolapProcessor:
+    """TvolapProcessor(ir, hop) facade (reference.cpp:328-342)."""
+
+    def __init__(self, ir, hop: int, device: int = 0):
+        self._engine = TvolapEngine(partition(ir, hop), device=device)
+
+    def name(self) -> str:
+        return "tvolap"
+
+    def hop(self) -> int:
+        return self._engine.hop()
+
+    def channels(self) -> int:
+        return self._engine.channels()
+
+    def latency(self) -> int:
+        return self._engine.latency()
+
+    def stream_delay(self) -> int:
+        return self._engine.stream_delay()
+
+    def switching_latency(self) -> int:
+        return self._engine.switching_latency()
+
+    def process(self, input) -> np.ndarray:
+        return self._engine.process(input)
+
+    def set_filter(self, ir) -> None:
+        """exchange_filter(partition(ir, L, M)) (reference.cpp:335-338)."""
+        e = self._engine
+        self._engine.exchange_filter(partition(ir, e.hop(), e.partition_count()))
+
+    def reset(self) -> None:
+        self._engine.reset()
+
+    def engine(self) -> TvolapEngine:
+        return self._engine
+
+
+def make_processor(name: str, ir, hop: int, device: int = 0) -> TvolapProcessor:
+    """make_processor (reference.cpp:346-365) — this tier implements the "tvolap" path."""
+    if name == "tvolap":
+        return TvolapProcessor(ir, hop, device=device)
+    raise InvalidConfigurationError(f"unknown algorithm: {name}")

@@ -1,0 +1,87 @@
+// Drop-in check of include/tvolap_b200.hpp: the reference's own engine tests
+// (proj/tests/test_engine.cpp:71-77 identity, :159-188 half-cosine crossfade,
+// :203-216 error classes) written against the C++ wrapper exactly as the
+// reference writes them against tvolap::TvolapEngine. Exit 0 = pass,
+// 77 = no GPU (the wrapper threw CudaError: there is no CPU fallback).
+#include <cmath>
+#include <cstdio>
+#include <memory>
+
+#include "tvolap_b200.hpp"
+
+using namespace tvolap_b200;
+
+static ImpulseResponse delta_ir(double gain, Index len) {
+    ImpulseResponse ir;
+    ir.samples = Frames(len, 1);
+    ir.samples(0, 0) = gain;
+    return ir;
+}
+
+static int fails = 0;
+#define CHECK(c)                                                   \
+    do {                                                           \
+        if (!(c)) {                                                \
+            std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c); \
+            ++fails;                                               \
+        }                                                          \
+    } while (0)
+
+int main() {
+    try {
+        // identity passthrough, L = 16
+        TvolapEngine id(partition(delta_ir(1.0, 1), 16));
+        Frames x(16, 1);
+        double worst = 0.0;
+        for (int h = 0; h < 10; ++h) {
+            for (Index i = 0; i < 16; ++i) x(i, 0) = std::sin(0.37 * (h * 16 + i));
+            Frames y = id.process(x);
+            if (h > 0)
+                for (Index i = 0; i < 16; ++i) worst = std::fmax(worst, std::fabs(y(i, 0) - std::sin(0.37 * (h * 16 + i - 16))));
+        }
+        CHECK(worst < 1e-5);
+
+        // polarity flip crosses over along the half-cosine
+        const Index hop = 256;
+        TvolapEngine eng(partition(delta_ir(1.0, 2048), hop));
+        CHECK(eng.partition_count() == 4 && eng.delay_line_depth() == 7 && eng.latency() == 512);
+        Frames ones(hop, 1, 1.0);
+        std::vector<double> stream;
+        for (int i = 0; i < 24; ++i) {
+            if (i == 12) eng.exchange_filter(partition(delta_ir(-1.0, 2048), hop));
+            Frames y = eng.process(ones);
+            for (Index u = 0; u < hop; ++u) stream.push_back(y(u, 0));
+        }
+        const Index boundary = 11 * hop + hop;  // + stream_delay
+        const double pi = 3.14159265358979323846;
+        double cerr = 0.0;
+        for (Index u = 0; u < hop; ++u) cerr = std::fmax(cerr, std::fabs(stream[boundary + u] - std::cos(pi * u / hop)));
+        CHECK(cerr < 1e-5);
+        CHECK(std::fabs(stream.back() + 1.0) < 1e-5);
+        EngineOpCounts c = eng.op_counts();
+        CHECK(c.forward_transforms == 24 && c.inverse_transforms == 24 && c.spectral_macs == 96);
+
+        // error classes
+        bool threw = false;
+        try { eng.process(Frames(hop - 1, 1)); } catch (const InvalidSizeError&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { eng.process(Frames(hop, 2)); } catch (const InvalidInputError&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { eng.exchange_filter(partition(delta_ir(1.0, 4096), hop)); } catch (const IncompatibleFilterError&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { TvolapEngine bad(std::shared_ptr<const FilterPartitionSet>{}); } catch (const InvalidConfigurationError&) { threw = true; }
+        CHECK(threw);
+
+        TvolapProcessor proc(delta_ir(0.5, 300), 64);
+        Frames y = proc.process(Frames(64, 1, 1.0));
+        CHECK(proc.name() == "tvolap" && y.rows() == 64);
+    } catch (const CudaError& e) {
+        std::printf("NO_GPU %s\n", e.what());
+        return 77;
+    }
+    std::printf(fails ? "FAILED %d\n" : "PASS\n", fails);
+    return fails ? 1 : 0;
+}

@@ -1,0 +1,138 @@
+"""GPU parity on the BASELINE.json configs: same seeded inputs/IRs into the CUDA
+engine (C-ABI) and the fp64 oracle; max|y_gpu - y_ref| <= 1e-4 max|y_ref|
+(north_star tolerance), across IR switches. Oracle legs run on lane subsets /
+hop prefixes sized to finish in seconds (each still spans >= 2(2M-1) hops where
+the ring must wrap); the GPU always runs the config's full lane count unless
+noted."""
+import numpy as np
+import pytest
+
+from paper_2310_00319_b200 import drive
+from paper_2310_00319_b200 import workload as W
+from parity import TOL, oracle_config, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def check(cfg, n_hops, sources=None, subset=None):
+    _, y = drive.run_host(cfg, n_hops, sources=sources)
+    subset = list(range(sources or cfg.sources)) if subset is None else subset
+    ref = oracle_config(cfg, n_hops, sources=sources, subset=subset)
+    rows = [s * cfg.ears + e for s in subset for e in range(cfg.ears)]
+    err = rel_err(y[rows], ref)
+    assert err <= TOL, f"{cfg.name}: rel err {err:.3g}"
+    return y, ref
+
+
+def test_c1_full_ten_seconds():
+    """C1: 1 lane, L=128, M=32, two IRs alternating every 64 blocks, all 3750 hops."""
+    cfg = W.CONFIGS["C1"]
+    check(cfg, cfg.hops)
+
+
+def test_c2_all_lanes_fresh_switches():
+    """C2: 64 lanes, L=256, M=64, fresh IR every 16 blocks; 160 hops (10 switches, ring wrapped)."""
+    cfg = W.CONFIGS["C2"]
+    check(cfg, 160)
+
+
+def test_c3_binaural_bank():
+    """C3: 1024 sources x 2 ears on the GPU; per-block bank choice; 16 sources checked over 520 hops."""
+    cfg = W.CONFIGS["C3"]
+    subset = list(range(0, 1024, 64))
+    y, ref = check(cfg, 520, subset=subset)
+
+
+def test_c4_long_reverb():
+    """C4: L=512, M=256, fresh IR every 8 blocks; 8 lanes over 1100 hops (ring wrapped)."""
+    cfg = W.CONFIGS["C4"]
+    check(cfg, 1100, sources=8)
+
+
+def test_c4_full_lane_count_prefix():
+    """C4 with all 256 lanes: 24 hops (3 switches), 8 strided lanes against the oracle."""
+    cfg = W.CONFIGS["C4"]
+    check(cfg, 24, subset=list(range(0, 256, 32)))
+
+
+def test_c5_low_latency_bank():
+    """C5: 4096 lanes, L=32, M=512, per-block choice from 1024 IRs; 1100 hops, 8 lanes checked."""
+    cfg = W.CONFIGS["C5"]
+    check(cfg, 1100, subset=list(range(0, 4096, 512)))
+
+
+def test_c3_mix_kernel_deterministic():
+    """C3 stereo mix: device reduction over sources == fp64 sum of per-source outputs."""
+    import torch
+
+    from paper_2310_00319_b200 import tvolap as T
+
+    cfg = W.CONFIGS["C3"]
+    n_hops = 40
+    eng = drive.make_engine(cfg)
+    L = cfg.hop
+    x = torch.from_numpy(W.white(cfg, 0, cfg.sources, 0, n_hops * L)).cuda()
+    out = torch.empty((cfg.lanes, n_hops * L), device="cuda")
+    sched = torch.from_numpy(W.schedule(cfg, 0, n_hops)).cuda()
+    eng.process_hops(x, out=out, schedule=sched)
+    eng.synchronize()
+    mix = torch.empty((cfg.ears, n_hops * L), device="cuda")
+    import ctypes
+
+    rc = T.lib().tvolap_mix_device(0, cfg.sources, cfg.ears, n_hops * L, ctypes.c_void_p(out.data_ptr()),
+                                   n_hops * L, ctypes.c_void_p(mix.data_ptr()), n_hops * L, None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    ref = out.double().view(cfg.sources, cfg.ears, -1).sum(0)
+    assert (mix.double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item()
+    mix2 = torch.empty_like(mix)
+    T.lib().tvolap_mix_device(0, cfg.sources, cfg.ears, n_hops * L, ctypes.c_void_p(out.data_ptr()), n_hops * L,
+                              ctypes.c_void_p(mix2.data_ptr()), n_hops * L, None)
+    torch.cuda.synchronize()
+    assert torch.equal(mix, mix2)
+
+
+def test_device_buffers_match_host_path():
+    """Device-resident (torch) process_hops == host pipeline, bit for bit (C2 prefix)."""
+    import torch
+
+    cfg = W.CONFIGS["C2"]
+    n = 48
+    _, y_host = drive.run_host(cfg, n)
+    eng = drive.make_engine(cfg)
+    x = torch.from_numpy(W.white(cfg, 0, cfg.sources, 0, n * cfg.hop)).cuda()
+    out = torch.empty_like(x)
+    for h0 in range(0, n, cfg.period):
+        k = h0 // cfg.period
+        if k:
+            ir = torch.from_numpy(np.ascontiguousarray(W.fresh_irs(cfg, k)[:, 0, :])).cuda()
+            eng.exchange_ir(ir)
+        sl = slice(h0 * cfg.hop, (h0 + cfg.period) * cfg.hop)
+        eng.process_hops(x[:, sl], out=out[:, sl])
+    eng.synchronize()
+    assert np.array_equal(out.cpu().numpy(), y_host)
+
+
+def test_device_generators_match_host():
+    """Device twins of the workload generators reproduce the host values (fp32, <= 1 ulp for IRs)."""
+    import ctypes
+
+    import torch
+
+    from paper_2310_00319_b200 import tvolap as T
+
+    cfg = W.CONFIGS["C2"]
+    d = torch.empty((3, 1000), device="cuda")
+    assert T.lib().tvolap_gen_white_device(0, cfg.seed, 5, 3, 77, 1000, ctypes.c_void_p(d.data_ptr()), 1000) == 0
+    assert np.array_equal(d.cpu().numpy(), W.white(cfg, 5, 3, 77, 1000))
+    items = [(3, 0, 2), (60, 0, 7)]
+    host = W.ir_items(cfg, items)
+    lanes = np.array([i[0] for i in items], np.int64)
+    ears = np.array([i[1] for i in items], np.int64)
+    ks = np.array([i[2] for i in items], np.int64)
+    t60 = np.array([W.t60_of(cfg, l, k) for l, _, k in items])
+    dev = torch.empty((2, cfg.ir_length), device="cuda")
+    assert T.lib().tvolap_gen_irs_device(0, cfg.seed, 2, lanes.ctypes.data, ears.ctypes.data, ks.ctypes.data,
+                                         t60.ctypes.data, W.FS, cfg.ir_length, ctypes.c_void_p(dev.data_ptr())) == 0
+    torch.cuda.synchronize()
+    assert np.abs(dev.cpu().numpy() - host).max() <= np.abs(host).max() * 2 ** -22

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle and the
+reference's known answers. Mirrors proj/tests/test_spectral.cpp,
+test_partition.cpp and test_engine.cpp at fp32 tolerances."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2310_00319_b200 import tvolap as T
+
+pytestmark = pytest.mark.gpu
+
+
+def rnd(n, seed, cols=None):
+    g = np.random.default_rng(seed)
+    return g.uniform(-1, 1, n if cols is None else (n, cols))
+
+
+def delta_ir(gain, length):
+    h = np.zeros(length)
+    h[0] = gain
+    return h
+
+
+def stream_through(eng, x, n_out):
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    hop = eng.hop()
+    total = n_out + eng.stream_delay()
+    calls = -(-total // hop)
+    padded = np.zeros((calls * hop, x.shape[1]))
+    padded[: x.shape[0]] = x
+    out = np.concatenate([eng.process(padded[i * hop:(i + 1) * hop]) for i in range(calls)])
+    return out[eng.stream_delay(): eng.stream_delay() + n_out].astype(np.float64)
+
+
+# ------------------------------------------------------------ spectral
+def test_forward_real_vs_oracle_and_dft():  # test_spectral.cpp:32-62
+    x = np.zeros(8)
+    x[0] = 1
+    s = T.forward_real(x)
+    assert np.allclose(s, 1.0, atol=1e-6)
+    assert abs(T.forward_real(np.ones(8))[0] - 8.0) < 1e-6
+    for n in (8, 16, 64, 256, 1024, 2048, 4096):
+        x = rnd(n, 100 + n).astype(np.float32)
+        got = T.forward_real(x)
+        ref = O.forward_real(x.astype(np.float64))
+        assert np.abs(got - ref).max() < 2e-6 * np.sqrt(n) * max(1.0, np.log2(n) / 4)
+        assert got[0].imag == 0 and got[-1].imag == 0
+
+
+def test_roundtrip_and_batch():  # test_spectral.cpp:64-71
+    for n in (8, 64, 512, 4096):
+        x = rnd(3 * n, 200 + n).reshape(3, n).astype(np.float32)
+        back = T.inverse_real(T.forward_real(x), n)
+        assert np.abs(back - x).max() < 5e-6
+
+
+def test_circular_conv_and_mac():  # test_spectral.cpp:96-141
+    for n in (8, 16, 32):
+        x, h = rnd(n, 300 + n), rnd(n, 400 + n)
+        prod = T.mac(np.zeros(n // 2 + 1, complex), T.forward_real(x), T.forward_real(h))
+        ref = O.inverse_real(O.mac(np.zeros(n // 2 + 1, complex), O.forward_real(x), O.forward_real(h)))
+        assert np.abs(T.inverse_real(prod, n) - ref).max() < 1e-5
+    g = np.random.default_rng(5)
+    f = lambda: (g.uniform(-1, 1, 33) + 1j * g.uniform(-1, 1, 33)).astype(np.complex64)  # noqa: E731
+    acc, a, b = f(), f(), f()
+    assert np.abs(T.mac(acc, a, b) - (acc + a * b)).max() < 1e-6
+
+
+def test_spectral_validation():  # test_spectral.cpp:143-161
+    for n in (4, 12):
+        with pytest.raises(T.InvalidSizeError):
+            T.forward_real(np.zeros(n))
+    bad = np.zeros(9, complex)
+    bad[0] = 1e-3j
+    with pytest.raises(T.InvalidSpectrumError):
+        T.inverse_real(bad, 16)
+    bad = np.zeros(9, complex)
+    bad[8] = 1e-3j
+    with pytest.raises(T.InvalidSpectrumError):
+        T.inverse_real(bad, 16)
+    with pytest.raises(T.InvalidSizeError):
+        T.inverse_real(np.zeros(4, complex), 16)
+
+
+def test_window():  # test_partition.cpp:25-47
+    w = T.hann_window(256)
+    assert w[0] == 0 and w[256] == 2.0
+    assert np.abs(w.astype(np.float64) - O.hann_window(256)).max() < 1e-7
+    with pytest.raises(T.InvalidSizeError):
+        T.hann_window(1)
+
+
+# ------------------------------------------------------------ partition
+@pytest.mark.parametrize("hop,n_ir,minp", [(256, 2048, 1), (128, 700, 1), (256, 512, 4), (16, 1, 1), (512, 32768, 1)])
+def test_partition_vs_oracle(hop, n_ir, minp):  # partition.cpp:20-51; test_partition.cpp:49-122
+    ir = rnd(n_ir, n_ir + hop).astype(np.float32)
+    g = T.partition(ir, hop, minp)
+    o = O.partition(ir.astype(np.float64), hop, minp)
+    assert g.partition_count == o.partition_count
+    gs, os_ = g.spectra(), o.spectra()
+    assert np.abs(gs - os_).max() < 3e-6 * np.sqrt(2 * hop)
+    if minp > 1:
+        assert np.abs(gs[0, 1:]).max() == 0.0
+
+
+def test_partition_validation():  # test_partition.cpp:124-130
+    with pytest.raises(T.InvalidInputError):
+        T.partition(np.zeros((0, 1)), 256)
+    for hop in (0, 24, 1):
+        with pytest.raises(T.InvalidSizeError):
+            T.partition(rnd(64, 15), hop)
+
+
+# ------------------------------------------------------------ engine
+def test_engine_geometry():  # test_engine.cpp:42-58
+    one = T.TvolapEngine(T.partition(delta_ir(1, 1), 256))
+    assert (one.partition_count(), one.latency(), one.switching_latency(), one.delay_line_depth()) == (1, 512, 256, 1)
+    four = T.TvolapEngine(T.partition(delta_ir(1, 2048), 256))
+    assert (four.partition_count(), four.delay_line_depth(), four.hop(), four.channels()) == (4, 7, 256, 1)
+    big = T.TvolapEngine(T.partition(delta_ir(1, 32768), 512))
+    assert big.partition_count() == 32 and big.switching_latency() == 512 and big.stream_delay() == 512
+
+
+def test_zero_stays_zero_after_reset():  # test_engine.cpp:60-69
+    eng = T.TvolapEngine(T.partition(delta_ir(1, 1024), 128))
+    z = np.zeros((128, 1))
+    for _ in range(5):
+        assert np.abs(eng.process(z)).max() == 0.0
+    eng.process(rnd(128, 1, 1))
+    eng.reset()
+    for _ in range(5):
+        assert np.abs(eng.process(z)).max() == 0.0
+
+
+def test_identity_passthrough():  # test_engine.cpp:71-77
+    eng = T.TvolapEngine(T.partition(delta_ir(1, 1), 16))
+    x = rnd(128, 2, 1)
+    assert np.abs(stream_through(eng, x, 128) - x).max() < 1e-6
+
+
+@pytest.mark.parametrize("n_ir", [256, 512, 1024])
+def test_fixed_filter_matches_oracle_and_linear_conv(n_ir):  # test_engine.cpp:79-89
+    h, x = rnd(n_ir, 10 + n_ir), rnd(4 * n_ir, 20 + n_ir)
+    y = stream_through(T.TvolapEngine(T.partition(h, 128)), x, x.size + n_ir - 1)[:, 0]
+    ref = np.convolve(x.astype(np.float32).astype(np.float64), h.astype(np.float32).astype(np.float64))
+    assert np.abs(y - ref).max() <= 1e-4 * np.abs(ref).max()
+    yo = O.stream_through(O.Engine(O.partition(h.astype(np.float32), 128)), x.astype(np.float32), y.size)[:, 0]
+    assert np.abs(y - yo).max() <= 1e-4 * np.abs(yo).max()
+
+
+def test_channels_independent():  # test_engine.cpp:91-102
+    ir, x = rnd(256, 30, 2), rnd(1024, 31, 2)
+    eng = T.TvolapEngine(T.partition(ir, 64))
+    assert eng.channels() == 2
+    y = stream_through(eng, x, 1024 + 255)
+    for c in range(2):
+        ref = np.convolve(x[:, c], ir[:, c])
+        assert np.abs(y[:, c] - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+def test_engine_linear():  # test_engine.cpp:104-116
+    s = T.partition(rnd(512, 40), 64)
+    x1, x2 = rnd(512, 41), rnd(512, 42)
+    a, b = 0.8, -2.5
+    y1 = stream_through(T.TvolapEngine(s), x1, 900)
+    y2 = stream_through(T.TvolapEngine(s), x2, 900)
+    ym = stream_through(T.TvolapEngine(s), a * x1 + b * x2, 900)
+    assert np.abs(ym - (a * y1 + b * y2)).max() < 1e-4 * np.abs(ym).max()
+
+
+def test_constant_op_counts_through_exchange():  # test_engine.cpp:118-139
+    a, b = T.partition(rnd(1024, 50), 128), T.partition(rnd(1024, 51), 128)
+    eng = T.TvolapEngine(a)
+    m = eng.partition_count()
+    for i in range(12):
+        if i == 6:
+            eng.exchange_filter(b)
+        eng.process(np.ones((128, 1)))
+        c = eng.op_counts()
+        assert (c.forward_transforms, c.inverse_transforms, c.spectral_macs) == (i + 1, i + 1, (i + 1) * m)
+
+
+def test_exchange_identical_is_bit_identical():  # test_engine.cpp:141-157
+    s = T.partition(rnd(512, 60), 64)
+    x = rnd(1024, 61)
+    plain, exch = T.TvolapEngine(s), T.TvolapEngine(s)
+    for i in range(16):
+        chunk = x[i * 64:(i + 1) * 64, None]
+        y1 = plain.process(chunk)
+        if i == 7:
+            exch.exchange_filter(s)
+        assert np.array_equal(y1, exch.process(chunk))
+
+
+def test_polarity_flip_half_cosine():  # test_engine.cpp:159-188 (analytic known answer)
+    hop, calls, switch_call = 256, 24, 12
+    eng = T.TvolapEngine(T.partition(delta_ir(1, 2048), hop))
+    stream = []
+    for i in range(calls):
+        if i == switch_call:
+            eng.exchange_filter(T.partition(delta_ir(-1, 2048), hop))
+        stream.append(eng.process(np.ones((hop, 1))))
+    out = np.concatenate(stream)[hop:, 0].astype(np.float64)
+    boundary = (switch_call - 1) * hop
+    w = O.hann_window(hop)
+    assert np.abs(out[2 * hop:boundary] - 1.0).max() < 1e-5
+    assert np.abs(out[boundary:boundary + hop] - (0.5 * w[hop:] - 0.5 * w[:hop])).max() < 1e-5
+    assert np.abs(out[boundary + hop:] + 1.0).max() < 1e-5
+    assert abs(out[boundary + hop - 1] + 1.0) > 1e-5
+
+
+def test_shorter_ir_via_min_partitions():  # test_engine.cpp:190-201
+    long_ir, short_ir = rnd(512, 70), rnd(100, 71)
+    eng = T.TvolapEngine(T.partition(long_ir, 64))
+    assert eng.partition_count() == 4
+    eng.exchange_filter(T.partition(short_ir, 64, eng.partition_count()))
+    x = rnd(2048, 72)
+    y = stream_through(eng, x, x.size + 99)[:, 0]
+    ref = np.convolve(x, short_ir)
+    assert np.abs(y - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+def test_framing_and_compatibility_enforced():  # test_engine.cpp:203-216
+    eng = T.TvolapEngine(T.partition(delta_ir(1, 512), 128))
+    with pytest.raises(T.InvalidSizeError):
+        eng.process(np.zeros((127, 1)))
+    with pytest.raises(T.InvalidInputError):
+        eng.process(np.zeros((128, 2)))
+    for bad in (T.partition(delta_ir(1, 512), 64), T.partition(delta_ir(1, 2048), 128),
+                T.partition(np.zeros((512, 2)) + np.eye(512, 2), 128)):
+        with pytest.raises(T.IncompatibleFilterError):
+            eng.exchange_filter(bad)
+    with pytest.raises(T.InvalidConfigurationError):
+        T.TvolapEngine(None)
+
+
+def test_reset_keeps_staged_filter():  # test_engine.cpp:218-232
+    eng = T.TvolapEngine(T.partition(delta_ir(1, 256), 64))
+    eng.process(rnd(64, 80, 1))
+    eng.exchange_filter(T.partition(delta_ir(-1, 256), 64))
+    eng.reset()
+    for _ in range(8):
+        last = eng.process(np.ones((64, 1)))
+    assert abs(last[63, 0] + 1.0) < 1e-5
+
+
+def test_processor_facade():  # test_reference.cpp:254-266 (facade == raw engine)
+    ir, x = rnd(1000, 3), rnd(64 * 20, 4)
+    proc = T.make_processor("tvolap", ir, 64)
+    eng = T.TvolapEngine(T.partition(ir, 64))
+    for i in range(20):
+        c = x[i * 64:(i + 1) * 64, None]
+        assert np.array_equal(proc.process(c), eng.process(c))
+    with pytest.raises(T.InvalidConfigurationError):
+        T.make_processor("nope", ir, 64)
+    proc.set_filter(rnd(900, 5))  # shorter IR: padded to M partitions
+    with pytest.raises(T.IncompatibleFilterError):
+        proc.set_filter(rnd(4096, 6))
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_cluster_sizes_agree(P):
+    """Every cluster size (CTAs per lane, DSMEM gather) produces the oracle's output."""
+    L, n_ir, S = 64, 1000, 3
+    ir = rnd(n_ir, 12, S)
+    x = rnd(L * 40, 13, S)
+    eng = T.TvolapEngine(T.partition(ir, L))
+    eng.set_launch_config(P, 128)
+    y = stream_through(eng, x, x.shape[0])
+    ref = O.stream_through(O.Engine(O.partition(ir.astype(np.float32), L)), x.astype(np.float32), x.shape[0])
+    assert np.abs(y - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("hop", [2, 4, 8, 32, 1024])
+def test_extreme_hops(hop):
+    """Smallest/largest hops (4L = 8 .. 4096) against the oracle."""
+    ir, x = rnd(3 * hop + 1, hop), rnd(12 * hop, hop + 1)
+    y = stream_through(T.TvolapEngine(T.partition(ir, hop)), x, x.size)[:, 0]
+    ref = O.stream_through(O.Engine(O.partition(ir.astype(np.float32), hop)), x.astype(np.float32), x.size)[:, 0]
+    assert np.abs(y - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+def test_process_hops_equals_process():
+    """Multi-hop call == the same hops one process() at a time (bit-exact)."""
+    ir, x = rnd(3000, 21, 4), rnd(128 * 30, 22, 4)
+    s = T.partition(ir, 128)
+    a, b = T.TvolapEngine(s), T.TvolapEngine(s)
+    one = np.concatenate([a.process(x[i * 128:(i + 1) * 128]) for i in range(30)])  # (T, C)
+    many = b.process_hops(np.ascontiguousarray(x.T))  # (C, T)
+    assert np.array_equal(one.T, many)
+    assert b.hops_processed() == 30
