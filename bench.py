@@ -48,18 +48,23 @@ def peaks():
 
 
 def config_block(cfg, n_hops, world):
+    if cfg.mode == "fresh":
+        sw = f"fresh seeded IR per channel every {cfg.period} blocks, T60~U[{cfg.t60[0]},{cfg.t60[1]}] s"
+    else:
+        sw = (f"bank of {cfg.n_bank} x {cfg.ears}-ear decaying-noise IRs (T60 {cfg.t60[0]} s), "
+              + ("alternating every %d blocks" % cfg.period if cfg.n_bank == 2 else "seeded random choice per block"))
     return {
-        "workload": f"{cfg.name}: {cfg.sources} independent channels per GPU, fp32, L={cfg.hop} (4L={4 * cfg.hop} FFT), "
-                    f"M={cfg.partitions} (IR {cfg.ir_length} taps), fresh seeded IR per channel every "
-                    f"{cfg.period} blocks, T60~U[{cfg.t60[0]},{cfg.t60[1]}] s, {cfg.seconds:g} s white noise",
-        "channels_per_gpu": cfg.sources,
+        "workload": f"{cfg.name}: {cfg.sources} source(s) x {cfg.ears} ear(s) per GPU, fp32, L={cfg.hop} "
+                    f"(4L={4 * cfg.hop} FFT), M={cfg.partitions} (IR {cfg.ir_length} taps), {sw}, "
+                    f"{cfg.seconds:g} s white noise" + (", summed into a stereo mix" if cfg.mix else ""),
+        "channels_per_gpu": cfg.lanes,
         "hop": cfg.hop,
         "partitions": cfg.partitions,
         "hops_per_step": n_hops,
-        "switch_period_blocks": cfg.period,
-        "l2": "inputs larger than L2: 368.6 MB input + 368.6 MB output streamed per step per GPU "
-              "(delay line + filter pool, 67 MB, stay L2-resident by design)",
-        "parallelism": f"lanes sharded, {world} GPU(s), no collective",
+        "l2": f"inputs larger than L2: {cfg.sources * n_hops * cfg.hop * 4 / 1e6:.1f} MB input + "
+              f"{cfg.lanes * n_hops * cfg.hop * 4 / 1e6:.1f} MB output streamed per step per GPU",
+        "parallelism": f"lanes sharded, {world} GPU(s), "
+                       + ("NCCL all-reduce of the stereo mix" if cfg.mix and world > 1 else "no collective"),
     }
 
 
@@ -159,6 +164,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-hops", type=int, default=512)
+    ap.add_argument("--latency-hops", type=int, default=0,
+                    help="also time this many single-hop process() calls (pinned host I/O): p50/p99 per-hop latency")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -174,7 +181,7 @@ def main():
 
     from paper_2310_00319_b200 import _build
     from paper_2310_00319_b200 import tvolap as T
-    from paper_2310_00319_b200.tvolap import TvolapEngine, partition
+    from paper_2310_00319_b200.tvolap import TvolapBankEngine, TvolapEngine, partition
 
     _build.build()
     torch.cuda.set_device(local)
@@ -193,32 +200,57 @@ def main():
     t0 = time.time()
     x = torch.empty((S, H * L), dtype=torch.float32, device=dev)
     T._check(lib.tvolap_gen_white_device(local, cfg.seed, lane0, S, 0, H * L, ctypes.c_void_p(x.data_ptr()), H * L))
-    irs = torch.empty((n_sw, S, cfg.ir_length), dtype=torch.float32, device=dev)
-    lanes_a = np.array([lane0 + s for k in range(n_sw) for s in range(S)], np.int64)
-    ears_a = np.zeros(n_sw * S, np.int64)
-    ks_a = np.array([k for k in range(n_sw) for s in range(S)], np.int64)
-    t60_a = np.array([W.t60_of(cfg, int(l), int(k)) for l, k in zip(lanes_a, ks_a)], np.float64)
-    T._check(lib.tvolap_gen_irs_device(local, cfg.seed, n_sw * S, lanes_a.ctypes.data, ears_a.ctypes.data,
-                                       ks_a.ctypes.data, t60_a.ctypes.data, W.FS, cfg.ir_length,
-                                       ctypes.c_void_p(irs.data_ptr())))
-    out = torch.empty_like(x)
-    torch.cuda.synchronize()
-    log(f"[rank {rank}] generated {x.numel() * 4 / 1e6:.0f} MB input + {irs.numel() * 4 / 1e9:.2f} GB IRs "
-        f"in {time.time() - t0:.1f} s")
+    out = torch.empty((cfg.lanes, H * L), dtype=torch.float32, device=dev)
 
-    ir0 = W.fresh_irs(cfg, 0, lane0, S)[:, 0, :]
-    eng = TvolapEngine(partition(ir0.T, L, M), device=local)
+    def gen_irs(items, dst):
+        la = np.array([i[0] for i in items], np.int64)
+        ea = np.array([i[1] for i in items], np.int64)
+        ka = np.array([i[2] for i in items], np.int64)
+        ta = np.array([W.t60_of(cfg, int(l), int(k)) for l, _, k in items], np.float64)
+        T._check(lib.tvolap_gen_irs_device(local, cfg.seed, len(items), la.ctypes.data, ea.ctypes.data,
+                                           ka.ctypes.data, ta.ctypes.data, W.FS, cfg.ir_length,
+                                           ctypes.c_void_p(dst.data_ptr())))
+
+    sched = mix = irs = None
+    if cfg.mode == "fresh":
+        irs = torch.empty((n_sw, S, cfg.ir_length), dtype=torch.float32, device=dev)
+        gen_irs([(lane0 + s, 0, k) for k in range(n_sw) for s in range(S)], irs)
+        ir0 = W.fresh_irs(cfg, 0, lane0, S)[:, 0, :]
+        eng = TvolapEngine(partition(ir0.T, L, M), device=local)
+        distinct = S
+    else:
+        bank = torch.empty((cfg.n_bank, cfg.ears, cfg.ir_length), dtype=torch.float32, device=dev)
+        gen_irs([(b, e, 0) for b in range(cfg.n_bank) for e in range(cfg.ears)], bank)
+        sched_h = W.schedule(cfg, 0, H, lane0, S)
+        sched = torch.from_numpy(sched_h).to(dev)
+        distinct = float(np.mean([np.unique(r).size for r in sched_h[: min(H, 512)]]))
+        eng = TvolapBankEngine(bank, L, S, min_partitions=M, device=local)
+        if cfg.mix:
+            mix = torch.empty((cfg.ears, H * L), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] {cfg.name}: generated {x.numel() * 4 / 1e6:.0f} MB input"
+        f"{'' if irs is None else f' + {irs.numel() * 4 / 1e9:.2f} GB IRs'} in {time.time() - t0:.1f} s")
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream.cuda_stream)
     P, NT = eng.launch_config()
     log(f"[rank {rank}] launch config: {P} CTAs/channel (cluster), {NT} threads/CTA")
 
-    def step(e, xs, outs, ir_set):
+    def step(e, xs, outs, ir_set, sch):
         e.reset()
-        for k in range(n_sw):
-            e.exchange_ir(ir_set[k])
-            sl = slice(k * cfg.period * L, min(H, (k + 1) * cfg.period) * L)
-            e.process_hops(xs[:, sl], out=outs[:, sl])
+        if cfg.mode == "fresh":
+            for k in range(n_sw):
+                e.exchange_ir(ir_set[k])
+                sl = slice(k * cfg.period * L, min(H, (k + 1) * cfg.period) * L)
+                e.process_hops(xs[:, sl], out=outs[:, sl])
+        else:
+            e.process_hops(xs, out=outs, schedule=sch)
+            if mix is not None and outs.is_cuda:
+                T._check(lib.tvolap_mix_device(local, S, cfg.ears, H * L, ctypes.c_void_p(outs.data_ptr()), H * L,
+                                               ctypes.c_void_p(mix.data_ptr()), H * L,
+                                               ctypes.c_void_p(stream.cuda_stream)))
+                if world > 1:
+                    with torch.cuda.stream(stream):
+                        torch.distributed.all_reduce(mix)
 
     def barrier():
         torch.cuda.synchronize()
@@ -227,7 +259,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step(eng, x, out, irs)
+        step(eng, x, out, irs, sched)
     barrier()
     launches0 = eng.kernel_launches()
     clocks = Clocks(local)
@@ -235,34 +267,35 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        step(eng, x, out, irs)
+        step(eng, x, out, irs, sched)
     ev1.record(stream)
     barrier()
     clk = clocks.stop()
     elapsed = ev0.elapsed_time(ev1)
     kern_ms, kern_n = eng.kernel_time()
     eng.set_profiling(False)
-    gpu_launches = eng.kernel_launches() - launches0
+    gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
     t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     elapsed = float(t.item())
     ms_per_step = elapsed / args.steps
-    samples_per_step = world * S * H * L
+    samples_per_step = world * cfg.lanes * H * L
     value = samples_per_step / (ms_per_step / 1e3)
 
-    # ---- roofline of the dominant kernel (fused hop kernel), algorithmic bytes per launch
+    # ---- roofline of the dominant kernel (fused hop kernel), algorithmic bytes per launch (SURVEY.md §8d)
     pk = peaks()
     hbm = pk.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     if not hbm:
         hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    hops_per_launch = H * args.steps / kern_n if kern_n else cfg.period
-    bytes_launch = W.bytes_per_hop(cfg) * hops_per_launch
+    hops_per_launch = H * args.steps / kern_n if kern_n else H
+    bytes_hop = W.bytes_per_hop(cfg, distinct_filters=distinct)
+    bytes_launch = bytes_hop * hops_per_launch
     avg_launch_ms = kern_ms / kern_n if kern_n else float("nan")
     achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
     traffic = None
-    summ = ROOT / "profiles" / "ncu_summary.json"
+    summ = ROOT / "profiles" / f"ncu_summary_{cfg.name}.json"
     if summ.exists():
         try:
             traffic = json.loads(summ.read_text()).get("dram_bytes_per_launch")
@@ -270,26 +303,37 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": "tvolap_hop_kernel (K1+K2+K3+K5 fused, per launch = 16 hops x 64 channels)",
-                "avg_launch_ms": avg_launch_ms, "launches": kern_n,
-                "bytes_per_launch": bytes_launch, "kernel_share_of_step": kern_ms / elapsed if elapsed else None,
-                "note": "delay line + filter pool (67 MB) are L2-resident in C2, so frac vs HBM can exceed 1"}
+                "kernel": f"tvolap_hop_kernel (K1+K2+K3+K5 fused), {hops_per_launch:g} hops x {S} sources per launch",
+                "avg_launch_ms": avg_launch_ms, "launches": kern_n, "bytes_per_hop": bytes_hop,
+                "bytes_per_launch": bytes_launch, "distinct_filters_per_hop": distinct,
+                "kernel_share_of_step": kern_ms / elapsed if elapsed else None}
+    if cfg.name in ("C1", "C2"):
+        roofline["note"] = "delay line + filter pool are L2-resident in this config, so frac vs HBM can exceed 1"
 
-    # ---- e2e through the public API with pinned host buffers (H2D inputs + IRs, D2H outputs)
+    # ---- e2e through the public API with pinned host buffers (H2D inputs [+ IRs], D2H outputs)
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
-        irh = torch.empty(irs.shape, dtype=torch.float32, pin_memory=True)
-        irh.copy_(irs)
-        oh = torch.empty(xh.shape, dtype=torch.float32, pin_memory=True)
-        eng2 = TvolapEngine(partition(ir0.T, L, M), device=local)
+        oh = torch.empty(tuple(out.shape), dtype=torch.float32, pin_memory=True)
+        h2d = xh.numel() * 4
+        if cfg.mode == "fresh":
+            irh = torch.empty(irs.shape, dtype=torch.float32, pin_memory=True)
+            irh.copy_(irs)
+            eng2 = TvolapEngine(partition(ir0.T, L, M), device=local)
+            h2d += irh.numel() * 4
+            schh = None
+        else:
+            irh = None
+            schh = sched.cpu().pin_memory()
+            h2d += schh.numel() * 4
+            eng2 = TvolapBankEngine(bank, L, S, min_partitions=M, device=local)
         eng2.set_host_async(True)
-        step(eng2, xh, oh, irh)
+        step(eng2, xh, oh, irh, schh)
         eng2.synchronize()
         barrier()
         tw = time.perf_counter()
         for _ in range(args.steps):
-            step(eng2, xh, oh, irh)
+            step(eng2, xh, oh, irh, schh)
             eng2.synchronize()
         barrier()
         e2e_s = (time.perf_counter() - tw) / args.steps
@@ -298,24 +342,54 @@ def main():
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
         same = bool(torch.equal(oh, out.cpu()))
-        e2e = {"value": samples_per_step / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": int(xh.numel() * 4 + irh.numel() * 4),
+        e2e = {"value": samples_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_s * 1e3,
                "timing": "host wall clock around each full pass incl. final synchronize",
                "matches_device_path": same}
         del irh
+
+    latency = None
+    if args.latency_hops:
+        lat_eng = (TvolapBankEngine(bank, L, S, min_partitions=M, device=local) if cfg.mode == "bank"
+                   else TvolapEngine(partition(ir0.T, L, M), device=local))
+        lat_eng.set_stream(stream.cuda_stream)
+        xin = torch.empty((S, L), dtype=torch.float32, pin_memory=True)
+        yout = torch.empty((cfg.lanes, L), dtype=torch.float32, pin_memory=True)
+        xsrc = x[:, : (args.latency_hops + 8) * L].cpu()
+        sch_np = sched.cpu().numpy() if sched is not None else None
+        gpu_ms, host_ms = [], []
+        for h in range(args.latency_hops + 8):
+            xin.copy_(xsrc[:, h * L:(h + 1) * L])
+            if sch_np is not None:
+                lat_eng.select_bank(sch_np[h])
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0h = time.perf_counter()
+            a.record(stream)
+            T._check(lib.tvolap_process(lat_eng._h, ctypes.c_void_p(xin.data_ptr()), L, L, S,
+                                        ctypes.c_void_p(yout.data_ptr()), L))
+            b.record(stream)
+            b.synchronize()
+            if h >= 8:
+                host_ms.append((time.perf_counter() - t0h) * 1e3)
+                gpu_ms.append(a.elapsed_time(b))
+        q = lambda v, p: float(np.percentile(v, p))  # noqa: E731
+        latency = {"hops": args.latency_hops, "gpu_ms_p50": q(gpu_ms, 50), "gpu_ms_p99": q(gpu_ms, 99),
+                   "host_ms_p50": q(host_ms, 50), "host_ms_p99": q(host_ms, 99),
+                   "hop_period_ms": 1e3 * L / W.FS,
+                   "what": "one process() call per hop: pinned H2D of the hop, fused kernel, D2H of the outputs; "
+                           "CUDA events on the engine stream (gpu) and host wall clock (host)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded white noise + decaying-noise IRs generated on device)",
         "config": config_block(cfg, H, world), "clocks": clk, "gpu_launches": int(gpu_launches),
-        "roofline": roofline, "e2e": e2e,
+        "roofline": roofline, "e2e": e2e, "latency": latency,
         "realtime_factor": (H * L / W.FS) / (ms_per_step / 1e3),
     }
 
     # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on host cores, bounded sample
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and cfg.mode == "fresh":
         threads = W.host_threads()
         ch = min(args.cpu_hops, H)
         secs, yref = cpu_sample(cfg, S, ch, threads, want_output=True)

@@ -415,13 +415,13 @@ class TvolapBankEngine(TvolapEngine):
     """
 
     def __init__(self, bank_ir, hop: int, sources: int, min_partitions: int = 1, device: int = 0):
-        b = _f32(bank_ir)
+        b = bank_ir if hasattr(bank_ir, "data_ptr") else _f32(bank_ir)
         if b.ndim == 2:
             b = b[:, None, :]
         n_bank, ears, taps = b.shape
         h = C.c_void_p()
-        _check(lib().tvolap_create_bank(C.byref(h), device, hop, sources, ears, n_bank, taps, b.ctypes.data,
-                                        min_partitions))
+        bp, _keep = _ptr(b)
+        _check(lib().tvolap_create_bank(C.byref(h), device, hop, sources, ears, n_bank, taps, bp, min_partitions))
         self._h = h
         self._filter = None
         self.device = device
