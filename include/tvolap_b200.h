@@ -163,6 +163,16 @@ int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* thre
 /* Override P (1, 2, 4 or 8) and threads per CTA (128..1024); 0 keeps the current value. */
 int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_per_cta);
 
+/*
+ * Hop blocking for multi-hop calls: process_hops calls with at least block_min
+ * hops run the hop-blocked kernel, which processes hops_per_block (2, 4, 8, 16)
+ * consecutive hops together and loads each delay-line / shared filter slice
+ * once per block instead of once per hop. Outputs are the same per-hop sums;
+ * 0 keeps the current value.
+ */
+int tvolap_set_block_config(tvolap_engine* e, int hops_per_block, long block_min);
+int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block_min, int* partition_groups);
+
 /* Number of kernels this engine has launched since creation. */
 uint64_t tvolap_kernel_launches(const tvolap_engine* e);
 

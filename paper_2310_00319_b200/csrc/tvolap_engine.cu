@@ -135,6 +135,8 @@ T* dalloc(size_t count) {
     return static_cast<T*>(p);
 }
 
+constexpr int kMaxJH = 8;  // largest hop block / 2 (ring slack per parity)
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
@@ -170,7 +172,10 @@ struct tvolap_engine {
     size_t prof_used = 0;
     long chunk_seq = 0;     // alternates the double-buffered staging across calls
     bool host_async = false;  // pinned host I/O returns before completion
-    int P = 1, NT = 256;
+    int P = 1, NT = 256;           // streaming (one hop at a time) kernel
+    int JH = 4, QB = 1, NTB = 256;   // hop-blocked kernel: 2*JH hops per block, QB partition groups
+    long D = 0;                      // delay-line slots per parity (M + kMaxJH)
+    long block_min = 4;              // process_hops calls with >= block_min hops use the blocked kernel
     uint64_t fwd = 0, inv = 0, macs = 0, launches = 0;
     long hops = 0;
     std::mutex mu;
@@ -209,6 +214,25 @@ void pick_launch_config(tvolap_engine* e) {
     const int ep = env_int("TVOLAP_P", 0), et = env_int("TVOLAP_NT", 0);
     if (ep > 0) e->P = ep;
     if (et > 0) e->NT = et;
+    e->JH = env_int("TVOLAP_JH", 4);
+    e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
+}
+
+// Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
+void pick_block_geometry(tvolap_engine* e) {
+    const long W = e->N / e->P;
+    e->NTB = 256;
+    e->QB = 1;
+    if (W < e->NTB) {
+        e->QB = (int)(e->NTB / W);
+        while (e->QB > e->M && e->QB > 1) {
+            e->QB /= 2;
+            e->NTB /= 2;
+        }
+    }
+    if (e->NTB < 32) e->NTB = 32, e->QB = (int)std::max<long>(1, 32 / W);
+    while (e->JH > 1 && tvb::block_kernel_smem_bytes((int)e->L, e->P, (int)e->E, e->JH, e->QB, e->NTB) > 227 * 1024)
+        e->JH /= 2;
 }
 
 void validate_launch(const tvolap_engine* e, int P, int NT) {
@@ -230,6 +254,7 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     e->S = sources;
     e->E = ears;
     e->M = partitions;
+    e->D = partitions + kMaxJH;
     CK(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
@@ -246,7 +271,7 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     CK(cudaMemcpy(e->tw, t.tw.data(), sizeof(float2) * e->N, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(e->pk, t.pk.data(), sizeof(float2) * (e->N + 2), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(e->win, w.data(), sizeof(float) * e->N, cudaMemcpyHostToDevice));
-    const size_t ring_elems = (size_t)e->S * 2 * e->M * e->N;
+    const size_t ring_elems = (size_t)e->S * 2 * e->D * e->N;
     e->ring = dalloc<float2>(ring_elems);
     e->hist = dalloc<float>((size_t)e->S * e->L);
     e->ola = dalloc<float>((size_t)e->S * e->E * 3 * e->L);
@@ -259,6 +284,7 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     CK(cudaMemsetAsync(e->d_sel, 0, sizeof(int) * e->S, e->stream));
     pick_launch_config(e);
     validate_launch(e, e->P, e->NT);
+    pick_block_geometry(e);
 }
 
 // Device copy of a host/device IR table; returns a device pointer valid on `s`.
@@ -293,6 +319,7 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     HopParams p;
     p.L = (int)e->L;
     p.M = (int)e->M;
+    p.D = (int)e->D;
     p.S = (int)e->S;
     p.P = e->P;
     p.hop0 = hop0;
@@ -324,7 +351,10 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
         ++e->prof_used;
         CK(cudaEventRecord(t0, e->stream));
     }
-    CK(tvb::launch_hop_kernel(p, (int)e->E, e->NT, e->stream));
+    if (n >= e->block_min)
+        CK(tvb::launch_block_kernel(p, (int)e->E, e->JH, e->QB, e->NTB, e->stream));
+    else
+        CK(tvb::launch_hop_kernel(p, (int)e->E, e->NT, e->stream));
     if (t1) CK(cudaEventRecord(t1, e->stream));
     ++e->launches;
     if (!e->bank) CK(cudaEventRecord(e->ev_slot[e->active], e->stream));
@@ -639,7 +669,7 @@ int tvolap_reset(tvolap_engine* e) {
     if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
     return guarded([&] {
         CK(cudaSetDevice(e->device));
-        CK(cudaMemsetAsync(e->ring, 0, (size_t)e->S * 2 * e->M * e->N * sizeof(float2), e->stream));
+        CK(cudaMemsetAsync(e->ring, 0, (size_t)e->S * 2 * e->D * e->N * sizeof(float2), e->stream));
         CK(cudaMemsetAsync(e->hist, 0, (size_t)e->S * e->L * sizeof(float), e->stream));
         CK(cudaMemsetAsync(e->ola, 0, (size_t)e->S * e->E * 3 * e->L * sizeof(float), e->stream));
         e->hops = 0;  // staged filters / selections stay staged (test_engine.cpp:218-232)
@@ -731,7 +761,31 @@ int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_
         validate_launch(e, P, NT);
         e->P = P;
         e->NT = NT;
+        pick_block_geometry(e);
     });
+}
+
+int tvolap_set_block_config(tvolap_engine* e, int hops_per_block, long block_min) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        if (hops_per_block != 0) {
+            if (hops_per_block != 2 && hops_per_block != 4 && hops_per_block != 8 && hops_per_block != 16)
+                throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hops per block must be 2, 4, 8 or 16"};
+            const int jh = hops_per_block / 2;
+            if (tvb::block_kernel_smem_bytes((int)e->L, e->P, (int)e->E, jh, e->QB, e->NTB) > 227 * 1024)
+                throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hop block does not fit in shared memory"};
+            e->JH = jh;
+        }
+        if (block_min > 0) e->block_min = block_min;
+    });
+}
+
+int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block_min, int* partition_groups) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (hops_per_block) *hops_per_block = 2 * e->JH;
+    if (block_min) *block_min = e->block_min;
+    if (partition_groups) *partition_groups = e->QB;
+    return TVOLAP_OK;
 }
 
 uint64_t tvolap_kernel_launches(const tvolap_engine* e) { return e ? e->launches : 0; }

@@ -10,6 +10,7 @@ namespace tvb {
 struct HopParams {
     int L;            // hop
     int M;            // partitions
+    int D;            // delay-line slots per parity (>= M + hops per block / 2)
     int S;            // sources (input lanes)
     int P;            // CTAs per source (= cluster size)
     long hop0;        // global index of the first hop of this launch
@@ -18,7 +19,7 @@ struct HopParams {
     long in_stride;
     float* out;       // out[(s * E + e) * out_stride + k * L + t]
     long out_stride;
-    float2* ring;          // frequency-domain delay line [S][2][M][2L] (packed bins)
+    float2* ring;          // frequency-domain delay line [S][2][D][2L] (packed bins)
     const float2* pool;    // filter spectra [entries][E][M][2L] (packed bins)
     const int* sched;      // bank entry per (hop, source) or per source; null -> entry_base + s
     long sched_stride;     // 0: same row for every hop
@@ -32,6 +33,10 @@ struct HopParams {
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int threads);
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
+
+// Hop-blocked variant (2*JH hops per block, Q partition groups; threads == Q * (2L/P) when 2L/P < threads).
+size_t block_kernel_smem_bytes(int L, int P, int E, int JH, int Q, int threads);
+cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int threads, cudaStream_t stream);
 
 // K4: partition `rows` time-domain IRs (ir[row * ir_stride + n], n < ir_len) into
 // M packed spectra each: pool[(row0 + row) * M + m][2L].

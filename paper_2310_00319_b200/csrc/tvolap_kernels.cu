@@ -77,7 +77,7 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 template <int E>
 __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int L = p.L, N = 2 * L, M = p.M, P = p.P;
+    const int L = p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
     const int tid = threadIdx.x, NT = blockDim.x;
     const int s = blockIdx.x / P;
     const int r = blockIdx.x % P;  // == cluster rank (1-D clusters of P consecutive CTAs)
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     for (int k = 0; k < p.n_hops; ++k) {
         const long hop = p.hop0 + k;
         const int par = (int)(hop & 1);
-        const int sl = (int)((hop >> 1) % M);
+        const int sl = (int)((hop >> 1) % D);
 
         // ---- K1: frame (previous hop | this hop) x Hann, zero-pad to 4L, FFT.
         const float* inp = p.in + (long)s * p.in_stride + (long)k * L;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
         const float2* Z = fft_stockham<false>(s_fa, s_fb, N, s_tw, true, tid, NT);
 
         // ---- K2: this CTA's slice of X_hop into the delay line.
-        float2* ringw = p.ring + (((long)s * 2 + par) * M + sl) * N + (long)r * Np;
+        float2* ringw = p.ring + (((long)s * 2 + par) * D + sl) * N + (long)r * Np;
         for (int kk = tid; kk < Np; kk += NT) ringw[kk] = untangle_packed(Z, N, r * Np + kk, s_pk);
         float* t = xprev;
         xprev = xcur;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
 
         // ---- K3: Y = sum_m H[m] X_{hop-2m} over the slice.
         const int entry = p.sched ? p.sched[(long)k * p.sched_stride + s] : p.entry_base + s;
-        const float4* xb = ring4 + (((long)s * 2 + par) * M) * spec4 + (long)r * V;
+        const float4* xb = ring4 + (((long)s * 2 + par) * D) * spec4 + (long)r * V;
         const float4* hb = pool4 + ((long)entry * E * M) * spec4 + (long)r * V;
         float2* yb = s_yb + (size_t)(k & 1) * E * Np;
         for (int fi = f0; fi < V; fi += VT) {
@@ -156,14 +156,14 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
                 aux[e] = 0.f;
             }
             int m = g;
-            int slot = ((sl - g) % M + M) % M;
+            int slot = ((sl - g) % D + D) % D;
             for (; m + 3 * G < M; m += 4 * G) {
                 int s1 = slot - G;
-                if (s1 < 0) s1 += M;
+                if (s1 < 0) s1 += D;
                 int s2 = s1 - G;
-                if (s2 < 0) s2 += M;
+                if (s2 < 0) s2 += D;
                 int s3 = s2 - G;
-                if (s3 < 0) s3 += M;
+                if (s3 < 0) s3 += D;
                 const float4 x0 = __ldcg(xb + slot * spec4 + fi);
                 const float4 x1 = __ldcg(xb + s1 * spec4 + fi);
                 const float4 x2 = __ldcg(xb + s2 * spec4 + fi);
@@ -185,14 +185,14 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
                     cmac4(acc[e], aux[e], h[e][3], x3);
                 }
                 slot = s3 - G;
-                if (slot < 0) slot += M;
+                if (slot < 0) slot += D;
             }
             for (; m < M; m += G) {
                 const float4 x0 = __ldcg(xb + slot * spec4 + fi);
 #pragma unroll
                 for (int e = 0; e < E; ++e) cmac4(acc[e], aux[e], __ldg(hb + ((long)e * M + m) * spec4 + fi), x0);
                 slot -= G;
-                if (slot < 0) slot += M;
+                if (slot < 0) slot += D;
             }
             if (r == 0 && fi == 0) {
 #pragma unroll
@@ -254,6 +254,372 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
 
     if (r == 0)
         for (int i = tid; i < L; i += NT) p.hist[(long)s * L + i] = xprev[i];
+    for (int i = tid; i < E * 3 * Lp; i += NT) {
+        const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
+        p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u] = s_ola[i];
+    }
+}
+
+// ============================================================================
+// Hop-blocked kernel: the same per-hop semantics, processed J = 2*JH hops at a
+// time when a call carries several hops (tvolap_process_hops). Within a block
+// all J forward FFTs run first (spread over the cluster), then the MAC for the
+// J outputs reuses every loaded spectrum: output i of parity group g (hop
+// l0+g+2i) needs X_{l0+g+2(i-m)}, so a sliding register window over the
+// delay line serves all JH outputs of a group with ONE delay-line load per
+// partition, and a filter slice shared by those hops is loaded once instead of
+// JH times. Every output is still the same sum over m in the same order, so
+// results equal hop-by-hop processing. Ring depth D >= M + JH keeps the slots a
+// block writes ahead from colliding with slots its earlier hops still read.
+// ============================================================================
+struct BlockLayout {
+    size_t tw, pk, win, xin, fa, fb, yb, red, ola, total;
+    __host__ __device__ BlockLayout(int L, int P, int E, int J, int Q, int threads) {
+        const size_t N = 2 * (size_t)L;
+        const size_t fpc = (J + P - 1) / P;  // frames owned per CTA
+        const size_t Np = N / P;
+        tw = 0;
+        pk = align16(tw + N * sizeof(float2));
+        win = align16(pk + (N + 2) * sizeof(float2));
+        xin = align16(win + N * sizeof(float));
+        fa = align16(xin + (size_t)(J + 1) * L * sizeof(float));
+        fb = align16(fa + fpc * E * N * sizeof(float2));
+        yb = align16(fb + fpc * E * N * sizeof(float2));
+        red = align16(yb + (size_t)J * E * Np * sizeof(float2));
+        const size_t red_bytes = Q > 1 ? (size_t)Q * J * E * (Np / 2) * sizeof(float4) : 0;
+        ola = align16(red + red_bytes);
+        total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
+        (void)threads;
+    }
+};
+
+// Batched Stockham over `nf` transforms of length N stored back to back.
+template <bool INV>
+__device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* __restrict__ tw, bool prune, int tid,
+                             int nthreads) {
+    float2* src = a;
+    float2* dst = b;
+    for (int Ns = 1; Ns < N;) {
+        const int R = ((N / Ns) & 3) == 0 ? 4 : 2;
+        const int nb = N / R;
+        const int tstep = N / (Ns * R);
+        const bool zero_hi = prune && Ns == 1;
+        for (int jj = tid; jj < nb * nf; jj += nthreads) {
+            const int f = jj / nb, j = jj - f * nb;
+            const float2* sf = src + (size_t)f * N;
+            float2* df = dst + (size_t)f * N;
+            const int k = j & (Ns - 1);
+            const int idxD = (j - k) * R + k;
+            if (R == 4) {
+                float2 v0 = sf[j];
+                float2 v1 = sf[j + nb];
+                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 2 * nb];
+                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 3 * nb];
+                if (Ns > 1) {
+                    const int t1 = k * tstep;
+                    const float2 w1 = tw[t1], w2 = tw[2 * t1], w3 = tw[3 * t1];
+                    if (INV) {
+                        v1 = cmulc(v1, w1);
+                        v2 = cmulc(v2, w2);
+                        v3 = cmulc(v3, w3);
+                    } else {
+                        v1 = cmul(v1, w1);
+                        v2 = cmul(v2, w2);
+                        v3 = cmul(v3, w3);
+                    }
+                }
+                const float2 a0 = cadd(v0, v2), a1 = csub(v0, v2);
+                const float2 a2 = cadd(v1, v3), a3 = csub(v1, v3);
+                df[idxD] = cadd(a0, a2);
+                df[idxD + 2 * Ns] = csub(a0, a2);
+                if (INV) {
+                    df[idxD + Ns] = make_float2(a1.x - a3.y, a1.y + a3.x);
+                    df[idxD + 3 * Ns] = make_float2(a1.x + a3.y, a1.y - a3.x);
+                } else {
+                    df[idxD + Ns] = make_float2(a1.x + a3.y, a1.y - a3.x);
+                    df[idxD + 3 * Ns] = make_float2(a1.x - a3.y, a1.y + a3.x);
+                }
+            } else {
+                float2 v0 = sf[j];
+                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[j + nb];
+                if (Ns > 1) {
+                    const float2 w1 = tw[k * tstep];
+                    v1 = INV ? cmulc(v1, w1) : cmul(v1, w1);
+                }
+                df[idxD] = cadd(v0, v1);
+                df[idxD + Ns] = csub(v0, v1);
+            }
+        }
+        __syncthreads();
+        float2* t = src;
+        src = dst;
+        dst = t;
+        Ns *= R;
+    }
+    return src;
+}
+
+__device__ __forceinline__ void block_sync(int P) {
+    if (P > 1)
+        cg::this_cluster().sync();
+    else
+        __syncthreads();
+}
+
+template <int E, int JH>
+__global__ void __launch_bounds__(256) tvolap_block_kernel(const HopParams p, const int Q) {
+    constexpr int J = 2 * JH;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int L = p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int s = blockIdx.x / P;
+    const int r = blockIdx.x % P;
+    const BlockLayout lay(L, P, E, J, Q, NT);
+    float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
+    float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
+    float* s_win = reinterpret_cast<float*>(smem + lay.win);
+    float* s_xin = reinterpret_cast<float*>(smem + lay.xin);
+    float2* s_fa = reinterpret_cast<float2*>(smem + lay.fa);
+    float2* s_fb = reinterpret_cast<float2*>(smem + lay.fb);
+    float2* s_yb = reinterpret_cast<float2*>(smem + lay.yb);
+    float4* s_red = reinterpret_cast<float4*>(smem + lay.red);
+    float* s_ola = reinterpret_cast<float*>(smem + lay.ola);
+
+    const int Np = N / P, V = Np / 2, Lp = L / P;
+    const long spec4 = N / 2;
+    const int W = 2 * V;             // (parity group, float4) work items
+    const int q = tid / W;           // partition group (Q groups when W < NT)
+    const int m0 = (int)((long)q * M / Q), m1 = (int)((long)(q + 1) * M / Q);
+
+    for (int i = tid; i < N; i += NT) {
+        s_tw[i] = p.tw[i];
+        s_win[i] = p.win[i];
+    }
+    for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    for (int i = tid; i < L; i += NT) s_xin[i] = p.hist[(long)s * L + i];
+    for (int i = tid; i < E * 3 * Lp; i += NT) {
+        const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
+        s_ola[i] = p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u];
+    }
+
+    const float4* ring4 = reinterpret_cast<const float4*>(p.ring);
+    const float4* pool4 = reinterpret_cast<const float4*>(p.pool);
+    cg::cluster_group cluster = cg::this_cluster();
+
+    for (int b0 = 0; b0 < p.n_hops; b0 += J) {
+        const long l0 = p.hop0 + b0;
+        const int jb = min(J, p.n_hops - b0);
+        // ---- inputs of the block (history already at s_xin[0..L))
+        const float* inp = p.in + (long)s * p.in_stride + (long)b0 * L;
+        for (int i = tid; i < jb * L; i += NT) s_xin[L + i] = inp[i];
+        __syncthreads();
+
+        // ---- K1/K2: this CTA's frames (j = r, r+P, ...): window, FFT, whole spectrum into the ring.
+        const int nf = jb > r ? (jb - r + P - 1) / P : 0;
+        for (int i = tid; i < nf * L; i += NT) {
+            const int f = i / L, jj = i - f * L;
+            const float* xs = s_xin + (size_t)(r + f * P) * L;  // (previous hop | this hop)
+            s_fa[(size_t)f * N + jj] = make_float2(xs[2 * jj] * s_win[2 * jj], xs[2 * jj + 1] * s_win[2 * jj + 1]);
+        }
+        __syncthreads();
+        if (nf > 0) {
+            const float2* Z = fft_batch<false>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
+            for (int i = tid; i < nf * N; i += NT) {
+                const int f = i / N, kk = i - f * N;
+                const long h = l0 + r + f * P;
+                float2* ringw = p.ring + (((long)s * 2 + (h & 1)) * D + (h >> 1) % D) * N;
+                ringw[kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
+            }
+        }
+        block_sync(P);  // ring writes of all frames visible cluster-wide
+
+        // ---- K3: hop-blocked MAC over this CTA's bin slice.
+        // W >= NT: Q == 1 and threads stride over the work items; W < NT: NT == Q * W, one item each.
+        for (int w = (W >= NT ? tid : tid % W); w < W; w += (W >= NT ? NT : W)) {
+            const int g = w / V, f = w - g * V;
+            const long hb = l0 + g;
+            const int par = (int)(hb & 1);
+            const long sb = hb >> 1;
+            const int ni = jb > g ? (jb - g + 1) / 2 : 0;  // outputs of this parity group
+            const float4* xr = ring4 + (((long)s * 2 + par) * D) * spec4 + (long)r * V + f;
+            auto xslot = [&](long t) -> const float4* {
+                long sl = (sb + t) % D;
+                if (sl < 0) sl += D;
+                return xr + sl * spec4;
+            };
+            int ent[JH];
+            bool shared = true;
+#pragma unroll
+            for (int i = 0; i < JH; ++i) {
+                const int jj = g + 2 * i;
+                ent[i] = p.sched ? p.sched[(long)(b0 + min(jj, jb - 1)) * p.sched_stride + s] : p.entry_base + s;
+                if (i < ni && ent[i] != ent[0]) shared = false;
+            }
+            float4 acc[JH][E];
+            float aux[JH][E];
+            float4 win[JH];
+#pragma unroll
+            for (int i = 0; i < JH; ++i) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    acc[i][e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    aux[i][e] = 0.f;
+                }
+                win[i] = __ldcg(xslot(i - m0));  // X_{t}, t = i - m
+            }
+            if (shared) {
+                const float4* hb4[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) hb4[e] = pool4 + (((long)ent[0] * E + e) * M) * spec4 + (long)r * V + f;
+                int m = m0;
+                constexpr int U = 4;
+                for (; m + U <= m1; m += U) {
+                    float4 xn[U], hh[U][E];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        xn[u] = __ldcg(xslot(-(m + u) - 1));
+#pragma unroll
+                        for (int e = 0; e < E; ++e) hh[u][e] = __ldg(hb4[e] + (long)(m + u) * spec4);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+#pragma unroll
+                        for (int i = 0; i < JH; ++i)
+#pragma unroll
+                            for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], hh[u][e], win[i]);
+#pragma unroll
+                        for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
+                        win[0] = xn[u];
+                    }
+                }
+                for (; m < m1; ++m) {
+                    const float4 xn = __ldcg(xslot(-m - 1));
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const float4 h = __ldg(hb4[e] + (long)m * spec4);
+#pragma unroll
+                        for (int i = 0; i < JH; ++i) cmac4(acc[i][e], aux[i][e], h, win[i]);
+                    }
+#pragma unroll
+                    for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
+                    win[0] = xn;
+                }
+            } else {
+                for (int m = m0; m < m1; ++m) {
+                    const float4 xn = __ldcg(xslot(-m - 1));
+#pragma unroll
+                    for (int i = 0; i < JH; ++i)
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const float4 h =
+                                __ldg(pool4 + (((long)ent[i] * E + e) * M + m) * spec4 + (long)r * V + f);
+                            cmac4(acc[i][e], aux[i][e], h, win[i]);
+                        }
+#pragma unroll
+                    for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
+                    win[0] = xn;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < JH; ++i) {
+                const int jj = g + 2 * i;
+                if (i >= ni) continue;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    float4 a = acc[i][e];
+                    if (r == 0 && f == 0) {  // packed bin 0: two real products
+                        a.x += aux[i][e];
+                        a.y = aux[i][e];
+                    }
+                    if (Q == 1)
+                        reinterpret_cast<float4*>(s_yb + ((size_t)jj * E + e) * Np)[f] = a;
+                    else
+                        s_red[(((size_t)q * J + jj) * E + e) * V + f] = a;
+                }
+            }
+        }
+        if (Q > 1) {
+            __syncthreads();
+            for (int i = tid; i < jb * E * V; i += NT) {
+                const int f = i % V, je = i / V;  // je = jj * E + e
+                float4 sum = s_red[(size_t)je * V + f];
+                for (int qq = 1; qq < Q; ++qq) sum = f4add(sum, s_red[((size_t)qq * J * E + je) * V + f]);
+                reinterpret_cast<float4*>(s_yb + (size_t)je * Np)[f] = sum;
+            }
+        }
+        block_sync(P);  // Y slices of all frames published
+
+        // ---- K5a: this CTA's frames: gather Y over DSMEM, tangle, inverse FFT.
+        const int nt = nf * E;  // transforms
+        for (int i = tid; i < nt * (N / 2); i += NT) {  // float4 granularity gather
+            const int t = i / (N / 2), k4 = i - t * (N / 2);
+            const int f = t / E, e = t - f * E;
+            const int jj = r + f * P;
+            const int qsrc = (2 * k4) / Np;
+            const float4* src = reinterpret_cast<const float4*>(s_yb + ((size_t)jj * E + e) * Np);
+            if (qsrc != r) src = cluster.map_shared_rank(src, qsrc);
+            reinterpret_cast<float4*>(s_fa + (size_t)t * N)[k4] = src[k4 - qsrc * (Np / 2)];
+        }
+        __syncthreads();
+        for (int i = tid; i < nt * N; i += NT) {
+            const int t = i / N, kk = i - t * N;
+            s_fb[(size_t)t * N + kk] = tangle_packed(s_fa + (size_t)t * N, N, kk, s_pk);
+        }
+        __syncthreads();
+        if (nt > 0) fft_batch<true>(s_fb, s_fa, N, nt, s_tw, false, tid, NT);
+        // the result buffer depends only on the stage count (same in every CTA of the cluster)
+        int stages = 0;
+        for (int Ns = 1; Ns < N; Ns *= (((N / Ns) & 3) == 0 ? 4 : 2)) ++stages;
+        const float* ytd = reinterpret_cast<const float*>((stages & 1) ? s_fa : s_fb);
+        // time-domain frame (f, e) of this CTA = ytd[(f * E + e) * 2N ...] (unscaled)
+        block_sync(P);  // all frames' time-domain blocks ready
+
+        // ---- K5b: hop-2 overlap-add for this CTA's sample slice, all frames of the block.
+        // Both ping-pong buffers hold the same transform count, so the result buffer
+        // offset is identical in every CTA of the cluster.
+        const size_t ytd_off = (size_t)((const unsigned char*)ytd - smem);
+        const float sc = 1.0f / (float)N;
+        for (int i = tid; i < E * Lp; i += NT) {
+            const int e = i / Lp, u = i - e * Lp;
+            const int ug = r * Lp + u;
+            float* A = s_ola + e * 3 * Lp;
+            float a0 = A[u], a1 = A[Lp + u], a2 = A[2 * Lp + u];
+            float y[J][4];
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) {
+                if (jj < jb) {
+                    const int owner = jj % P, f = jj / P;
+                    const float* base = reinterpret_cast<const float*>(smem + ytd_off);
+                    if (owner != r) base = cluster.map_shared_rank(base, owner);
+                    const float* yf = base + ((size_t)f * E + e) * 2 * N;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) y[jj][d] = yf[d * L + ug] * sc;
+                } else {
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) y[jj][d] = 0.f;
+                }
+            }
+            float* o = p.out + ((long)s * E + e) * p.out_stride + (long)b0 * L + ug;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) {
+                if (jj >= jb) break;
+                // pending = contributions of earlier frames: rolling (a0, a1, a2)
+                o[(long)jj * L] = 0.5f * (y[jj][0] + a0);
+                a0 = a1 + y[jj][1];
+                a1 = a2 + y[jj][2];
+                a2 = y[jj][3];
+            }
+            A[u] = a0;
+            A[Lp + u] = a1;
+            A[2 * Lp + u] = a2;
+        }
+        // history for the next block = last input hop of this block
+        __syncthreads();
+        for (int i = tid; i < L; i += NT) s_xin[i] = s_xin[(size_t)jb * L + i];
+        block_sync(P);  // peers done reading this CTA's Y slices / time-domain frames
+    }
+    if (r == 0)
+        for (int i = tid; i < L; i += NT) p.hist[(long)s * L + i] = s_xin[i];
     for (int i = tid; i < E * 3 * Lp; i += NT) {
         const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
         p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u] = s_ola[i];
@@ -400,6 +766,52 @@ int fft_threads(int N) { return std::max(32, std::min(256, N / 4)); }
 }  // namespace
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int threads) { return SmemLayout(L, P, E, threads).total; }
+
+size_t block_kernel_smem_bytes(int L, int P, int E, int JH, int Q, int threads) {
+    return BlockLayout(L, P, E, 2 * JH, Q, threads).total;
+}
+
+template <int E, int JH>
+static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaStream_t stream) {
+    const size_t smem = block_kernel_smem_bytes(p.L, p.P, E, JH, Q, threads);
+    void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH>;
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    if (p.P > 1) {
+        err = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (err != cudaSuccess) return err;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.S * p.P));
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = p.P > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, p, Q);
+}
+
+cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int threads, cudaStream_t stream) {
+    if (E == 2) {
+        switch (JH) {
+            case 1: return launch_block_t<2, 1>(p, Q, threads, stream);
+            case 2: return launch_block_t<2, 2>(p, Q, threads, stream);
+            case 4: return launch_block_t<2, 4>(p, Q, threads, stream);
+            default: return launch_block_t<2, 8>(p, Q, threads, stream);
+        }
+    }
+    switch (JH) {
+        case 1: return launch_block_t<1, 1>(p, Q, threads, stream);
+        case 2: return launch_block_t<1, 2>(p, Q, threads, stream);
+        case 4: return launch_block_t<1, 4>(p, Q, threads, stream);
+        default: return launch_block_t<1, 8>(p, Q, threads, stream);
+    }
+}
 
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {
     const size_t smem = hop_kernel_smem_bytes(p.L, p.P, E, threads);

@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
             "tvolap_launch_config": (ip, [vp, fp, fp]),
             "tvolap_set_launch_config": (ip, [vp, ip, ip]),
             "tvolap_kernel_launches": (C.c_uint64, [vp]),
+            "tvolap_set_block_config": (ip, [vp, ip, lg]),
+            "tvolap_block_config": (ip, [vp, fp, fp, fp]),
             "tvolap_forward_real": (ip, [ip, lg, lg, fp, fp]),
             "tvolap_inverse_real": (ip, [ip, lg, lg, fp, fp]),
             "tvolap_mac": (ip, [ip, lg, lg, fp, fp, fp, fp]),
@@ -124,7 +126,7 @@ EXPORTED_SYMBOLS = (
     "tvolap_process_hops tvolap_exchange_filter tvolap_select_bank tvolap_reset tvolap_hop tvolap_channels "
     "tvolap_output_channels tvolap_partition_count tvolap_delay_line_depth tvolap_latency "
     "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
-    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches "
+    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_set_block_config tvolap_block_config "
     "tvolap_forward_real tvolap_inverse_real tvolap_mac tvolap_hann_window tvolap_partition "
     "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device"
 ).split()
@@ -389,6 +391,14 @@ class TvolapEngine:
 
     def set_launch_config(self, ctas_per_source: int = 0, threads: int = 0) -> None:
         _check(lib().tvolap_set_launch_config(self._h, ctas_per_source, threads))
+
+    def set_block_config(self, hops_per_block: int = 0, block_min: int = 0) -> None:
+        _check(lib().tvolap_set_block_config(self._h, hops_per_block, block_min))
+
+    def block_config(self):
+        j, b, q = C.c_int(), C.c_long(), C.c_int()
+        _check(lib().tvolap_block_config(self._h, C.byref(j), C.byref(b), C.byref(q)))
+        return j.value, b.value, q.value
 
     def kernel_launches(self) -> int:
         return lib().tvolap_kernel_launches(self._h)

@@ -289,5 +289,91 @@ def test_process_hops_equals_process():
     a, b = T.TvolapEngine(s), T.TvolapEngine(s)
     one = np.concatenate([a.process(x[i * 128:(i + 1) * 128]) for i in range(30)])  # (T, C)
     many = b.process_hops(np.ascontiguousarray(x.T))  # (C, T)
-    assert np.array_equal(one.T, many)
+    # multi-hop calls run the hop-blocked kernel: same per-hop sums, partition groups may differ
+    assert np.abs(one.T - many).max() <= 1e-5 * np.abs(one).max()
+    b.set_block_config(0, 1 << 30)  # force the one-hop-at-a-time kernel for multi-hop calls
+    c = T.TvolapEngine(s)
+    c.set_block_config(0, 1 << 30)
+    assert np.array_equal(one.T, c.process_hops(np.ascontiguousarray(x.T)))
     assert b.hops_processed() == 30
+
+
+# ------------------------------------------------------------ hop-blocked kernel == hop-by-hop kernel
+def _relerr(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+@pytest.mark.parametrize("jb", [2, 4, 8, 16])
+@pytest.mark.parametrize("hop,n_ir,P", [(64, 64, 1), (64, 200, 2), (32, 64 * 3, 4), (128, 3000, 1), (256, 32768, 4)])
+def test_block_kernel_matches_streaming(jb, hop, n_ir, P):
+    """process_hops (hop-blocked kernel, partial blocks, odd start) == process() hop by hop."""
+    S = 3
+    ir = rnd(n_ir, n_ir + jb, S)
+    n = 3 * jb + 3
+    x = rnd(hop * (n + 1), 7 + jb, S)
+    s = T.partition(ir, hop)
+    a, b = T.TvolapEngine(s), T.TvolapEngine(s)
+    a.set_launch_config(P, 0)
+    b.set_launch_config(P, 0)
+    try:
+        a.set_block_config(jb, 2)
+    except T.InvalidConfigurationError:
+        pytest.skip("block does not fit in shared memory")
+    ref = np.concatenate([b.process(x[i * hop:(i + 1) * hop]) for i in range(n + 1)])  # (T, S)
+    xs = np.ascontiguousarray(x.T)
+    first = a.process(x[:hop])  # one streaming hop first: the block starts at an odd hop
+    rest = a.process_hops(xs[:, hop:])
+    got = np.concatenate([first.T, rest], axis=1)
+    assert _relerr(got, ref.T) <= 1e-5
+
+
+def test_block_kernel_with_exchanges_between_calls():
+    hop, S = 64, 2
+    sets = [T.partition(rnd(900, 40 + k, S), hop, 15) for k in range(4)]
+    x = rnd(hop * 64, 99, S)
+    a, b = T.TvolapEngine(sets[0]), T.TvolapEngine(sets[0])
+    a.set_block_config(8, 2)
+    outs_a, outs_b = [], []
+    for k in range(4):
+        if k:
+            a.exchange_filter(sets[k])
+            b.exchange_filter(sets[k])
+        seg = x[k * 16 * hop:(k + 1) * 16 * hop]
+        outs_a.append(a.process_hops(np.ascontiguousarray(seg.T)))
+        outs_b.append(np.concatenate([b.process(seg[i * hop:(i + 1) * hop]) for i in range(16)]).T)
+    assert _relerr(np.concatenate(outs_a, 1), np.concatenate(outs_b, 1)) <= 1e-5
+
+
+@pytest.mark.parametrize("ears", [1, 2])
+@pytest.mark.parametrize("jb", [4, 16])
+def test_block_kernel_bank_schedule(ears, jb):
+    """Per-hop bank switching inside blocks (non-shared filters) == streaming kernel, ears share X."""
+    hop, S, n_bank, n = 32, 5, 7, 41
+    bank = rnd(n_bank * ears * 500, 5).reshape(n_bank, ears, 500)
+    sched = np.random.default_rng(8).integers(0, n_bank, (n, S)).astype(np.int32)
+    sched[:10] = 3  # a run of shared filters
+    x = np.ascontiguousarray(rnd(hop * n, 6, S).T)
+    a = T.TvolapBankEngine(bank, hop, S)
+    b = T.TvolapBankEngine(bank, hop, S)
+    a.set_block_config(jb, 2)
+    b.set_block_config(0, 1 << 30)  # never block
+    ya = a.process_hops(x, schedule=sched)
+    yb = b.process_hops(x, schedule=sched)
+    assert _relerr(ya, yb) <= 1e-5
+    # and against the oracle, ear by ear
+    for s in range(S):
+        cur = None
+        eng = None
+        for h in range(n):
+            if sched[h, s] != cur:
+                st = O.partition(bank[sched[h, s]].T.astype(np.float32), hop)
+                if eng is None:
+                    eng = O.Engine(st)
+                else:
+                    eng.exchange_filter(st)
+                cur = sched[h, s]
+            seg = np.repeat(x[s, h * hop:(h + 1) * hop, None].astype(np.float64), ears, axis=1)
+            yo = eng.process(seg)
+            for e in range(ears):
+                assert np.abs(ya[s * ears + e, h * hop:(h + 1) * hop] - yo[:, e]).max() <= 1e-4 * max(
+                    np.abs(yo).max(), 1e-3)
