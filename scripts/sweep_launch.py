@@ -1,0 +1,76 @@
+"""Launch-geometry sweep of the hop kernels on one GPU: cluster size P x hops per
+block (0 = one-hop-at-a-time kernel) for each BASELINE config, device-resident
+inputs, fixed filter (fresh configs) or the per-hop bank schedule (bank configs).
+Prints one JSON line per point: us per hop and the §8(d) algorithmic GB/s."""
+import ctypes
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2310_00319_b200 import tvolap as T  # noqa: E402
+from paper_2310_00319_b200 import workload as W  # noqa: E402
+from paper_2310_00319_b200.tvolap import TvolapBankEngine, TvolapEngine, partition  # noqa: E402
+
+HOPS = {"C1": 3750, "C2": 1024, "C3": 512, "C4": 128, "C5": 1024}
+
+
+def run(name, Ps, JHs, reps=3):
+    cfg = W.CONFIGS[name]
+    H, L, S = HOPS[name], cfg.hop, cfg.sources
+    lib = T.lib()
+    x = torch.empty((S, H * L), device="cuda")
+    T._check(lib.tvolap_gen_white_device(0, cfg.seed, 0, S, 0, H * L, ctypes.c_void_p(x.data_ptr()), H * L))
+    out = torch.empty((cfg.lanes, H * L), device="cuda")
+    sched = None
+    if cfg.mode == "bank":
+        bank = torch.from_numpy(W.bank_irs(cfg)).cuda()
+        sched_h = W.schedule(cfg, 0, H)
+        sched = torch.from_numpy(sched_h).cuda()
+        distinct = float(np.mean([np.unique(r).size for r in sched_h[:256]]))
+        eng = TvolapBankEngine(bank, L, S, min_partitions=cfg.partitions)
+    else:
+        eng = TvolapEngine(partition(W.fresh_irs(cfg, 0)[:, 0, :].T, L, cfg.partitions))
+        distinct = S
+    st = torch.cuda.Stream()
+    eng.set_stream(st.cuda_stream)
+    bph = W.bytes_per_hop(cfg, distinct_filters=distinct)
+    for P in Ps:
+        if P > L:
+            continue
+        for jh in JHs:
+            try:
+                eng.set_launch_config(P, 0)
+                if jh == 0:
+                    eng.set_block_config(0, 1 << 30)
+                else:
+                    eng.set_block_config(2 * jh, 2)
+            except (T.InvalidConfigurationError, T.CudaError) as e:
+                print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "skip": str(e)}), flush=True)
+                continue
+            try:
+                eng.process_hops(x, out=out, schedule=sched)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                for _ in range(reps):
+                    eng.process_hops(x, out=out, schedule=sched)
+                b.record(st)
+                b.synchronize()
+                ms = a.elapsed_time(b) / reps
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "error": str(e)}), flush=True)
+                continue
+            j, bm, q = eng.block_config()
+            print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "Q": q, "us_per_hop": 1e3 * ms / H,
+                              "GBps_alg": bph * H / (ms / 1e3) / 1e9, "frac": bph * H / (ms / 1e3) / 1e9 / 6542.1}),
+                  flush=True)
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
+    for n in names:
+        run(n, [1, 2, 4, 8], [0, 1, 2, 4, 8])
