@@ -286,10 +286,12 @@ struct BlockLayout {
         fb = align16(fa + fpc * E * N * sizeof(float2));
         yb = align16(fb + fpc * E * N * sizeof(float2));
         red = align16(yb + (size_t)J * E * Np * sizeof(float2));
-        const size_t red_bytes = Q > 1 ? (size_t)Q * J * E * (Np / 2) * sizeof(float4) : 0;
+        const size_t V = Np / 2;
+        const size_t qmax = V < (size_t)threads ? threads / V : 1;  // unified mapping: threads / V groups
+        const size_t red_bytes = qmax > 1 ? qmax * J * E * V * sizeof(float4) : 0;
+        (void)Q;
         ola = align16(red + red_bytes);
         total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
-        (void)threads;
     }
 };
 
@@ -366,8 +368,11 @@ __device__ __forceinline__ void block_sync(int P) {
         __syncthreads();
 }
 
-template <int E, int JH>
-__global__ void __launch_bounds__(256) tvolap_block_kernel(const HopParams p, const int Q) {
+// BANK = false: filter-set engines (one set for every hop of a block) — only the unified
+// mapping (JH <= 4) or the per-parity shared mapping (JH == 8) is compiled. BANK = true:
+// per-hop bank selections — per-parity mapping with shared or per-output filter loads.
+template <int E, int JH, bool BANK>
+__global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p, const int Q) {
     constexpr int J = 2 * JH;
     extern __shared__ __align__(16) unsigned char smem[];
     const int L = p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
@@ -434,7 +439,117 @@ __global__ void __launch_bounds__(256) tvolap_block_kernel(const HopParams p, co
         block_sync(P);  // ring writes of all frames visible cluster-wide
 
         // ---- K3: hop-blocked MAC over this CTA's bin slice.
-        // W >= NT: Q == 1 and threads stride over the work items; W < NT: NT == Q * W, one item each.
+        // Does every hop of the block use the same filter set (set engines: always)?
+        bool all_same = true;
+        int ent0 = p.entry_base + s;
+        if (p.sched) {
+            ent0 = p.sched[(long)b0 * p.sched_stride + s];
+            for (int jj = 1; jj < jb; ++jj) all_same &= p.sched[(long)(b0 + jj) * p.sched_stride + s] == ent0;
+        }
+        int Qeff;
+        if (!BANK && JH <= 4) {
+            // Unified mapping: one thread per float4 covers both parity groups, so each filter
+            // slice is loaded once per block for all J outputs; two sliding delay-line windows.
+            Qeff = V < NT ? NT / V : 1;
+            const int qq = V < NT ? tid / V : 0;
+            const int mu0 = (int)((long)qq * M / Qeff), mu1 = (int)((long)(qq + 1) * M / Qeff);
+            constexpr int JU = JH <= 4 ? JH : 1;
+            for (int f = (V >= NT ? tid : tid % V); f < V; f += (V >= NT ? NT : V)) {
+                const float4* xr[2];
+                long sbp[2];
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    const long hbg = l0 + g;
+                    xr[g] = ring4 + (((long)s * 2 + (hbg & 1)) * D) * spec4 + (long)r * V + f;
+                    sbp[g] = hbg >> 1;
+                }
+                auto xs = [&](int g, long t) -> const float4* {
+                    long sl = (sbp[g] + t) % D;
+                    if (sl < 0) sl += D;
+                    return xr[g] + sl * spec4;
+                };
+                const float4* hb4[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) hb4[e] = pool4 + (((long)ent0 * E + e) * M) * spec4 + (long)r * V + f;
+                float4 acc[2][JU][E];
+                float aux[2][JU][E];
+                float4 win[2][JU];
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int i = 0; i < JU; ++i) {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            acc[g][i][e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            aux[g][i][e] = 0.f;
+                        }
+                        win[g][i] = __ldcg(xs(g, i - mu0));
+                    }
+                int m = mu0;
+                constexpr int U = 2;
+                for (; m + U <= mu1; m += U) {
+                    float4 xn[U][2], hh[U][E];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        xn[u][0] = __ldcg(xs(0, -(m + u) - 1));
+                        xn[u][1] = __ldcg(xs(1, -(m + u) - 1));
+#pragma unroll
+                        for (int e = 0; e < E; ++e) hh[u][e] = __ldg(hb4[e] + (long)(m + u) * spec4);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+#pragma unroll
+                            for (int i = 0; i < JU; ++i)
+#pragma unroll
+                                for (int e = 0; e < E; ++e) cmac4(acc[g][i][e], aux[g][i][e], hh[u][e], win[g][i]);
+#pragma unroll
+                            for (int i = JU - 1; i > 0; --i) win[g][i] = win[g][i - 1];
+                            win[g][0] = xn[u][g];
+                        }
+                    }
+                }
+                for (; m < mu1; ++m) {
+                    const float4 x0 = __ldcg(xs(0, -m - 1)), x1 = __ldcg(xs(1, -m - 1));
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const float4 h = __ldg(hb4[e] + (long)m * spec4);
+#pragma unroll
+                        for (int g = 0; g < 2; ++g)
+#pragma unroll
+                            for (int i = 0; i < JU; ++i) cmac4(acc[g][i][e], aux[g][i][e], h, win[g][i]);
+                    }
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+#pragma unroll
+                        for (int i = JU - 1; i > 0; --i) win[g][i] = win[g][i - 1];
+                        win[g][0] = g ? x1 : x0;
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int i = 0; i < JU; ++i) {
+                        const int jj = g + 2 * i;
+                        if (jj >= jb) continue;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            float4 a = acc[g][i][e];
+                            if (r == 0 && f == 0) {  // packed bin 0: two real products
+                                a.x += aux[g][i][e];
+                                a.y = aux[g][i][e];
+                            }
+                            if (Qeff == 1)
+                                reinterpret_cast<float4*>(s_yb + ((size_t)jj * E + e) * Np)[f] = a;
+                            else
+                                s_red[(((size_t)qq * J + jj) * E + e) * V + f] = a;
+                        }
+                    }
+            }
+        } else {
+        Qeff = W < NT ? NT / W : 1;
+        // Per-parity mapping (W >= NT: threads stride over the work items; W < NT: Qeff groups of W).
         for (int w = (W >= NT ? tid : tid % W); w < W; w += (W >= NT ? NT : W)) {
             const int g = w / V, f = w - g * V;
             const long hb = l0 + g;
@@ -467,12 +582,12 @@ __global__ void __launch_bounds__(256) tvolap_block_kernel(const HopParams p, co
                 }
                 win[i] = __ldcg(xslot(i - m0));  // X_{t}, t = i - m
             }
-            if (shared) {
+            if (!BANK || shared) {
                 const float4* hb4[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) hb4[e] = pool4 + (((long)ent[0] * E + e) * M) * spec4 + (long)r * V + f;
                 int m = m0;
-                constexpr int U = 4;
+                constexpr int U = JH >= 8 ? 2 : 4;
                 for (; m + U <= m1; m += U) {
                     float4 xn[U], hh[U][E];
 #pragma unroll
@@ -505,16 +620,19 @@ __global__ void __launch_bounds__(256) tvolap_block_kernel(const HopParams p, co
                     win[0] = xn;
                 }
             } else {
+                // per-output filters (bank switching inside the block)
+                const float4* hbi[JH][E];
+#pragma unroll
+                for (int i = 0; i < JH; ++i)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) hbi[i][e] = pool4 + (((long)ent[i] * E + e) * M) * spec4 + (long)r * V + f;
+#pragma unroll 2
                 for (int m = m0; m < m1; ++m) {
                     const float4 xn = __ldcg(xslot(-m - 1));
 #pragma unroll
                     for (int i = 0; i < JH; ++i)
 #pragma unroll
-                        for (int e = 0; e < E; ++e) {
-                            const float4 h =
-                                __ldg(pool4 + (((long)ent[i] * E + e) * M + m) * spec4 + (long)r * V + f);
-                            cmac4(acc[i][e], aux[i][e], h, win[i]);
-                        }
+                        for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], __ldg(hbi[i][e] + (long)m * spec4), win[i]);
 #pragma unroll
                     for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
                     win[0] = xn;
@@ -531,19 +649,20 @@ __global__ void __launch_bounds__(256) tvolap_block_kernel(const HopParams p, co
                         a.x += aux[i][e];
                         a.y = aux[i][e];
                     }
-                    if (Q == 1)
+                    if (Qeff == 1)
                         reinterpret_cast<float4*>(s_yb + ((size_t)jj * E + e) * Np)[f] = a;
                     else
                         s_red[(((size_t)q * J + jj) * E + e) * V + f] = a;
                 }
             }
         }
-        if (Q > 1) {
+        }
+        if (Qeff > 1) {
             __syncthreads();
             for (int i = tid; i < jb * E * V; i += NT) {
                 const int f = i % V, je = i / V;  // je = jj * E + e
                 float4 sum = s_red[(size_t)je * V + f];
-                for (int qq = 1; qq < Q; ++qq) sum = f4add(sum, s_red[((size_t)qq * J * E + je) * V + f]);
+                for (int qq = 1; qq < Qeff; ++qq) sum = f4add(sum, s_red[((size_t)qq * J * E + je) * V + f]);
                 reinterpret_cast<float4*>(s_yb + (size_t)je * Np)[f] = sum;
             }
         }
@@ -771,10 +890,10 @@ size_t block_kernel_smem_bytes(int L, int P, int E, int JH, int Q, int threads) 
     return BlockLayout(L, P, E, 2 * JH, Q, threads).total;
 }
 
-template <int E, int JH>
+template <int E, int JH, bool BANK>
 static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaStream_t stream) {
     const size_t smem = block_kernel_smem_bytes(p.L, p.P, E, JH, Q, threads);
-    void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH>;
+    void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH, BANK>;
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     if (p.P > 1) {
@@ -797,44 +916,28 @@ static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaSt
 }
 
 cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int threads, cudaStream_t stream) {
+    if (p.sched == nullptr && E == 1) {
+        switch (JH) {
+            case 1: return launch_block_t<1, 1, false>(p, Q, threads, stream);
+            case 2: return launch_block_t<1, 2, false>(p, Q, threads, stream);
+            case 4: return launch_block_t<1, 4, false>(p, Q, threads, stream);
+            default: return launch_block_t<1, 8, false>(p, Q, threads, stream);
+        }
+    }
     if (E == 2) {
         switch (JH) {
-            case 1: return launch_block_t<2, 1>(p, Q, threads, stream);
-            case 2: return launch_block_t<2, 2>(p, Q, threads, stream);
-            case 4: return launch_block_t<2, 4>(p, Q, threads, stream);
-            default: return launch_block_t<2, 8>(p, Q, threads, stream);
+            case 1: return launch_block_t<2, 1, true>(p, Q, threads, stream);
+            case 2: return launch_block_t<2, 2, true>(p, Q, threads, stream);
+            case 4: return launch_block_t<2, 4, true>(p, Q, threads, stream);
+            default: return launch_block_t<2, 8, true>(p, Q, threads, stream);
         }
     }
     switch (JH) {
-        case 1: return launch_block_t<1, 1>(p, Q, threads, stream);
-        case 2: return launch_block_t<1, 2>(p, Q, threads, stream);
-        case 4: return launch_block_t<1, 4>(p, Q, threads, stream);
-        default: return launch_block_t<1, 8>(p, Q, threads, stream);
+        case 1: return launch_block_t<1, 1, true>(p, Q, threads, stream);
+        case 2: return launch_block_t<1, 2, true>(p, Q, threads, stream);
+        case 4: return launch_block_t<1, 4, true>(p, Q, threads, stream);
+        default: return launch_block_t<1, 8, true>(p, Q, threads, stream);
     }
-}
-
-cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {
-    const size_t smem = hop_kernel_smem_bytes(p.L, p.P, E, threads);
-    void (*fn)(const HopParams) = E == 2 ? tvolap_hop_kernel<2> : tvolap_hop_kernel<1>;
-    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    if (p.P > 1) {
-        err = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (err != cudaSuccess) return err;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(p.S * p.P));
-    cfg.blockDim = dim3((unsigned)threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)p.P;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = p.P > 1 ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
