@@ -940,6 +940,30 @@ cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int th
     }
 }
 
+cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {
+    const size_t smem = hop_kernel_smem_bytes(p.L, p.P, E, threads);
+    void (*fn)(const HopParams) = E == 2 ? tvolap_hop_kernel<2> : tvolap_hop_kernel<1>;
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    if (p.P > 1) {
+        err = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (err != cudaSuccess) return err;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.S * p.P));
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.P;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = p.P > 1 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, p);
+}
+
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
                              long row0, const float2* tw, const float2* pk, cudaStream_t stream) {
     const int N = 2 * L;
