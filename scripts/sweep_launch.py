@@ -71,6 +71,16 @@ def run(name, Ps, JHs, reps=3):
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
-    for n in names:
-        run(n, [1, 2, 4, 8], [0, 1, 2, 4, 8])
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--P", type=int, nargs="*", default=[1, 2, 4, 8])
+    ap.add_argument("--J", type=int, nargs="*", default=[0, 2, 4, 8, 16], help="hops per block (0 = streaming)")
+    ap.add_argument("--hops", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    for n in a.configs:
+        if a.hops:
+            HOPS[n] = a.hops
+        run(n, a.P, [j // 2 for j in a.J], reps=a.reps)
