@@ -282,7 +282,7 @@ struct BlockLayout {
         pk = align16(tw + N * sizeof(float2));
         win = align16(pk + (N + 2) * sizeof(float2));
         xin = align16(win + N * sizeof(float));
-        fa = align16(xin + (size_t)(J + 1) * L * sizeof(float));
+        fa = align16(xin + 2 * (size_t)(J + 1) * L * sizeof(float));  // double-buffered block inputs
         fb = align16(fa + fpc * E * N * sizeof(float2));
         yb = align16(fb + fpc * E * N * sizeof(float2));
         red = align16(yb + (size_t)J * E * Np * sizeof(float2));
@@ -401,7 +401,19 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         s_win[i] = p.win[i];
     }
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
-    for (int i = tid; i < L; i += NT) s_xin[i] = p.hist[(long)s * L + i];
+    float* xcur = s_xin;                       // this block's inputs: [history | J hops]
+    float* xnxt = s_xin + (size_t)(J + 1) * L;  // next block's, prefetched with cp.async
+    for (int i = tid; i < L; i += NT) xcur[i] = p.hist[(long)s * L + i];
+    auto prefetch_block = [&](float* dst, int b) {  // hops b .. b+J-1 of this source into dst[L..]
+        const int jn = min(J, p.n_hops - b);
+        const float* src = p.in + (long)s * p.in_stride + (long)b * L;
+        for (int i = tid; i < jn * L; i += NT) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + L + i);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + i));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    prefetch_block(xcur, 0);
     for (int i = tid; i < E * 3 * Lp; i += NT) {
         const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
         s_ola[i] = p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u];
@@ -414,16 +426,19 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     for (int b0 = 0; b0 < p.n_hops; b0 += J) {
         const long l0 = p.hop0 + b0;
         const int jb = min(J, p.n_hops - b0);
-        // ---- inputs of the block (history already at s_xin[0..L))
-        const float* inp = p.in + (long)s * p.in_stride + (long)b0 * L;
-        for (int i = tid; i < jb * L; i += NT) s_xin[L + i] = inp[i];
+        // ---- inputs: this block's landed (prefetched one block ago); start the next block's copy
+        if (b0 + J < p.n_hops)
+            prefetch_block(xnxt, b0 + J);
+        else
+            asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::);
         __syncthreads();
 
         // ---- K1/K2: this CTA's frames (j = r, r+P, ...): window, FFT, whole spectrum into the ring.
         const int nf = jb > r ? (jb - r + P - 1) / P : 0;
         for (int i = tid; i < nf * L; i += NT) {
             const int f = i / L, jj = i - f * L;
-            const float* xs = s_xin + (size_t)(r + f * P) * L;  // (previous hop | this hop)
+            const float* xs = xcur + (size_t)(r + f * P) * L;  // (previous hop | this hop)
             s_fa[(size_t)f * N + jj] = make_float2(xs[2 * jj] * s_win[2 * jj], xs[2 * jj + 1] * s_win[2 * jj + 1]);
         }
         __syncthreads();
@@ -463,11 +478,15 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     xr[g] = ring4 + (((long)s * 2 + (hbg & 1)) * D) * spec4 + (long)r * V + f;
                     sbp[g] = hbg >> 1;
                 }
-                auto xs = [&](int g, long t) -> const float4* {
+                auto xs = [&](int g, long t) -> const float4* {  // window init only
                     long sl = (sbp[g] + t) % D;
                     if (sl < 0) sl += D;
                     return xr[g] + sl * spec4;
                 };
+                // slot cursors for the next delay-line load (t = -m-1), decremented per partition
+                int cur[2];
+#pragma unroll
+                for (int g = 0; g < 2; ++g) cur[g] = (int)(((sbp[g] - mu0 - 1) % D + D) % D);
                 const float4* hb4[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) hb4[e] = pool4 + (((long)ent0 * E + e) * M) * spec4 + (long)r * V + f;
@@ -491,8 +510,11 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     float4 xn[U][2], hh[U][E];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        xn[u][0] = __ldcg(xs(0, -(m + u) - 1));
-                        xn[u][1] = __ldcg(xs(1, -(m + u) - 1));
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            xn[u][g] = __ldcg(xr[g] + (long)cur[g] * spec4);
+                            cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
+                        }
 #pragma unroll
                         for (int e = 0; e < E; ++e) hh[u][e] = __ldg(hb4[e] + (long)(m + u) * spec4);
                     }
@@ -511,7 +533,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     }
                 }
                 for (; m < mu1; ++m) {
-                    const float4 x0 = __ldcg(xs(0, -m - 1)), x1 = __ldcg(xs(1, -m - 1));
+                    const float4 x0 = __ldcg(xr[0] + (long)cur[0] * spec4), x1 = __ldcg(xr[1] + (long)cur[1] * spec4);
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
                         const float4 h = __ldg(hb4[e] + (long)m * spec4);
@@ -557,10 +581,16 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             const long sb = hb >> 1;
             const int ni = jb > g ? (jb - g + 1) / 2 : 0;  // outputs of this parity group
             const float4* xr = ring4 + (((long)s * 2 + par) * D) * spec4 + (long)r * V + f;
-            auto xslot = [&](long t) -> const float4* {
+            auto xslot = [&](long t) -> const float4* {  // window init only
                 long sl = (sb + t) % D;
                 if (sl < 0) sl += D;
                 return xr + sl * spec4;
+            };
+            int cur = (int)(((sb - m0 - 1) % D + D) % D);  // slot of the next load (t = -m-1)
+            auto xnext = [&]() -> float4 {
+                const float4 v = __ldcg(xr + (long)cur * spec4);
+                cur = cur == 0 ? D - 1 : cur - 1;
+                return v;
             };
             int ent[JH];
             bool shared = true;
@@ -592,7 +622,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     float4 xn[U], hh[U][E];
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        xn[u] = __ldcg(xslot(-(m + u) - 1));
+                        xn[u] = xnext();
 #pragma unroll
                         for (int e = 0; e < E; ++e) hh[u][e] = __ldg(hb4[e] + (long)(m + u) * spec4);
                     }
@@ -608,7 +638,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     }
                 }
                 for (; m < m1; ++m) {
-                    const float4 xn = __ldcg(xslot(-m - 1));
+                    const float4 xn = xnext();
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
                         const float4 h = __ldg(hb4[e] + (long)m * spec4);
@@ -628,7 +658,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     for (int e = 0; e < E; ++e) hbi[i][e] = pool4 + (((long)ent[i] * E + e) * M) * spec4 + (long)r * V + f;
 #pragma unroll 2
                 for (int m = m0; m < m1; ++m) {
-                    const float4 xn = __ldcg(xslot(-m - 1));
+                    const float4 xn = xnext();
 #pragma unroll
                     for (int i = 0; i < JH; ++i)
 #pragma unroll
@@ -734,11 +764,15 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         }
         // history for the next block = last input hop of this block
         __syncthreads();
-        for (int i = tid; i < L; i += NT) s_xin[i] = s_xin[(size_t)jb * L + i];
+        for (int i = tid; i < L; i += NT) xnxt[i] = xcur[(size_t)jb * L + i];
+        float* t = xcur;
+        xcur = xnxt;
+        xnxt = t;
         block_sync(P);  // peers done reading this CTA's Y slices / time-domain frames
     }
+    asm volatile("cp.async.wait_all;\n" ::);
     if (r == 0)
-        for (int i = tid; i < L; i += NT) p.hist[(long)s * L + i] = s_xin[i];
+        for (int i = tid; i < L; i += NT) p.hist[(long)s * L + i] = xcur[i];
     for (int i = tid; i < E * 3 * Lp; i += NT) {
         const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
         p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u] = s_ola[i];
