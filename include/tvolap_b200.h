@@ -158,9 +158,11 @@ int tvolap_set_host_async(tvolap_engine* e, int enable);
 int tvolap_set_profiling(tvolap_engine* e, int enable);
 int tvolap_kernel_time(tvolap_engine* e, double* total_ms, long* launches);
 
-/* Launch configuration chosen for this engine: CTAs per source (cluster size P) and threads per CTA. */
+/* Launch configuration: CTAs per source (thread-block cluster size) of the multi-hop (blocked)
+ * kernel and threads per CTA of the one-hop kernel. */
 int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* threads_per_cta);
-/* Override P (1, 2, 4 or 8) and threads per CTA (128..1024); 0 keeps the current value. */
+/* Override the cluster size P (1, 2, 4 or 8; both kernels) and the one-hop kernel's threads per CTA
+ * (32..1024); 0 keeps the current value. */
 int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_per_cta);
 
 /*

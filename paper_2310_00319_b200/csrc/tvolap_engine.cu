@@ -174,6 +174,8 @@ struct tvolap_engine {
     bool host_async = false;  // pinned host I/O returns before completion
     int P = 1, NT = 256;           // streaming (one hop at a time) kernel
     int JH = 4, QB = 1, NTB = 256;   // hop-blocked kernel: 2*JH hops per block, QB partition groups
+    int PB = 1;                      // hop-blocked kernel: CTAs (cluster size) per source
+    bool geometry_fixed = false;     // set by tvolap_set_launch_config / set_block_config / env
     long D = 0;                      // delay-line slots per parity (M + kMaxJH)
     long block_min = 4;              // process_hops calls with >= block_min hops use the blocked kernel
     uint64_t fwd = 0, inv = 0, macs = 0, launches = 0;
@@ -214,13 +216,31 @@ void pick_launch_config(tvolap_engine* e) {
     const int ep = env_int("TVOLAP_P", 0), et = env_int("TVOLAP_NT", 0);
     if (ep > 0) e->P = ep;
     if (et > 0) e->NT = et;
-    e->JH = env_int("TVOLAP_JH", 4);
     e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
 void pick_block_geometry(tvolap_engine* e) {
-    const long W = e->N / e->P;
+    // Heuristic from the launch sweep (scripts/sweep_launch.py, profiles/): filter-set engines
+    // want ~128+ CTAs and the longest block that fits; long hops want the largest cluster (the
+    // per-CTA spectrum slice shrinks, two CTAs fit per SM); bank engines one CTA per source.
+    if (!e->geometry_fixed) {
+        long pb = 1;
+        const long cap = std::min<long>(8, e->L);
+        if (e->bank) {
+            while (pb < cap && e->S * pb < 256) pb *= 2;
+            e->JH = e->E == 2 ? 2 : 4;
+        } else {
+            while (pb < cap && e->S * pb < 128) pb *= 2;
+            if (e->L >= 512) pb = cap;
+            e->JH = e->L >= 512 ? 4 : 8;
+        }
+        e->PB = (int)pb;
+        const int eb = env_int("TVOLAP_PB", 0), ej = env_int("TVOLAP_JH", 0);
+        if (eb > 0) e->PB = eb;
+        if (ej > 0) e->JH = ej;
+    }
+    const long W = e->N / e->PB;
     e->NTB = 256;
     e->QB = 1;
     if (W < e->NTB) {
@@ -231,7 +251,7 @@ void pick_block_geometry(tvolap_engine* e) {
         }
     }
     if (e->NTB < 32) e->NTB = 32, e->QB = (int)std::max<long>(1, 32 / W);
-    while (e->JH > 1 && tvb::block_kernel_smem_bytes((int)e->L, e->P, (int)e->E, e->JH, e->QB, e->NTB) > 227 * 1024)
+    while (e->JH > 1 && tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, e->JH, e->QB, e->NTB) > 227 * 1024)
         e->JH /= 2;
 }
 
@@ -321,7 +341,8 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.M = (int)e->M;
     p.D = (int)e->D;
     p.S = (int)e->S;
-    p.P = e->P;
+    const bool blocked = n >= e->block_min;
+    p.P = blocked ? e->PB : e->P;
     p.hop0 = hop0;
     p.n_hops = (int)n;
     p.in = in;
@@ -351,7 +372,7 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
         ++e->prof_used;
         CK(cudaEventRecord(t0, e->stream));
     }
-    if (n >= e->block_min)
+    if (blocked)
         CK(tvb::launch_block_kernel(p, (int)e->E, e->JH, e->QB, e->NTB, e->stream));
     else
         CK(tvb::launch_hop_kernel(p, (int)e->E, e->NT, e->stream));
@@ -575,6 +596,7 @@ int tvolap_create_bank(tvolap_engine** out, int device, long hop, long sources, 
             init_common(e, device, hop, sources, ears, M);
             e->bank = true;
             e->n_bank = n_bank;
+            pick_block_geometry(e);
             const long rows = n_bank * ears;
             e->pool = dalloc<float2>((size_t)rows * M * e->N);
             const float* src = stage_ir(e, bank_ir, (size_t)rows * ir_length, e->stream);
@@ -748,7 +770,7 @@ int tvolap_synchronize(tvolap_engine* e) {
 
 int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* threads_per_cta) {
     if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
-    if (ctas_per_source) *ctas_per_source = e->P;
+    if (ctas_per_source) *ctas_per_source = e->PB;
     if (threads_per_cta) *threads_per_cta = e->NT;
     return TVOLAP_OK;
 }
@@ -761,6 +783,10 @@ int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_
         validate_launch(e, P, NT);
         e->P = P;
         e->NT = NT;
+        if (ctas_per_source > 0) {
+            e->PB = P;
+            e->geometry_fixed = true;
+        }
         pick_block_geometry(e);
     });
 }
@@ -772,9 +798,10 @@ int tvolap_set_block_config(tvolap_engine* e, int hops_per_block, long block_min
             if (hops_per_block != 2 && hops_per_block != 4 && hops_per_block != 8 && hops_per_block != 16)
                 throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hops per block must be 2, 4, 8 or 16"};
             const int jh = hops_per_block / 2;
-            if (tvb::block_kernel_smem_bytes((int)e->L, e->P, (int)e->E, jh, e->QB, e->NTB) > 227 * 1024)
+            if (tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, jh, e->QB, e->NTB) > 227 * 1024)
                 throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hop block does not fit in shared memory"};
             e->JH = jh;
+            e->geometry_fixed = true;
         }
         if (block_min > 0) e->block_min = block_min;
     });
