@@ -251,7 +251,7 @@ void pick_block_geometry(tvolap_engine* e) {
         }
     }
     if (e->NTB < 32) e->NTB = 32, e->QB = (int)std::max<long>(1, 32 / W);
-    while (e->JH > 1 && tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, e->JH, e->QB, e->NTB) > 227 * 1024)
+    while (e->JH > 1 && tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, e->JH, e->bank, e->NTB) > 227 * 1024)
         e->JH /= 2;
 }
 
@@ -798,7 +798,7 @@ int tvolap_set_block_config(tvolap_engine* e, int hops_per_block, long block_min
             if (hops_per_block != 2 && hops_per_block != 4 && hops_per_block != 8 && hops_per_block != 16)
                 throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hops per block must be 2, 4, 8 or 16"};
             const int jh = hops_per_block / 2;
-            if (tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, jh, e->QB, e->NTB) > 227 * 1024)
+            if (tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, jh, e->bank, e->NTB) > 227 * 1024)
                 throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hop block does not fit in shared memory"};
             e->JH = jh;
             e->geometry_fixed = true;

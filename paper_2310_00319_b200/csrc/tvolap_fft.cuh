@@ -23,65 +23,127 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
-// Stockham FFT of N complex points (N a power of two >= 2) held in `a`,
-// using `b` as the ping-pong buffer. tw[t] = e^{-2 pi i t / N}, t < N.
-// INV selects the conjugate-twiddle (unscaled) inverse. When `prune` is set the
-// input's upper half a[N/2..N) is taken as zero and never read (the engine's
-// 4L block is zero-padded past 2L, proj/src/engine.cpp:77-80). All threads of
-// the CTA must call this (it contains __syncthreads); returns the buffer that
-// holds the result in natural order.
+// Radix of the Stockham stage that starts at sub-transform length Ns (8, then 4, then 2).
+__host__ __device__ __forceinline__ int fft_radix(int N, int Ns) {
+    const int rem = N / Ns;
+    return (rem & 7) == 0 ? 8 : ((rem & 3) == 0 ? 4 : 2);
+}
+
+// Number of Stockham stages for length N (decides which ping-pong buffer holds the result).
+__host__ __device__ __forceinline__ int fft_stage_count(int N) {
+    int k = 0;
+    for (int Ns = 1; Ns < N; Ns *= fft_radix(N, Ns)) ++k;
+    return k;
+}
+
 template <bool INV>
-__device__ float2* fft_stockham(float2* a, float2* b, int N, const float2* __restrict__ tw, bool prune, int tid,
-                                int nthreads) {
+__device__ __forceinline__ float2 twmul(float2 v, float2 w) {
+    return INV ? cmulc(v, w) : cmul(v, w);
+}
+
+// In-register 4-point DFT (sign -1 forward, +1 inverse).
+template <bool INV>
+__device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2& v3) {
+    const float2 a0 = cadd(v0, v2), a1 = csub(v0, v2);
+    const float2 a2 = cadd(v1, v3), a3 = csub(v1, v3);
+    v0 = cadd(a0, a2);
+    v2 = csub(a0, a2);
+    if (INV) {  // y1 = a1 + i a3, y3 = a1 - i a3
+        v1 = make_float2(a1.x - a3.y, a1.y + a3.x);
+        v3 = make_float2(a1.x + a3.y, a1.y - a3.x);
+    } else {    // y1 = a1 - i a3, y3 = a1 + i a3
+        v1 = make_float2(a1.x + a3.y, a1.y - a3.x);
+        v3 = make_float2(a1.x - a3.y, a1.y + a3.x);
+    }
+}
+
+// In-register 8-point DFT: radix-2 split n = n1 + 4 n2, then two 4-point DFTs
+// (even outputs from b0..b3, odd outputs from W8^n1 * b(n1+4)).
+template <bool INV>
+__device__ __forceinline__ void dft8(float2 (&v)[8]) {
+    constexpr float c = 0.70710678118654752440f;
+    float2 b[8];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+        b[n] = cadd(v[n], v[n + 4]);
+        b[n + 4] = csub(v[n], v[n + 4]);
+    }
+    // W8^1, W8^2, W8^3 (conjugated for the inverse)
+    if (INV) {
+        b[5] = make_float2((b[5].x - b[5].y) * c, (b[5].x + b[5].y) * c);
+        b[6] = make_float2(-b[6].y, b[6].x);
+        b[7] = make_float2(-(b[7].x + b[7].y) * c, (b[7].x - b[7].y) * c);
+    } else {
+        b[5] = make_float2((b[5].x + b[5].y) * c, (b[5].y - b[5].x) * c);
+        b[6] = make_float2(b[6].y, -b[6].x);
+        b[7] = make_float2((b[7].y - b[7].x) * c, -(b[7].x + b[7].y) * c);
+    }
+    dft4<INV>(b[0], b[1], b[2], b[3]);
+    dft4<INV>(b[4], b[5], b[6], b[7]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = b[k];
+        v[2 * k + 1] = b[k + 4];
+    }
+}
+
+// Batched Stockham FFT of `nf` length-N transforms stored back to back in `a`
+// (N a power of two >= 2), `b` the ping-pong buffer. tw[t] = e^{-2 pi i t / N}.
+// Radix-8 stages (radix-4/2 for the remainder): each thread keeps one butterfly's
+// 8 points in registers, so a 512-point transform is 3 shared-memory passes.
+// When `prune` is set the upper half of every input is taken as zero and never
+// read (the engine's 4L block is zero-padded past 2L, proj/src/engine.cpp:77-80).
+// All threads of the CTA must call this; returns the buffer holding the result.
+template <bool INV>
+__device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* __restrict__ tw, bool prune, int tid,
+                             int nthreads) {
     float2* src = a;
     float2* dst = b;
     for (int Ns = 1; Ns < N;) {
-        const int R = ((N / Ns) & 3) == 0 ? 4 : 2;
-        const int nb = N / R;       // butterflies this stage
-        const int stride = nb;      // input stride between the R legs
+        const int R = fft_radix(N, Ns);
+        const int nb = N / R;
         const int tstep = N / (Ns * R);
-        const bool zero_hi = prune && Ns == 1;
-        for (int j = tid; j < nb; j += nthreads) {
+        const bool zero_hi = prune && Ns == 1;  // legs r >= R/2 read the zero upper half
+        for (int jj = tid; jj < nb * nf; jj += nthreads) {
+            const int f = jj / nb, j = jj - f * nb;
+            const float2* sf = src + (size_t)f * N;
+            float2* df = dst + (size_t)f * N;
             const int k = j & (Ns - 1);
             const int idxD = (j - k) * R + k;
-            if (R == 4) {
-                float2 v0 = src[j];
-                float2 v1 = src[j + stride];
-                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : src[j + 2 * stride];
-                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : src[j + 3 * stride];
+            if (R == 8) {
+                float2 v[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) v[r] = (zero_hi && r >= 4) ? make_float2(0.f, 0.f) : sf[j + r * nb];
                 if (Ns > 1) {
                     const int t1 = k * tstep;
-                    const float2 w1 = tw[t1], w2 = tw[2 * t1], w3 = tw[3 * t1];
-                    if (INV) {
-                        v1 = cmulc(v1, w1);
-                        v2 = cmulc(v2, w2);
-                        v3 = cmulc(v3, w3);
-                    } else {
-                        v1 = cmul(v1, w1);
-                        v2 = cmul(v2, w2);
-                        v3 = cmul(v3, w3);
-                    }
+#pragma unroll
+                    for (int r = 1; r < 8; ++r) v[r] = twmul<INV>(v[r], tw[r * t1]);
                 }
-                const float2 a0 = cadd(v0, v2), a1 = csub(v0, v2);
-                const float2 a2 = cadd(v1, v3), a3 = csub(v1, v3);
-                dst[idxD] = cadd(a0, a2);
-                dst[idxD + 2 * Ns] = csub(a0, a2);
-                if (INV) {  // y1 = a1 + i a3, y3 = a1 - i a3
-                    dst[idxD + Ns] = make_float2(a1.x - a3.y, a1.y + a3.x);
-                    dst[idxD + 3 * Ns] = make_float2(a1.x + a3.y, a1.y - a3.x);
-                } else {    // y1 = a1 - i a3, y3 = a1 + i a3
-                    dst[idxD + Ns] = make_float2(a1.x + a3.y, a1.y - a3.x);
-                    dst[idxD + 3 * Ns] = make_float2(a1.x - a3.y, a1.y + a3.x);
-                }
-            } else {
-                float2 v0 = src[j];
-                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : src[j + stride];
+                dft8<INV>(v);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) df[idxD + r * Ns] = v[r];
+            } else if (R == 4) {
+                float2 v0 = sf[j];
+                float2 v1 = sf[j + nb];
+                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 2 * nb];
+                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 3 * nb];
                 if (Ns > 1) {
-                    const float2 w1 = tw[k * tstep];
-                    v1 = INV ? cmulc(v1, w1) : cmul(v1, w1);
+                    const int t1 = k * tstep;
+                    v1 = twmul<INV>(v1, tw[t1]);
+                    v2 = twmul<INV>(v2, tw[2 * t1]);
+                    v3 = twmul<INV>(v3, tw[3 * t1]);
                 }
-                dst[idxD] = cadd(v0, v1);
-                dst[idxD + Ns] = csub(v0, v1);
+                dft4<INV>(v0, v1, v2, v3);
+                df[idxD] = v0;
+                df[idxD + Ns] = v1;
+                df[idxD + 2 * Ns] = v2;
+                df[idxD + 3 * Ns] = v3;
+            } else {
+                float2 v0 = sf[j];
+                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[j + nb];
+                if (Ns > 1) v1 = twmul<INV>(v1, tw[k * tstep]);
+                df[idxD] = cadd(v0, v1);
+                df[idxD + Ns] = csub(v0, v1);
             }
         }
         __syncthreads();
@@ -91,6 +153,13 @@ __device__ float2* fft_stockham(float2* a, float2* b, int N, const float2* __res
         Ns *= R;
     }
     return src;
+}
+
+// Single transform (nf = 1).
+template <bool INV>
+__device__ float2* fft_stockham(float2* a, float2* b, int N, const float2* __restrict__ tw, bool prune, int tid,
+                                int nthreads) {
+    return fft_batch<INV>(a, b, N, 1, tw, prune, tid, nthreads);
 }
 
 // Untangle bin k (0 <= k <= N) of the real 2N-point transform from the

@@ -35,7 +35,7 @@ size_t hop_kernel_smem_bytes(int L, int P, int E, int threads);
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
 
 // Hop-blocked variant (2*JH hops per block, Q partition groups; threads == Q * (2L/P) when 2L/P < threads).
-size_t block_kernel_smem_bytes(int L, int P, int E, int JH, int Q, int threads);
+size_t block_kernel_smem_bytes(int L, int P, int E, int JH, bool bank, int threads);
 cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int threads, cudaStream_t stream);
 
 // K4: partition `rows` time-domain IRs (ir[row * ir_stride + n], n < ir_len) into

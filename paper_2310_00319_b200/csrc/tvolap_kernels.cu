@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
 // ============================================================================
 struct BlockLayout {
     size_t tw, pk, win, xin, fa, fb, yb, red, ola, total;
-    __host__ __device__ BlockLayout(int L, int P, int E, int J, int Q, int threads) {
+    // bank: per-parity MAC mapping (threads / 2V partition groups); else unified for J <= 8 (threads / V).
+    __host__ __device__ BlockLayout(int L, int P, int E, int J, bool bank, int threads) {
         const size_t N = 2 * (size_t)L;
         const size_t fpc = (J + P - 1) / P;  // frames owned per CTA
         const size_t Np = N / P;
@@ -287,79 +288,14 @@ struct BlockLayout {
         yb = align16(fb + fpc * E * N * sizeof(float2));
         red = align16(yb + (size_t)J * E * Np * sizeof(float2));
         const size_t V = Np / 2;
-        const size_t qmax = V < (size_t)threads ? threads / V : 1;  // unified mapping: threads / V groups
+        const bool unified = !bank && J <= 8;
+        const size_t W = unified ? V : 2 * V;
+        const size_t qmax = W < (size_t)threads ? threads / W : 1;
         const size_t red_bytes = qmax > 1 ? qmax * J * E * V * sizeof(float4) : 0;
-        (void)Q;
         ola = align16(red + red_bytes);
         total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
     }
 };
-
-// Batched Stockham over `nf` transforms of length N stored back to back.
-template <bool INV>
-__device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* __restrict__ tw, bool prune, int tid,
-                             int nthreads) {
-    float2* src = a;
-    float2* dst = b;
-    for (int Ns = 1; Ns < N;) {
-        const int R = ((N / Ns) & 3) == 0 ? 4 : 2;
-        const int nb = N / R;
-        const int tstep = N / (Ns * R);
-        const bool zero_hi = prune && Ns == 1;
-        for (int jj = tid; jj < nb * nf; jj += nthreads) {
-            const int f = jj / nb, j = jj - f * nb;
-            const float2* sf = src + (size_t)f * N;
-            float2* df = dst + (size_t)f * N;
-            const int k = j & (Ns - 1);
-            const int idxD = (j - k) * R + k;
-            if (R == 4) {
-                float2 v0 = sf[j];
-                float2 v1 = sf[j + nb];
-                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 2 * nb];
-                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 3 * nb];
-                if (Ns > 1) {
-                    const int t1 = k * tstep;
-                    const float2 w1 = tw[t1], w2 = tw[2 * t1], w3 = tw[3 * t1];
-                    if (INV) {
-                        v1 = cmulc(v1, w1);
-                        v2 = cmulc(v2, w2);
-                        v3 = cmulc(v3, w3);
-                    } else {
-                        v1 = cmul(v1, w1);
-                        v2 = cmul(v2, w2);
-                        v3 = cmul(v3, w3);
-                    }
-                }
-                const float2 a0 = cadd(v0, v2), a1 = csub(v0, v2);
-                const float2 a2 = cadd(v1, v3), a3 = csub(v1, v3);
-                df[idxD] = cadd(a0, a2);
-                df[idxD + 2 * Ns] = csub(a0, a2);
-                if (INV) {
-                    df[idxD + Ns] = make_float2(a1.x - a3.y, a1.y + a3.x);
-                    df[idxD + 3 * Ns] = make_float2(a1.x + a3.y, a1.y - a3.x);
-                } else {
-                    df[idxD + Ns] = make_float2(a1.x + a3.y, a1.y - a3.x);
-                    df[idxD + 3 * Ns] = make_float2(a1.x - a3.y, a1.y + a3.x);
-                }
-            } else {
-                float2 v0 = sf[j];
-                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[j + nb];
-                if (Ns > 1) {
-                    const float2 w1 = tw[k * tstep];
-                    v1 = INV ? cmulc(v1, w1) : cmul(v1, w1);
-                }
-                df[idxD] = cadd(v0, v1);
-                df[idxD + Ns] = csub(v0, v1);
-            }
-        }
-        __syncthreads();
-        float2* t = src;
-        src = dst;
-        dst = t;
-        Ns *= R;
-    }
-    return src;
-}
 
 __device__ __forceinline__ void block_sync(int P) {
     if (P > 1)
@@ -379,7 +315,8 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     const int tid = threadIdx.x, NT = blockDim.x;
     const int s = blockIdx.x / P;
     const int r = blockIdx.x % P;
-    const BlockLayout lay(L, P, E, J, Q, NT);
+    const BlockLayout lay(L, P, E, J, BANK, NT);
+    (void)Q;
     float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
     float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
     float* s_win = reinterpret_cast<float*>(smem + lay.win);
@@ -717,8 +654,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         __syncthreads();
         if (nt > 0) fft_batch<true>(s_fb, s_fa, N, nt, s_tw, false, tid, NT);
         // the result buffer depends only on the stage count (same in every CTA of the cluster)
-        int stages = 0;
-        for (int Ns = 1; Ns < N; Ns *= (((N / Ns) & 3) == 0 ? 4 : 2)) ++stages;
+        const int stages = fft_stage_count(N);
         const float* ytd = reinterpret_cast<const float*>((stages & 1) ? s_fa : s_fb);
         // time-domain frame (f, e) of this CTA = ytd[(f * E + e) * 2N ...] (unscaled)
         block_sync(P);  // all frames' time-domain blocks ready
@@ -920,13 +856,13 @@ int fft_threads(int N) { return std::max(32, std::min(256, N / 4)); }
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int threads) { return SmemLayout(L, P, E, threads).total; }
 
-size_t block_kernel_smem_bytes(int L, int P, int E, int JH, int Q, int threads) {
-    return BlockLayout(L, P, E, 2 * JH, Q, threads).total;
+size_t block_kernel_smem_bytes(int L, int P, int E, int JH, bool bank, int threads) {
+    return BlockLayout(L, P, E, 2 * JH, bank, threads).total;
 }
 
 template <int E, int JH, bool BANK>
 static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaStream_t stream) {
-    const size_t smem = block_kernel_smem_bytes(p.L, p.P, E, JH, Q, threads);
+    const size_t smem = block_kernel_smem_bytes(p.L, p.P, E, JH, BANK, threads);
     void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH, BANK>;
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
