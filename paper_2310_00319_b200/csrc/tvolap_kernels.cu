@@ -719,32 +719,38 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
 __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows, const float* __restrict__ ir,
                                                         long ir_stride, long ir_len, float2* __restrict__ pool,
                                                         long row0, const float2* __restrict__ tw,
-                                                        const float2* __restrict__ pk) {
+                                                        const float2* __restrict__ pk, int nf) {
+    // nf partitions per CTA iteration through one batched FFT (fewer barriers per transform)
     extern __shared__ __align__(16) unsigned char smem[];
     const int N = 2 * L, tid = threadIdx.x, NT = blockDim.x;
     float2* s_tw = reinterpret_cast<float2*>(smem);
     float2* s_pk = s_tw + N;
     float2* s_fa = s_pk + N + 2;
-    float2* s_fb = s_fa + N;
+    float2* s_fb = s_fa + (size_t)nf * N;
     for (int i = tid; i < N; i += NT) s_tw[i] = tw[i];
     for (int i = tid; i <= N; i += NT) s_pk[i] = pk[i];
     __syncthreads();
     const long tasks = rows * M;
-    for (long task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const long row = task / M;
-        const int m = (int)(task % M);
-        const float* h = ir + row * ir_stride;
-        const long base = (long)m * N;
-        for (int j = tid; j < L; j += NT) {
-            const long i0 = base + 2 * j;
+    for (long t0 = (long)blockIdx.x * nf; t0 < tasks; t0 += (long)gridDim.x * nf) {
+        const int nt = (int)min((long)nf, tasks - t0);
+        for (int i = tid; i < nt * L; i += NT) {
+            const int f = i / L, j = i - f * L;
+            const long task = t0 + f;
+            const long row = task / M;
+            const long i0 = (task % M) * N + 2 * j;
+            const float* h = ir + row * ir_stride;
             const float a = i0 < ir_len ? h[i0] : 0.f;
             const float b = i0 + 1 < ir_len ? h[i0 + 1] : 0.f;
-            s_fa[j] = make_float2(a, b);
+            s_fa[(size_t)f * N + j] = make_float2(a, b);
         }
         __syncthreads();
-        const float2* Z = fft_stockham<false>(s_fa, s_fb, N, s_tw, true, tid, NT);
-        float2* outp = pool + ((row0 + row) * M + m) * N;
-        for (int kk = tid; kk < N; kk += NT) outp[kk] = untangle_packed(Z, N, kk, s_pk);
+        const float2* Z = fft_batch<false>(s_fa, s_fb, N, nt, s_tw, true, tid, NT);
+        for (int i = tid; i < nt * N; i += NT) {
+            const int f = i / N, kk = i - f * N;
+            const long task = t0 + f;
+            const long row = task / M;
+            pool[((row0 + row) * M + task % M) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
+        }
         __syncthreads();
     }
 }
@@ -937,13 +943,14 @@ cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
                              long row0, const float2* tw, const float2* pk, cudaStream_t stream) {
     const int N = 2 * L;
-    const int threads = fft_threads(N);
-    const size_t smem = (size_t)(4 * N + 2) * sizeof(float2);
+    const int threads = 256;
+    const long tasks = rows * M;
+    const int nf = (int)std::max<long>(1, std::min<long>({8L, 32768L / (16L * N) > 0 ? 32768L / (16L * N) : 1L, tasks}));
+    const size_t smem = (size_t)(2 * N + 2 + 2 * (size_t)nf * N) * sizeof(float2);
     cudaError_t err = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    const long tasks = rows * M;
-    const int grid = (int)std::max<long>(1, std::min<long>(tasks, 148L * 8));
-    partition_kernel<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk);
+    const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 4));
+    partition_kernel<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, nf);
     return cudaGetLastError();
 }
 

@@ -18,7 +18,7 @@ from paper_2310_00319_b200.tvolap import TvolapBankEngine, TvolapEngine, partiti
 HOPS = {"C1": 3750, "C2": 1024, "C3": 512, "C4": 128, "C5": 1024}
 
 
-def run(name, Ps, JHs, reps=3):
+def run(name, Ps, JHs, reps=3, period=0, exchange=False):
     cfg = W.CONFIGS[name]
     H, L, S = HOPS[name], cfg.hop, cfg.sources
     lib = T.lib()
@@ -35,6 +35,17 @@ def run(name, Ps, JHs, reps=3):
     else:
         eng = TvolapEngine(partition(W.fresh_irs(cfg, 0)[:, 0, :].T, L, cfg.partitions))
         distinct = S
+        irs = torch.from_numpy(np.stack([W.fresh_irs(cfg, k)[:, 0, :] for k in range(2)])).cuda() if exchange else None
+
+    def step():
+        if not period:
+            eng.process_hops(x, out=out, schedule=sched)
+            return
+        for h0 in range(0, H, period):
+            if exchange:
+                eng.exchange_ir(irs[(h0 // period) & 1])
+            sl = slice(h0 * L, min(H, h0 + period) * L)
+            eng.process_hops(x[:, sl], out=out[:, sl], schedule=None if sched is None else sched[h0:h0 + period])
     st = torch.cuda.Stream()
     eng.set_stream(st.cuda_stream)
     bph = W.bytes_per_hop(cfg, distinct_filters=distinct)
@@ -52,12 +63,12 @@ def run(name, Ps, JHs, reps=3):
                 print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "skip": str(e)}), flush=True)
                 continue
             try:
-                eng.process_hops(x, out=out, schedule=sched)
+                step()
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(st)
                 for _ in range(reps):
-                    eng.process_hops(x, out=out, schedule=sched)
+                    step()
                 b.record(st)
                 b.synchronize()
                 ms = a.elapsed_time(b) / reps
@@ -65,7 +76,8 @@ def run(name, Ps, JHs, reps=3):
                 print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "error": str(e)}), flush=True)
                 continue
             j, bm, q = eng.block_config()
-            print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "Q": q, "us_per_hop": 1e3 * ms / H,
+            print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "Q": q, "period": period, "exchange": exchange,
+                              "us_per_hop": 1e3 * ms / H,
                               "GBps_alg": bph * H / (ms / 1e3) / 1e9, "frac": bph * H / (ms / 1e3) / 1e9 / 6542.1}),
                   flush=True)
 
@@ -79,8 +91,10 @@ if __name__ == "__main__":
     ap.add_argument("--J", type=int, nargs="*", default=[0, 2, 4, 8, 16], help="hops per block (0 = streaming)")
     ap.add_argument("--hops", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--period", type=int, default=0, help="hops per process_hops call (0 = one call)")
+    ap.add_argument("--exchange", action="store_true", help="exchange_filter before every call (fresh configs)")
     a = ap.parse_args()
     for n in a.configs:
         if a.hops:
             HOPS[n] = a.hops
-        run(n, a.P, [j // 2 for j in a.J], reps=a.reps)
+        run(n, a.P, [j // 2 for j in a.J], reps=a.reps, period=a.period, exchange=a.exchange)
