@@ -276,7 +276,10 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     e->M = partitions;
     e->D = partitions + kMaxJH;
     CK(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    // staged-filter transforms sit on the critical path of the next hop: schedule them first
+    CK(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, prio_hi));
     CK(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
     e->stream = e->own;

@@ -942,14 +942,17 @@ cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream
 
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
                              long row0, const float2* tw, const float2* pk, cudaStream_t stream) {
+    // Small CTAs (2 partitions, one radix-8 butterfly per thread per stage), enough of them to
+    // cover every task in about one wave, so the transform of a staged set finishes quickly
+    // next to the running hop kernel.
     const int N = 2 * L;
-    const int threads = 256;
     const long tasks = rows * M;
-    const int nf = (int)std::max<long>(1, std::min<long>({8L, 32768L / (16L * N) > 0 ? 32768L / (16L * N) : 1L, tasks}));
+    const int nf = (int)std::min<long>(2, tasks);
+    const int threads = std::max(32, std::min(256, nf * N / 8));
     const size_t smem = (size_t)(2 * N + 2 + 2 * (size_t)nf * N) * sizeof(float2);
     cudaError_t err = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 4));
+    const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 16));
     partition_kernel<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, nf);
     return cudaGetLastError();
 }
