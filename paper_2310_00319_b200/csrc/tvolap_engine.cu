@@ -136,6 +136,9 @@ T* dalloc(size_t count) {
 }
 
 constexpr int kMaxJH = 8;  // largest hop block / 2 (ring slack per parity)
+// Filter-set slots: active + staged + one more, so the transform of the next staged set
+// may start while the two previous periods' hop kernels still read their sets.
+constexpr int kSlots = 3;
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -151,7 +154,7 @@ struct tvolap_engine {
     long n_bank = 0;
     cudaStream_t own = nullptr, stream = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_side = nullptr, ev_main = nullptr, ev_start = nullptr;
-    cudaEvent_t ev_slot[2] = {};  // last hop kernel that read filter slot 0 / 1
+    cudaEvent_t ev_slot[kSlots] = {};  // last hop kernel that read each filter slot
     float2 *ring = nullptr, *pool = nullptr, *tw = nullptr, *pk = nullptr;
     float *win = nullptr, *hist = nullptr, *ola = nullptr;
     int* d_sel = nullptr;
@@ -193,7 +196,7 @@ struct tvolap_engine {
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
         for (cudaEvent_t ev : {ev_side, ev_main, ev_start, ev_in[0], ev_in[1], ev_k[0], ev_k[1], ev_o[0], ev_o[1],
-                                ev_slot[0], ev_slot[1]})
+                                ev_slot[0], ev_slot[1], ev_slot[2]})
             if (ev) cudaEventDestroy(ev);
         for (auto& pr : prof_events) {
             cudaEventDestroy(pr.first);
@@ -284,7 +287,8 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     CK(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
     e->stream = e->own;
     for (cudaEvent_t* ev : {&e->ev_side, &e->ev_main, &e->ev_start, &e->ev_in[0], &e->ev_in[1], &e->ev_k[0],
-                            &e->ev_k[1], &e->ev_o[0], &e->ev_o[1], &e->ev_slot[0], &e->ev_slot[1]})
+                            &e->ev_k[1], &e->ev_o[0], &e->ev_o[1], &e->ev_slot[0], &e->ev_slot[1],
+                            &e->ev_slot[2]})
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     Tables t(e->N);
     std::vector<float> w = hann(hop);
@@ -327,7 +331,7 @@ void latch(tvolap_engine* e) {  // engine.cpp:54-58
     std::lock_guard<std::mutex> lock(e->mu);
     if (e->pending) {
         CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
-        e->active ^= 1;
+        e->active = (e->active + 1) % kSlots;
         e->pending = false;
     }
     if (e->sel_staged) {
@@ -563,8 +567,8 @@ int tvolap_create(tvolap_engine** out, int device, long hop, long channels, long
         try {
             init_common(e, device, hop, channels, 1, M);
             const size_t slot = (size_t)channels * M * e->N;
-            e->pool = dalloc<float2>(2 * slot);
-            CK(cudaMemsetAsync(e->pool, 0, 2 * slot * sizeof(float2), e->stream));
+            e->pool = dalloc<float2>(kSlots * slot);
+            CK(cudaMemsetAsync(e->pool, 0, kSlots * slot * sizeof(float2), e->stream));
             const float* src = stage_ir(e, ir, (size_t)channels * ir_length, e->stream);
             CK(tvb::launch_partition((int)hop, (int)M, channels, src, ir_length, ir_length, e->pool, 0, e->tw, e->pk,
                                      e->stream));
@@ -666,7 +670,7 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
     return guarded([&] {
         CK(cudaSetDevice(e->device));
         std::lock_guard<std::mutex> lock(e->mu);
-        const int target = e->active ^ 1;
+        const int target = (e->active + 1) % kSlots;  // staged slot; last staged wins
         const float* src = stage_ir(e, ir, (size_t)channels * ir_length, e->side);
         // the target slot may still be read by hops queued before the last latch
         CK(cudaStreamWaitEvent(e->side, e->ev_slot[target], 0));
