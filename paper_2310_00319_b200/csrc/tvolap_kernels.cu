@@ -952,7 +952,8 @@ cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_s
     const size_t smem = (size_t)(2 * N + 2 + 2 * (size_t)nf * N) * sizeof(float2);
     cudaError_t err = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 16));
+    // 4 CTAs per SM amortise the per-CTA twiddle-table load over several task groups
+    const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 4));
     partition_kernel<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, nf);
     return cudaGetLastError();
 }
