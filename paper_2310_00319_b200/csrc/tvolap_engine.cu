@@ -164,6 +164,17 @@ struct tvolap_engine {
     bool pending = false;
     float* d_irstage = nullptr;
     size_t irstage_cap = 0;
+    // staged replacement set, transformed by the first kernel of the next process call
+    const float* staged_ir = nullptr;
+    long staged_len = 0;
+    int staged_buf = -1;             // upload buffer holding it (-1: caller's device memory)
+    float* d_irst[2] = {};           // double-buffered host-IR uploads
+    size_t irst_cap[2] = {};
+    int irst_next = 0;
+    cudaEvent_t ev_up[2] = {}, ev_used[2] = {};  // upload landed / consuming kernel done
+    const float* launch_new_ir = nullptr;  // latched: the next launch transforms this set
+    long launch_new_len = 0;
+    int launch_buf = -1;
     // chunked host pipeline
     long chunk_hops = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
@@ -190,13 +201,14 @@ struct tvolap_engine {
         if (stream) cudaStreamSynchronize(stream);
         if (side) cudaStreamSynchronize(side);
         for (void* p : {(void*)ring, (void*)pool, (void*)tw, (void*)pk, (void*)win, (void*)hist, (void*)ola,
-                        (void*)d_sel, (void*)d_irstage, (void*)d_in[0], (void*)d_in[1], (void*)d_out[0],
+                        (void*)d_sel, (void*)d_irstage, (void*)d_irst[0], (void*)d_irst[1], (void*)d_in[0],
+                        (void*)d_in[1], (void*)d_out[0],
                         (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1]})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
         for (cudaEvent_t ev : {ev_side, ev_main, ev_start, ev_in[0], ev_in[1], ev_k[0], ev_k[1], ev_o[0], ev_o[1],
-                                ev_slot[0], ev_slot[1], ev_slot[2]})
+                                ev_slot[0], ev_slot[1], ev_slot[2], ev_up[0], ev_up[1], ev_used[0], ev_used[1]})
             if (ev) cudaEventDestroy(ev);
         for (auto& pr : prof_events) {
             cudaEventDestroy(pr.first);
@@ -288,7 +300,7 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     e->stream = e->own;
     for (cudaEvent_t* ev : {&e->ev_side, &e->ev_main, &e->ev_start, &e->ev_in[0], &e->ev_in[1], &e->ev_k[0],
                             &e->ev_k[1], &e->ev_o[0], &e->ev_o[1], &e->ev_slot[0], &e->ev_slot[1],
-                            &e->ev_slot[2]})
+                            &e->ev_slot[2], &e->ev_up[0], &e->ev_up[1], &e->ev_used[0], &e->ev_used[1]})
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     Tables t(e->N);
     std::vector<float> w = hann(hop);
@@ -330,8 +342,12 @@ const float* stage_ir(tvolap_engine* e, const float* ir, size_t count, cudaStrea
 void latch(tvolap_engine* e) {  // engine.cpp:54-58
     std::lock_guard<std::mutex> lock(e->mu);
     if (e->pending) {
-        CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+        // the first kernel of this call transforms the staged set into the next slot (K4 fused)
+        if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_up[e->staged_buf], 0));
         e->active = (e->active + 1) % kSlots;
+        e->launch_new_ir = e->staged_ir;
+        e->launch_new_len = e->staged_len;
+        e->launch_buf = e->staged_buf;
         e->pending = false;
     }
     if (e->sel_staged) {
@@ -366,6 +382,11 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.tw = e->tw;
     p.pk = e->pk;
     p.win = e->win;
+    p.new_ir = e->launch_new_ir;
+    p.new_ir_stride = e->launch_new_len;
+    p.new_ir_len = e->launch_new_len;
+    p.pool_w = e->pool;
+    p.new_entry_base = e->active * (int)e->S;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (e->profiling) {
         if (e->prof_used == e->prof_events.size()) {
@@ -386,6 +407,11 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     if (t1) CK(cudaEventRecord(t1, e->stream));
     ++e->launches;
     if (!e->bank) CK(cudaEventRecord(e->ev_slot[e->active], e->stream));
+    if (e->launch_new_ir) {
+        if (e->launch_buf >= 0) CK(cudaEventRecord(e->ev_used[e->launch_buf], e->stream));
+        e->launch_new_ir = nullptr;
+        e->launch_buf = -1;
+    }
 }
 
 void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
@@ -670,14 +696,29 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
     return guarded([&] {
         CK(cudaSetDevice(e->device));
         std::lock_guard<std::mutex> lock(e->mu);
-        const int target = (e->active + 1) % kSlots;  // staged slot; last staged wins
-        const float* src = stage_ir(e, ir, (size_t)channels * ir_length, e->side);
-        // the target slot may still be read by hops queued before the last latch
-        CK(cudaStreamWaitEvent(e->side, e->ev_slot[target], 0));
-        CK(tvb::launch_partition((int)e->L, (int)e->M, channels, src, ir_length, ir_length, e->pool,
-                                 (long)target * e->S, e->tw, e->pk, e->side));
-        ++e->launches;
-        CK(cudaEventRecord(e->ev_side, e->side));
+        // Stage only: the next process call's first kernel transforms the set (K4 fused).
+        // Device IRs are used in place; host IRs are uploaded on the side stream into one of
+        // two buffers, after the kernel that consumed that buffer last time.
+        const size_t count = (size_t)channels * ir_length;
+        if (classify(ir) == Mem::Device) {
+            e->staged_ir = ir;
+            e->staged_buf = -1;
+        } else {
+            const int b = e->irst_next;
+            e->irst_next ^= 1;
+            CK(cudaStreamWaitEvent(e->side, e->ev_used[b], 0));
+            if (e->irst_cap[b] < count) {
+                CK(cudaStreamSynchronize(e->side));
+                if (e->d_irst[b]) CK(cudaFree(e->d_irst[b]));
+                e->d_irst[b] = dalloc<float>(count);
+                e->irst_cap[b] = count;
+            }
+            CK(cudaMemcpyAsync(e->d_irst[b], ir, count * sizeof(float), cudaMemcpyHostToDevice, e->side));
+            CK(cudaEventRecord(e->ev_up[b], e->side));
+            e->staged_ir = e->d_irst[b];
+            e->staged_buf = b;
+        }
+        e->staged_len = ir_length;
         e->pending = true;  // last staged filter wins (engine.cpp:47)
     });
 }

@@ -29,6 +29,12 @@ struct HopParams {
     const float2* tw;      // e^{-2 pi i t / 2L}, t < 2L
     const float2* pk;      // e^{-2 pi i k / 4L}, k <= 2L
     const float* win;      // periodic Hann, 2L
+    // staged filter set transformed at the start of this launch (K4 fused), or new_ir == null
+    const float* new_ir;   // new_ir[s * new_ir_stride + n], n < new_ir_len
+    long new_ir_stride;
+    long new_ir_len;
+    float2* pool_w;        // writable view of pool
+    int new_entry_base;    // pool entry of source 0 for the staged set
 };
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int threads);

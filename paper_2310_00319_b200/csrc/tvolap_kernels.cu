@@ -74,6 +74,35 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 
+// K4 fused into the hop kernels: at the start of the launch that latches a staged
+// filter set, each cluster transforms its own source's new IR (partition.cpp:20-51):
+// CTA r of the cluster takes partitions m = r, r+P, ..., `cap` of them per batched
+// FFT, and writes the whole packed spectrum of each into the pool entry the MAC of
+// this launch reads. The caller synchronises the cluster before the MAC.
+__device__ void fused_partition(const HopParams& p, int s, int r, int P, float2* fa, float2* fb, int cap,
+                                const float2* tw, const float2* pk, int tid, int NT) {
+    const int L = p.L, N = 2 * L, M = p.M;
+    const float* h = p.new_ir + (long)s * p.new_ir_stride;
+    float2* dst = p.pool_w + ((long)(p.new_entry_base + s) * M) * N;
+    const int nm = r < M ? (M - r + P - 1) / P : 0;
+    for (int i0 = 0; i0 < nm; i0 += cap) {
+        const int nt = min(cap, nm - i0);
+        for (int i = tid; i < nt * L; i += NT) {
+            const int f = i / L, j = i - f * L;
+            const long idx = (long)(r + (i0 + f) * P) * N + 2 * j;
+            fa[(size_t)f * N + j] =
+                make_float2(idx < p.new_ir_len ? h[idx] : 0.f, idx + 1 < p.new_ir_len ? h[idx + 1] : 0.f);
+        }
+        __syncthreads();
+        const float2* Z = fft_batch<false>(fa, fb, N, nt, tw, true, tid, NT);
+        for (int i = tid; i < nt * N; i += NT) {
+            const int f = i / N, kk = i - f * N;
+            dst[(long)(r + (i0 + f) * P) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, pk);
+        }
+        __syncthreads();
+    }
+}
+
 template <int E>
 __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -112,6 +141,13 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
         s_ola[i] = p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u];
     }
     __syncthreads();
+    if (p.new_ir) {  // latch a staged filter set: transform it here (K4), then the whole cluster sees it
+        fused_partition(p, s, r, P, s_fa, s_fb, 1, s_tw, s_pk, tid, NT);
+        if (P > 1)
+            cg::this_cluster().sync();
+        else
+            __syncthreads();
+    }
 
     const float4* ring4 = reinterpret_cast<const float4*>(p.ring);
     const float4* pool4 = reinterpret_cast<const float4*>(p.pool);
@@ -172,10 +208,10 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const float4* he = hb + ((long)e * M + m) * spec4 + fi;
-                    h[e][0] = __ldg(he);
-                    h[e][1] = __ldg(he + G * spec4);
-                    h[e][2] = __ldg(he + 2 * G * spec4);
-                    h[e][3] = __ldg(he + 3 * G * spec4);
+                    h[e][0] = __ldcg(he);
+                    h[e][1] = __ldcg(he + G * spec4);
+                    h[e][2] = __ldcg(he + 2 * G * spec4);
+                    h[e][3] = __ldcg(he + 3 * G * spec4);
                 }
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
@@ -190,7 +226,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
             for (; m < M; m += G) {
                 const float4 x0 = __ldcg(xb + slot * spec4 + fi);
 #pragma unroll
-                for (int e = 0; e < E; ++e) cmac4(acc[e], aux[e], __ldg(hb + ((long)e * M + m) * spec4 + fi), x0);
+                for (int e = 0; e < E; ++e) cmac4(acc[e], aux[e], __ldcg(hb + ((long)e * M + m) * spec4 + fi), x0);
                 slot -= G;
                 if (slot < 0) slot += D;
             }
@@ -351,6 +387,11 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         asm volatile("cp.async.commit_group;\n" ::);
     };
     prefetch_block(xcur, 0);
+    if (p.new_ir) {  // latch a staged filter set: transform it here (K4) while block 0's input lands
+        __syncthreads();
+        fused_partition(p, s, r, P, s_fa, s_fb, ((J + P - 1) / P) * E, s_tw, s_pk, tid, NT);
+        block_sync(P);
+    }
     for (int i = tid; i < E * 3 * Lp; i += NT) {
         const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
         s_ola[i] = p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u];
@@ -453,7 +494,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                             cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
                         }
 #pragma unroll
-                        for (int e = 0; e < E; ++e) hh[u][e] = __ldg(hb4[e] + (long)(m + u) * spec4);
+                        for (int e = 0; e < E; ++e) hh[u][e] = __ldcg(hb4[e] + (long)(m + u) * spec4);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
@@ -475,7 +516,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     for (int g = 0; g < 2; ++g) cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
-                        const float4 h = __ldg(hb4[e] + (long)m * spec4);
+                        const float4 h = __ldcg(hb4[e] + (long)m * spec4);
 #pragma unroll
                         for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -561,7 +602,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     for (int u = 0; u < U; ++u) {
                         xn[u] = xnext();
 #pragma unroll
-                        for (int e = 0; e < E; ++e) hh[u][e] = __ldg(hb4[e] + (long)(m + u) * spec4);
+                        for (int e = 0; e < E; ++e) hh[u][e] = __ldcg(hb4[e] + (long)(m + u) * spec4);
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
@@ -578,7 +619,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                     const float4 xn = xnext();
 #pragma unroll
                     for (int e = 0; e < E; ++e) {
-                        const float4 h = __ldg(hb4[e] + (long)m * spec4);
+                        const float4 h = __ldcg(hb4[e] + (long)m * spec4);
 #pragma unroll
                         for (int i = 0; i < JH; ++i) cmac4(acc[i][e], aux[i][e], h, win[i]);
                     }
@@ -599,7 +640,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
 #pragma unroll
                     for (int i = 0; i < JH; ++i)
 #pragma unroll
-                        for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], __ldg(hbi[i][e] + (long)m * spec4), win[i]);
+                        for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], __ldcg(hbi[i][e] + (long)m * spec4), win[i]);
 #pragma unroll
                     for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
                     win[0] = xn;
