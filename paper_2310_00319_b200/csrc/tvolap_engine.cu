@@ -175,6 +175,8 @@ struct tvolap_engine {
     const float* launch_new_ir = nullptr;  // latched: the next launch transforms this set
     long launch_new_len = 0;
     int launch_buf = -1;
+    bool k4_side = false;            // true: transform staged sets on the side stream (overlapping hops)
+    bool staged_on_side = false;     // the pending set was transformed on the side stream
     // chunked host pipeline
     long chunk_hops = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
@@ -232,6 +234,7 @@ void pick_launch_config(tvolap_engine* e) {
     if (ep > 0) e->P = ep;
     if (et > 0) e->NT = et;
     e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
+    e->k4_side = env_int("TVOLAP_K4_SIDE", 0) != 0;
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -342,12 +345,15 @@ const float* stage_ir(tvolap_engine* e, const float* ir, size_t count, cudaStrea
 void latch(tvolap_engine* e) {  // engine.cpp:54-58
     std::lock_guard<std::mutex> lock(e->mu);
     if (e->pending) {
-        // the first kernel of this call transforms the staged set into the next slot (K4 fused)
-        if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_up[e->staged_buf], 0));
+        if (e->staged_on_side) {  // already transformed on the side stream
+            CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+        } else {  // the first kernel of this call transforms the staged set into the next slot (K4 fused)
+            if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_up[e->staged_buf], 0));
+            e->launch_new_ir = e->staged_ir;
+            e->launch_new_len = e->staged_len;
+            e->launch_buf = e->staged_buf;
+        }
         e->active = (e->active + 1) % kSlots;
-        e->launch_new_ir = e->staged_ir;
-        e->launch_new_len = e->staged_len;
-        e->launch_buf = e->staged_buf;
         e->pending = false;
     }
     if (e->sel_staged) {
@@ -719,6 +725,16 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
             e->staged_buf = b;
         }
         e->staged_len = ir_length;
+        e->staged_on_side = e->k4_side;
+        if (e->k4_side) {  // transform now on the side stream, after the last reader of the target slot
+            const int target = (e->active + 1) % kSlots;
+            CK(cudaStreamWaitEvent(e->side, e->ev_slot[target], 0));
+            CK(tvb::launch_partition((int)e->L, (int)e->M, channels, e->staged_ir, ir_length, ir_length, e->pool,
+                                     (long)target * e->S, e->tw, e->pk, e->side));
+            ++e->launches;
+            CK(cudaEventRecord(e->ev_side, e->side));
+            if (e->staged_buf >= 0) CK(cudaEventRecord(e->ev_used[e->staged_buf], e->side));
+        }
         e->pending = true;  // last staged filter wins (engine.cpp:47)
     });
 }

@@ -104,8 +104,9 @@ __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* 
         const int nb = N / R;
         const int tstep = N / (Ns * R);
         const bool zero_hi = prune && Ns == 1;  // legs r >= R/2 read the zero upper half
+        const int lgnb = 31 - __clz(nb);
         for (int jj = tid; jj < nb * nf; jj += nthreads) {
-            const int f = jj / nb, j = jj - f * nb;
+            const int f = jj >> lgnb, j = jj & (nb - 1);
             const float2* sf = src + (size_t)f * N;
             float2* df = dst + (size_t)f * N;
             const int k = j & (Ns - 1);

@@ -85,10 +85,11 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
     const float* h = p.new_ir + (long)s * p.new_ir_stride;
     float2* dst = p.pool_w + ((long)(p.new_entry_base + s) * M) * N;
     const int nm = r < M ? (M - r + P - 1) / P : 0;
+    const int lgL = 31 - __clz(L), lgN = lgL + 1;
     for (int i0 = 0; i0 < nm; i0 += cap) {
         const int nt = min(cap, nm - i0);
         for (int i = tid; i < nt * L; i += NT) {
-            const int f = i / L, j = i - f * L;
+            const int f = i >> lgL, j = i & (L - 1);
             const long idx = (long)(r + (i0 + f) * P) * N + 2 * j;
             fa[(size_t)f * N + j] =
                 make_float2(idx < p.new_ir_len ? h[idx] : 0.f, idx + 1 < p.new_ir_len ? h[idx + 1] : 0.f);
@@ -96,7 +97,7 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
         __syncthreads();
         const float2* Z = fft_batch<false>(fa, fb, N, nt, tw, true, tid, NT);
         for (int i = tid; i < nt * N; i += NT) {
-            const int f = i / N, kk = i - f * N;
+            const int f = i >> lgN, kk = i & (N - 1);
             dst[(long)(r + (i0 + f) * P) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, pk);
         }
         __syncthreads();
@@ -364,6 +365,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     float* s_ola = reinterpret_cast<float*>(smem + lay.ola);
 
     const int Np = N / P, V = Np / 2, Lp = L / P;
+    // all of L, N, P, Np, V, Lp are powers of two: index math by shifts (no runtime divisions)
+    const int lgL = 31 - __clz(L), lgN = lgL + 1, lgP = 31 - __clz(P);
+    const int lgNp = lgN - lgP, lgV = lgNp - 1, lgLp = lgL - lgP, lgN2 = lgN - 1;
     const long spec4 = N / 2;
     const int W = 2 * V;             // (parity group, float4) work items
     const int q = tid / W;           // partition group (Q groups when W < NT)
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         // ---- K1/K2: this CTA's frames (j = r, r+P, ...): window, FFT, whole spectrum into the ring.
         const int nf = jb > r ? (jb - r + P - 1) / P : 0;
         for (int i = tid; i < nf * L; i += NT) {
-            const int f = i / L, jj = i - f * L;
+            const int f = i >> lgL, jj = i & (L - 1);
             const float* xs = xcur + (size_t)(r + f * P) * L;  // (previous hop | this hop)
             s_fa[(size_t)f * N + jj] = make_float2(xs[2 * jj] * s_win[2 * jj], xs[2 * jj + 1] * s_win[2 * jj + 1]);
         }
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         if (nf > 0) {
             const float2* Z = fft_batch<false>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
             for (int i = tid; i < nf * N; i += NT) {
-                const int f = i / N, kk = i - f * N;
+                const int f = i >> lgN, kk = i & (N - 1);
                 const long h = l0 + r + f * P;
                 float2* ringw = p.ring + (((long)s * 2 + (h & 1)) * D + (h >> 1) % D) * N;
                 ringw[kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
@@ -668,7 +672,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         if (Qeff > 1) {
             __syncthreads();
             for (int i = tid; i < jb * E * V; i += NT) {
-                const int f = i % V, je = i / V;  // je = jj * E + e
+                const int f = i & (V - 1), je = i >> lgV;  // je = jj * E + e
                 float4 sum = s_red[(size_t)je * V + f];
                 for (int qq = 1; qq < Qeff; ++qq) sum = f4add(sum, s_red[((size_t)qq * J * E + je) * V + f]);
                 reinterpret_cast<float4*>(s_yb + (size_t)je * Np)[f] = sum;
@@ -679,17 +683,17 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         // ---- K5a: this CTA's frames: gather Y over DSMEM, tangle, inverse FFT.
         const int nt = nf * E;  // transforms
         for (int i = tid; i < nt * (N / 2); i += NT) {  // float4 granularity gather
-            const int t = i / (N / 2), k4 = i - t * (N / 2);
+            const int t = i >> lgN2, k4 = i & (N / 2 - 1);
             const int f = t / E, e = t - f * E;
             const int jj = r + f * P;
-            const int qsrc = (2 * k4) / Np;
+            const int qsrc = k4 >> lgV;
             const float4* src = reinterpret_cast<const float4*>(s_yb + ((size_t)jj * E + e) * Np);
             if (qsrc != r) src = cluster.map_shared_rank(src, qsrc);
             reinterpret_cast<float4*>(s_fa + (size_t)t * N)[k4] = src[k4 - qsrc * (Np / 2)];
         }
         __syncthreads();
         for (int i = tid; i < nt * N; i += NT) {
-            const int t = i / N, kk = i - t * N;
+            const int t = i >> lgN, kk = i & (N - 1);
             s_fb[(size_t)t * N + kk] = tangle_packed(s_fa + (size_t)t * N, N, kk, s_pk);
         }
         __syncthreads();
@@ -706,7 +710,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         const size_t ytd_off = (size_t)((const unsigned char*)ytd - smem);
         const float sc = 1.0f / (float)N;
         for (int i = tid; i < E * Lp; i += NT) {
-            const int e = i / Lp, u = i - e * Lp;
+            const int e = i >> lgLp, u = i & (Lp - 1);
             const int ug = r * Lp + u;
             float* A = s_ola + e * 3 * Lp;
             float a0 = A[u], a1 = A[Lp + u], a2 = A[2 * Lp + u];
@@ -714,7 +718,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
 #pragma unroll
             for (int jj = 0; jj < J; ++jj) {
                 if (jj < jb) {
-                    const int owner = jj % P, f = jj / P;
+                    const int owner = jj & (P - 1), f = jj >> lgP;
                     const float* base = reinterpret_cast<const float*>(smem + ytd_off);
                     if (owner != r) base = cluster.map_shared_rank(base, owner);
                     const float* yf = base + ((size_t)f * E + e) * 2 * N;
@@ -772,13 +776,17 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
     for (int i = tid; i <= N; i += NT) s_pk[i] = pk[i];
     __syncthreads();
     const long tasks = rows * M;
+    const int lgL = 31 - __clz(L), lgN = lgL + 1;  // L, N powers of two: shifts, no divisions
     for (long t0 = (long)blockIdx.x * nf; t0 < tasks; t0 += (long)gridDim.x * nf) {
         const int nt = (int)min((long)nf, tasks - t0);
+        const long row0t = t0 / M;  // one 64-bit division per group
+        const int m0t = (int)(t0 - row0t * M);
         for (int i = tid; i < nt * L; i += NT) {
-            const int f = i / L, j = i - f * L;
-            const long task = t0 + f;
-            const long row = task / M;
-            const long i0 = (task % M) * N + 2 * j;
+            const int f = i >> lgL, j = i & (L - 1);
+            int m = m0t + f;
+            long row = row0t;
+            while (m >= M) m -= M, ++row;
+            const long i0 = (long)m * N + 2 * j;
             const float* h = ir + row * ir_stride;
             const float a = i0 < ir_len ? h[i0] : 0.f;
             const float b = i0 + 1 < ir_len ? h[i0 + 1] : 0.f;
@@ -787,10 +795,8 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
         __syncthreads();
         const float2* Z = fft_batch<false>(s_fa, s_fb, N, nt, s_tw, true, tid, NT);
         for (int i = tid; i < nt * N; i += NT) {
-            const int f = i / N, kk = i - f * N;
-            const long task = t0 + f;
-            const long row = task / M;
-            pool[((row0 + row) * M + task % M) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
+            const int f = i >> lgN, kk = i & (N - 1);
+            pool[(row0 * M + t0 + f) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
         }
         __syncthreads();
     }
