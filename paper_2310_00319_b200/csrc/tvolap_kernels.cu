@@ -765,6 +765,7 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
                                                         long ir_stride, long ir_len, float2* __restrict__ pool,
                                                         long row0, const float2* __restrict__ tw,
                                                         const float2* __restrict__ pk, int nf) {
+    const bool vec = L >= 2 && (ir_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(ir) & 15) == 0;
     // nf partitions per CTA iteration through one batched FFT (fewer barriers per transform)
     extern __shared__ __align__(16) unsigned char smem[];
     const int N = 2 * L, tid = threadIdx.x, NT = blockDim.x;
@@ -781,16 +782,38 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
         const int nt = (int)min((long)nf, tasks - t0);
         const long row0t = t0 / M;  // one 64-bit division per group
         const int m0t = (int)(t0 - row0t * M);
-        for (int i = tid; i < nt * L; i += NT) {
-            const int f = i >> lgL, j = i & (L - 1);
-            int m = m0t + f;
-            long row = row0t;
-            while (m >= M) m -= M, ++row;
-            const long i0 = (long)m * N + 2 * j;
-            const float* h = ir + row * ir_stride;
-            const float a = i0 < ir_len ? h[i0] : 0.f;
-            const float b = i0 + 1 < ir_len ? h[i0 + 1] : 0.f;
-            s_fa[(size_t)f * N + j] = make_float2(a, b);
+        if (vec) {  // 16-byte loads: z[j], z[j+1] = (h[2j], h[2j+1]), (h[2j+2], h[2j+3])
+            const int L2 = L >> 1, lgL2 = lgL - 1;
+            for (int i = tid; i < nt * L2; i += NT) {
+                const int f = i >> lgL2, j = (i & (L2 - 1)) * 2;
+                int m = m0t + f;
+                long row = row0t;
+                while (m >= M) m -= M, ++row;
+                const long i0 = (long)m * N + 2 * j;
+                const float* h = ir + row * ir_stride;
+                float4 v;
+                if (i0 + 3 < ir_len) {
+                    v = __ldcs(reinterpret_cast<const float4*>(h + i0));
+                } else {
+                    v.x = i0 < ir_len ? h[i0] : 0.f;
+                    v.y = i0 + 1 < ir_len ? h[i0 + 1] : 0.f;
+                    v.z = i0 + 2 < ir_len ? h[i0 + 2] : 0.f;
+                    v.w = i0 + 3 < ir_len ? h[i0 + 3] : 0.f;
+                }
+                reinterpret_cast<float4*>(s_fa + (size_t)f * N)[j >> 1] = v;
+            }
+        } else {
+            for (int i = tid; i < nt * L; i += NT) {
+                const int f = i >> lgL, j = i & (L - 1);
+                int m = m0t + f;
+                long row = row0t;
+                while (m >= M) m -= M, ++row;
+                const long i0 = (long)m * N + 2 * j;
+                const float* h = ir + row * ir_stride;
+                const float a = i0 < ir_len ? h[i0] : 0.f;
+                const float b = i0 + 1 < ir_len ? h[i0 + 1] : 0.f;
+                s_fa[(size_t)f * N + j] = make_float2(a, b);
+            }
         }
         __syncthreads();
         const float2* Z = fft_batch<false>(s_fa, s_fb, N, nt, s_tw, true, tid, NT);
@@ -989,17 +1012,15 @@ cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream
 
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
                              long row0, const float2* tw, const float2* pk, cudaStream_t stream) {
-    // Small CTAs (2 partitions, one radix-8 butterfly per thread per stage), enough of them to
-    // cover every task in about one wave, so the transform of a staged set finishes quickly
-    // next to the running hop kernel.
+    // Batches of up to 8 partitions per CTA, 16-byte IR loads: enough bytes in flight to
+    // stream the time-domain IRs near HBM speed.
     const int N = 2 * L;
     const long tasks = rows * M;
-    const int nf = (int)std::min<long>(2, tasks);
+    const int nf = (int)std::max<long>(1, std::min<long>({8L, tasks, std::max<long>(1, 8192L / N)}));
     const int threads = std::max(32, std::min(256, nf * N / 8));
     const size_t smem = (size_t)(2 * N + 2 + 2 * (size_t)nf * N) * sizeof(float2);
     cudaError_t err = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    // 4 CTAs per SM amortise the per-CTA twiddle-table load over several task groups
     const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 4));
     partition_kernel<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, nf);
     return cudaGetLastError();
