@@ -234,7 +234,7 @@ void pick_launch_config(tvolap_engine* e) {
     if (ep > 0) e->P = ep;
     if (et > 0) e->NT = et;
     e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
-    e->k4_side = env_int("TVOLAP_K4_SIDE", 0) != 0;
+    e->k4_side = env_int("TVOLAP_K4_SIDE", 1) != 0;
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -249,9 +249,9 @@ void pick_block_geometry(tvolap_engine* e) {
             while (pb < cap && e->S * pb < 256) pb *= 2;
             e->JH = e->E == 2 ? 2 : 4;
         } else {
-            while (pb < cap && e->S * pb < 128) pb *= 2;
+            while (pb < cap && e->S * pb < 256) pb *= 2;
             if (e->L >= 512) pb = cap;
-            e->JH = e->L >= 512 ? 4 : 8;
+            e->JH = (e->L >= 512 || e->S * pb >= 256) ? 4 : 8;
         }
         e->PB = (int)pb;
         const int eb = env_int("TVOLAP_PB", 0), ej = env_int("TVOLAP_JH", 0);
