@@ -179,7 +179,7 @@ def main():
 
     import torch
 
-    from paper_2310_00319_b200 import _build
+    from paper_2310_00319_b200 import _build, shard
     from paper_2310_00319_b200 import tvolap as T
     from paper_2310_00319_b200.tvolap import TvolapBankEngine, TvolapEngine, partition
 
@@ -193,7 +193,7 @@ def main():
     L, S, M = cfg.hop, cfg.sources, cfg.partitions
     H = args.hops or cfg.hops
     n_sw = -(-H // cfg.period)
-    lane0 = rank * S
+    lane0, _ = shard.weak_lanes(S, rank)
     lib = T.lib()
 
     # ---- inputs resident in HBM (device twins of the seeded generators)
@@ -250,7 +250,7 @@ def main():
                                                ctypes.c_void_p(stream.cuda_stream)))
                 if world > 1:
                     with torch.cuda.stream(stream):
-                        torch.distributed.all_reduce(mix)
+                        shard.mix_allreduce(mix)
 
     def barrier():
         torch.cuda.synchronize()
@@ -275,10 +275,7 @@ def main():
     kern_ms, kern_n = eng.kernel_time()
     eng.set_profiling(False)
     gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
-    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    elapsed = float(t.item())
+    elapsed = shard.max_over_ranks(elapsed, dev)
     ms_per_step = elapsed / args.steps
     samples_per_step = world * cfg.lanes * H * L
     value = samples_per_step / (ms_per_step / 1e3)
@@ -337,10 +334,7 @@ def main():
             eng2.synchronize()
         barrier()
         e2e_s = (time.perf_counter() - tw) / args.steps
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = shard.max_over_ranks(e2e_s, dev)
         same = bool(torch.equal(oh, out.cpu()))
         e2e = {"value": samples_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_s * 1e3,
