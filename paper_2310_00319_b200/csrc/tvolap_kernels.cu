@@ -1016,7 +1016,9 @@ cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_s
     // stream the time-domain IRs near HBM speed.
     const int N = 2 * L;
     const long tasks = rows * M;
-    const int nf = (int)std::max<long>(1, std::min<long>({8L, tasks, std::max<long>(1, 8192L / N)}));
+    // ~56 KB of shared memory per CTA (tables + two batch buffers): 4 CTAs per SM stay resident
+    const long budget = 56L * 1024 - 16L * N;
+    const int nf = (int)std::max<long>(1, std::min<long>({8L, tasks, budget / (16L * N)}));
     const int threads = std::max(32, std::min(256, nf * N / 8));
     const size_t smem = (size_t)(2 * N + 2 + 2 * (size_t)nf * N) * sizeof(float2);
     cudaError_t err = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
