@@ -5,6 +5,7 @@ Python mirror of the reference's C++ operator interface over that C-ABI.
 """
 from .tvolap import (  # noqa: F401
     CudaError,
+    FrameAdapter,
     FilterPartitionSet,
     IncompatibleFilterError,
     InvalidConfigurationError,

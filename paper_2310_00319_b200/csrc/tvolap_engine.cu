@@ -191,6 +191,7 @@ struct tvolap_engine {
     int P = 1, NT = 256;           // streaming (one hop at a time) kernel
     int JH = 4, QB = 1, NTB = 256;   // hop-blocked kernel: 2*JH hops per block, QB partition groups
     int PB = 1;                      // hop-blocked kernel: CTAs (cluster size) per source
+    int QM = 1;                      // partition groups of both kernels (bit-identical sums)
     bool geometry_fixed = false;     // set by tvolap_set_launch_config / set_block_config / env
     long D = 0;                      // delay-line slots per parity (M + kMaxJH)
     long block_min = 4;              // process_hops calls with >= block_min hops use the blocked kernel
@@ -271,6 +272,19 @@ void pick_block_geometry(tvolap_engine* e) {
     if (e->NTB < 32) e->NTB = 32, e->QB = (int)std::max<long>(1, 32 / W);
     while (e->JH > 1 && tvb::block_kernel_smem_bytes((int)e->L, e->PB, (int)e->E, e->JH, e->bank, e->NTB) > 227 * 1024)
         e->JH /= 2;
+    // The blocked kernel splits the partitions into NTB / (items per group) contiguous groups;
+    // the one-hop kernel uses the same grouping so process() and process_hops() agree bit for bit.
+    const long Vb = e->N / (2 * e->PB);
+    const long items = (!e->bank && e->JH <= 4) ? Vb : 2 * Vb;  // unified vs per-parity mapping
+    e->QM = items < e->NTB ? (int)(e->NTB / items) : 1;
+}
+
+// Threads of the one-hop kernel: QM partition groups x the slice's float4 columns.
+int hop_threads(const tvolap_engine* e) {
+    const long V = e->N / (2 * e->P);
+    long t = std::min<long>(1024, e->QM * V);
+    t = std::max<long>(32, (t + 31) / 32 * 32);
+    return (int)t;
 }
 
 void validate_launch(const tvolap_engine* e, int P, int NT) {
@@ -278,7 +292,8 @@ void validate_launch(const tvolap_engine* e, int P, int NT) {
         throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "cluster size P must be 1, 2, 4 or 8 and <= L"};
     if (NT < 32 || NT > 1024 || !is_pow2(NT))
         throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "threads per CTA must be a power of two in [32, 1024]"};
-    const size_t smem = tvb::hop_kernel_smem_bytes((int)e->L, P, (int)e->E, NT);
+    const size_t smem = tvb::hop_kernel_smem_bytes((int)e->L, P, (int)e->E, std::max(1, e->QM));
+    (void)NT;
     if (smem > 227 * 1024)
         throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION,
                        "hop L=" + std::to_string(e->L) + " needs " + std::to_string(smem) +
@@ -393,6 +408,7 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.new_ir_len = e->launch_new_len;
     p.pool_w = e->pool;
     p.new_entry_base = e->active * (int)e->S;
+    p.qm = e->QM;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (e->profiling) {
         if (e->prof_used == e->prof_events.size()) {
@@ -409,7 +425,7 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     if (blocked)
         CK(tvb::launch_block_kernel(p, (int)e->E, e->JH, e->QB, e->NTB, e->stream));
     else
-        CK(tvb::launch_hop_kernel(p, (int)e->E, e->NT, e->stream));
+        CK(tvb::launch_hop_kernel(p, (int)e->E, hop_threads(e), e->stream));
     if (t1) CK(cudaEventRecord(t1, e->stream));
     ++e->launches;
     if (!e->bank) CK(cudaEventRecord(e->ev_slot[e->active], e->stream));

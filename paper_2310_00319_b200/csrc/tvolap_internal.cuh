@@ -35,9 +35,10 @@ struct HopParams {
     long new_ir_len;
     float2* pool_w;        // writable view of pool
     int new_entry_base;    // pool entry of source 0 for the staged set
+    int qm;                // one-hop kernel: partition groups (== the blocked kernel's, for bit-identical sums)
 };
 
-size_t hop_kernel_smem_bytes(int L, int P, int E, int threads);
+size_t hop_kernel_smem_bytes(int L, int P, int E, int qm);
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
 
 // Hop-blocked variant (2*JH hops per block, Q partition groups; threads == Q * (2L/P) when 2L/P < threads).

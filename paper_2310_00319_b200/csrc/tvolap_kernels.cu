@@ -42,7 +42,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 
 struct SmemLayout {
     size_t tw, pk, win, x0, x1, fa, fb, red, yb, ola, total;
-    __host__ __device__ SmemLayout(int L, int P, int E, int threads) {
+    __host__ __device__ SmemLayout(int L, int P, int E, int qm) {
         const size_t N = 2 * (size_t)L;
         tw = 0;
         pk = align16(tw + N * sizeof(float2));
@@ -52,7 +52,7 @@ struct SmemLayout {
         fa = align16(x1 + L * sizeof(float));
         fb = align16(fa + N * sizeof(float2));
         red = align16(fb + N * sizeof(float2));
-        yb = align16(red + (size_t)threads * E * sizeof(float4));
+        yb = align16(red + (qm > 1 ? (size_t)qm * (L / P) * E * sizeof(float4) : 0));
         ola = align16(yb + 2 * (size_t)E * (N / P) * sizeof(float2));
         total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
     }
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     const int tid = threadIdx.x, NT = blockDim.x;
     const int s = blockIdx.x / P;
     const int r = blockIdx.x % P;  // == cluster rank (1-D clusters of P consecutive CTAs)
-    const SmemLayout lay(L, P, E, NT);
+    const SmemLayout lay(L, P, E, p.qm);
     float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
     float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
     float* s_win = reinterpret_cast<float*>(smem + lay.win);
@@ -126,9 +126,13 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     const int Np = N / P;   // packed bins owned by this CTA
     const int V = Np / 2;   // float4 per slice
     const int Lp = L / P;   // output samples owned by this CTA
-    const int VT = V < NT ? V : NT;
-    const int G = NT / VT;  // partition groups
+    // Partition groups: G = p.qm contiguous ranges [g M / G, (g+1) M / G), summed in g order —
+    // the same grouping as the hop-blocked kernel, so both produce bit-identical outputs.
+    const int G = p.qm;
+    const int VT = max(1, min(V, NT / G));  // threads per group (each strides over the slice)
+    const bool mac_thread = tid < G * VT;
     const int f0 = tid % VT, g = tid / VT;
+    const int m0 = (int)((long)g * M / G), m1 = (int)((long)(g + 1) * M / G);
     const long spec4 = N / 2;  // float4 per spectrum
 
     for (int i = tid; i < N; i += NT) {
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
         const float4* xb = ring4 + (((long)s * 2 + par) * D) * spec4 + (long)r * V;
         const float4* hb = pool4 + ((long)entry * E * M) * spec4 + (long)r * V;
         float2* yb = s_yb + (size_t)(k & 1) * E * Np;
-        for (int fi = f0; fi < V; fi += VT) {
+        for (int fi = f0; mac_thread && fi < V; fi += VT) {
             float4 acc[E];
             float aux[E];
 #pragma unroll
@@ -192,44 +196,28 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
                 acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
                 aux[e] = 0.f;
             }
-            int m = g;
-            int slot = ((sl - g) % D + D) % D;
-            for (; m + 3 * G < M; m += 4 * G) {
-                int s1 = slot - G;
-                if (s1 < 0) s1 += D;
-                int s2 = s1 - G;
-                if (s2 < 0) s2 += D;
-                int s3 = s2 - G;
-                if (s3 < 0) s3 += D;
-                const float4 x0 = __ldcg(xb + slot * spec4 + fi);
-                const float4 x1 = __ldcg(xb + s1 * spec4 + fi);
-                const float4 x2 = __ldcg(xb + s2 * spec4 + fi);
-                const float4 x3 = __ldcg(xb + s3 * spec4 + fi);
+            int slot = ((sl - m0) % D + D) % D;  // X_{hop-2m}: slot decrements with m
+            int m = m0;
+            for (; m + 4 <= m1; m += 4) {
+                float4 x[4];
                 float4 h[E][4];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const float4* he = hb + ((long)e * M + m) * spec4 + fi;
-                    h[e][0] = __ldcg(he);
-                    h[e][1] = __ldcg(he + G * spec4);
-                    h[e][2] = __ldcg(he + 2 * G * spec4);
-                    h[e][3] = __ldcg(he + 3 * G * spec4);
+                for (int u = 0; u < 4; ++u) {
+                    x[u] = __ldcg(xb + slot * spec4 + fi);
+                    slot = slot == 0 ? D - 1 : slot - 1;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) h[e][u] = __ldcg(hb + ((long)e * M + m + u) * spec4 + fi);
                 }
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    cmac4(acc[e], aux[e], h[e][0], x0);
-                    cmac4(acc[e], aux[e], h[e][1], x1);
-                    cmac4(acc[e], aux[e], h[e][2], x2);
-                    cmac4(acc[e], aux[e], h[e][3], x3);
-                }
-                slot = s3 - G;
-                if (slot < 0) slot += D;
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) cmac4(acc[e], aux[e], h[e][u], x[u]);
             }
-            for (; m < M; m += G) {
+            for (; m < m1; ++m) {
                 const float4 x0 = __ldcg(xb + slot * spec4 + fi);
+                slot = slot == 0 ? D - 1 : slot - 1;
 #pragma unroll
                 for (int e = 0; e < E; ++e) cmac4(acc[e], aux[e], __ldcg(hb + ((long)e * M + m) * spec4 + fi), x0);
-                slot -= G;
-                if (slot < 0) slot += D;
             }
             if (r == 0 && fi == 0) {
 #pragma unroll
@@ -243,15 +231,15 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
                 for (int e = 0; e < E; ++e) reinterpret_cast<float4*>(yb + (size_t)e * Np)[fi] = acc[e];
             } else {
 #pragma unroll
-                for (int e = 0; e < E; ++e) s_red[(g * VT + f0) * E + e] = acc[e];
+                for (int e = 0; e < E; ++e) s_red[((size_t)g * V + fi) * E + e] = acc[e];
             }
         }
         if (G > 1) {
             __syncthreads();
-            for (int i = tid; i < VT * E; i += NT) {
+            for (int i = tid; i < V * E; i += NT) {
                 const int f = i / E, e = i % E;
-                float4 sum = s_red[f * E + e];
-                for (int gg = 1; gg < G; ++gg) sum = f4add(sum, s_red[(gg * VT + f) * E + e]);
+                float4 sum = s_red[(size_t)f * E + e];
+                for (int gg = 1; gg < G; ++gg) sum = f4add(sum, s_red[((size_t)gg * V + f) * E + e]);
                 reinterpret_cast<float4*>(yb + (size_t)e * Np)[f] = sum;
             }
         }
@@ -930,7 +918,7 @@ int fft_threads(int N) { return std::max(32, std::min(256, N / 4)); }
 
 }  // namespace
 
-size_t hop_kernel_smem_bytes(int L, int P, int E, int threads) { return SmemLayout(L, P, E, threads).total; }
+size_t hop_kernel_smem_bytes(int L, int P, int E, int qm) { return SmemLayout(L, P, E, qm).total; }
 
 size_t block_kernel_smem_bytes(int L, int P, int E, int JH, bool bank, int threads) {
     return BlockLayout(L, P, E, 2 * JH, bank, threads).total;
@@ -987,7 +975,7 @@ cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int th
 }
 
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {
-    const size_t smem = hop_kernel_smem_bytes(p.L, p.P, E, threads);
+    const size_t smem = hop_kernel_smem_bytes(p.L, p.P, E, p.qm);
     void (*fn)(const HopParams) = E == 2 ? tvolap_hop_kernel<2> : tvolap_hop_kernel<1>;
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;

@@ -491,3 +491,66 @@ def make_processor(name: str, ir, hop: int, device: int = 0) -> TvolapProcessor:
     if name == "tvolap":
         return TvolapProcessor(ir, hop, device=device)
     raise InvalidConfigurationError(f"unknown algorithm: {name}")
+
+
+# ---------------------------------------------------------------- frame adapter (frame_adapter.hpp)
+class FrameAdapter:
+    """Arbitrary host chunks -> exact hops (proj/include/tvolap/frame_adapter.hpp, frame_adapter.cpp:13-43).
+
+    Buffers input until a full hop is available and returns output as it is produced, so the
+    concatenated output equals feeding strict hops. Complete hops inside one pushed chunk go
+    to the engine as a single multi-hop call (the hop-blocked kernel), which gives bit-identical
+    results to one process() per hop.
+    """
+
+    def __init__(self, proc):
+        self._proc = proc
+        self._eng = proc.engine() if hasattr(proc, "engine") else proc
+        self._hop = proc.hop()
+        self._ch = proc.channels()
+        self._staging = np.zeros((self._hop, self._ch), dtype=np.float32)
+        self._fill = 0
+
+    def buffered(self) -> int:
+        return self._fill
+
+    def push(self, chunk) -> np.ndarray:
+        """frame_adapter.cpp:13-35: feed any number of frames (rows x channels)."""
+        x = np.asarray(chunk, dtype=np.float32)
+        if x.ndim == 1:
+            x = x[:, None]
+        if x.shape[1] != self._ch:
+            raise InvalidInputError("adapter chunk channel count does not match the processor")
+        hop, outs, pos = self._hop, [], 0
+        if self._fill:  # complete the partial hop first
+            take = min(hop - self._fill, x.shape[0])
+            self._staging[self._fill:self._fill + take] = x[:take]
+            self._fill += take
+            pos = take
+            if self._fill == hop:
+                outs.append(self._proc.process(self._staging))
+                self._fill = 0
+        n_full = (x.shape[0] - pos) // hop
+        if n_full:
+            seg = x[pos:pos + n_full * hop]
+            if n_full > 1:
+                y = self._eng.process_hops(np.ascontiguousarray(seg.T))  # (lanes, n*hop)
+                outs.append(y.T)
+            else:
+                outs.append(self._proc.process(seg))
+            pos += n_full * hop
+        rest = x.shape[0] - pos
+        if rest:
+            self._staging[:rest] = x[pos:]
+            self._fill = rest
+        if not outs:
+            return np.zeros((0, self._eng.channels_out()), dtype=np.float32)
+        return np.concatenate(outs, axis=0)
+
+    def flush(self) -> np.ndarray:
+        """frame_adapter.cpp:37-43: zero-pad the partial hop, if any, and process it."""
+        if self._fill == 0:
+            return np.zeros((0, self._eng.channels_out()), dtype=np.float32)
+        self._staging[self._fill:] = 0.0
+        self._fill = 0
+        return self._proc.process(self._staging)
