@@ -42,7 +42,10 @@ def _run(cmd):
 def build(force: bool = False, verbose: bool = False) -> None:
     LIB.mkdir(exist_ok=True)
     if force or _stale(LIB_CUDA, CUDA_DEPS):
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+        # --fmad=false: no implicit multiply-add contraction, so the one-hop and hop-blocked
+        # kernels (same operations, different code around them) round identically; every
+        # intended FMA is an explicit fmaf().
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
                "-I", INCLUDE, "-o", LIB_CUDA, *CUDA_SOURCES]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

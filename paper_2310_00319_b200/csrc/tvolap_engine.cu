@@ -882,6 +882,7 @@ int tvolap_set_block_config(tvolap_engine* e, int hops_per_block, long block_min
                 throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hop block does not fit in shared memory"};
             e->JH = jh;
             e->geometry_fixed = true;
+            pick_block_geometry(e);  // threads / partition groups follow the new block length
         }
         if (block_min > 0) e->block_min = block_min;
     });

@@ -412,6 +412,9 @@ class OpCounts:
 
 
 def _stride(a) -> int:
+    """Lane stride in elements (a size-1 leading dim may carry an arbitrary stride: use the row length)."""
+    if a.shape[0] == 1:
+        return a.shape[-1]
     if hasattr(a, "stride") and callable(a.stride):
         return a.stride(0)
     return a.strides[0] // a.itemsize
