@@ -395,6 +395,10 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.out_stride = out_stride;
     p.ring = e->ring;
     p.pool = e->pool;
+    if (e->bank && !sched) {  // bank engines without a per-hop schedule: the latched selection
+        sched = e->d_sel;
+        sched_stride = 0;
+    }
     p.sched = sched;
     p.sched_stride = sched_stride;
     p.entry_base = e->bank ? 0 : e->active * (int)e->S;

@@ -415,3 +415,22 @@ def test_adapter_flush_zero_pads():  # test_adapter.cpp:65-90
     assert ad.flush().shape[0] == 0
     with pytest.raises(T.InvalidInputError):
         ad.push(np.zeros((10, 2)))
+
+
+@pytest.mark.parametrize("S", [3, 64])
+def test_bank_engine_single_hop_select(S):
+    """process() on a bank engine uses the latched select_bank choice (== per-hop schedule)."""
+    hop, n_bank, n = 32, 6, 12
+    bank = rnd(n_bank * 300, 17).reshape(n_bank, 1, 300)
+    sched = np.random.default_rng(9).integers(0, n_bank, (n, S)).astype(np.int32)
+    x = rnd(hop * n, 18, S)
+    a, b = T.TvolapBankEngine(bank, hop, S), T.TvolapBankEngine(bank, hop, S)
+    ya = []
+    for h in range(n):
+        a.select_bank(sched[h])
+        ya.append(a.process(x[h * hop:(h + 1) * hop]))
+    ya = np.concatenate(ya).T
+    yb = b.process_hops(np.ascontiguousarray(x.T), schedule=sched)
+    assert np.array_equal(ya, yb)
+    with pytest.raises(T.InvalidInputError):
+        a.select_bank(np.full(S, n_bank, np.int32))
