@@ -36,6 +36,12 @@ __host__ __device__ __forceinline__ int fft_stage_count(int N) {
     return k;
 }
 
+// Intermediate Stockham stages store to a swizzled layout (low 3 index bits XOR bits 3..5):
+// a permutation inside aligned groups of 8 elements that spreads the stride-R stores of the
+// early stages over the shared-memory banks. The first stage reads and the last stage writes
+// the natural layout, so callers never see it.
+__device__ __forceinline__ int fsw(int i, bool on) { return on ? (i ^ ((i >> 3) & 7)) : i; }
+
 template <bool INV>
 __device__ __forceinline__ float2 twmul(float2 v, float2 w) {
     return INV ? cmulc(v, w) : cmul(v, w);
@@ -105,6 +111,7 @@ __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* 
         const int tstep = N / (Ns * R);
         const bool zero_hi = prune && Ns == 1;  // legs r >= R/2 read the zero upper half
         const int lgnb = 31 - __clz(nb);
+        const bool rs = Ns > 1, ws = Ns * R < N;  // read / write the swizzled intermediate layout
         for (int jj = tid; jj < nb * nf; jj += nthreads) {
             const int f = jj >> lgnb, j = jj & (nb - 1);
             const float2* sf = src + (size_t)f * N;
@@ -114,7 +121,7 @@ __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* 
             if (R == 8) {
                 float2 v[8];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) v[r] = (zero_hi && r >= 4) ? make_float2(0.f, 0.f) : sf[j + r * nb];
+                for (int r = 0; r < 8; ++r) v[r] = (zero_hi && r >= 4) ? make_float2(0.f, 0.f) : sf[fsw(j + r * nb, rs)];
                 if (Ns > 1) {
                     const int t1 = k * tstep;
 #pragma unroll
@@ -122,12 +129,12 @@ __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* 
                 }
                 dft8<INV>(v);
 #pragma unroll
-                for (int r = 0; r < 8; ++r) df[idxD + r * Ns] = v[r];
+                for (int r = 0; r < 8; ++r) df[fsw(idxD + r * Ns, ws)] = v[r];
             } else if (R == 4) {
-                float2 v0 = sf[j];
-                float2 v1 = sf[j + nb];
-                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 2 * nb];
-                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[j + 3 * nb];
+                float2 v0 = sf[fsw(j, rs)];
+                float2 v1 = sf[fsw(j + nb, rs)];
+                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 2 * nb, rs)];
+                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 3 * nb, rs)];
                 if (Ns > 1) {
                     const int t1 = k * tstep;
                     v1 = twmul<INV>(v1, tw[t1]);
@@ -135,16 +142,16 @@ __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* 
                     v3 = twmul<INV>(v3, tw[3 * t1]);
                 }
                 dft4<INV>(v0, v1, v2, v3);
-                df[idxD] = v0;
-                df[idxD + Ns] = v1;
-                df[idxD + 2 * Ns] = v2;
-                df[idxD + 3 * Ns] = v3;
+                df[fsw(idxD, ws)] = v0;
+                df[fsw(idxD + Ns, ws)] = v1;
+                df[fsw(idxD + 2 * Ns, ws)] = v2;
+                df[fsw(idxD + 3 * Ns, ws)] = v3;
             } else {
-                float2 v0 = sf[j];
-                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[j + nb];
+                float2 v0 = sf[fsw(j, rs)];
+                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + nb, rs)];
                 if (Ns > 1) v1 = twmul<INV>(v1, tw[k * tstep]);
-                df[idxD] = cadd(v0, v1);
-                df[idxD + Ns] = csub(v0, v1);
+                df[fsw(idxD, ws)] = cadd(v0, v1);
+                df[fsw(idxD + Ns, ws)] = csub(v0, v1);
             }
         }
         __syncthreads();
@@ -183,6 +190,18 @@ __device__ __forceinline__ float2 untangle_packed(const float2* Z, int N, int k,
         return make_float2(z0.x + z0.y, z0.x - z0.y);
     }
     return untangle(Z, N, k, pk);
+}
+
+// Untangle a whole packed spectrum into dst[0..N) (16-byte aligned): two bins per thread and
+// one 16-byte store, no per-element address arithmetic beyond the bin index.
+__device__ __forceinline__ void untangle_store(const float2* Z, int N, const float2* __restrict__ pk,
+                                               float2* __restrict__ dst, int tid, int nthreads) {
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int k2 = tid; k2 < N / 2; k2 += nthreads) {
+        const float2 a = untangle_packed(Z, N, 2 * k2, pk);
+        const float2 b = untangle(Z, N, 2 * k2 + 1, pk);
+        d4[k2] = make_float4(a.x, a.y, b.x, b.y);
+    }
 }
 
 // Tangle bin k < N for the inverse (spectral.cpp:142-148), from a packed

@@ -85,7 +85,7 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
     const float* h = p.new_ir + (long)s * p.new_ir_stride;
     float2* dst = p.pool_w + ((long)(p.new_entry_base + s) * M) * N;
     const int nm = r < M ? (M - r + P - 1) / P : 0;
-    const int lgL = 31 - __clz(L), lgN = lgL + 1;
+    const int lgL = 31 - __clz(L);
     for (int i0 = 0; i0 < nm; i0 += cap) {
         const int nt = min(cap, nm - i0);
         for (int i = tid; i < nt * L; i += NT) {
@@ -96,10 +96,8 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
         }
         __syncthreads();
         const float2* Z = fft_batch<false>(fa, fb, N, nt, tw, true, tid, NT);
-        for (int i = tid; i < nt * N; i += NT) {
-            const int f = i >> lgN, kk = i & (N - 1);
-            dst[(long)(r + (i0 + f) * P) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, pk);
-        }
+        for (int f = 0; f < nt; ++f)
+            untangle_store(Z + (size_t)f * N, N, pk, dst + (long)(r + (i0 + f) * P) * N, tid, NT);
         __syncthreads();
     }
 }
@@ -414,11 +412,10 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         __syncthreads();
         if (nf > 0) {
             const float2* Z = fft_batch<false>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
-            for (int i = tid; i < nf * N; i += NT) {
-                const int f = i >> lgN, kk = i & (N - 1);
+            for (int f = 0; f < nf; ++f) {
                 const long h = l0 + r + f * P;
                 float2* ringw = p.ring + (((long)s * 2 + (h & 1)) * D + (h >> 1) % D) * N;
-                ringw[kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
+                untangle_store(Z + (size_t)f * N, N, s_pk, ringw, tid, NT);
             }
         }
         block_sync(P);  // ring writes of all frames visible cluster-wide
@@ -765,7 +762,7 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
     for (int i = tid; i <= N; i += NT) s_pk[i] = pk[i];
     __syncthreads();
     const long tasks = rows * M;
-    const int lgL = 31 - __clz(L), lgN = lgL + 1;  // L, N powers of two: shifts, no divisions
+    const int lgL = 31 - __clz(L);  // L a power of two: shifts, no divisions
     for (long t0 = (long)blockIdx.x * nf; t0 < tasks; t0 += (long)gridDim.x * nf) {
         const int nt = (int)min((long)nf, tasks - t0);
         const long row0t = t0 / M;  // one 64-bit division per group
@@ -805,10 +802,8 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
         }
         __syncthreads();
         const float2* Z = fft_batch<false>(s_fa, s_fb, N, nt, s_tw, true, tid, NT);
-        for (int i = tid; i < nt * N; i += NT) {
-            const int f = i >> lgN, kk = i & (N - 1);
-            pool[(row0 * M + t0 + f) * N + kk] = untangle_packed(Z + (size_t)f * N, N, kk, s_pk);
-        }
+        for (int f = 0; f < nt; ++f)
+            untangle_store(Z + (size_t)f * N, N, s_pk, pool + (row0 * M + t0 + f) * N, tid, NT);
         __syncthreads();
     }
 }
