@@ -93,81 +93,103 @@ __device__ __forceinline__ void dft8(float2 (&v)[8]) {
     }
 }
 
+// One Stockham stage: nf transforms, sub-transform length Ns -> Ns*R.
+template <bool INV>
+__device__ __forceinline__ void fft_stage(const float2* src, float2* dst, int N, int Ns, int nf,
+                                          const float2* __restrict__ tw, bool prune, int tid, int nthreads) {
+    const int R = fft_radix(N, Ns);
+    const int nb = N / R;
+    const int tstep = N / (Ns * R);
+    const bool zero_hi = prune && Ns == 1;  // legs r >= R/2 read the zero upper half
+    const int lgnb = 31 - __clz(nb);
+    const bool rs = Ns > 1, ws = Ns * R < N;  // read / write the swizzled intermediate layout
+    for (int jj = tid; jj < nb * nf; jj += nthreads) {
+        const int f = jj >> lgnb, j = jj & (nb - 1);
+        const float2* sf = src + (size_t)f * N;
+        float2* df = dst + (size_t)f * N;
+        const int k = j & (Ns - 1);
+        const int idxD = (j - k) * R + k;
+        if (R == 8) {
+            float2 v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = (zero_hi && r >= 4) ? make_float2(0.f, 0.f) : sf[fsw(j + r * nb, rs)];
+            if (Ns > 1) {
+                const int t1 = k * tstep;
+#pragma unroll
+                for (int r = 1; r < 8; ++r) v[r] = twmul<INV>(v[r], tw[r * t1]);
+            }
+            dft8<INV>(v);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) df[fsw(idxD + r * Ns, ws)] = v[r];
+        } else if (R == 4) {
+            float2 v0 = sf[fsw(j, rs)];
+            float2 v1 = sf[fsw(j + nb, rs)];
+            float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 2 * nb, rs)];
+            float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 3 * nb, rs)];
+            if (Ns > 1) {
+                const int t1 = k * tstep;
+                v1 = twmul<INV>(v1, tw[t1]);
+                v2 = twmul<INV>(v2, tw[2 * t1]);
+                v3 = twmul<INV>(v3, tw[3 * t1]);
+            }
+            dft4<INV>(v0, v1, v2, v3);
+            df[fsw(idxD, ws)] = v0;
+            df[fsw(idxD + Ns, ws)] = v1;
+            df[fsw(idxD + 2 * Ns, ws)] = v2;
+            df[fsw(idxD + 3 * Ns, ws)] = v3;
+        } else {
+            float2 v0 = sf[fsw(j, rs)];
+            float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + nb, rs)];
+            if (Ns > 1) v1 = twmul<INV>(v1, tw[k * tstep]);
+            df[fsw(idxD, ws)] = cadd(v0, v1);
+            df[fsw(idxD + Ns, ws)] = csub(v0, v1);
+        }
+    }
+    __syncthreads();
+}
+
 // Batched Stockham FFT of `nf` length-N transforms stored back to back in `a`
 // (N a power of two >= 2), `b` the ping-pong buffer. tw[t] = e^{-2 pi i t / N}.
 // Radix-8 stages (radix-4/2 for the remainder): each thread keeps one butterfly's
 // 8 points in registers, so a 512-point transform is 3 shared-memory passes.
 // When `prune` is set the upper half of every input is taken as zero and never
 // read (the engine's 4L block is zero-padded past 2L, proj/src/engine.cpp:77-80).
+// NC != 0 fixes N at compile time: the stages unroll and all index math folds.
 // All threads of the CTA must call this; returns the buffer holding the result.
-template <bool INV>
+template <bool INV, int NC = 0>
 __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* __restrict__ tw, bool prune, int tid,
                              int nthreads) {
     float2* src = a;
     float2* dst = b;
-    for (int Ns = 1; Ns < N;) {
-        const int R = fft_radix(N, Ns);
-        const int nb = N / R;
-        const int tstep = N / (Ns * R);
-        const bool zero_hi = prune && Ns == 1;  // legs r >= R/2 read the zero upper half
-        const int lgnb = 31 - __clz(nb);
-        const bool rs = Ns > 1, ws = Ns * R < N;  // read / write the swizzled intermediate layout
-        for (int jj = tid; jj < nb * nf; jj += nthreads) {
-            const int f = jj >> lgnb, j = jj & (nb - 1);
-            const float2* sf = src + (size_t)f * N;
-            float2* df = dst + (size_t)f * N;
-            const int k = j & (Ns - 1);
-            const int idxD = (j - k) * R + k;
-            if (R == 8) {
-                float2 v[8];
+    if constexpr (NC != 0) {
+        (void)N;
+        int Ns = 1;
 #pragma unroll
-                for (int r = 0; r < 8; ++r) v[r] = (zero_hi && r >= 4) ? make_float2(0.f, 0.f) : sf[fsw(j + r * nb, rs)];
-                if (Ns > 1) {
-                    const int t1 = k * tstep;
-#pragma unroll
-                    for (int r = 1; r < 8; ++r) v[r] = twmul<INV>(v[r], tw[r * t1]);
-                }
-                dft8<INV>(v);
-#pragma unroll
-                for (int r = 0; r < 8; ++r) df[fsw(idxD + r * Ns, ws)] = v[r];
-            } else if (R == 4) {
-                float2 v0 = sf[fsw(j, rs)];
-                float2 v1 = sf[fsw(j + nb, rs)];
-                float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 2 * nb, rs)];
-                float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 3 * nb, rs)];
-                if (Ns > 1) {
-                    const int t1 = k * tstep;
-                    v1 = twmul<INV>(v1, tw[t1]);
-                    v2 = twmul<INV>(v2, tw[2 * t1]);
-                    v3 = twmul<INV>(v3, tw[3 * t1]);
-                }
-                dft4<INV>(v0, v1, v2, v3);
-                df[fsw(idxD, ws)] = v0;
-                df[fsw(idxD + Ns, ws)] = v1;
-                df[fsw(idxD + 2 * Ns, ws)] = v2;
-                df[fsw(idxD + 3 * Ns, ws)] = v3;
-            } else {
-                float2 v0 = sf[fsw(j, rs)];
-                float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + nb, rs)];
-                if (Ns > 1) v1 = twmul<INV>(v1, tw[k * tstep]);
-                df[fsw(idxD, ws)] = cadd(v0, v1);
-                df[fsw(idxD + Ns, ws)] = csub(v0, v1);
-            }
+        for (int st = 0; st < 12; ++st) {
+            if (Ns >= NC) break;
+            fft_stage<INV>(src, dst, NC, Ns, nf, tw, prune, tid, nthreads);
+            float2* t = src;
+            src = dst;
+            dst = t;
+            Ns *= fft_radix(NC, Ns);
         }
-        __syncthreads();
-        float2* t = src;
-        src = dst;
-        dst = t;
-        Ns *= R;
+    } else {
+        for (int Ns = 1; Ns < N;) {
+            fft_stage<INV>(src, dst, N, Ns, nf, tw, prune, tid, nthreads);
+            float2* t = src;
+            src = dst;
+            dst = t;
+            Ns *= fft_radix(N, Ns);
+        }
     }
     return src;
 }
 
 // Single transform (nf = 1).
-template <bool INV>
+template <bool INV, int NC = 0>
 __device__ float2* fft_stockham(float2* a, float2* b, int N, const float2* __restrict__ tw, bool prune, int tid,
                                 int nthreads) {
-    return fft_batch<INV>(a, b, N, 1, tw, prune, tid, nthreads);
+    return fft_batch<INV, NC>(a, b, N, 1, tw, prune, tid, nthreads);
 }
 
 // Untangle bin k (0 <= k <= N) of the real 2N-point transform from the
@@ -194,8 +216,10 @@ __device__ __forceinline__ float2 untangle_packed(const float2* Z, int N, int k,
 
 // Untangle a whole packed spectrum into dst[0..N) (16-byte aligned): two bins per thread and
 // one 16-byte store, no per-element address arithmetic beyond the bin index.
+template <int NC = 0>
 __device__ __forceinline__ void untangle_store(const float2* Z, int N, const float2* __restrict__ pk,
                                                float2* __restrict__ dst, int tid, int nthreads) {
+    if constexpr (NC != 0) N = NC;
     float4* d4 = reinterpret_cast<float4*>(dst);
     for (int k2 = tid; k2 < N / 2; k2 += nthreads) {
         const float2 a = untangle_packed(Z, N, 2 * k2, pk);

@@ -79,9 +79,10 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 // CTA r of the cluster takes partitions m = r, r+P, ..., `cap` of them per batched
 // FFT, and writes the whole packed spectrum of each into the pool entry the MAC of
 // this launch reads. The caller synchronises the cluster before the MAC.
+template <int NC>
 __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2* fa, float2* fb, int cap,
                                 const float2* tw, const float2* pk, int tid, int NT) {
-    const int L = p.L, N = 2 * L, M = p.M;
+    const int L = NC ? NC / 2 : p.L, N = 2 * L, M = p.M;
     const float* h = p.new_ir + (long)s * p.new_ir_stride;
     float2* dst = p.pool_w + ((long)(p.new_entry_base + s) * M) * N;
     const int nm = r < M ? (M - r + P - 1) / P : 0;
@@ -95,17 +96,17 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
                 make_float2(idx < p.new_ir_len ? h[idx] : 0.f, idx + 1 < p.new_ir_len ? h[idx + 1] : 0.f);
         }
         __syncthreads();
-        const float2* Z = fft_batch<false>(fa, fb, N, nt, tw, true, tid, NT);
+        const float2* Z = fft_batch<false, NC>(fa, fb, N, nt, tw, true, tid, NT);
         for (int f = 0; f < nt; ++f)
-            untangle_store(Z + (size_t)f * N, N, pk, dst + (long)(r + (i0 + f) * P) * N, tid, NT);
+            untangle_store<NC>(Z + (size_t)f * N, N, pk, dst + (long)(r + (i0 + f) * P) * N, tid, NT);
         __syncthreads();
     }
 }
 
-template <int E>
+template <int E, int NC>
 __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int L = p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
+    const int L = NC ? NC / 2 : p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
     const int tid = threadIdx.x, NT = blockDim.x;
     const int s = blockIdx.x / P;
     const int r = blockIdx.x % P;  // == cluster rank (1-D clusters of P consecutive CTAs)
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     }
     __syncthreads();
     if (p.new_ir) {  // latch a staged filter set: transform it here (K4), then the whole cluster sees it
-        fused_partition(p, s, r, P, s_fa, s_fb, 1, s_tw, s_pk, tid, NT);
+        fused_partition<NC>(p, s, r, P, s_fa, s_fb, 1, s_tw, s_pk, tid, NT);
         if (P > 1)
             cg::this_cluster().sync();
         else
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
             s_fa[j] = make_float2(a, b);
         }
         __syncthreads();
-        const float2* Z = fft_stockham<false>(s_fa, s_fb, N, s_tw, true, tid, NT);
+        const float2* Z = fft_stockham<false, NC>(s_fa, s_fb, N, s_tw, true, tid, NT);
 
         // ---- K2: this CTA's slice of X_hop into the delay line.
         float2* ringw = p.ring + (((long)s * 2 + par) * D + sl) * N + (long)r * Np;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
             __syncthreads();
             for (int i = tid; i < N; i += NT) s_fb[i] = tangle_packed(s_fa, N, i, s_pk);
             __syncthreads();
-            const float* yf = reinterpret_cast<const float*>(fft_stockham<true>(s_fb, s_fa, N, s_tw, false, tid, NT));
+            const float* yf = reinterpret_cast<const float*>(fft_stockham<true, NC>(s_fb, s_fa, N, s_tw, false, tid, NT));
             const float sc = 1.0f / (float)N;
             float* A = s_ola + e * 3 * Lp;
             float* o = p.out + ((long)s * E + e) * p.out_stride + (long)k * L;
@@ -330,11 +331,11 @@ __device__ __forceinline__ void block_sync(int P) {
 // BANK = false: filter-set engines (one set for every hop of a block) — only the unified
 // mapping (JH <= 4) or the per-parity shared mapping (JH == 8) is compiled. BANK = true:
 // per-hop bank selections — per-parity mapping with shared or per-output filter loads.
-template <int E, int JH, bool BANK>
+template <int E, int JH, bool BANK, int NC>
 __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p, const int Q) {
     constexpr int J = 2 * JH;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int L = p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
+    const int L = NC ? NC / 2 : p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
     const int tid = threadIdx.x, NT = blockDim.x;
     const int s = blockIdx.x / P;
     const int r = blockIdx.x % P;
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     prefetch_block(xcur, 0);
     if (p.new_ir) {  // latch a staged filter set: transform it here (K4) while block 0's input lands
         __syncthreads();
-        fused_partition(p, s, r, P, s_fa, s_fb, ((J + P - 1) / P) * E, s_tw, s_pk, tid, NT);
+        fused_partition<NC>(p, s, r, P, s_fa, s_fb, ((J + P - 1) / P) * E, s_tw, s_pk, tid, NT);
         block_sync(P);
     }
     for (int i = tid; i < E * 3 * Lp; i += NT) {
@@ -411,11 +412,11 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         }
         __syncthreads();
         if (nf > 0) {
-            const float2* Z = fft_batch<false>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
+            const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
             for (int f = 0; f < nf; ++f) {
                 const long h = l0 + r + f * P;
                 float2* ringw = p.ring + (((long)s * 2 + (h & 1)) * D + (h >> 1) % D) * N;
-                untangle_store(Z + (size_t)f * N, N, s_pk, ringw, tid, NT);
+                untangle_store<NC>(Z + (size_t)f * N, N, s_pk, ringw, tid, NT);
             }
         }
         block_sync(P);  // ring writes of all frames visible cluster-wide
@@ -682,7 +683,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             s_fb[(size_t)t * N + kk] = tangle_packed(s_fa + (size_t)t * N, N, kk, s_pk);
         }
         __syncthreads();
-        if (nt > 0) fft_batch<true>(s_fb, s_fa, N, nt, s_tw, false, tid, NT);
+        if (nt > 0) fft_batch<true, NC>(s_fb, s_fa, N, nt, s_tw, false, tid, NT);
         // the result buffer depends only on the stage count (same in every CTA of the cluster)
         const int stages = fft_stage_count(N);
         const float* ytd = reinterpret_cast<const float*>((stages & 1) ? s_fa : s_fb);
@@ -746,10 +747,12 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
 }
 
 // K4: transform IR slices into packed partition spectra (partition.cpp:20-51).
+template <int NC>
 __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows, const float* __restrict__ ir,
                                                         long ir_stride, long ir_len, float2* __restrict__ pool,
                                                         long row0, const float2* __restrict__ tw,
                                                         const float2* __restrict__ pk, int nf) {
+    if constexpr (NC != 0) L = NC / 2;
     const bool vec = L >= 2 && (ir_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(ir) & 15) == 0;
     // nf partitions per CTA iteration through one batched FFT (fewer barriers per transform)
     extern __shared__ __align__(16) unsigned char smem[];
@@ -801,9 +804,9 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
             }
         }
         __syncthreads();
-        const float2* Z = fft_batch<false>(s_fa, s_fb, N, nt, s_tw, true, tid, NT);
+        const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nt, s_tw, true, tid, NT);
         for (int f = 0; f < nt; ++f)
-            untangle_store(Z + (size_t)f * N, N, s_pk, pool + (row0 * M + t0 + f) * N, tid, NT);
+            untangle_store<NC>(Z + (size_t)f * N, N, s_pk, pool + (row0 * M + t0 + f) * N, tid, NT);
         __syncthreads();
     }
 }
@@ -922,7 +925,21 @@ size_t block_kernel_smem_bytes(int L, int P, int E, int JH, bool bank, int threa
 template <int E, int JH, bool BANK>
 static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaStream_t stream) {
     const size_t smem = block_kernel_smem_bytes(p.L, p.P, E, JH, BANK, threads);
-    void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH, BANK>;
+    // compile-time transform length for the BASELINE geometries (and the one each kernel
+    // variant actually serves), runtime N otherwise
+    void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH, BANK, 0>;
+    const int N = 2 * p.L;
+    if constexpr (!BANK && E == 1 && (JH == 4 || JH == 8)) {
+        if (N == 256) fn = tvolap_block_kernel<E, JH, BANK, 256>;
+        if (N == 512) fn = tvolap_block_kernel<E, JH, BANK, 512>;
+        if (N == 1024) fn = tvolap_block_kernel<E, JH, BANK, 1024>;
+    }
+    if constexpr (BANK && E == 1 && JH == 4) {
+        if (N == 64) fn = tvolap_block_kernel<E, JH, BANK, 64>;
+    }
+    if constexpr (BANK && E == 2 && JH == 2) {
+        if (N == 256) fn = tvolap_block_kernel<E, JH, BANK, 256>;
+    }
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     if (p.P > 1) {
@@ -971,7 +988,16 @@ cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int th
 
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {
     const size_t smem = hop_kernel_smem_bytes(p.L, p.P, E, p.qm);
-    void (*fn)(const HopParams) = E == 2 ? tvolap_hop_kernel<2> : tvolap_hop_kernel<1>;
+    void (*fn)(const HopParams) = nullptr;
+#define TV_HOP(NCV) fn = E == 2 ? tvolap_hop_kernel<2, NCV> : tvolap_hop_kernel<1, NCV>
+    switch (2 * p.L) {
+        case 64: TV_HOP(64); break;
+        case 256: TV_HOP(256); break;
+        case 512: TV_HOP(512); break;
+        case 1024: TV_HOP(1024); break;
+        default: TV_HOP(0);
+    }
+#undef TV_HOP
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     if (p.P > 1) {
@@ -1004,10 +1030,18 @@ cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_s
     const int nf = (int)std::max<long>(1, std::min<long>({8L, tasks, budget / (16L * N)}));
     const int threads = std::max(32, std::min(256, nf * N / 8));
     const size_t smem = (size_t)(2 * N + 2 + 2 * (size_t)nf * N) * sizeof(float2);
-    cudaError_t err = cudaFuncSetAttribute(partition_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    decltype(&partition_kernel<0>) fn = partition_kernel<0>;
+    switch (N) {
+        case 64: fn = partition_kernel<64>; break;
+        case 256: fn = partition_kernel<256>; break;
+        case 512: fn = partition_kernel<512>; break;
+        case 1024: fn = partition_kernel<1024>; break;
+        default: break;
+    }
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     const int grid = (int)std::max<long>(1, std::min<long>((tasks + nf - 1) / nf, 148L * 4));
-    partition_kernel<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, nf);
+    fn<<<grid, threads, smem, stream>>>(L, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, nf);
     return cudaGetLastError();
 }
 
