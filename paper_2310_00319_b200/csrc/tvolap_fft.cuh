@@ -23,9 +23,12 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
-// Radix of the Stockham stage that starts at sub-transform length Ns (8, then 4, then 2).
+// Radix of the Stockham stage that starts at sub-transform length Ns: 8 while possible, but a
+// remaining factor of 16 is done as 4 x 4 rather than 8 x 2 (a radix-2 pass costs more per
+// point than a radix-8 one). 1024 = 8.8.4.4, 512 = 8.8.8, 256 = 8.8.4, 64 = 8.8.
 __host__ __device__ __forceinline__ int fft_radix(int N, int Ns) {
     const int rem = N / Ns;
+    if (rem == 16) return 4;
     return (rem & 7) == 0 ? 8 : ((rem & 3) == 0 ? 4 : 2);
 }
 
