@@ -934,7 +934,7 @@ static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaSt
         if (N == 512) fn = tvolap_block_kernel<E, JH, BANK, 512>;
         if (N == 1024) fn = tvolap_block_kernel<E, JH, BANK, 1024>;
     }
-    if constexpr (BANK && E == 1 && JH == 4) {
+    if constexpr (BANK && E == 1 && JH == 8) {
         if (N == 64) fn = tvolap_block_kernel<E, JH, BANK, 64>;
     }
     if constexpr (BANK && E == 2 && JH == 2) {
