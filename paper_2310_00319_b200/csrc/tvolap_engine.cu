@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "../../include/tvolap_b200.h"
+#include "tvolap_fft.cuh"
 #include "tvolap_internal.cuh"
 
 using tvb::HopParams;
@@ -108,10 +109,8 @@ struct Tables {
     explicit Tables(long nc) {
         const double pi = 3.14159265358979323846264338327950288;
         tw.resize(nc);
-        for (long t = 0; t < nc; ++t) {
-            const double a = -2.0 * pi * (double)t / (double)nc;
-            tw[t] = make_float2((float)std::cos(a), (float)std::sin(a));
-        }
+        tvb::fft_stage_twiddles((int)nc, tw.data(),
+                                [](double c, double s) { return make_float2((float)c, (float)s); });
         pk.resize(nc + 2);
         for (long k = 0; k <= nc; ++k) {
             const double a = -2.0 * pi * (double)k / (double)(2 * nc);

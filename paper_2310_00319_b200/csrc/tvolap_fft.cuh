@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 namespace tvb {
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
@@ -44,6 +46,22 @@ __host__ __device__ __forceinline__ int fft_stage_count(int N) {
 // early stages over the shared-memory banks. The first stage reads and the last stage writes
 // the natural layout, so callers never see it.
 __device__ __forceinline__ int fsw(int i, bool on) { return on ? (i ^ ((i >> 3) & 7)) : i; }
+
+// Host side: the stage twiddle table for length N (fp64 angles, rounded once), N entries.
+template <class F2, class MAKE>
+inline void fft_stage_twiddles(int N, F2* out, MAKE make) {
+    const double pi = 3.14159265358979323846264338327950288;
+    for (int Ns = 1; Ns < N;) {
+        const int R = fft_radix(N, Ns);
+        for (int k = 0; k < Ns; ++k)
+            for (int r = 1; r < R; ++r) {
+                const double a = -2.0 * pi * (double)k * (double)r / (double)(Ns * R);
+                out[(Ns - 1) + k * (R - 1) + (r - 1)] = make(std::cos(a), std::sin(a));
+            }
+        Ns *= R;
+    }
+    out[N - 1] = make(0.0, 0.0);  // unused pad entry (the table has N - 1 live entries)
+}
 
 template <bool INV>
 __device__ __forceinline__ float2 twmul(float2 v, float2 w) {
@@ -102,10 +120,10 @@ __device__ __forceinline__ void fft_stage(const float2* src, float2* dst, int N,
                                           const float2* __restrict__ tw, bool prune, int tid, int nthreads) {
     const int R = fft_radix(N, Ns);
     const int nb = N / R;
-    const int tstep = N / (Ns * R);
     const bool zero_hi = prune && Ns == 1;  // legs r >= R/2 read the zero upper half
     const int lgnb = 31 - __clz(nb);
     const bool rs = Ns > 1, ws = Ns * R < N;  // read / write the swizzled intermediate layout
+    const float2* tws = tw + (Ns - 1);        // this stage's twiddles: [k][r-1], k < Ns, r < R
     for (int jj = tid; jj < nb * nf; jj += nthreads) {
         const int f = jj >> lgnb, j = jj & (nb - 1);
         const float2* sf = src + (size_t)f * N;
@@ -117,9 +135,9 @@ __device__ __forceinline__ void fft_stage(const float2* src, float2* dst, int N,
 #pragma unroll
             for (int r = 0; r < 8; ++r) v[r] = (zero_hi && r >= 4) ? make_float2(0.f, 0.f) : sf[fsw(j + r * nb, rs)];
             if (Ns > 1) {
-                const int t1 = k * tstep;
+                const float2* w = tws + k * 7;
 #pragma unroll
-                for (int r = 1; r < 8; ++r) v[r] = twmul<INV>(v[r], tw[r * t1]);
+                for (int r = 1; r < 8; ++r) v[r] = twmul<INV>(v[r], w[r - 1]);
             }
             dft8<INV>(v);
 #pragma unroll
@@ -130,10 +148,10 @@ __device__ __forceinline__ void fft_stage(const float2* src, float2* dst, int N,
             float2 v2 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 2 * nb, rs)];
             float2 v3 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + 3 * nb, rs)];
             if (Ns > 1) {
-                const int t1 = k * tstep;
-                v1 = twmul<INV>(v1, tw[t1]);
-                v2 = twmul<INV>(v2, tw[2 * t1]);
-                v3 = twmul<INV>(v3, tw[3 * t1]);
+                const float2* w = tws + k * 3;
+                v1 = twmul<INV>(v1, w[0]);
+                v2 = twmul<INV>(v2, w[1]);
+                v3 = twmul<INV>(v3, w[2]);
             }
             dft4<INV>(v0, v1, v2, v3);
             df[fsw(idxD, ws)] = v0;
@@ -143,7 +161,7 @@ __device__ __forceinline__ void fft_stage(const float2* src, float2* dst, int N,
         } else {
             float2 v0 = sf[fsw(j, rs)];
             float2 v1 = zero_hi ? make_float2(0.f, 0.f) : sf[fsw(j + nb, rs)];
-            if (Ns > 1) v1 = twmul<INV>(v1, tw[k * tstep]);
+            if (Ns > 1) v1 = twmul<INV>(v1, tws[k]);
             df[fsw(idxD, ws)] = cadd(v0, v1);
             df[fsw(idxD + Ns, ws)] = csub(v0, v1);
         }
@@ -152,7 +170,10 @@ __device__ __forceinline__ void fft_stage(const float2* src, float2* dst, int N,
 }
 
 // Batched Stockham FFT of `nf` length-N transforms stored back to back in `a`
-// (N a power of two >= 2), `b` the ping-pong buffer. tw[t] = e^{-2 pi i t / N}.
+// (N a power of two >= 2), `b` the ping-pong buffer. `tw` is the stage twiddle table built by
+// fft_stage_twiddles(): stage with sub-length Ns and radix R keeps W^(k r) for k < Ns, 1 <= r < R
+// contiguously per k at offset Ns - 1 (N - 1 entries in all), so each thread reads consecutive
+// entries and a warp's twiddle loads spread over the banks.
 // Radix-8 stages (radix-4/2 for the remainder): each thread keeps one butterfly's
 // 8 points in registers, so a 512-point transform is 3 shared-memory passes.
 // When `prune` is set the upper half of every input is taken as zero and never
