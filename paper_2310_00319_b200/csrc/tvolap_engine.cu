@@ -2,16 +2,18 @@
 //
 // Mirrors tvolap::TvolapEngine / TvolapProcessor (proj/include/tvolap/engine.hpp:33-94,
 // proj/src/engine.cpp:9-118, proj/src/reference.cpp:328-342): construction
-// partitions the IRs on the device, process() runs the fused hop kernel,
-// exchange_filter() stages a replacement set that is latched at the next hop
-// boundary (last staged wins, a staged set survives reset). Device state:
-//   ring  [S][2][M][2L] complex64  frequency-domain delay line (two parity rings)
+// partitions the IRs on the device, process() runs the one-hop kernel,
+// process_hops() the hop-blocked kernel, exchange_filter() stages a replacement
+// set that is latched at the next hop boundary (last staged wins, a staged set
+// survives reset). Device state:
+//   ring  [S][2][D][2L] complex64  frequency-domain delay line, D = M + 8 slots per parity
 //   pool  [entries][E][M][2L]       filter partition spectra; set engines keep
-//                                   two slots of S entries (active / staged),
+//                                   three slots of S entries (active / staged / spare),
 //                                   bank engines the whole bank
 //   hist  [S][L], ola [S][E][3L]    per-lane time-domain state
 // Host pointers are streamed through pinned staging buffers: H2D, kernel and
 // D2H of consecutive chunks run on three streams so copies overlap compute.
+// Staged filter sets are transformed (K4) on a high-priority side stream.
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -1,25 +1,27 @@
 // TVOLAP hot-path kernels for sm_100a.
 //
 // The reference processes one hop per lane with scalar fp64 code
-// (proj/src/engine.cpp:60-106). Here one fused kernel runs n_hops consecutive
-// hops for all sources. Each source is owned by a cluster of P CTAs (thread
-// block cluster, distributed shared memory); per hop every CTA
-//   K1  frames the hop with the periodic Hann window and takes the 4L real
-//       FFT as a pruned 2L-point complex Stockham FFT in shared memory
+// (proj/src/engine.cpp:60-106). Here each source (lane) is owned by a thread
+// block cluster of P CTAs (distributed shared memory); every CTA owns 1/P of
+// the spectrum bins and 1/P of the output samples. Per hop:
+//   K1  frame the hop with the periodic Hann window and take the 4L real FFT as
+//       a pruned 2L-point complex Stockham FFT in shared memory
 //       (engine.cpp:77-82, spectral.cpp:99-125),
-//   K2  writes its 1/P slice of the packed spectrum into the HBM delay line,
-//       two parity rings of depth M (ring[s][hop&1][(hop>>1) mod M]) —
-//       equivalent to the reference's 2M-1 ring read at stride 2
-//       (engine.hpp:41, engine.cpp:69-70,88),
-//   K3  accumulates Y = sum_m H[m] (.) X_{hop-2m} over its bin slice with
-//       coalesced 128-bit loads, M split over thread groups and reduced in smem
+//   K2  write the packed spectrum into the HBM delay line: two parity rings of
+//       D = M + 8 slots (ring[s][hop&1][(hop>>1) mod D]) — equivalent to the
+//       reference's 2M-1 ring read at stride 2 (engine.hpp:41, engine.cpp:69-70,88),
+//   K3  accumulate Y = sum_m H[m] (.) X_{hop-2m} over the bin slice with
+//       coalesced 128-bit loads, partitions in contiguous groups reduced in smem
 //       (engine.cpp:85-92, spectral.cpp:160-166),
-//   K5  gathers the full Y from the cluster over DSMEM, takes the inverse real
-//       FFT and does the hop-2 overlap-add with gain 1/2 for its 1/P share of
-//       the output (spectral.cpp:127-158, engine.cpp:94-102).
-// Lanes never wait on each other, so the kernel needs no grid-wide sync and
-// state (input history, OLA accumulators) stays in shared memory across the
-// hops of one launch.
+//   K5  gather Y over DSMEM, inverse real FFT, hop-2 overlap-add with gain 1/2
+//       (spectral.cpp:127-158, engine.cpp:94-102).
+// tvolap_hop_kernel runs one hop at a time (process(), the latency path);
+// tvolap_block_kernel runs blocks of J hops with the delay-line / filter slices
+// shared across the block's hops (process_hops(), the throughput path). Both
+// use the same operations in the same order, so their outputs are bit-identical.
+// partition_kernel is K4 (partition.cpp:20-51) for staged filter sets.
+// Lanes never wait on each other: no grid-wide sync; history and OLA state stay
+// in shared memory across the hops of a launch.
 //
 // Spectra are stored packed: 2L complex64 per frame, bin 0 holding
 // (Re X_0, Re X_2L) — both are exactly real (spectral.cpp:121-123) — so a frame
