@@ -140,6 +140,8 @@ constexpr int kMaxJH = 8;  // largest hop block / 2 (ring slack per parity)
 // Filter-set slots: active + staged + one more, so the transform of the next staged set
 // may start while the two previous periods' hop kernels still read their sets.
 constexpr int kSlots = 3;
+// Host-IR upload buffers: uploads run on their own stream up to this many sets ahead.
+constexpr int kIrStage = 4;
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -153,7 +155,7 @@ struct tvolap_engine {
     long L = 0, M = 0, S = 0, E = 1, N = 0;
     bool bank = false;
     long n_bank = 0;
-    cudaStream_t own = nullptr, stream = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaStream_t own = nullptr, stream = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr, upl = nullptr;
     cudaEvent_t ev_side = nullptr, ev_main = nullptr, ev_start = nullptr;
     cudaEvent_t ev_slot[kSlots] = {};  // last hop kernel that read each filter slot
     float2 *ring = nullptr, *pool = nullptr, *tw = nullptr, *pk = nullptr;
@@ -169,10 +171,10 @@ struct tvolap_engine {
     const float* staged_ir = nullptr;
     long staged_len = 0;
     int staged_buf = -1;             // upload buffer holding it (-1: caller's device memory)
-    float* d_irst[2] = {};           // double-buffered host-IR uploads
-    size_t irst_cap[2] = {};
+    float* d_irst[kIrStage] = {};    // host-IR upload buffers (round robin)
+    size_t irst_cap[kIrStage] = {};
     int irst_next = 0;
-    cudaEvent_t ev_up[2] = {}, ev_used[2] = {};  // upload landed / consuming kernel done
+    cudaEvent_t ev_up[kIrStage] = {}, ev_used[kIrStage] = {};  // upload landed / consuming kernel done
     const float* launch_new_ir = nullptr;  // latched: the next launch transforms this set
     long launch_new_len = 0;
     int launch_buf = -1;
@@ -205,20 +207,22 @@ struct tvolap_engine {
         if (stream) cudaStreamSynchronize(stream);
         if (side) cudaStreamSynchronize(side);
         for (void* p : {(void*)ring, (void*)pool, (void*)tw, (void*)pk, (void*)win, (void*)hist, (void*)ola,
-                        (void*)d_sel, (void*)d_irstage, (void*)d_irst[0], (void*)d_irst[1], (void*)d_in[0],
+                        (void*)d_sel, (void*)d_irstage, (void*)d_irst[0], (void*)d_irst[1], (void*)d_irst[2],
+                        (void*)d_irst[3], (void*)d_in[0],
                         (void*)d_in[1], (void*)d_out[0],
                         (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1]})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
         for (cudaEvent_t ev : {ev_side, ev_main, ev_start, ev_in[0], ev_in[1], ev_k[0], ev_k[1], ev_o[0], ev_o[1],
-                                ev_slot[0], ev_slot[1], ev_slot[2], ev_up[0], ev_up[1], ev_used[0], ev_used[1]})
+                                ev_slot[0], ev_slot[1], ev_slot[2], ev_up[0], ev_up[1], ev_up[2], ev_up[3],
+                                ev_used[0], ev_used[1], ev_used[2], ev_used[3]})
             if (ev) cudaEventDestroy(ev);
         for (auto& pr : prof_events) {
             cudaEventDestroy(pr.first);
             cudaEventDestroy(pr.second);
         }
-        for (cudaStream_t s : {own, side, h2d, d2h})
+        for (cudaStream_t s : {own, side, h2d, d2h, upl})
             if (s) cudaStreamDestroy(s);
     }
 };
@@ -316,10 +320,12 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     CK(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, prio_hi));
     CK(cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->upl, cudaStreamNonBlocking));
     e->stream = e->own;
     for (cudaEvent_t* ev : {&e->ev_side, &e->ev_main, &e->ev_start, &e->ev_in[0], &e->ev_in[1], &e->ev_k[0],
                             &e->ev_k[1], &e->ev_o[0], &e->ev_o[1], &e->ev_slot[0], &e->ev_slot[1],
-                            &e->ev_slot[2], &e->ev_up[0], &e->ev_up[1], &e->ev_used[0], &e->ev_used[1]})
+                            &e->ev_slot[2], &e->ev_up[0], &e->ev_up[1], &e->ev_up[2], &e->ev_up[3],
+                            &e->ev_used[0], &e->ev_used[1], &e->ev_used[2], &e->ev_used[3]})
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     Tables t(e->N);
     std::vector<float> w = hann(hop);
@@ -732,16 +738,18 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
             e->staged_buf = -1;
         } else {
             const int b = e->irst_next;
-            e->irst_next ^= 1;
-            CK(cudaStreamWaitEvent(e->side, e->ev_used[b], 0));
+            e->irst_next = (b + 1) % kIrStage;
+            CK(cudaStreamWaitEvent(e->upl, e->ev_used[b], 0));
             if (e->irst_cap[b] < count) {
+                CK(cudaStreamSynchronize(e->upl));
                 CK(cudaStreamSynchronize(e->side));
+                CK(cudaStreamSynchronize(e->stream));
                 if (e->d_irst[b]) CK(cudaFree(e->d_irst[b]));
                 e->d_irst[b] = dalloc<float>(count);
                 e->irst_cap[b] = count;
             }
-            CK(cudaMemcpyAsync(e->d_irst[b], ir, count * sizeof(float), cudaMemcpyHostToDevice, e->side));
-            CK(cudaEventRecord(e->ev_up[b], e->side));
+            CK(cudaMemcpyAsync(e->d_irst[b], ir, count * sizeof(float), cudaMemcpyHostToDevice, e->upl));
+            CK(cudaEventRecord(e->ev_up[b], e->upl));
             e->staged_ir = e->d_irst[b];
             e->staged_buf = b;
         }
@@ -750,6 +758,7 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
         if (e->k4_side) {  // transform now on the side stream, after the last reader of the target slot
             const int target = (e->active + 1) % kSlots;
             CK(cudaStreamWaitEvent(e->side, e->ev_slot[target], 0));
+            if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->side, e->ev_up[e->staged_buf], 0));
             CK(tvb::launch_partition((int)e->L, (int)e->M, channels, e->staged_ir, ir_length, ir_length, e->pool,
                                      (long)target * e->S, e->tw, e->pk, e->side));
             ++e->launches;
