@@ -174,6 +174,7 @@ struct tvolap_engine {
     float* d_irst[kIrStage] = {};    // host-IR upload buffers (round robin)
     size_t irst_cap[kIrStage] = {};
     int irst_next = 0;
+    int ir_stages = 2;               // upload buffers in use (<= kIrStage)
     cudaEvent_t ev_up[kIrStage] = {}, ev_used[kIrStage] = {};  // upload landed / consuming kernel done
     const float* launch_new_ir = nullptr;  // latched: the next launch transforms this set
     long launch_new_len = 0;
@@ -241,6 +242,7 @@ void pick_launch_config(tvolap_engine* e) {
     if (et > 0) e->NT = et;
     e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
     e->k4_side = env_int("TVOLAP_K4_SIDE", 1) != 0;
+    e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 2)));
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -738,7 +740,7 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
             e->staged_buf = -1;
         } else {
             const int b = e->irst_next;
-            e->irst_next = (b + 1) % kIrStage;
+            e->irst_next = (b + 1) % e->ir_stages;
             CK(cudaStreamWaitEvent(e->upl, e->ev_used[b], 0));
             if (e->irst_cap[b] < count) {
                 CK(cudaStreamSynchronize(e->upl));
