@@ -174,7 +174,8 @@ struct tvolap_engine {
     float* d_irst[kIrStage] = {};    // host-IR upload buffers (round robin)
     size_t irst_cap[kIrStage] = {};
     int irst_next = 0;
-    int ir_stages = 2;               // upload buffers in use (<= kIrStage)
+    int ir_stages = 1;               // upload buffers in use (<= kIrStage); 1 measured best: uploads
+                                     // running ahead delay the audio H2D on the critical path
     cudaEvent_t ev_up[kIrStage] = {}, ev_used[kIrStage] = {};  // upload landed / consuming kernel done
     const float* launch_new_ir = nullptr;  // latched: the next launch transforms this set
     long launch_new_len = 0;
@@ -242,7 +243,7 @@ void pick_launch_config(tvolap_engine* e) {
     if (et > 0) e->NT = et;
     e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
     e->k4_side = env_int("TVOLAP_K4_SIDE", 1) != 0;
-    e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 2)));
+    e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 1)));
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
