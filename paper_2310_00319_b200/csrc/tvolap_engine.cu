@@ -256,7 +256,10 @@ void pick_block_geometry(tvolap_engine* e) {
         const long cap = std::min<long>(8, e->L);
         if (e->bank) {
             while (pb < cap && e->S * pb < 256) pb *= 2;
-            e->JH = e->E == 2 ? 2 : 8;  // C5 sweep: 16-hop blocks 131 us/hop vs 170 (8) vs 292 (one-hop)
+            // sweep: C5 (one ear) 16-hop blocks 118 us/hop vs 158 (8) vs 292 (one-hop kernel);
+            // C3 (two ears) cluster of 2 with 8-hop blocks 60 us/hop vs 65 (P1, J4)
+            e->JH = e->E == 2 ? 4 : 8;
+            if (e->E == 2) pb = std::min<long>(cap, std::max<long>(pb, 2));
         } else {
             while (pb < cap && e->S * pb < 256) pb *= 2;
             if (e->L >= 512) pb = cap;

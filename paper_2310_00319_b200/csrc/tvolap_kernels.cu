@@ -939,7 +939,7 @@ static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaSt
     if constexpr (BANK && E == 1 && JH == 8) {
         if (N == 64) fn = tvolap_block_kernel<E, JH, BANK, 64>;
     }
-    if constexpr (BANK && E == 2 && JH == 2) {
+    if constexpr (BANK && E == 2 && JH == 4) {
         if (N == 256) fn = tvolap_block_kernel<E, JH, BANK, 256>;
     }
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
