@@ -97,7 +97,7 @@ def test_cli_process_identity_and_flip(tmp_path):
     y, fs = wav.read_wav(str(out))
     assert y.shape == (4096, 1) and np.abs(y[256:] - 1.0).max() < 1e-5  # first hop: window ramp-in
     inp = tmp_path / "i.wav"
-    x = rnd(3000, 2, 5) * 0.5
+    x = rnd(3000, 1, 5) * 0.5  # mono input (a 2-channel input needs a 2-channel IR, as in the reference)
     wav.write_wav(str(inp), x, 48000.0)
     r = _cli("process", "--input", str(inp), "--ir", "delta:-0.5:3", "--output", str(out), "--block", "256")
     assert r.returncode == 0, r.stderr
