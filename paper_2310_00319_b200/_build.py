@@ -62,6 +62,17 @@ def build(force: bool = False, verbose: bool = False) -> None:
               f"-Wl,-rpath,{LIB}", "-Wl,-rpath,$ORIGIN"])
 
 
+def build_variant(name: str, defines, verbose: bool = False) -> Path:
+    """Diagnostic build of the CUDA library into lib/<name>/ (e.g. TVOLAP_PHASE_PROF for
+    scripts/phase_prof.py). Never loaded by the product path."""
+    out = LIB / name / "libtvolap_b200.so"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    if _stale(out, CUDA_DEPS):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", out, *CUDA_SOURCES])
+    return out
+
+
 def build_oracle(force: bool = False) -> None:
     """TEST INFRASTRUCTURE: the fp64 CPU oracle (oracle/Makefile)."""
     args = ["make", "-s", "-C", ROOT / "oracle"]

@@ -261,9 +261,12 @@ void pick_block_geometry(tvolap_engine* e) {
             e->JH = e->E == 2 ? 4 : 8;
             if (e->E == 2) pb = std::min<long>(cap, std::max<long>(pb, 2));
         } else {
+            // sweep (profiles/r01_sweep_j16.jsonl): 16-hop blocks with the float2 unified MAC win
+            // everywhere they fit — C2 1.60 vs 2.34 us/hop (8-hop), C1 0.83 vs 1.21, C4 (P = 8)
+            // 31.6 vs 42.2; the shared-memory check below halves JH where they do not fit.
             while (pb < cap && e->S * pb < 256) pb *= 2;
             if (e->L >= 512) pb = cap;
-            e->JH = (e->L >= 512 || e->S * pb >= 256) ? 4 : 8;
+            e->JH = 8;
         }
         e->PB = (int)pb;
         const int eb = env_int("TVOLAP_PB", 0), ej = env_int("TVOLAP_JH", 0);
@@ -286,7 +289,7 @@ void pick_block_geometry(tvolap_engine* e) {
     // The blocked kernel splits the partitions into NTB / (items per group) contiguous groups;
     // the one-hop kernel uses the same grouping so process() and process_hops() agree bit for bit.
     const long Vb = e->N / (2 * e->PB);
-    const long items = (!e->bank && e->JH <= 4) ? Vb : 2 * Vb;  // unified vs per-parity mapping
+    const long items = (!e->bank && e->JH <= 4) ? Vb : 2 * Vb;  // float4 unified vs float2 unified / per-parity
     e->QM = items < e->NTB ? (int)(e->NTB / items) : 1;
 }
 

@@ -30,12 +30,35 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "tvolap_fft.cuh"
 #include "tvolap_internal.cuh"
 #include "workload.h"
 
 namespace cg = cooperative_groups;
+
+#ifdef TVOLAP_PHASE_PROF
+// Diagnostic build only (scripts/phase_prof.py): SM cycles per block-kernel phase, summed over
+// CTAs (thread 0 of each CTA), read back with tvolap_phase_counters().
+__device__ unsigned long long g_phase[16];
+#define PHASE_MARK(k)                                          \
+    do {                                                       \
+        if (threadIdx.x == 0) {                                \
+            const long long t_ = clock64();                    \
+            atomicAdd(&g_phase[k], (unsigned long long)(t_ - ph_t)); \
+            ph_t = t_;                                         \
+        }                                                      \
+    } while (0)
+#define PHASE_START() long long ph_t = clock64()
+#else
+#define PHASE_MARK(k) \
+    do {              \
+    } while (0)
+#define PHASE_START() \
+    do {              \
+    } while (0)
+#endif
 
 namespace tvb {
 namespace {
@@ -70,6 +93,11 @@ __device__ __forceinline__ void cmac4(float4& acc, float& aux, const float4 h, c
     acc.w = fmaf(h.z, x.w, acc.w);
     acc.w = fmaf(h.w, x.z, acc.w);
     aux = fmaf(h.y, x.y, aux);  // Nyquist product, only kept for the packed bin 0
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
 }
 
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
@@ -298,9 +326,21 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
 // results equal hop-by-hop processing. Ring depth D >= M + JH keeps the slots a
 // block writes ahead from colliding with slots its earlier hops still read.
 // ============================================================================
+// Staging depth of the unified MAC: m-steps whose delay-line / filter float4s are in flight
+// (cp.async, L2 -> shared) per thread ahead of the FMAs.
+constexpr int kMacStages = 4;
+
+// MAC work mapping of the hop-blocked kernel: per thread one float4 (two packed bins) for both
+// parity groups (set engines, J <= 8), one float2 (one bin) for both parity groups (set engines,
+// J = 16: half the accumulator registers per output), or one float4 of one parity group (bank).
+enum MacMap { kUni4, kUni2, kParity };
+__host__ __device__ constexpr MacMap mac_map(bool bank, int J) { return bank ? kParity : (J <= 8 ? kUni4 : kUni2); }
+
 struct BlockLayout {
-    size_t tw, pk, win, xin, fa, fb, yb, red, ola, total;
-    // bank: per-parity MAC mapping (threads / 2V partition groups); else unified for J <= 8 (threads / V).
+    size_t tw, pk, win, xin, yb, fa, fb, red, stg, ola, total;
+    // fa | fb (FFT ping-pong) are idle during the MAC: the unified MAC's per-thread staging ring
+    // and the partition-group partial sums (red) alias them; red is written only after every
+    // thread has drained its ring, and is consumed before the inverse FFT reuses fa.
     __host__ __device__ BlockLayout(int L, int P, int E, int J, bool bank, int threads) {
         const size_t N = 2 * (size_t)L;
         const size_t fpc = (J + P - 1) / P;  // frames owned per CTA
@@ -309,16 +349,21 @@ struct BlockLayout {
         pk = align16(tw + N * sizeof(float2));
         win = align16(pk + (N + 2) * sizeof(float2));
         xin = align16(win + N * sizeof(float));
-        fa = align16(xin + 2 * (size_t)(J + 1) * L * sizeof(float));  // double-buffered block inputs
+        yb = align16(xin + (size_t)(J + 1) * L * sizeof(float));  // [history | J hops]
+        fa = align16(yb + (size_t)J * E * Np * sizeof(float2));
         fb = align16(fa + fpc * E * N * sizeof(float2));
-        yb = align16(fb + fpc * E * N * sizeof(float2));
-        red = align16(yb + (size_t)J * E * Np * sizeof(float2));
         const size_t V = Np / 2;
-        const bool unified = !bank && J <= 8;
-        const size_t W = unified ? V : 2 * V;
+        const MacMap mm = mac_map(bank, J);
+        const size_t W = mm == kUni4 ? V : 2 * V;  // work items per partition group
         const size_t qmax = W < (size_t)threads ? threads / W : 1;
         const size_t red_bytes = qmax > 1 ? qmax * J * E * V * sizeof(float4) : 0;
-        ola = align16(red + red_bytes);
+        red = fa;
+        stg = fa;
+        const size_t stg_bytes = mm == kUni4 ? (size_t)threads * kMacStages * (2 + E) * sizeof(float4) : 0;
+        size_t end = fb + fpc * E * N * sizeof(float2);
+        if (red + red_bytes > end) end = red + red_bytes;
+        if (stg + stg_bytes > end) end = stg + stg_bytes;
+        ola = align16(end);
         total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
     }
 };
@@ -343,6 +388,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     const int r = blockIdx.x % P;
     const BlockLayout lay(L, P, E, J, BANK, NT);
     (void)Q;
+    PHASE_START();
     float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
     float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
     float* s_win = reinterpret_cast<float*>(smem + lay.win);
@@ -367,19 +413,24 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         s_win[i] = p.win[i];
     }
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
-    float* xcur = s_xin;                       // this block's inputs: [history | J hops]
-    float* xnxt = s_xin + (size_t)(J + 1) * L;  // next block's, prefetched with cp.async
+    float* xcur = s_xin;  // this block's inputs: [history | J hops]
     for (int i = tid; i < L; i += NT) xcur[i] = p.hist[(long)s * L + i];
-    auto prefetch_block = [&](float* dst, int b) {  // hops b .. b+J-1 of this source into dst[L..]
+    // hops b .. b+J-1 of this source into xcur[L..] (cp.async; lands while the block's MAC runs)
+    const bool in_vec = (L & 3) == 0 && (p.in_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(p.in) & 15) == 0;
+    auto prefetch_block = [&](int b) {
         const int jn = min(J, p.n_hops - b);
         const float* src = p.in + (long)s * p.in_stride + (long)b * L;
-        for (int i = tid; i < jn * L; i += NT) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + L + i);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + i));
+        if (in_vec) {
+            for (int i = 4 * tid; i < jn * L; i += 4 * NT) cp_async16(xcur + L + i, src + i);
+        } else {
+            for (int i = tid; i < jn * L; i += NT) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(xcur + L + i);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + i));
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::);
     };
-    prefetch_block(xcur, 0);
+    prefetch_block(0);
     if (p.new_ir) {  // latch a staged filter set: transform it here (K4) while block 0's input lands
         __syncthreads();
         fused_partition<NC>(p, s, r, P, s_fa, s_fb, ((J + P - 1) / P) * E, s_tw, s_pk, tid, NT);
@@ -393,17 +444,15 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     const float4* ring4 = reinterpret_cast<const float4*>(p.ring);
     const float4* pool4 = reinterpret_cast<const float4*>(p.pool);
     cg::cluster_group cluster = cg::this_cluster();
+    PHASE_MARK(11);
 
     for (int b0 = 0; b0 < p.n_hops; b0 += J) {
         const long l0 = p.hop0 + b0;
         const int jb = min(J, p.n_hops - b0);
-        // ---- inputs: this block's landed (prefetched one block ago); start the next block's copy
-        if (b0 + J < p.n_hops)
-            prefetch_block(xnxt, b0 + J);
-        else
-            asm volatile("cp.async.commit_group;\n" ::);
-        asm volatile("cp.async.wait_group 1;\n" ::);
+        // ---- inputs: this block's landed (prefetched during the previous block)
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
+        PHASE_MARK(0);
 
         // ---- K1/K2: this CTA's frames (j = r, r+P, ...): window, FFT, whole spectrum into the ring.
         const int nf = jb > r ? (jb - r + P - 1) / P : 0;
@@ -413,6 +462,11 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             s_fa[(size_t)f * N + jj] = make_float2(xs[2 * jj] * s_win[2 * jj], xs[2 * jj + 1] * s_win[2 * jj + 1]);
         }
         __syncthreads();
+        // history for the next block = last input hop of this block; then start the next
+        // block's input copy into the (now free) hop area
+        for (int i = tid; i < L; i += NT) xcur[i] = xcur[(size_t)jb * L + i];
+        __syncthreads();
+        if (b0 + J < p.n_hops) prefetch_block(b0 + J);
         if (nf > 0) {
             const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
             for (int f = 0; f < nf; ++f) {
@@ -421,7 +475,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                 untangle_store<NC>(Z + (size_t)f * N, N, s_pk, ringw, tid, NT);
             }
         }
+        PHASE_MARK(1);
         block_sync(P);  // ring writes of all frames visible cluster-wide
+        PHASE_MARK(2);
 
         // ---- K3: hop-blocked MAC over this CTA's bin slice.
         // Does every hop of the block use the same filter set (set engines: always)?
@@ -432,7 +488,8 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             for (int jj = 1; jj < jb; ++jj) all_same &= p.sched[(long)(b0 + jj) * p.sched_stride + s] == ent0;
         }
         int Qeff;
-        if (!BANK && JH <= 4) {
+        constexpr MacMap kMap = mac_map(BANK, J);
+        if constexpr (kMap == kUni4) {
             // Unified mapping: one thread per float4 covers both parity groups, so each filter
             // slice is loaded once per block for all J outputs; two sliding delay-line windows.
             Qeff = V < NT ? NT / V : 1;
@@ -474,53 +531,54 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                         }
                         win[g][i] = __ldcg(xs(g, i - mu0));
                     }
-                int m = mu0;
-                constexpr int U = 2;
-                for (; m + U <= mu1; m += U) {
-                    float4 xn[U][2], hh[U][E];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
+                // Per-thread staging ring in shared memory: step m's two delay-line float4s and
+                // E filter float4s land in slot (m - mu0) % kMacStages via cp.async (L2 -> smem),
+                // kMacStages steps ahead of the FMAs. Each thread reads back only what it copied
+                // itself, so wait_group is the only synchronisation needed.
+                float4* stg = reinterpret_cast<float4*>(smem + lay.stg) + tid;
+                constexpr int CS = 2 + E;
+                auto stage = [&](int mm, int k) {
+                    if (mm < mu1) {
 #pragma unroll
                         for (int g = 0; g < 2; ++g) {
-                            xn[u][g] = __ldcg(xr[g] + (long)cur[g] * spec4);
+                            cp_async16(stg + (size_t)(k * CS + g) * NT, xr[g] + (long)cur[g] * spec4);
                             cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
                         }
 #pragma unroll
-                        for (int e = 0; e < E; ++e) hh[u][e] = __ldcg(hb4[e] + (long)(m + u) * spec4);
+                        for (int e = 0; e < E; ++e)
+                            cp_async16(stg + (size_t)(k * CS + 2 + e) * NT, hb4[e] + (long)mm * spec4);
                     }
+                    asm volatile("cp.async.commit_group;\n" ::);
+                };
+                auto step = [&](int mm, int k) {
+                    asm volatile("cp.async.wait_group %0;\n" ::"n"(kMacStages - 1));
+                    float4 xn[2], hh[E];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
+                    for (int g = 0; g < 2; ++g) xn[g] = stg[(size_t)(k * CS + g) * NT];
 #pragma unroll
-                        for (int g = 0; g < 2; ++g) {
-#pragma unroll
-                            for (int i = 0; i < JU; ++i)
-#pragma unroll
-                                for (int e = 0; e < E; ++e) cmac4(acc[g][i][e], aux[g][i][e], hh[u][e], win[g][i]);
-#pragma unroll
-                            for (int i = JU - 1; i > 0; --i) win[g][i] = win[g][i - 1];
-                            win[g][0] = xn[u][g];
-                        }
-                    }
-                }
-                for (; m < mu1; ++m) {
-                    const float4 x0 = __ldcg(xr[0] + (long)cur[0] * spec4), x1 = __ldcg(xr[1] + (long)cur[1] * spec4);
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
-#pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const float4 h = __ldcg(hb4[e] + (long)m * spec4);
-#pragma unroll
-                        for (int g = 0; g < 2; ++g)
-#pragma unroll
-                            for (int i = 0; i < JU; ++i) cmac4(acc[g][i][e], aux[g][i][e], h, win[g][i]);
-                    }
+                    for (int e = 0; e < E; ++e) hh[e] = stg[(size_t)(k * CS + 2 + e) * NT];
 #pragma unroll
                     for (int g = 0; g < 2; ++g) {
 #pragma unroll
+                        for (int i = 0; i < JU; ++i)
+#pragma unroll
+                            for (int e = 0; e < E; ++e) cmac4(acc[g][i][e], aux[g][i][e], hh[e], win[g][i]);
+#pragma unroll
                         for (int i = JU - 1; i > 0; --i) win[g][i] = win[g][i - 1];
-                        win[g][0] = g ? x1 : x0;
+                        win[g][0] = xn[g];
                     }
+                    stage(mm + kMacStages, k);
+                };
+#pragma unroll
+                for (int k = 0; k < kMacStages; ++k) stage(mu0 + k, k);
+                int m = mu0;
+                for (; m + kMacStages <= mu1; m += kMacStages) {
+#pragma unroll
+                    for (int k = 0; k < kMacStages; ++k) step(m + k, k);
                 }
+                for (int k = 0; m < mu1; ++m, ++k) step(m, k);
+                asm volatile("cp.async.wait_all;\n" ::);
+                if (Qeff > 1) __syncthreads();  // s_red aliases the staging rings (one f per thread here)
 #pragma unroll
                 for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -540,6 +598,114 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                                 s_red[(((size_t)qq * J + jj) * E + e) * V + f] = a;
                         }
                     }
+            }
+        } else if constexpr (kMap == kUni2) {
+            // Unified float2 mapping (16-hop blocks): one thread per packed bin covers both parity
+            // groups, 8 outputs each, so every filter and delay-line element is loaded once per
+            // 16 hops. Partition groups: Qeff = threads / Np (same count as the per-parity mapping).
+            static_assert(E == 1, "filter-set engines have one ear");
+            Qeff = Np < NT ? NT / Np : 1;
+            const int qq = Np < NT ? tid / Np : 0;
+            const int mu0 = (int)((long)qq * M / Qeff), mu1 = (int)((long)(qq + 1) * M / Qeff);
+            const float2* ring2 = p.ring;
+            const float2* pool2 = p.pool;
+            for (int f = (Np >= NT ? tid : tid % Np); f < Np; f += (Np >= NT ? NT : Np)) {
+                // the packed bin 0 (r == 0, f == 0) needs the Nyquist product: warps holding it
+                // run the variant with the extra accumulator (warp-uniform branch)
+                const bool pkw = __any_sync(0xffffffffu, r == 0 && f == 0);
+                auto mac = [&](auto pk_tag) {
+                    constexpr bool PK = decltype(pk_tag)::value;
+                    const float2* xr[2];
+                    long sbp[2];
+                    int cur[2];
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        const long hbg = l0 + g;
+                        xr[g] = ring2 + (((long)s * 2 + (hbg & 1)) * D) * N + (long)r * Np + f;
+                        sbp[g] = hbg >> 1;
+                        cur[g] = (int)(((sbp[g] - mu0 - 1) % D + D) % D);
+                    }
+                    const float2* hb = pool2 + ((long)ent0 * M) * N + (long)r * Np + f;
+                    float2 acc[2][JH];
+                    float aux[2][PK ? JH : 1];
+                    float2 win[2][JH];
+#pragma unroll
+                    for (int g = 0; g < 2; ++g)
+#pragma unroll
+                        for (int i = 0; i < JH; ++i) {
+                            acc[g][i] = make_float2(0.f, 0.f);
+                            if constexpr (PK) aux[g][i] = 0.f;
+                            long sl = (sbp[g] + i - mu0) % D;
+                            if (sl < 0) sl += D;
+                            win[g][i] = __ldcg(xr[g] + sl * N);
+                        }
+                    auto mac_step = [&](const float2 (&xn)[2], const float2 h) {
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+#pragma unroll
+                            for (int i = 0; i < JH; ++i) {
+                                float2& a = acc[g][i];
+                                const float2 x = win[g][i];
+                                a.x = fmaf(h.x, x.x, a.x);
+                                a.x = fmaf(-h.y, x.y, a.x);
+                                a.y = fmaf(h.x, x.y, a.y);
+                                a.y = fmaf(h.y, x.x, a.y);
+                                if constexpr (PK) aux[g][i] = fmaf(h.y, x.y, aux[g][i]);
+                            }
+#pragma unroll
+                            for (int i = JH - 1; i > 0; --i) win[g][i] = win[g][i - 1];
+                            win[g][0] = xn[g];
+                        }
+                    };
+                    int m = mu0;
+                    constexpr int U = 4;
+                    for (; m + U <= mu1; m += U) {
+                        float2 xn[U][2], hh[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+#pragma unroll
+                            for (int g = 0; g < 2; ++g) {
+                                xn[u][g] = __ldcg(xr[g] + (long)cur[g] * N);
+                                cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
+                            }
+                            hh[u] = __ldcg(hb + (long)(m + u) * N);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) mac_step(xn[u], hh[u]);
+                    }
+                    for (; m < mu1; ++m) {
+                        float2 xn[2];
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            xn[g] = __ldcg(xr[g] + (long)cur[g] * N);
+                            cur[g] = cur[g] == 0 ? D - 1 : cur[g] - 1;
+                        }
+                        mac_step(xn, __ldcg(hb + (long)m * N));
+                    }
+                    float2* red2 = reinterpret_cast<float2*>(s_red);
+#pragma unroll
+                    for (int g = 0; g < 2; ++g)
+#pragma unroll
+                        for (int i = 0; i < JH; ++i) {
+                            const int jj = g + 2 * i;
+                            if (jj >= jb) continue;
+                            float2 a = acc[g][i];
+                            if constexpr (PK) {
+                                if (r == 0 && f == 0) {  // packed bin 0: two real products
+                                    a.x += aux[g][i];
+                                    a.y = aux[g][i];
+                                }
+                            }
+                            if (Qeff == 1)
+                                s_yb[(size_t)jj * Np + f] = a;
+                            else
+                                red2[((size_t)qq * J + jj) * Np + f] = a;
+                        }
+                };
+                if (pkw)
+                    mac(std::true_type{});
+                else
+                    mac(std::false_type{});
             }
         } else {
         Qeff = W < NT ? NT / W : 1;
@@ -657,6 +823,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             }
         }
         }
+        PHASE_MARK(3);
         if (Qeff > 1) {
             __syncthreads();
             for (int i = tid; i < jb * E * V; i += NT) {
@@ -666,7 +833,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                 reinterpret_cast<float4*>(s_yb + (size_t)je * Np)[f] = sum;
             }
         }
+        PHASE_MARK(4);
         block_sync(P);  // Y slices of all frames published
+        PHASE_MARK(5);
 
         // ---- K5a: this CTA's frames: gather Y over DSMEM, tangle, inverse FFT.
         const int nt = nf * E;  // transforms
@@ -690,7 +859,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         const int stages = fft_stage_count(N);
         const float* ytd = reinterpret_cast<const float*>((stages & 1) ? s_fa : s_fb);
         // time-domain frame (f, e) of this CTA = ytd[(f * E + e) * 2N ...] (unscaled)
+        PHASE_MARK(6);
         block_sync(P);  // all frames' time-domain blocks ready
+        PHASE_MARK(7);
 
         // ---- K5b: hop-2 overlap-add for this CTA's sample slice, all frames of the block.
         // Both ping-pong buffers hold the same transform count, so the result buffer
@@ -702,42 +873,49 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             const int ug = r * Lp + u;
             float* A = s_ola + e * 3 * Lp;
             float a0 = A[u], a1 = A[Lp + u], a2 = A[2 * Lp + u];
-            float y[J][4];
-#pragma unroll
-            for (int jj = 0; jj < J; ++jj) {
-                if (jj < jb) {
-                    const int owner = jj & (P - 1), f = jj >> lgP;
-                    const float* base = reinterpret_cast<const float*>(smem + ytd_off);
-                    if (owner != r) base = cluster.map_shared_rank(base, owner);
-                    const float* yf = base + ((size_t)f * E + e) * 2 * N;
-#pragma unroll
-                    for (int d = 0; d < 4; ++d) y[jj][d] = yf[d * L + ug] * sc;
-                } else {
-#pragma unroll
-                    for (int d = 0; d < 4; ++d) y[jj][d] = 0.f;
-                }
-            }
             float* o = p.out + ((long)s * E + e) * p.out_stride + (long)b0 * L + ug;
+            constexpr int JC = J < 8 ? J : 8;  // frames gathered per chunk (register bound)
 #pragma unroll
-            for (int jj = 0; jj < J; ++jj) {
-                if (jj >= jb) break;
-                // pending = contributions of earlier frames: rolling (a0, a1, a2)
-                o[(long)jj * L] = 0.5f * (y[jj][0] + a0);
-                a0 = a1 + y[jj][1];
-                a1 = a2 + y[jj][2];
-                a2 = y[jj][3];
+            for (int j0 = 0; j0 < J; j0 += JC) {
+                if (j0 >= jb) break;
+                float y[JC][4];
+#pragma unroll
+                for (int jc = 0; jc < JC; ++jc) {
+                    const int jj = j0 + jc;
+                    if (jj < jb) {
+                        const int owner = jj & (P - 1), f = jj >> lgP;
+                        const float* base = reinterpret_cast<const float*>(smem + ytd_off);
+                        if (owner != r) base = cluster.map_shared_rank(base, owner);
+                        const float* yf = base + ((size_t)f * E + e) * 2 * N;
+#pragma unroll
+                        for (int d = 0; d < 4; ++d) y[jc][d] = yf[d * L + ug] * sc;
+                    } else {
+#pragma unroll
+                        for (int d = 0; d < 4; ++d) y[jc][d] = 0.f;
+                    }
+                }
+#pragma unroll
+                for (int jc = 0; jc < JC; ++jc) {
+                    const int jj = j0 + jc;
+                    if (jj >= jb) break;
+                    // pending = contributions of earlier frames: rolling (a0, a1, a2)
+                    o[(long)jj * L] = 0.5f * (y[jc][0] + a0);
+                    a0 = a1 + y[jc][1];
+                    a1 = a2 + y[jc][2];
+                    a2 = y[jc][3];
+                }
             }
             A[u] = a0;
             A[Lp + u] = a1;
             A[2 * Lp + u] = a2;
         }
-        // history for the next block = last input hop of this block
-        __syncthreads();
-        for (int i = tid; i < L; i += NT) xnxt[i] = xcur[(size_t)jb * L + i];
-        float* t = xcur;
-        xcur = xnxt;
-        xnxt = t;
+        PHASE_MARK(8);
+        PHASE_MARK(9);
         block_sync(P);  // peers done reading this CTA's Y slices / time-domain frames
+        PHASE_MARK(10);
+#ifdef TVOLAP_PHASE_PROF
+        if (tid == 0) atomicAdd(&g_phase[12], 1ull);
+#endif
     }
     asm volatile("cp.async.wait_all;\n" ::);
     if (r == 0)
@@ -1097,3 +1275,13 @@ cudaError_t launch_mix(long sources, long ears, long samples, const float* out, 
 }
 
 }  // namespace tvb
+
+#ifdef TVOLAP_PHASE_PROF
+extern "C" int tvolap_phase_counters(unsigned long long* out, int n) {
+    unsigned long long zero[16] = {};
+    n = n < 16 ? n : 16;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 6;
+    if (cudaMemcpyFromSymbol(out, g_phase, n * sizeof(unsigned long long)) != cudaSuccess) return 6;
+    return cudaMemcpyToSymbol(g_phase, zero, sizeof(zero)) == cudaSuccess ? 0 : 6;
+}
+#endif
