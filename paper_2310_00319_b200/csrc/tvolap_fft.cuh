@@ -209,6 +209,69 @@ __device__ float2* fft_batch(float2* a, float2* b, int N, int nf, const float2* 
     return src;
 }
 
+// One warp, one transform, in place in a warp-private smem buffer (no CTA barriers): every
+// Stockham stage gathers this lane's butterflies into registers, __syncwarp, scatters the
+// outputs over the same buffer, __syncwarp. Each butterfly does exactly the operations of
+// fft_stage (same twiddles, same radix kernels), so results are bit-identical to fft_batch.
+// The first stage reads its inputs through `load0(n)` (natural order, n < N/2: the upper half
+// is zero, `prune`); the result is left in natural order in `buf`.
+__host__ __device__ constexpr int fft_radix_c(int N, int Ns) {
+    return (N / Ns == 16) ? 4 : (((N / Ns) & 7) == 0 ? 8 : (((N / Ns) & 3) == 0 ? 4 : 2));
+}
+
+template <bool INV, int N, int Ns, class LOAD0>
+__device__ __forceinline__ void fft_warp_stages(float2* buf, const float2* __restrict__ tw, int lane,
+                                                const LOAD0& load0) {
+    if constexpr (Ns < N) {
+        constexpr int R = fft_radix_c(N, Ns);
+        constexpr int nb = N / R;
+        constexpr int BPL = (nb + 31) / 32;  // butterflies per lane
+        constexpr bool rs = Ns > 1, ws = Ns * R < N;
+        const float2* tws = tw + (Ns - 1);
+        float2 v[BPL][R];
+#pragma unroll
+        for (int b = 0; b < BPL; ++b) {
+            const int j = lane + 32 * b;
+            if (nb >= 32 || j < nb) {
+                const int k = j & (Ns - 1);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if constexpr (Ns == 1)
+                        v[b][r] = r < R / 2 ? load0(j + r * nb) : make_float2(0.f, 0.f);
+                    else
+                        v[b][r] = buf[fsw(j + r * nb, rs)];
+                }
+                if constexpr (Ns > 1) {
+#pragma unroll
+                    for (int r = 1; r < R; ++r) v[b][r] = twmul<INV>(v[b][r], tws[k * (R - 1) + (r - 1)]);
+                }
+                if constexpr (R == 8) {
+                    dft8<INV>(v[b]);
+                } else if constexpr (R == 4) {
+                    dft4<INV>(v[b][0], v[b][1], v[b][2], v[b][3]);
+                } else {
+                    const float2 t0 = cadd(v[b][0], v[b][1]), t1 = csub(v[b][0], v[b][1]);
+                    v[b][0] = t0;
+                    v[b][1] = t1;
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < BPL; ++b) {
+            const int j = lane + 32 * b;
+            if (nb >= 32 || j < nb) {
+                const int k = j & (Ns - 1);
+                const int idxD = (j - k) * R + k;
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[fsw(idxD + r * Ns, ws)] = v[b][r];
+            }
+        }
+        __syncwarp();
+        fft_warp_stages<INV, N, Ns * R>(buf, tw, lane, load0);
+    }
+}
+
 // Single transform (nf = 1).
 template <bool INV, int NC = 0>
 __device__ float2* fft_stockham(float2* a, float2* b, int N, const float2* __restrict__ tw, bool prune, int tid,

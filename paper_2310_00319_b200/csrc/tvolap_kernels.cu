@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "tvolap_fft.cuh"
@@ -111,10 +112,38 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 // this launch reads. The caller synchronises the cluster before the MAC.
 template <int NC>
 __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2* fa, float2* fb, int cap,
-                                const float2* tw, const float2* pk, int tid, int NT) {
+                                size_t avail, const float2* tw, const float2* pk, int tid, int NT) {
     const int L = NC ? NC / 2 : p.L, N = 2 * L, M = p.M;
     const float* h = p.new_ir + (long)s * p.new_ir_stride;
     float2* dst = p.pool_w + ((long)(p.new_entry_base + s) * M) * N;
+    if constexpr (NC != 0 && NC <= 1024) {
+        // one warp per partition (as partition_warp_kernel, bit-identical), warp-private buffers
+        // carved from the `avail` bytes at fa; partitions m = r, r + P, ... of this CTA
+        const int wfit = min(NT >> 5, (int)(avail / (NC * sizeof(float2))));
+        const int warp = tid >> 5, lane = tid & 31;
+        const bool vec = (p.new_ir_stride & 1) == 0 && (reinterpret_cast<uintptr_t>(p.new_ir) & 7) == 0;
+        if (warp < wfit) {
+            float2* buf = fa + (size_t)warp * NC;
+            for (int m = r + warp * P; m < M; m += wfit * P) {
+                const long base = (long)m * NC;
+                auto load0 = [&](int n) -> float2 {
+                    const long i0 = base + 2 * n;
+                    if (vec && i0 + 1 < p.new_ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
+                    return make_float2(i0 < p.new_ir_len ? h[i0] : 0.f, i0 + 1 < p.new_ir_len ? h[i0 + 1] : 0.f);
+                };
+                fft_warp_stages<false, NC, 1>(buf, tw, lane, load0);
+                float4* d4 = reinterpret_cast<float4*>(dst + (long)m * NC);
+                for (int k2 = lane; k2 < NC / 2; k2 += 32) {
+                    const float2 a = untangle_packed(buf, NC, 2 * k2, pk);
+                    const float2 b = untangle(buf, NC, 2 * k2 + 1, pk);
+                    d4[k2] = make_float4(a.x, a.y, b.x, b.y);
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        return;
+    }
     const int nm = r < M ? (M - r + P - 1) / P : 0;
     const int lgL = 31 - __clz(L);
     for (int i0 = 0; i0 < nm; i0 += cap) {
@@ -176,7 +205,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     }
     __syncthreads();
     if (p.new_ir) {  // latch a staged filter set: transform it here (K4), then the whole cluster sees it
-        fused_partition<NC>(p, s, r, P, s_fa, s_fb, 1, s_tw, s_pk, tid, NT);
+        fused_partition<NC>(p, s, r, P, s_fa, s_fb, 1, lay.red - lay.fa, s_tw, s_pk, tid, NT);
         if (P > 1)
             cg::this_cluster().sync();
         else
@@ -433,7 +462,8 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     prefetch_block(0);
     if (p.new_ir) {  // latch a staged filter set: transform it here (K4) while block 0's input lands
         __syncthreads();
-        fused_partition<NC>(p, s, r, P, s_fa, s_fb, ((J + P - 1) / P) * E, s_tw, s_pk, tid, NT);
+        fused_partition<NC>(p, s, r, P, s_fa, s_fb, ((J + P - 1) / P) * E, lay.ola - lay.fa, s_tw, s_pk, tid,
+                            NT);
         block_sync(P);
     }
     for (int i = tid; i < E * 3 * Lp; i += NT) {
@@ -991,6 +1021,45 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
     }
 }
 
+// K4, one warp per partition (N <= 1024): no CTA barriers, a warp-private 8N-byte buffer, IR
+// slices read straight into the first FFT stage's registers. Bit-identical to partition_kernel.
+template <int NC>
+__global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows, const float* __restrict__ ir,
+                                                             long ir_stride, long ir_len, float2* __restrict__ pool,
+                                                             long row0, const float2* __restrict__ tw,
+                                                             const float2* __restrict__ pk) {
+    constexpr int N = NC;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* s_tw = reinterpret_cast<float2*>(smem);
+    float2* s_pk = s_tw + N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    float2* buf = reinterpret_cast<float2*>(smem + align16((2 * N + 2) * sizeof(float2))) + (size_t)warp * N;
+    for (int i = tid; i < N; i += blockDim.x) s_tw[i] = tw[i];
+    for (int i = tid; i <= N; i += blockDim.x) s_pk[i] = pk[i];
+    __syncthreads();
+    const bool vec = (ir_stride & 1) == 0 && (reinterpret_cast<uintptr_t>(ir) & 7) == 0;
+    const long tasks = rows * M;
+    for (long t = (long)blockIdx.x * nw + warp; t < tasks; t += (long)gridDim.x * nw) {
+        const long row = t / M;
+        const int m = (int)(t - row * M);
+        const float* h = ir + row * ir_stride;
+        const long base = (long)m * N;  // partition m = IR samples [m N, (m + 1) N), N = 2L
+        auto load0 = [&](int n) -> float2 {  // z_n = (h[2n], h[2n+1])
+            const long i0 = base + 2 * n;
+            if (vec && i0 + 1 < ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
+            return make_float2(i0 < ir_len ? h[i0] : 0.f, i0 + 1 < ir_len ? h[i0 + 1] : 0.f);
+        };
+        fft_warp_stages<false, N, 1>(buf, s_tw, lane, load0);
+        float4* d4 = reinterpret_cast<float4*>(pool + ((row0 + row) * M + m) * N);
+        for (int k2 = lane; k2 < N / 2; k2 += 32) {
+            const float2 a = untangle_packed(buf, N, 2 * k2, s_pk);
+            const float2 b = untangle(buf, N, 2 * k2 + 1, s_pk);
+            d4[k2] = make_float4(a.x, a.y, b.x, b.y);
+        }
+        __syncwarp();
+    }
+}
+
 // forward_real on a batch (spectral.cpp:99-125): full real input of n = 2N samples.
 __global__ void forward_real_kernel(int N, const float* __restrict__ x, float2* __restrict__ bins,
                                     const float2* __restrict__ tw, const float2* __restrict__ pk) {
@@ -1199,8 +1268,45 @@ cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream
     return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
+template <int NC>
+static cudaError_t launch_partition_warp(int M, long rows, const float* ir, long ir_stride, long ir_len,
+                                        float2* pool, long row0, const float2* tw, const float2* pk,
+                                        cudaStream_t stream) {
+    constexpr int kWarps = 8;
+    const size_t smem = align16((2 * NC + 2) * sizeof(float2)) + (size_t)kWarps * NC * sizeof(float2);
+    cudaError_t err = cudaFuncSetAttribute(partition_warp_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+    if (err != cudaSuccess) return err;
+    int per_sm = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, partition_warp_kernel<NC>, 32 * kWarps, smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long tasks = rows * M;
+    const long grid = std::max<long>(1, std::min<long>((tasks + kWarps - 1) / kWarps, (long)sms * std::max(1, per_sm)));
+    partition_warp_kernel<NC><<<(unsigned)grid, 32 * kWarps, smem, stream>>>(M, rows, ir, ir_stride, ir_len, pool,
+                                                                           row0, tw, pk);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
                              long row0, const float2* tw, const float2* pk, cudaStream_t stream) {
+    // one warp per partition for the common transform lengths (TVOLAP_K4_WARP=0: CTA batches)
+    static const bool warp_k4 = [] {
+        const char* v = std::getenv("TVOLAP_K4_WARP");
+        return !(v && v[0] == '0');
+    }();
+    if (warp_k4) {
+        switch (2 * L) {
+            case 64: return launch_partition_warp<64>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
+            case 128: return launch_partition_warp<128>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
+            case 256: return launch_partition_warp<256>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
+            case 512: return launch_partition_warp<512>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
+            case 1024: return launch_partition_warp<1024>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
+            default: break;
+        }
+    }
     // Batches of up to 8 partitions per CTA, 16-byte IR loads: enough bytes in flight to
     // stream the time-domain IRs near HBM speed.
     const int N = 2 * L;

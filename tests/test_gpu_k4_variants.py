@@ -1,0 +1,60 @@
+"""K4 variants agree bit for bit: the warp-per-partition kernel (default), the CTA-batched
+kernel (TVOLAP_K4_WARP=0), and the partition transform fused into the hop kernels
+(TVOLAP_K4_SIDE=0) all run the same butterflies, so spectra and engine outputs are identical."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2310_00319_b200 import tvolap as T
+out = {}
+g = np.random.default_rng(5)
+for hop, n_ir, ch in [(32, 2000, 2), (64, 900, 1), (128, 3000, 3), (256, 33000, 2), (512, 9000, 1), (1024, 5000, 1)]:
+    ir = g.uniform(-1, 1, (n_ir, ch))
+    out[f"p{hop}"] = T.partition(ir, hop).spectra()
+# engine with an exchange every 16 hops (side or fused K4 per the environment)
+hop, S = 256, 4
+sets = [T.partition(g.uniform(-1, 1, (5000, S)), hop, 20) for _ in range(3)]
+x = np.ascontiguousarray(g.uniform(-1, 1, (S, hop * 48)).astype(np.float32))
+e = T.TvolapEngine(sets[0])
+ys = []
+for k in range(3):
+    if k:
+        e.exchange_filter(sets[k])
+    ys.append(e.process_hops(np.ascontiguousarray(x[:, k * 16 * hop:(k + 1) * 16 * hop])))
+out["engine"] = np.concatenate(ys, 1)
+# one-hop kernel path with exchanges (fused K4 in the hop kernel when TVOLAP_K4_SIDE=0)
+e1 = T.TvolapEngine(sets[0])
+y1 = []
+for h in range(6):
+    if h in (2, 4):
+        e1.exchange_filter(sets[h // 2])
+    y1.append(e1.process(np.ascontiguousarray(x[:, h * hop:(h + 1) * hop].T)))
+out["hop"] = np.concatenate(y1)
+np.savez(sys.argv[2], **out)
+"""
+
+
+def _run(tmp_path, name, env_extra):
+    env = dict(os.environ, **env_extra)
+    path = tmp_path / f"{name}.npz"
+    subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), str(path)], check=True, env=env, timeout=600)
+    return np.load(path)
+
+
+def test_k4_variants_bit_identical(tmp_path):
+    base = _run(tmp_path, "warp", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "1"})
+    for name, env in [("cta", {"TVOLAP_K4_WARP": "0", "TVOLAP_K4_SIDE": "1"}),
+                      ("fused", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "0"})]:
+        other = _run(tmp_path, name, env)
+        for k in base.files:
+            assert np.array_equal(base[k], other[k]), (name, k)
