@@ -110,9 +110,11 @@ struct Tables {
     std::vector<float2> tw, pk;
     explicit Tables(long nc) {
         const double pi = 3.14159265358979323846264338327950288;
-        tw.resize(nc);
-        tvb::fft_stage_twiddles((int)nc, tw.data(),
-                                [](double c, double s) { return make_float2((float)c, (float)s); });
+        // [stage table (nc) | warp four-step tables (nc + 32)]
+        auto mk = [](double c, double s) { return make_float2((float)c, (float)s); };
+        tw.assign(2 * nc + 32, make_float2(0.f, 0.f));
+        tvb::fft_stage_twiddles((int)nc, tw.data(), mk);
+        if (nc >= 64 && nc <= 1024) tvb::fft_warp_twiddles((int)nc, tw.data() + nc, mk);
         pk.resize(nc + 2);
         for (long k = 0; k <= nc; ++k) {
             const double a = -2.0 * pi * (double)k / (double)(2 * nc);
@@ -182,6 +184,8 @@ struct tvolap_engine {
     int launch_buf = -1;
     bool k4_side = false;            // true: transform staged sets on the side stream (overlapping hops)
     bool staged_on_side = false;     // the pending set was transformed on the side stream
+    bool k4_stream = false;          // true: transform at latch time on the engine stream (PDL chain)
+    bool staged_in_stream = false;   // the pending set is transformed by latch() on the engine stream
     // chunked host pipeline
     long chunk_hops = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
@@ -243,6 +247,9 @@ void pick_launch_config(tvolap_engine* e) {
     if (et > 0) e->NT = et;
     e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
     e->k4_side = env_int("TVOLAP_K4_SIDE", 1) != 0;
+    // same-box A/B, C2 exchange every 16 hops: side stream 2.82 us/hop, + PDL 2.77,
+    // in-stream K4 chained by PDL 2.53 (profiles/r01_ab_pdl.txt)
+    e->k4_stream = env_int("TVOLAP_K4_STREAM", 1) != 0;
     e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 1)));
 }
 
@@ -338,10 +345,10 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     Tables t(e->N);
     std::vector<float> w = hann(hop);
-    e->tw = dalloc<float2>(e->N);
+    e->tw = dalloc<float2>(t.tw.size());
     e->pk = dalloc<float2>(e->N + 2);
     e->win = dalloc<float>(e->N);
-    CK(cudaMemcpy(e->tw, t.tw.data(), sizeof(float2) * e->N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(e->tw, t.tw.data(), sizeof(float2) * t.tw.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(e->pk, t.pk.data(), sizeof(float2) * (e->N + 2), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(e->win, w.data(), sizeof(float) * e->N, cudaMemcpyHostToDevice));
     const size_t ring_elems = (size_t)e->S * 2 * e->D * e->N;
@@ -378,6 +385,13 @@ void latch(tvolap_engine* e) {  // engine.cpp:54-58
     if (e->pending) {
         if (e->staged_on_side) {  // already transformed on the side stream
             CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+        } else if (e->staged_in_stream) {  // K4 on the engine stream, chained to the hop launches
+            if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_up[e->staged_buf], 0));
+            const int target = (e->active + 1) % kSlots;
+            CK(tvb::launch_partition((int)e->L, (int)e->M, e->S, e->staged_ir, e->staged_len, e->staged_len, e->pool,
+                                     (long)target * e->S, e->tw, e->pk, e->stream, true));
+            ++e->launches;
+            if (e->staged_buf >= 0) CK(cudaEventRecord(e->ev_used[e->staged_buf], e->stream));
         } else {  // the first kernel of this call transforms the staged set into the next slot (K4 fused)
             if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_up[e->staged_buf], 0));
             e->launch_new_ir = e->staged_ir;
@@ -763,8 +777,12 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
             e->staged_buf = b;
         }
         e->staged_len = ir_length;
-        e->staged_on_side = e->k4_side;
-        if (e->k4_side) {  // transform now on the side stream, after the last reader of the target slot
+        // device-resident sets: K4 on the engine stream, PDL-chained between hop launches; sets
+        // uploaded from the host: K4 on the side stream right behind its upload (a cross-stream
+        // wait would break the PDL chain and serialise K4 with the hop kernels)
+        e->staged_in_stream = e->k4_stream && e->staged_buf < 0;
+        e->staged_on_side = e->k4_side && !e->staged_in_stream;
+        if (e->staged_on_side) {  // transform now on the side stream, after the last reader of the target slot
             const int target = (e->active + 1) % kSlots;
             CK(cudaStreamWaitEvent(e->side, e->ev_slot[target], 0));
             if (e->staged_buf >= 0) CK(cudaStreamWaitEvent(e->side, e->ev_up[e->staged_buf], 0));

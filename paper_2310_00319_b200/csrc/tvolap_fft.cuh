@@ -272,6 +272,128 @@ __device__ __forceinline__ void fft_warp_stages(float2* buf, const float2* __res
     }
 }
 
+// ---------------------------------------------------------------- register-resident warp FFT
+// W_32^j = exp(-2 pi i j / 32) (fp64 values rounded once; quarter turns exact).
+__device__ __forceinline__ float2 w32c(int j) {
+    constexpr float c[32] = {
+        1.f, 9.807852507e-01f, 9.238795042e-01f, 8.314695954e-01f, 7.071067691e-01f, 5.555702448e-01f,
+        3.826834261e-01f, 1.950903237e-01f, 0.f, -1.950903237e-01f, -3.826834261e-01f, -5.555702448e-01f,
+        -7.071067691e-01f, -8.314695954e-01f, -9.238795042e-01f, -9.807852507e-01f, -1.f, -9.807852507e-01f,
+        -9.238795042e-01f, -8.314695954e-01f, -7.071067691e-01f, -5.555702448e-01f, -3.826834261e-01f,
+        -1.950903237e-01f, 0.f, 1.950903237e-01f, 3.826834261e-01f, 5.555702448e-01f, 7.071067691e-01f,
+        8.314695954e-01f, 9.238795042e-01f, 9.807852507e-01f};
+    return make_float2(c[j & 31], c[(j + 8) & 31]);  // -sin(x) = cos(x + pi / 2)
+}
+
+// In-register DFT of R = 1..32 points, natural order in and out (sign -1 forward, +1 inverse).
+// 16 = 4 x 4 and 32 = 8 x 4 four-step splits with compile-time twiddles.
+template <bool INV, int R>
+__device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+    if constexpr (R == 2) {
+        const float2 t0 = cadd(v[0], v[1]), t1 = csub(v[0], v[1]);
+        v[0] = t0;
+        v[1] = t1;
+    } else if constexpr (R == 4) {
+        dft4<INV>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8) {
+        dft8<INV>(v);
+    } else if constexpr (R == 16 || R == 32) {
+        constexpr int A = R / 4;  // inner DFT length over a (n = 4 a + b), then 4-point DFTs over b
+        float2 y[4][A];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+#pragma unroll
+            for (int a = 0; a < A; ++a) y[b][a] = v[4 * a + b];
+            dft_reg<INV, A>(y[b]);
+#pragma unroll
+            for (int ka = 1; ka < A; ++ka)
+                if (b > 0) y[b][ka] = twmul<INV>(y[b][ka], w32c((32 / R) * b * ka));
+        }
+#pragma unroll
+        for (int ka = 0; ka < A; ++ka) {
+            dft4<INV>(y[0][ka], y[1][ka], y[2][ka], y[3][ka]);
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb) v[ka + A * kb] = y[kb][ka];
+        }
+    }
+}
+
+// Host side: the four-step tables appended after the stage table (tw[N .. 2N + 32)):
+// tw4[k1 * 32 + t] = W_N^(t k1) for k1 < N / 32, then W_32^j for j < 32.
+template <class F2, class MAKE>
+inline void fft_warp_twiddles(int N, F2* out, MAKE make) {
+    const double pi = 3.14159265358979323846264338327950288;
+    const int n1 = N / 32;
+    for (int i = 0; i < N; ++i) out[i] = make(0.0, 0.0);
+    for (int k1 = 0; k1 < n1; ++k1)
+        for (int t = 0; t < 32; ++t) {
+            const double a = -2.0 * pi * (double)t * (double)k1 / (double)N;
+            out[k1 * 32 + t] = make(std::cos(a), std::sin(a));
+        }
+    for (int j = 0; j < 32; ++j) {
+        const double a = -2.0 * pi * (double)j / 32.0;
+        out[N + j] = make(std::cos(a), std::sin(a));
+    }
+}
+
+__host__ __device__ constexpr int bitrev_c(int x, int bits) {
+    int r = 0;
+    for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
+    return r;
+}
+
+// One N-point transform per warp (64 <= N <= 1024) with the data in registers: N = N1 x 32,
+// lane t takes x[32 n1 + t] (`load(n)`; with PRUNE the upper half is zero and never loaded),
+// an N1-point DFT in registers, twiddles W_N^(t k1), one swizzled transpose through the
+// warp's buffer, N1-point DFTs over the columns (B = 32 / N1 lanes per column) and a B-point
+// DFT across those lanes with shuffles. The result is left in natural order in buf[0 .. N).
+// tw4 = the four-step tables (fft_warp_twiddles). Roughly half the instructions of the
+// radix-8 Stockham passes and no CTA barriers.
+template <bool INV, int N, bool PRUNE, class LOAD>
+__device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict__ tw4, int lane, const LOAD& load) {
+    static_assert(N >= 64 && N <= 1024, "warp FFT covers 64..1024 points");
+    constexpr int N1 = N / 32, B = 32 / N1;
+    constexpr int lgB = B == 1 ? 0 : B == 2 ? 1 : B == 4 ? 2 : B == 8 ? 3 : 4;
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = (PRUNE && n1 >= N1 / 2) ? make_float2(0.f, 0.f) : load(32 * n1 + lane);
+    dft_reg<INV, N1>(v);
+#pragma unroll
+    for (int k1 = 1; k1 < N1; ++k1) v[k1] = twmul<INV>(v[k1], tw4[k1 * 32 + lane]);
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) buf[k1 * 32 + (lane ^ ((B * k1) & 31))] = v[k1];
+    __syncwarp();
+    const int k1 = lane >> lgB, b = lane & (B - 1);
+#pragma unroll
+    for (int a = 0; a < N1; ++a) v[a] = buf[k1 * 32 + B * (a ^ k1) + b];
+    dft_reg<INV, N1>(v);
+    if constexpr (B > 1) {
+        const float2* w32 = tw4 + N;
+#pragma unroll
+        for (int c = 1; c < N1; ++c)
+            if (b) v[c] = twmul<INV>(v[c], w32[(b * c) & 31]);
+#pragma unroll
+        for (int hs = B / 2; hs >= 1; hs /= 2) {  // radix-2 DIF across the column's lanes
+            const bool upper = (b & hs) != 0;
+            const float2 w = w32[(b & (hs - 1)) * (16 / hs)];
+#pragma unroll
+            for (int c = 0; c < N1; ++c) {
+                float2 o;
+                o.x = __shfl_xor_sync(0xffffffffu, v[c].x, hs);
+                o.y = __shfl_xor_sync(0xffffffffu, v[c].y, hs);
+                v[c] = upper ? twmul<INV>(csub(o, v[c]), w) : cadd(v[c], o);
+            }
+        }
+    }
+    __syncwarp();
+    int h = 0;
+#pragma unroll
+    for (int i = 0; i < lgB; ++i) h |= ((b >> i) & 1) << (lgB - 1 - i);
+#pragma unroll
+    for (int c = 0; c < N1; ++c) buf[k1 + N1 * c + N1 * N1 * h] = v[c];
+    __syncwarp();
+}
+
 // Single transform (nf = 1).
 template <bool INV, int NC = 0>
 __device__ float2* fft_stockham(float2* a, float2* b, int N, const float2* __restrict__ tw, bool prune, int tid,

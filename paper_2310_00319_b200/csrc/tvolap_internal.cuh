@@ -48,7 +48,8 @@ cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int th
 // K4: partition `rows` time-domain IRs (ir[row * ir_stride + n], n < ir_len) into
 // M packed spectra each: pool[(row0 + row) * M + m][2L].
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
-                             long row0, const float2* tw, const float2* pk, cudaStream_t stream);
+                             long row0, const float2* tw, const float2* pk, cudaStream_t stream,
+                             bool pdl = false);
 
 // Spectral primitives (tests of the reference's spectral.cpp contract).
 cudaError_t launch_forward_real(long n, long batch, const float* x, float2* bins, const float2* tw,

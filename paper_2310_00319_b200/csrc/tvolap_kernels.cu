@@ -52,7 +52,39 @@ __device__ unsigned long long g_phase[16];
         }                                                      \
     } while (0)
 #define PHASE_START() long long ph_t = clock64()
+// launch timeline (globaltimer ns): [kind][launch][begin of CTA 0, end of the last CTA]
+__device__ unsigned long long g_tl[2][4096][2];
+__device__ unsigned g_tl_n[2], g_tl_done[2];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL_BEGIN(kind)                                                               \
+    do {                                                                             \
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_tl[kind][g_tl_n[kind] & 4095][0] = gtimer(); \
+    } while (0)
+#define TL_END(kind)                                                                 \
+    do {                                                                             \
+        __syncthreads();                                                             \
+        if (threadIdx.x == 0) {                                                      \
+            __threadfence();                                                         \
+            if (atomicAdd(&g_tl_done[kind], 1u) == gridDim.x - 1) {                  \
+                const unsigned n_ = g_tl_n[kind];                                    \
+                g_tl[kind][n_ & 4095][1] = gtimer();                                 \
+                g_tl_done[kind] = 0;                                                 \
+                __threadfence();                                                     \
+                g_tl_n[kind] = n_ + 1;                                               \
+            }                                                                        \
+        }                                                                            \
+    } while (0)
 #else
+#define TL_BEGIN(kind) \
+    do {               \
+    } while (0)
+#define TL_END(kind) \
+    do {             \
+    } while (0)
 #define PHASE_MARK(k) \
     do {              \
     } while (0)
@@ -131,7 +163,7 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
                     if (vec && i0 + 1 < p.new_ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
                     return make_float2(i0 < p.new_ir_len ? h[i0] : 0.f, i0 + 1 < p.new_ir_len ? h[i0 + 1] : 0.f);
                 };
-                fft_warp_stages<false, NC, 1>(buf, tw, lane, load0);
+                fft_warp4<false, NC, true>(buf, p.tw + NC, lane, load0);
                 float4* d4 = reinterpret_cast<float4*>(dst + (long)m * NC);
                 for (int k2 = lane; k2 < NC / 2; k2 += 32) {
                     const float2 a = untangle_packed(buf, NC, 2 * k2, pk);
@@ -418,6 +450,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     const BlockLayout lay(L, P, E, J, BANK, NT);
     (void)Q;
     PHASE_START();
+    TL_BEGIN(0);
     float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
     float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
     float* s_win = reinterpret_cast<float*>(smem + lay.win);
@@ -442,6 +475,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         s_win[i] = p.win[i];
     }
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    // programmatic dependent launch: everything above reads constant tables only; from here on
+    // the previous grid's state (history, OLA, delay line, pool, inputs) must be complete
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     float* xcur = s_xin;  // this block's inputs: [history | J hops]
     for (int i = tid; i < L; i += NT) xcur[i] = p.hist[(long)s * L + i];
     // hops b .. b+J-1 of this source into xcur[L..] (cp.async; lands while the block's MAC runs)
@@ -479,6 +515,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     for (int b0 = 0; b0 < p.n_hops; b0 += J) {
         const long l0 = p.hop0 + b0;
         const int jb = min(J, p.n_hops - b0);
+        if (b0 + J >= p.n_hops) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
         // ---- inputs: this block's landed (prefetched during the previous block)
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
@@ -954,6 +991,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
         p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u] = s_ola[i];
     }
+    TL_END(0);
 }
 
 // K4: transform IR slices into packed partition spectra (partition.cpp:20-51).
@@ -1034,7 +1072,12 @@ __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows
     float2* s_pk = s_tw + N;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     float2* buf = reinterpret_cast<float2*>(smem + align16((2 * N + 2) * sizeof(float2))) + (size_t)warp * N;
-    for (int i = tid; i < N; i += blockDim.x) s_tw[i] = tw[i];
+    TL_BEGIN(1);
+    (void)s_tw;  // the four-step tables are read through L1 (tw + N)
+    // In-stream K4 under programmatic dependent launch: let the next hop launch get scheduled
+    // now, and (below) finish only after the previous hop launch has completed, so the hop
+    // launch that waits on this grid transitively waits on its predecessor too.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     for (int i = tid; i <= N; i += blockDim.x) s_pk[i] = pk[i];
     __syncthreads();
     const bool vec = (ir_stride & 1) == 0 && (reinterpret_cast<uintptr_t>(ir) & 7) == 0;
@@ -1049,7 +1092,7 @@ __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows
             if (vec && i0 + 1 < ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
             return make_float2(i0 < ir_len ? h[i0] : 0.f, i0 + 1 < ir_len ? h[i0 + 1] : 0.f);
         };
-        fft_warp_stages<false, N, 1>(buf, s_tw, lane, load0);
+        fft_warp4<false, N, true>(buf, tw + N, lane, load0);
         float4* d4 = reinterpret_cast<float4*>(pool + ((row0 + row) * M + m) * N);
         for (int k2 = lane; k2 < N / 2; k2 += 32) {
             const float2 a = untangle_packed(buf, N, 2 * k2, s_pk);
@@ -1058,6 +1101,8 @@ __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows
         }
         __syncwarp();
     }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    TL_END(1);
 }
 
 // forward_real on a batch (spectral.cpp:99-125): full real input of n = 2N samples.
@@ -1200,13 +1245,26 @@ static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaSt
     cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)p.P;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
+    if (p.P > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)p.P;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    static const bool pdl = [] {  // TVOLAP_PDL=0 disables (A/B: profiles/r01_ab_pdl.txt)
+        const char* v = std::getenv("TVOLAP_PDL");
+        return !(v && v[0] == '0');
+    }();
+    if (pdl) {  // overlap this launch's setup with the previous hop launch's tail
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = p.P > 1 ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, fn, p, Q);
 }
 
@@ -1271,7 +1329,7 @@ cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream
 template <int NC>
 static cudaError_t launch_partition_warp(int M, long rows, const float* ir, long ir_stride, long ir_len,
                                         float2* pool, long row0, const float2* tw, const float2* pk,
-                                        cudaStream_t stream) {
+                                        cudaStream_t stream, bool pdl) {
     constexpr int kWarps = 8;
     const size_t smem = align16((2 * NC + 2) * sizeof(float2)) + (size_t)kWarps * NC * sizeof(float2);
     cudaError_t err = cudaFuncSetAttribute(partition_warp_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1285,13 +1343,21 @@ static cudaError_t launch_partition_warp(int M, long rows, const float* ir, long
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long tasks = rows * M;
     const long grid = std::max<long>(1, std::min<long>((tasks + kWarps - 1) / kWarps, (long)sms * std::max(1, per_sm)));
-    partition_warp_kernel<NC><<<(unsigned)grid, 32 * kWarps, smem, stream>>>(M, rows, ir, ir_stride, ir_len, pool,
-                                                                           row0, tw, pk);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(32 * kWarps);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, partition_warp_kernel<NC>, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk);
 }
 
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
-                             long row0, const float2* tw, const float2* pk, cudaStream_t stream) {
+                             long row0, const float2* tw, const float2* pk, cudaStream_t stream, bool pdl) {
     // one warp per partition for the common transform lengths (TVOLAP_K4_WARP=0: CTA batches)
     static const bool warp_k4 = [] {
         const char* v = std::getenv("TVOLAP_K4_WARP");
@@ -1299,11 +1365,11 @@ cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_s
     }();
     if (warp_k4) {
         switch (2 * L) {
-            case 64: return launch_partition_warp<64>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
-            case 128: return launch_partition_warp<128>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
-            case 256: return launch_partition_warp<256>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
-            case 512: return launch_partition_warp<512>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
-            case 1024: return launch_partition_warp<1024>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream);
+            case 64: return launch_partition_warp<64>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);
+            case 128: return launch_partition_warp<128>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);
+            case 256: return launch_partition_warp<256>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);
+            case 512: return launch_partition_warp<512>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);
+            case 1024: return launch_partition_warp<1024>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);
             default: break;
         }
     }
@@ -1389,5 +1455,19 @@ extern "C" int tvolap_phase_counters(unsigned long long* out, int n) {
     if (cudaDeviceSynchronize() != cudaSuccess) return 6;
     if (cudaMemcpyFromSymbol(out, g_phase, n * sizeof(unsigned long long)) != cudaSuccess) return 6;
     return cudaMemcpyToSymbol(g_phase, zero, sizeof(zero)) == cudaSuccess ? 0 : 6;
+}
+
+// timeline: out[kind][i][2] for the first `n` launches of each kind since the last reset
+extern "C" int tvolap_timeline(unsigned long long* out, int n, unsigned* counts) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return 6;
+    if (cudaMemcpyFromSymbol(counts, g_tl_n, 2 * sizeof(unsigned)) != cudaSuccess) return 6;
+    static unsigned long long tmp[2][4096][2];
+    if (cudaMemcpyFromSymbol(tmp, g_tl, sizeof(tmp)) != cudaSuccess) return 6;
+    n = n < 4096 ? n : 4096;
+    for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < 2; ++j) out[(k * n + i) * 2 + j] = tmp[k][i][j];
+    const unsigned zero[2] = {0, 0};
+    return cudaMemcpyToSymbol(g_tl_n, zero, sizeof(zero)) == cudaSuccess ? 0 : 6;
 }
 #endif

@@ -1,6 +1,7 @@
-"""K4 variants agree bit for bit: the warp-per-partition kernel (default), the CTA-batched
-kernel (TVOLAP_K4_WARP=0), and the partition transform fused into the hop kernels
-(TVOLAP_K4_SIDE=0) all run the same butterflies, so spectra and engine outputs are identical."""
+"""K4 variants: the warp-per-partition kernel (default, register four-step FFT) and the partition
+transform fused into the hop kernels (TVOLAP_K4_SIDE=0) run the same warp FFT, so spectra and
+engine outputs are bit-identical; the CTA-batched Stockham kernel (TVOLAP_K4_WARP=0) is a
+different factorisation and agrees to fp32 rounding."""
 import os
 import subprocess
 import sys
@@ -51,10 +52,12 @@ def _run(tmp_path, name, env_extra):
     return np.load(path)
 
 
-def test_k4_variants_bit_identical(tmp_path):
+def test_k4_variants(tmp_path):
     base = _run(tmp_path, "warp", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "1"})
-    for name, env in [("cta", {"TVOLAP_K4_WARP": "0", "TVOLAP_K4_SIDE": "1"}),
-                      ("fused", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "0"})]:
-        other = _run(tmp_path, name, env)
-        for k in base.files:
-            assert np.array_equal(base[k], other[k]), (name, k)
+    fused = _run(tmp_path, "fused", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "0"})
+    for k in base.files:
+        assert np.array_equal(base[k], fused[k]), k
+    cta = _run(tmp_path, "cta", {"TVOLAP_K4_WARP": "0", "TVOLAP_K4_SIDE": "1"})
+    for k in base.files:
+        scale = max(np.abs(cta[k]).max(), 1e-30)
+        assert np.abs(base[k] - cta[k]).max() <= 2e-6 * scale, k
