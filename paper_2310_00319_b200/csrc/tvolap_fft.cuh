@@ -349,40 +349,57 @@ __host__ __device__ constexpr int bitrev_c(int x, int bits) {
 // DFT across those lanes with shuffles. The result is left in natural order in buf[0 .. N).
 // tw4 = the four-step tables (fft_warp_twiddles). Roughly half the instructions of the
 // radix-8 Stockham passes and no CTA barriers.
-template <bool INV, int N, bool PRUNE, class LOAD>
+template <bool INV, int N, bool PRUNE, int NB = 1, class LOAD>
 __device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict__ tw4, int lane, const LOAD& load) {
+    // NB transforms in lockstep (independent instruction streams for ILP): transform t uses
+    // buf + t N and reads its input through load(t, n).
     static_assert(N >= 64 && N <= 1024, "warp FFT covers 64..1024 points");
     constexpr int N1 = N / 32, B = 32 / N1;
     constexpr int lgB = B == 1 ? 0 : B == 2 ? 1 : B == 4 ? 2 : B == 8 ? 3 : 4;
-    float2 v[N1];
+    float2 v[NB][N1];
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = (PRUNE && n1 >= N1 / 2) ? make_float2(0.f, 0.f) : load(32 * n1 + lane);
-    dft_reg<INV, N1>(v);
+    for (int t = 0; t < NB; ++t)
 #pragma unroll
-    for (int k1 = 1; k1 < N1; ++k1) v[k1] = twmul<INV>(v[k1], tw4[k1 * 32 + lane]);
+        for (int n1 = 0; n1 < N1; ++n1)
+            v[t][n1] = (PRUNE && n1 >= N1 / 2) ? make_float2(0.f, 0.f) : load(t, 32 * n1 + lane);
 #pragma unroll
-    for (int k1 = 0; k1 < N1; ++k1) buf[k1 * 32 + (lane ^ ((B * k1) & 31))] = v[k1];
+    for (int t = 0; t < NB; ++t) {
+        dft_reg<INV, N1>(v[t]);
+#pragma unroll
+        for (int k1 = 1; k1 < N1; ++k1) v[t][k1] = twmul<INV>(v[t][k1], tw4[k1 * 32 + lane]);
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) buf[t * N + k1 * 32 + (lane ^ ((B * k1) & 31))] = v[t][k1];
+    }
     __syncwarp();
     const int k1 = lane >> lgB, b = lane & (B - 1);
 #pragma unroll
-    for (int a = 0; a < N1; ++a) v[a] = buf[k1 * 32 + B * (a ^ k1) + b];
-    dft_reg<INV, N1>(v);
+    for (int t = 0; t < NB; ++t) {
+#pragma unroll
+        for (int a = 0; a < N1; ++a) v[t][a] = buf[t * N + k1 * 32 + B * (a ^ k1) + b];
+        dft_reg<INV, N1>(v[t]);
+    }
     if constexpr (B > 1) {
         const float2* w32 = tw4 + N;
 #pragma unroll
-        for (int c = 1; c < N1; ++c)
-            if (b) v[c] = twmul<INV>(v[c], w32[(b * c) & 31]);
+        for (int c = 1; c < N1; ++c) {
+            const float2 w = w32[(b * c) & 31];
+#pragma unroll
+            for (int t = 0; t < NB; ++t)
+                if (b) v[t][c] = twmul<INV>(v[t][c], w);
+        }
 #pragma unroll
         for (int hs = B / 2; hs >= 1; hs /= 2) {  // radix-2 DIF across the column's lanes
             const bool upper = (b & hs) != 0;
             const float2 w = w32[(b & (hs - 1)) * (16 / hs)];
 #pragma unroll
-            for (int c = 0; c < N1; ++c) {
-                float2 o;
-                o.x = __shfl_xor_sync(0xffffffffu, v[c].x, hs);
-                o.y = __shfl_xor_sync(0xffffffffu, v[c].y, hs);
-                v[c] = upper ? twmul<INV>(csub(o, v[c]), w) : cadd(v[c], o);
-            }
+            for (int t = 0; t < NB; ++t)
+#pragma unroll
+                for (int c = 0; c < N1; ++c) {
+                    float2 o;
+                    o.x = __shfl_xor_sync(0xffffffffu, v[t][c].x, hs);
+                    o.y = __shfl_xor_sync(0xffffffffu, v[t][c].y, hs);
+                    v[t][c] = upper ? twmul<INV>(csub(o, v[t][c]), w) : cadd(v[t][c], o);
+                }
         }
     }
     __syncwarp();
@@ -390,7 +407,9 @@ __device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict_
 #pragma unroll
     for (int i = 0; i < lgB; ++i) h |= ((b >> i) & 1) << (lgB - 1 - i);
 #pragma unroll
-    for (int c = 0; c < N1; ++c) buf[k1 + N1 * c + N1 * N1 * h] = v[c];
+    for (int t = 0; t < NB; ++t)
+#pragma unroll
+        for (int c = 0; c < N1; ++c) buf[t * N + k1 + N1 * c + N1 * N1 * h] = v[t][c];
     __syncwarp();
 }
 

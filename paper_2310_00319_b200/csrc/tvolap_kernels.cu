@@ -151,26 +151,47 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
     if constexpr (NC != 0 && NC <= 1024) {
         // one warp per partition (as partition_warp_kernel, bit-identical), warp-private buffers
         // carved from the `avail` bytes at fa; partitions m = r, r + P, ... of this CTA
-        const int wfit = min(NT >> 5, (int)(avail / (NC * sizeof(float2))));
+        // two partitions per warp in lockstep when the buffers allow (independent FFT chains)
+        const int slots = (int)(avail / (NC * sizeof(float2)));
         const int warp = tid >> 5, lane = tid & 31;
         const bool vec = (p.new_ir_stride & 1) == 0 && (reinterpret_cast<uintptr_t>(p.new_ir) & 7) == 0;
-        if (warp < wfit) {
-            float2* buf = fa + (size_t)warp * NC;
-            for (int m = r + warp * P; m < M; m += wfit * P) {
-                const long base = (long)m * NC;
-                auto load0 = [&](int n) -> float2 {
-                    const long i0 = base + 2 * n;
-                    if (vec && i0 + 1 < p.new_ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
-                    return make_float2(i0 < p.new_ir_len ? h[i0] : 0.f, i0 + 1 < p.new_ir_len ? h[i0 + 1] : 0.f);
-                };
-                fft_warp4<false, NC, true>(buf, p.tw + NC, lane, load0);
-                float4* d4 = reinterpret_cast<float4*>(dst + (long)m * NC);
-                for (int k2 = lane; k2 < NC / 2; k2 += 32) {
-                    const float2 a = untangle_packed(buf, NC, 2 * k2, pk);
-                    const float2 b = untangle(buf, NC, 2 * k2 + 1, pk);
-                    d4[k2] = make_float4(a.x, a.y, b.x, b.y);
-                }
+        auto loader = [&](int m) {
+            return [&, m](int, int n) -> float2 {
+                const long i0 = (long)m * NC + 2 * n;
+                if (m >= M) return make_float2(0.f, 0.f);
+                if (vec && i0 + 1 < p.new_ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
+                return make_float2(i0 < p.new_ir_len ? h[i0] : 0.f, i0 + 1 < p.new_ir_len ? h[i0 + 1] : 0.f);
+            };
+        };
+        auto store = [&](const float2* buf, int m) {
+            float4* d4 = reinterpret_cast<float4*>(dst + (long)m * NC);
+            for (int k2 = lane; k2 < NC / 2; k2 += 32) {
+                const float2 a = untangle_packed(buf, NC, 2 * k2, pk);
+                const float2 b = untangle(buf, NC, 2 * k2 + 1, pk);
+                d4[k2] = make_float4(a.x, a.y, b.x, b.y);
+            }
+        };
+        if (slots >= 2 * (NT >> 5) && NC <= 512) {
+            float2* buf = fa + (size_t)warp * 2 * NC;
+            const int nw = NT >> 5;
+            for (int m = r + warp * P; m < M; m += 2 * nw * P) {
+                const int m2 = m + nw * P;  // second partition of this warp (may be past M)
+                auto l0 = loader(m), l1 = loader(m2);
+                auto load2 = [&](int t, int n) -> float2 { return t ? l1(t, n) : l0(t, n); };
+                fft_warp4<false, NC, true, 2>(buf, p.tw + NC, lane, load2);
+                store(buf, m);
+                if (m2 < M) store(buf + NC, m2);
                 __syncwarp();
+            }
+        } else {
+            const int wfit = min(NT >> 5, slots);
+            if (warp < wfit) {
+                float2* buf = fa + (size_t)warp * NC;
+                for (int m = r + warp * P; m < M; m += wfit * P) {
+                    fft_warp4<false, NC, true>(buf, p.tw + NC, lane, loader(m));
+                    store(buf, m);
+                    __syncwarp();
+                }
             }
         }
         __syncthreads();
@@ -424,6 +445,9 @@ struct BlockLayout {
         size_t end = fb + fpc * E * N * sizeof(float2);
         if (red + red_bytes > end) end = red + red_bytes;
         if (stg + stg_bytes > end) end = stg + stg_bytes;
+        // the fused K4 prologue runs two partitions per warp in lockstep (warp-private buffers)
+        const size_t k4_bytes = N <= 512 ? 2 * (size_t)(threads / 32) * N * sizeof(float2) : 0;
+        if (!bank && fa + k4_bytes > end) end = fa + k4_bytes;
         ola = align16(end);
         total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
     }
@@ -725,7 +749,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                         }
                     };
                     int m = mu0;
-                    constexpr int U = 4;
+                    constexpr int U = 4;  // same-box A/B: U = 2 +1.5 %, one aux-everywhere variant +9 %
                     for (; m + U <= mu1; m += U) {
                         float2 xn[U][2], hh[U];
 #pragma unroll
@@ -1087,7 +1111,7 @@ __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows
         const int m = (int)(t - row * M);
         const float* h = ir + row * ir_stride;
         const long base = (long)m * N;  // partition m = IR samples [m N, (m + 1) N), N = 2L
-        auto load0 = [&](int n) -> float2 {  // z_n = (h[2n], h[2n+1])
+        auto load0 = [&](int, int n) -> float2 {  // z_n = (h[2n], h[2n+1])
             const long i0 = base + 2 * n;
             if (vec && i0 + 1 < ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
             return make_float2(i0 < ir_len ? h[i0] : 0.f, i0 + 1 < ir_len ? h[i0 + 1] : 0.f);

@@ -19,13 +19,15 @@ device, the call is then asynchronous on the engine stream).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Optional
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libtvolap_b200.so"
+# TVOLAP_LIB: a diagnostic build (scripts/, _build.build_variant) instead of the in-tree library
+_LIB_PATH = Path(os.environ.get("TVOLAP_LIB") or Path(__file__).resolve().parent / "lib" / "libtvolap_b200.so")
 
 
 # ---------------------------------------------------------------- errors (errors.hpp)
