@@ -217,6 +217,46 @@ int tvolap_gen_irs_device(int device, uint64_t seed, long count, const long* lan
 int tvolap_mix_device(int device, long sources, long ears, long samples, const float* out, long out_stride,
                       float* mix, long mix_stride, void* stream);
 
+
+/* ------------------------------------------------------ comparison convolvers
+ * The reference's other streaming convolvers (reference.hpp:53-200, reference.cpp:34-320) on the
+ * GPU, for switching comparisons against TVOLAP:
+ *   TVOLAP_CMP_TDC    DirectProcessor "tdc"    direct-form FIR, hard switch at hop boundaries
+ *   TVOLAP_CMP_CF_TDC CfTdcProcessor "cf-tdc"  direct form with a crossfade of the two outputs
+ *   TVOLAP_CMP_OLA    OlaProcessor "ola"       block = IR length, hop = block
+ *   TVOLAP_CMP_OLS    OlsProcessor "ols"       block = IR length, hop = block
+ *   TVOLAP_CMP_WOLA   WolaProcessor "wola"     sqrt-Hann analysis/synthesis, hop = block / 2
+ * ir is channel-major (ir[c * ir_stride + t], t < taps). "tdc"/"cf-tdc" take `hop`; the block
+ * forms need a power-of-two taps >= 4 (GPU limit: taps <= 4096). Errors as the reference's
+ * constructors / set_filter / switch_filter (InvalidSize, InvalidInput, InvalidConfiguration,
+ * IncompatibleFilter, SwitchInProgress). Calls are synchronous; buffers may be host or device. */
+#define TVOLAP_ERR_SWITCH_IN_PROGRESS 7    /* tvolap::SwitchInProgressError     errors.hpp:46-49 */
+#define TVOLAP_CMP_TDC 0
+#define TVOLAP_CMP_CF_TDC 1
+#define TVOLAP_CMP_OLA 2
+#define TVOLAP_CMP_OLS 3
+#define TVOLAP_CMP_WOLA 4
+#define TVOLAP_FADE_HANN 0   /* CrossfadeConfig::Shape::HannComplementary (reference.hpp:19) */
+#define TVOLAP_FADE_LINEAR 1 /* CrossfadeConfig::Shape::Linear */
+typedef struct tvolap_cmp tvolap_cmp;
+
+/* Constructors (reference.cpp:59-66, 97-108, 184-190, 221-227, 259-267). */
+int tvolap_cmp_create(tvolap_cmp** out, int device, int kind, long taps, long channels, const float* ir,
+                      long ir_stride, long hop, long fade_duration, int fade_shape);
+int tvolap_cmp_destroy(tvolap_cmp* p);
+/* n_hops consecutive process() calls (reference.cpp:68-93, 136-172, 192-216, 229-252, 269-308):
+ * in[c * in_stride + t], out[c * out_stride + t], t < n_hops * hop. */
+int tvolap_cmp_process_hops(tvolap_cmp* p, const float* in, long in_stride, float* out, long out_stride,
+                            long n_hops);
+/* set_filter (reference.cpp:78-82, 134-136, 192-196, 229-233, 269-273): staged, applied at the next hop. */
+int tvolap_cmp_set_filter(tvolap_cmp* p, const float* ir, long taps, long channels, long ir_stride);
+/* CfTdcProcessor::switch_filter (reference.cpp:122-132). */
+int tvolap_cmp_switch_filter(tvolap_cmp* p, const float* ir, long taps, long channels, long ir_stride,
+                             long fade_duration, int fade_shape);
+int tvolap_cmp_reset(tvolap_cmp* p);
+/* out6 = {hop, channels, latency, stream_delay, switching_latency, fading} (reference.hpp:53-200). */
+int tvolap_cmp_geometry(const tvolap_cmp* p, long* out6);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,7 +7,9 @@
 //   FilterPartitionSet                           proj/include/tvolap/partition.hpp:21-32
 //   TvolapEngine                                 proj/include/tvolap/engine.hpp:33-94
 //   TvolapProcessor / StreamingProcessor face    proj/include/tvolap/reference.hpp:202-221
-//   exception classes                            proj/include/tvolap/errors.hpp:10-43
+//   DirectProcessor, CfTdcProcessor, OlaProcessor, OlsProcessor, WolaProcessor,
+//   make_processor                               proj/include/tvolap/reference.hpp:26-200,224-226
+//   exception classes                            proj/include/tvolap/errors.hpp:10-49
 // Eigen is not required: Frames is a minimal column-major (rows = samples,
 // cols = channels) fp64 array with the same indexing as Eigen::ArrayXXd, and
 // INTEGRATION.md shows the two-line Eigen adapter. Compute is fp32 on the GPU.
@@ -51,6 +53,10 @@ class CudaError : public std::runtime_error {
 public:
     using std::runtime_error::runtime_error;
 };
+class SwitchInProgressError : public std::logic_error {
+public:
+    using std::logic_error::logic_error;
+};
 
 inline void check(int rc) {
     if (rc == TVOLAP_OK) return;
@@ -61,6 +67,7 @@ inline void check(int rc) {
         case TVOLAP_ERR_INVALID_CONFIGURATION: throw InvalidConfigurationError(msg);
         case TVOLAP_ERR_INCOMPATIBLE_FILTER: throw IncompatibleFilterError(msg);
         case TVOLAP_ERR_INVALID_SPECTRUM: throw InvalidSpectrumError(msg);
+        case TVOLAP_ERR_SWITCH_IN_PROGRESS: throw SwitchInProgressError(msg);
         default: throw CudaError(msg);
     }
 }
@@ -185,26 +192,153 @@ private:
     std::unique_ptr<tvolap_engine, Del> h_;
 };
 
+// reference.hpp:26-50 — the common face of the streaming convolvers.
+class StreamingProcessor {
+public:
+    virtual ~StreamingProcessor() = default;
+    virtual std::string name() const = 0;
+    virtual Index hop() const = 0;
+    virtual Index channels() const = 0;
+    virtual Index latency() const = 0;
+    virtual Index stream_delay() const = 0;
+    virtual Index switching_latency() const = 0;
+    virtual Frames process(const Frames& input) = 0;
+    virtual void set_filter(const ImpulseResponse& ir) = 0;
+    virtual void reset() = 0;
+};
+
+struct CrossfadeConfig {  // reference.hpp:18-22
+    enum class Shape { HannComplementary = TVOLAP_FADE_HANN, Linear = TVOLAP_FADE_LINEAR };
+    Index duration = 1;
+    Shape shape = Shape::HannComplementary;
+};
+
+namespace detail {
+inline std::vector<float> channel_major(const ImpulseResponse& ir) {
+    std::vector<float> t((size_t)(ir.length() * ir.channels()));
+    for (Index c = 0; c < ir.channels(); ++c)
+        for (Index n = 0; n < ir.length(); ++n) t[(size_t)(c * ir.length() + n)] = (float)ir.samples(n, c);
+    return t;
+}
+struct CmpDel {
+    void operator()(tvolap_cmp* p) const { tvolap_cmp_destroy(p); }
+};
+}  // namespace detail
+
+// The reference's comparison convolvers (reference.hpp:53-200) over tvolap_cmp_* (GPU, fp32).
+class CmpProcessor : public StreamingProcessor {
+public:
+    CmpProcessor(int kind, std::string name, const ImpulseResponse& ir, Index hop, CrossfadeConfig fade, int device)
+        : name_(std::move(name)) {
+        const std::vector<float> t = detail::channel_major(ir);
+        tvolap_cmp* h = nullptr;
+        check(tvolap_cmp_create(&h, device, kind, ir.length(), ir.channels(), t.empty() ? nullptr : t.data(),
+                                std::max<Index>(ir.length(), 1), hop, fade.duration, (int)fade.shape));
+        h_.reset(h);
+    }
+    std::string name() const override { return name_; }
+    Index hop() const override { return geo()[0]; }
+    Index channels() const override { return geo()[1]; }
+    Index latency() const override { return geo()[2]; }
+    Index stream_delay() const override { return geo()[3]; }
+    Index switching_latency() const override { return geo()[4]; }
+    bool fading() const { return geo()[5] != 0; }
+    Frames process(const Frames& input) override {
+        const Index L = hop(), C = channels();
+        if (input.rows() != L) throw InvalidSizeError("process() expects exactly one hop of input per call");
+        if (input.cols() != C) throw InvalidInputError("input channel count does not match the filter");
+        std::vector<float> in((size_t)(L * C)), out((size_t)(L * C));
+        for (Index c = 0; c < C; ++c)
+            for (Index t = 0; t < L; ++t) in[(size_t)(c * L + t)] = (float)input(t, c);
+        check(tvolap_cmp_process_hops(h_.get(), in.data(), L, out.data(), L, 1));
+        Frames y(L, C);
+        for (Index c = 0; c < C; ++c)
+            for (Index t = 0; t < L; ++t) y(t, c) = out[(size_t)(c * L + t)];
+        return y;
+    }
+    void set_filter(const ImpulseResponse& ir) override {
+        const std::vector<float> t = detail::channel_major(ir);
+        check(tvolap_cmp_set_filter(h_.get(), t.data(), ir.length(), ir.channels(), ir.length()));
+    }
+    void reset() override { check(tvolap_cmp_reset(h_.get())); }
+
+protected:
+    std::vector<long> geo() const {
+        std::vector<long> g(6);
+        check(tvolap_cmp_geometry(h_.get(), g.data()));
+        return g;
+    }
+    std::string name_;
+    std::unique_ptr<tvolap_cmp, detail::CmpDel> h_;
+};
+
+class DirectProcessor : public CmpProcessor {  // reference.hpp:53-77
+public:
+    DirectProcessor(const ImpulseResponse& ir, Index hop, int device = 0)
+        : CmpProcessor(TVOLAP_CMP_TDC, "tdc", ir, hop, CrossfadeConfig{}, device) {}
+};
+
+class CfTdcProcessor : public CmpProcessor {  // reference.hpp:79-118
+public:
+    CfTdcProcessor(const ImpulseResponse& ir, Index hop, CrossfadeConfig fade, int device = 0)
+        : CmpProcessor(TVOLAP_CMP_CF_TDC, "cf-tdc", ir, hop, fade, device) {}
+    void switch_filter(const ImpulseResponse& ir, const CrossfadeConfig& fade) {
+        const std::vector<float> t = detail::channel_major(ir);
+        check(tvolap_cmp_switch_filter(h_.get(), t.data(), ir.length(), ir.channels(), ir.length(), fade.duration,
+                                       (int)fade.shape));
+    }
+};
+
+class OlaProcessor : public CmpProcessor {  // reference.hpp:120-145
+public:
+    explicit OlaProcessor(const ImpulseResponse& ir, int device = 0)
+        : CmpProcessor(TVOLAP_CMP_OLA, "ola", ir, 0, CrossfadeConfig{}, device) {}
+};
+
+class OlsProcessor : public CmpProcessor {  // reference.hpp:147-173
+public:
+    explicit OlsProcessor(const ImpulseResponse& ir, int device = 0)
+        : CmpProcessor(TVOLAP_CMP_OLS, "ols", ir, 0, CrossfadeConfig{}, device) {}
+};
+
+class WolaProcessor : public CmpProcessor {  // reference.hpp:175-200
+public:
+    explicit WolaProcessor(const ImpulseResponse& ir, int device = 0)
+        : CmpProcessor(TVOLAP_CMP_WOLA, "wola", ir, 0, CrossfadeConfig{}, device) {}
+};
+
 // reference.hpp:202-221
-class TvolapProcessor {
+class TvolapProcessor : public StreamingProcessor {
 public:
     TvolapProcessor(const ImpulseResponse& ir, Index hop, int device = 0)
         : engine_(std::make_shared<FilterPartitionSet>(partition(ir, hop)), device) {}
-    std::string name() const { return "tvolap"; }
-    Index hop() const { return engine_.hop(); }
-    Index channels() const { return engine_.channels(); }
-    Index latency() const { return engine_.latency(); }
-    Index stream_delay() const { return engine_.stream_delay(); }
-    Index switching_latency() const { return engine_.switching_latency(); }
-    Frames process(const Frames& input) { return engine_.process(input); }
-    void set_filter(const ImpulseResponse& ir) {  // reference.cpp:335-338
+    std::string name() const override { return "tvolap"; }
+    Index hop() const override { return engine_.hop(); }
+    Index channels() const override { return engine_.channels(); }
+    Index latency() const override { return engine_.latency(); }
+    Index stream_delay() const override { return engine_.stream_delay(); }
+    Index switching_latency() const override { return engine_.switching_latency(); }
+    Frames process(const Frames& input) override { return engine_.process(input); }
+    void set_filter(const ImpulseResponse& ir) override {  // reference.cpp:335-338
         engine_.exchange_filter(std::make_shared<FilterPartitionSet>(partition(ir, engine_.hop(), engine_.partition_count())));
     }
-    void reset() { engine_.reset(); }
+    void reset() override { engine_.reset(); }
     TvolapEngine& engine() { return engine_; }
 
 private:
     TvolapEngine engine_;
 };
+
+// reference.cpp:345-363
+inline std::unique_ptr<StreamingProcessor> make_processor(const std::string& name, const ImpulseResponse& ir,
+                                                          Index hop, int device = 0) {
+    if (name == "tdc") return std::make_unique<DirectProcessor>(ir, hop, device);
+    if (name == "cf-tdc") return std::make_unique<CfTdcProcessor>(ir, hop, CrossfadeConfig{hop}, device);
+    if (name == "ola") return std::make_unique<OlaProcessor>(ir, device);
+    if (name == "ols") return std::make_unique<OlsProcessor>(ir, device);
+    if (name == "wola") return std::make_unique<WolaProcessor>(ir, device);
+    if (name == "tvolap") return std::make_unique<TvolapProcessor>(ir, hop, device);
+    throw InvalidConfigurationError("unknown algorithm: " + name);
+}
 
 }  // namespace tvolap_b200

@@ -275,3 +275,108 @@ def run_workload(hop, min_partitions, sources, ears, n_hops, x, mode, fresh_ir=N
                                   out.ctypes.data if out is not None else None, n_hops * hop, threads, C.byref(st))
     _chk(st.value)
     return secs, out
+
+
+# ----------------------------------------------------------------- comparison convolvers
+# reference.cpp:34-363: "tdc", "cf-tdc", "ola", "ols", "wola".
+KINDS = {"tdc": 0, "cf-tdc": 1, "ola": 2, "ols": 3, "wola": 4}
+HANN, LINEAR = 0, 1
+
+
+def _cmp_sigs(L):
+    vp, lg, ip = C.c_void_p, C.c_long, C.c_int
+    if getattr(L, "_cmp_ready", False):
+        return L
+    L.orc_cmp_create.argtypes = [ip, vp, lg, lg, lg, lg, ip, C.POINTER(ip)]
+    L.orc_cmp_create.restype = vp
+    L.orc_cmp_free.argtypes = [vp]
+    L.orc_cmp_process.argtypes = [vp, vp, lg, lg, lg, vp, lg]
+    L.orc_cmp_set_filter.argtypes = [vp, vp, lg, lg]
+    L.orc_cmp_switch_filter.argtypes = [vp, vp, lg, lg, lg, ip]
+    L.orc_cmp_reset.argtypes = [vp]
+    L.orc_cmp_geometry.argtypes = [vp, vp]
+    L._cmp_ready = True
+    return L
+
+
+def _taps(ir):
+    h = np.asarray(ir, dtype=np.float64)
+    if h.ndim == 1:
+        h = h[:, None]
+    return h, np.ascontiguousarray(h.T)
+
+
+class Processor:
+    """A reference comparison convolver (reference.hpp:53-200): process() takes hop() x channels()."""
+
+    def __init__(self, name, ir, hop=0, fade_duration=1, fade_shape=HANN):
+        L = _cmp_sigs(lib())
+        h, t = _taps(ir)
+        st = C.c_int()
+        self.name = name
+        self._h = L.orc_cmp_create(KINDS[name], t.ctypes.data if t.size else None, h.shape[0], h.shape[1], hop,
+                                   fade_duration, fade_shape, C.byref(st))
+        _chk(st.value)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_cmp_free(self._h)
+            self._h = None
+
+    def _geo(self):
+        g = np.zeros(6, dtype=np.int64)
+        lib().orc_cmp_geometry(self._h, g.ctypes.data)
+        return g
+
+    def hop(self):
+        return int(self._geo()[0])
+
+    def channels(self):
+        return int(self._geo()[1])
+
+    def latency(self):
+        return int(self._geo()[2])
+
+    def stream_delay(self):
+        return int(self._geo()[3])
+
+    def switching_latency(self):
+        return int(self._geo()[4])
+
+    def fading(self):
+        return bool(self._geo()[5])
+
+    def process(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if x.ndim == 1:
+            x = x[:, None]
+        rows, cols = x.shape
+        xf = np.ascontiguousarray(x.T)
+        out = np.empty((max(cols, 1), max(rows, 1)))
+        _chk(lib().orc_cmp_process(self._h, xf.ctypes.data if xf.size else None, max(rows, 1), rows, cols,
+                                   out.ctypes.data, max(rows, 1)))
+        return out.T.copy()
+
+    def set_filter(self, ir):
+        h, t = _taps(ir)
+        _chk(lib().orc_cmp_set_filter(self._h, t.ctypes.data, h.shape[0], h.shape[1]))
+
+    def switch_filter(self, ir, fade_duration, fade_shape=HANN):
+        h, t = _taps(ir)
+        _chk(lib().orc_cmp_switch_filter(self._h, t.ctypes.data, h.shape[0], h.shape[1], fade_duration, fade_shape))
+
+    def reset(self):
+        lib().orc_cmp_reset(self._h)
+
+
+def make_processor(name, ir, hop):
+    """reference.cpp:345-363: the factory (cf-tdc fades over one hop, Hann-complementary)."""
+    if name == "tdc":
+        return Processor("tdc", ir, hop)
+    if name == "cf-tdc":
+        return Processor("cf-tdc", ir, hop, fade_duration=hop)
+    if name in ("ola", "ols", "wola"):
+        return Processor(name, ir)
+    if name == "tvolap":
+        return Engine(partition(np.asarray(ir, dtype=np.float64), hop))
+    raise OracleError(3, "unknown algorithm: " + name)

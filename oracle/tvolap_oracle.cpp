@@ -16,6 +16,9 @@
 //   * TvolapEngine ctor / exchange / latch / process / reset
 //                                                    proj/src/engine.cpp:9-118
 //   * direct_convolve (brute force truth) ........... proj/src/reference.cpp:10-32
+//   * comparison convolvers: DirectProcessor "tdc",
+//     CfTdcProcessor "cf-tdc", OlaProcessor "ola", OlsProcessor "ols",
+//     WolaProcessor "wola" ............................ proj/src/reference.cpp:34-320
 // Parity is pinned by porting the reference's known-answer and property tests
 // (proj/tests/test_spectral.cpp, test_partition.cpp, test_engine.cpp,
 // acceptance.cpp crit 2-4) in tests/test_oracle.py — the reference ships no
@@ -53,6 +56,7 @@ enum Status : int {
     kInvalidConfiguration = 3,  // tvolap::InvalidConfigurationError
     kIncompatibleFilter = 4,    // tvolap::IncompatibleFilterError
     kInvalidSpectrum = 5,       // tvolap::InvalidSpectrumError
+    kSwitchInProgress = 7,      // tvolap::SwitchInProgressError
 };
 
 struct Error {
@@ -408,6 +412,217 @@ struct SetHandle {
     std::shared_ptr<const FilterSet> set;
 };
 
+// ---------------------------------------------------------------- comparison convolvers
+// reference.cpp:34-320. All state is channel-major; process() takes exactly hop() rows.
+enum CmpKind : int { kTdc = 0, kCfTdc = 1, kOla = 2, kOls = 3, kWola = 4 };
+
+struct Cmp {
+    int kind = kTdc;
+    Index hop = 0, taps = 0, channels = 0, block = 0;
+    // time-domain forms (reference.cpp:57-180)
+    std::vector<double> coeffs, old_coeffs, pending_coeffs, history;  // [c][taps], history [c][taps-1]
+    bool pending = false;
+    Index fade_duration = 1, pending_duration = 1, fade_remaining = 0, fade_elapsed = 0;
+    int fade_shape = 0, pending_shape = 0;  // 0 Hann-complementary, 1 linear
+    // block forms (reference.cpp:182-320)
+    std::vector<Spectrum> spectra, pending_spectra;  // per channel, transform 2*block
+    std::vector<double> remainder, previous, analysis, wola_hist, acc;
+
+    Index latency() const { return kind == kOla || kind == kOls || kind == kWola ? block : 0; }
+    Index stream_delay() const { return kind == kWola ? block / 2 : 0; }
+    Index switching_latency() const { return kind == kCfTdc ? fade_duration : (kind == kWola ? block / 2 : 0); }
+
+    // reference.cpp:44-55: zero-padded spectrum of each channel, transform length 2*block
+    std::vector<Spectrum> block_spectra(const double* ir) const {
+        std::vector<Spectrum> out;
+        std::vector<double> padded(2 * block);
+        for (Index c = 0; c < channels; ++c) {
+            std::fill(padded.begin(), padded.end(), 0.0);
+            for (Index i = 0; i < block; ++i) padded[i] = ir[c * block + i];
+            out.push_back(forward_real(padded.data(), 2 * block));
+        }
+        return out;
+    }
+
+    // reference.cpp:110-120
+    double new_gain(Index t) const {
+        const Index d = fade_duration;
+        if (t >= d || d == 1) return 1.0;
+        const double phase = double(t) / double(d);
+        if (fade_shape == 1) return phase;
+        return 0.5 * (1.0 - std::cos(kPi * phase));
+    }
+
+    void check(Index rows, Index cols) const {
+        if (rows != hop) throw Error{kInvalidSize, "process() expects exactly one hop of input per call"};
+        if (cols != channels) throw Error{kInvalidInput, "input channel count does not match the filter"};
+    }
+
+    void set_filter(const double* ir, Index n_taps, Index n_ch) {
+        if (kind == kCfTdc) return switch_filter(ir, n_taps, n_ch, fade_duration, fade_shape);
+        if (n_taps != taps || n_ch != channels) throw Error{kIncompatibleFilter, "replacement filter shape differs"};
+        if (kind == kTdc) {
+            pending_coeffs.assign(ir, ir + taps * channels);
+            pending = true;
+        } else {
+            pending_spectra = block_spectra(ir);
+        }
+    }
+
+    // reference.cpp:122-132
+    void switch_filter(const double* ir, Index n_taps, Index n_ch, Index duration, int shape) {
+        if (fade_remaining > 0 || pending) throw Error{kSwitchInProgress, "a crossfade is already in progress"};
+        if (n_taps != taps || n_ch != channels) throw Error{kIncompatibleFilter, "replacement filter shape differs"};
+        if (duration < 1) throw Error{kInvalidConfiguration, "crossfade duration must be >= 1"};
+        pending_coeffs.assign(ir, ir + taps * channels);
+        pending_duration = duration;
+        pending_shape = shape;
+        pending = true;
+    }
+
+    // y_i = sum_q h[q] * buf[i + taps - 1 - q] (reference.cpp:87-90, 157-159)
+    static double fir(const double* h, const double* buf, Index i, Index taps) {
+        double s = 0.0;
+        for (Index q = 0; q < taps; ++q) s += h[q] * buf[i + taps - 1 - q];
+        return s;
+    }
+
+    void process(const double* in, Index in_stride, Index rows, Index cols, double* out, Index out_stride) {
+        if (kind == kTdc || kind == kCfTdc) {
+            if (pending) {  // reference.cpp:72-76 / 137-146
+                if (kind == kCfTdc) {
+                    old_coeffs.swap(coeffs);
+                    fade_duration = pending_duration;
+                    fade_shape = pending_shape;
+                    fade_remaining = fade_duration;
+                    fade_elapsed = 0;
+                }
+                coeffs = pending_coeffs;
+                pending = false;
+            }
+            check(rows, cols);
+            std::vector<double> buf(taps - 1 + hop);
+            std::vector<Index> elapsed(hop);
+            std::vector<char> blend(hop);
+            for (Index i = 0; i < hop; ++i) {  // the fade clock advances per sample (reference.cpp:153-171)
+                blend[i] = kind == kCfTdc && fade_remaining > 0;
+                elapsed[i] = fade_elapsed;
+                if (blend[i]) {
+                    ++fade_elapsed;
+                    --fade_remaining;
+                }
+            }
+            for (Index c = 0; c < channels; ++c) {
+                std::copy(history.begin() + c * (taps - 1), history.begin() + (c + 1) * (taps - 1), buf.begin());
+                for (Index i = 0; i < hop; ++i) buf[taps - 1 + i] = in[c * in_stride + i];
+                const double* h = coeffs.data() + c * taps;
+                for (Index i = 0; i < hop; ++i) {
+                    const double y_new = fir(h, buf.data(), i, taps);
+                    if (blend[i]) {
+                        const double g_new = new_gain(elapsed[i]);
+                        out[c * out_stride + i] =
+                            (1.0 - g_new) * fir(old_coeffs.data() + c * taps, buf.data(), i, taps) + g_new * y_new;
+                    } else {
+                        out[c * out_stride + i] = y_new;
+                    }
+                }
+                std::copy(buf.begin() + hop, buf.end(), history.begin() + c * (taps - 1));
+            }
+            return;
+        }
+        if (!pending_spectra.empty()) {  // the saved tails keep whatever filter produced them
+            spectra = std::move(pending_spectra);
+            pending_spectra.clear();
+        }
+        check(rows, cols);
+        const Index n = 2 * block;
+        std::vector<double> frame(n), y(n);
+        for (Index c = 0; c < channels; ++c) {
+            const double* x = in + c * in_stride;
+            double* o = out + c * out_stride;
+            std::fill(frame.begin(), frame.end(), 0.0);
+            if (kind == kOla) {  // reference.cpp:205-216
+                for (Index i = 0; i < block; ++i) frame[i] = x[i];
+            } else if (kind == kOls) {  // reference.cpp:241-252
+                for (Index i = 0; i < block; ++i) frame[i] = previous[c * block + i];
+                for (Index i = 0; i < block; ++i) frame[block + i] = x[i];
+            } else {  // WOLA, reference.cpp:283-306
+                const Index half = block / 2;
+                for (Index i = 0; i < half; ++i) frame[i] = wola_hist[c * half + i] * analysis[i];
+                for (Index i = 0; i < half; ++i) frame[half + i] = x[i] * analysis[half + i];
+                for (Index i = 0; i < half; ++i) wola_hist[c * half + i] = x[i];
+            }
+            const Spectrum xs = forward_real(frame.data(), n);
+            Spectrum accs = Spectrum::zero(n);
+            mac_in_place(accs, xs, spectra[c]);
+            inverse_real(accs, y.data());
+            if (kind == kOla) {
+                for (Index i = 0; i < block; ++i) o[i] = y[i] + remainder[c * block + i];
+                for (Index i = 0; i < block; ++i) remainder[c * block + i] = y[block + i];
+            } else if (kind == kOls) {
+                for (Index i = 0; i < block; ++i) o[i] = y[block + i];  // first half carries the circular wrap
+                for (Index i = 0; i < block; ++i) previous[c * block + i] = x[i];
+            } else {
+                const Index half = block / 2;
+                for (Index i = 0; i < block; ++i) y[i] *= analysis[i];  // synthesis window over the block
+                double* a = acc.data() + c * n;
+                for (Index i = 0; i < n; ++i) a[i] += y[i];
+                for (Index i = 0; i < half; ++i) o[i] = 0.5 * a[i];
+                for (Index i = 0; i < n - half; ++i) a[i] = a[i + half];
+                for (Index i = n - half; i < n; ++i) a[i] = 0.0;
+            }
+        }
+    }
+
+    void reset() {
+        std::fill(history.begin(), history.end(), 0.0);
+        fade_remaining = 0;
+        fade_elapsed = 0;
+        std::fill(remainder.begin(), remainder.end(), 0.0);
+        std::fill(previous.begin(), previous.end(), 0.0);
+        std::fill(wola_hist.begin(), wola_hist.end(), 0.0);
+        std::fill(acc.begin(), acc.end(), 0.0);
+    }
+};
+
+// Constructors (reference.cpp:59-66, 97-108, 184-190, 221-227, 259-267); `ir` channel-major.
+Cmp* make_cmp(int kind, const double* ir, Index taps, Index channels, Index hop, Index fade_duration,
+              int fade_shape) {
+    auto p = std::make_unique<Cmp>();
+    p->kind = kind;
+    p->taps = taps;
+    p->channels = channels;
+    if (kind == kTdc || kind == kCfTdc) {
+        if (hop < 1) throw Error{kInvalidConfiguration, "hop must be positive"};
+        if (taps < 1 || channels < 1) throw Error{kInvalidInput, "empty impulse response"};
+        if (kind == kCfTdc && fade_duration < 1) throw Error{kInvalidConfiguration, "crossfade duration must be >= 1"};
+        p->hop = hop;
+        p->coeffs.assign(ir, ir + taps * channels);
+        p->old_coeffs.assign(taps * channels, 0.0);
+        p->history.assign((taps - 1) * channels, 0.0);
+        p->fade_duration = fade_duration;
+        p->fade_shape = fade_shape;
+    } else if (kind == kOla || kind == kOls || kind == kWola) {
+        if (taps < 4 || !is_power_of_two(taps))
+            throw Error{kInvalidSize, "block fast convolution needs a power-of-two response length >= 4"};
+        if (channels < 1) throw Error{kInvalidInput, "empty impulse response"};
+        p->block = taps;
+        p->hop = kind == kWola ? taps / 2 : taps;
+        p->spectra = p->block_spectra(ir);
+        p->remainder.assign(taps * channels, 0.0);
+        p->previous.assign(taps * channels, 0.0);
+        if (kind == kWola) {
+            p->analysis = hann_window(taps / 2);
+            for (double& v : p->analysis) v = std::sqrt(v);
+            p->wola_hist.assign(taps / 2 * channels, 0.0);
+            p->acc.assign(2 * taps * channels, 0.0);
+        }
+    } else {
+        throw Error{kInvalidConfiguration, "unknown algorithm"};
+    }
+    return p.release();
+}
+
 }  // namespace
 
 // ======================================================================= C ABI
@@ -630,6 +845,46 @@ double orc_run_workload(long hop, long min_partitions, long sources, long ears, 
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *status = err.load();
     return secs;
+}
+
+
+// ---- comparison convolvers; kind: 0 tdc, 1 cf-tdc, 2 ola, 3 ols, 4 wola
+void* orc_cmp_create(int kind, const double* ir, long taps, long channels, long hop, long fade_duration,
+                     int fade_shape, int* status) {
+    Cmp* p = nullptr;
+    *status = guarded([&] { p = make_cmp(kind, ir, taps, channels, hop, fade_duration, fade_shape); });
+    return p;
+}
+
+void orc_cmp_free(void* p) { delete static_cast<Cmp*>(p); }
+
+int orc_cmp_process(void* p, const double* in, long in_stride, long rows, long cols, double* out, long out_stride) {
+    return guarded([&] { static_cast<Cmp*>(p)->process(in, in_stride, rows, cols, out, out_stride); });
+}
+
+int orc_cmp_set_filter(void* p, const double* ir, long taps, long channels) {
+    return guarded([&] { static_cast<Cmp*>(p)->set_filter(ir, taps, channels); });
+}
+
+int orc_cmp_switch_filter(void* p, const double* ir, long taps, long channels, long duration, int shape) {
+    return guarded([&] {
+        auto* c = static_cast<Cmp*>(p);
+        if (c->kind != kCfTdc) throw Error{kInvalidConfiguration, "switch_filter needs a cf-tdc processor"};
+        c->switch_filter(ir, taps, channels, duration, shape);
+    });
+}
+
+void orc_cmp_reset(void* p) { static_cast<Cmp*>(p)->reset(); }
+
+// hop, channels, latency, stream_delay, switching_latency, fading
+void orc_cmp_geometry(void* p, long* out6) {
+    const auto* c = static_cast<Cmp*>(p);
+    out6[0] = c->hop;
+    out6[1] = c->channels;
+    out6[2] = c->latency();
+    out6[3] = c->stream_delay();
+    out6[4] = c->switching_latency();
+    out6[5] = c->fade_remaining > 0 ? 1 : 0;
 }
 
 }  // extern "C"

@@ -1117,4 +1117,302 @@ int tvolap_mix_device(int device, long sources, long ears, long samples, const f
     });
 }
 
+// ======================================================================= comparison convolvers
+// the reference's OLA / OLS / WOLA / TDC / CF-TDC processors
+// (reference.cpp:34-320) on the GPU. Host state mirrors the reference classes; the arithmetic
+// runs in tvb::launch_fbconv (block FFT forms, the TVOLAP FFT/MAC building blocks with M = 1)
+// and tvb::launch_fir (direct forms).
+struct tvolap_cmp {
+    int device = 0, kind = 0;
+    long taps = 0, channels = 0, hop = 0, block = 0;
+    cudaStream_t stream = nullptr;
+    // direct forms: coefficient sets [C][taps], history [C][taps-1], fade clock (reference.cpp:97-172)
+    float *coeffs = nullptr, *old_coeffs = nullptr, *pend_coeffs = nullptr, *history = nullptr, *xx = nullptr;
+    long xx_cap = 0;
+    bool pending = false;
+    long fade_duration = 1, pending_duration = 1, fade_remaining = 0, fade_elapsed = 0;
+    int fade_shape = 0, pending_shape = 0;
+    // block forms: packed filter spectra [C][B] (active / staged), carried state, scratch frames
+    float2 *spec = nullptr, *spec_pend = nullptr, *tw = nullptr, *pk = nullptr;
+    bool spec_staged = false;
+    float *win = nullptr, *prev = nullptr, *rem = nullptr, *yhat = nullptr;
+    long yhat_cap = 0;
+    // staging for host buffers
+    float *d_in = nullptr, *d_out = nullptr;
+    long io_cap = 0;
+};
+
+namespace {
+
+void cmp_free(tvolap_cmp* p) {
+    for (void* q : {(void*)p->coeffs, (void*)p->old_coeffs, (void*)p->pend_coeffs, (void*)p->history, (void*)p->xx,
+                    (void*)p->spec, (void*)p->spec_pend, (void*)p->tw, (void*)p->pk, (void*)p->win, (void*)p->prev,
+                    (void*)p->rem, (void*)p->yhat, (void*)p->d_in, (void*)p->d_out})
+        if (q) cudaFree(q);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+}
+
+// channel-major IR (stride ir_stride) -> dense device [C][taps]
+void cmp_upload(tvolap_cmp* p, float* dst, const float* ir, long ir_stride) {
+    const cudaMemcpyKind k = classify(ir) == Mem::Device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpy2DAsync(dst, sizeof(float) * p->taps, ir, sizeof(float) * ir_stride, sizeof(float) * p->taps,
+                         p->channels, k, p->stream));
+}
+
+// block_filter_spectra (reference.cpp:44-55): IR zero-padded to 2B, real 2B FFT, packed bins —
+// the K4 partition transform with hop B/2 and one partition.
+void cmp_spectra(tvolap_cmp* p, float2* dst, const float* ir, long ir_stride) {
+    const float* src = ir;
+    DevBuf* tmp = nullptr;
+    if (classify(ir) != Mem::Device) {
+        tmp = new DevBuf(sizeof(float) * p->taps * p->channels);
+        CK(cudaMemcpy2DAsync(tmp->p, sizeof(float) * p->taps, ir, sizeof(float) * ir_stride, sizeof(float) * p->taps,
+                             p->channels, cudaMemcpyHostToDevice, p->stream));
+        src = (const float*)tmp->p;
+        ir_stride = p->taps;
+    }
+    const cudaError_t err = tvb::launch_partition((int)(p->block / 2), 1, p->channels, src, ir_stride, p->taps, dst, 0,
+                                                  p->tw, p->pk, p->stream);
+    if (tmp) {
+        cudaStreamSynchronize(p->stream);
+        delete tmp;
+    }
+    CK(err);
+}
+
+void cmp_check_filter(const tvolap_cmp* p, const float* ir, long taps, long channels, long ir_stride) {
+    if (!ir) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "null impulse response"};
+    if (taps != p->taps || channels != p->channels)
+        throw ApiError{TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter shape differs"};
+    if (ir_stride < taps) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "IR channel stride shorter than the response"};
+}
+
+}  // namespace
+
+int tvolap_cmp_create(tvolap_cmp** out, int device, int kind, long taps, long channels, const float* ir,
+                      long ir_stride, long hop, long fade_duration, int fade_shape) {
+    if (!out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null output handle");
+    *out = nullptr;
+    tvolap_cmp* p = new tvolap_cmp;
+    const int rc = guarded([&] {
+        const bool direct = kind == TVOLAP_CMP_TDC || kind == TVOLAP_CMP_CF_TDC;
+        const bool block = kind == TVOLAP_CMP_OLA || kind == TVOLAP_CMP_OLS || kind == TVOLAP_CMP_WOLA;
+        if (!direct && !block) throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "unknown algorithm"};
+        if (direct && hop < 1) throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "hop must be positive"};
+        if (direct && (taps < 1 || channels < 1)) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "empty impulse response"};
+        if (kind == TVOLAP_CMP_CF_TDC && fade_duration < 1)
+            throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "crossfade duration must be >= 1"};
+        if (block && (taps < 4 || !is_pow2(taps)))
+            throw ApiError{TVOLAP_ERR_INVALID_SIZE,
+                           "block fast convolution needs a power-of-two response length >= 4"};
+        if (block && taps > 4096)  // one real 2B transform per CTA in shared memory
+            throw ApiError{TVOLAP_ERR_INVALID_SIZE, "GPU block convolvers support responses up to 4096 taps"};
+        if (block && channels < 1) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "empty impulse response"};
+        if (!ir) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "null impulse response"};
+        if (ir_stride < taps) throw ApiError{TVOLAP_ERR_INVALID_INPUT, "IR channel stride shorter than the response"};
+        require_device(device);
+        CK(cudaSetDevice(device));
+        p->device = device;
+        p->kind = kind;
+        p->taps = taps;
+        p->channels = channels;
+        CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+        if (direct) {
+            p->hop = hop;
+            p->fade_duration = fade_duration;
+            p->fade_shape = fade_shape;
+            p->coeffs = dalloc<float>(taps * channels);
+            p->old_coeffs = dalloc<float>(taps * channels);
+            p->pend_coeffs = dalloc<float>(taps * channels);
+            p->history = dalloc<float>(std::max<long>(1, (taps - 1) * channels));
+            CK(cudaMemsetAsync(p->old_coeffs, 0, sizeof(float) * taps * channels, p->stream));
+            CK(cudaMemsetAsync(p->history, 0, sizeof(float) * std::max<long>(1, (taps - 1) * channels), p->stream));
+            cmp_upload(p, p->coeffs, ir, ir_stride);
+        } else {
+            p->block = taps;
+            p->hop = kind == TVOLAP_CMP_WOLA ? taps / 2 : taps;
+            Tables t(taps);
+            p->tw = dalloc<float2>(t.tw.size());
+            p->pk = dalloc<float2>(t.pk.size());
+            CK(cudaMemcpy(p->tw, t.tw.data(), sizeof(float2) * t.tw.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(p->pk, t.pk.data(), sizeof(float2) * t.pk.size(), cudaMemcpyHostToDevice));
+            p->spec = dalloc<float2>(taps * channels);
+            p->spec_pend = dalloc<float2>(taps * channels);
+            const long rem_len = (kind == TVOLAP_CMP_WOLA ? 3 * p->hop : taps) * channels;
+            p->rem = dalloc<float>(rem_len);
+            p->prev = dalloc<float>(p->hop * channels);
+            CK(cudaMemsetAsync(p->rem, 0, sizeof(float) * rem_len, p->stream));
+            CK(cudaMemsetAsync(p->prev, 0, sizeof(float) * p->hop * channels, p->stream));
+            std::vector<float> w(taps);  // sqrt(hann_window(B/2)) (reference.cpp:262)
+            const double pi = 3.14159265358979323846264338327950288;
+            for (long i = 0; i < taps; ++i) w[i] = (float)std::sqrt(1.0 - std::cos(2.0 * pi * (double)i / (double)taps));
+            p->win = dalloc<float>(taps);
+            CK(cudaMemcpy(p->win, w.data(), sizeof(float) * taps, cudaMemcpyHostToDevice));
+            cmp_spectra(p, p->spec, ir, ir_stride);
+        }
+        CK(cudaStreamSynchronize(p->stream));
+    });
+    if (rc != TVOLAP_OK) {
+        cmp_free(p);
+        return rc;
+    }
+    *out = p;
+    return TVOLAP_OK;
+}
+
+int tvolap_cmp_destroy(tvolap_cmp* p) {
+    if (!p) return TVOLAP_OK;
+    cudaSetDevice(p->device);
+    cudaStreamSynchronize(p->stream);
+    cmp_free(p);
+    return TVOLAP_OK;
+}
+
+int tvolap_cmp_process_hops(tvolap_cmp* p, const float* in, long in_stride, float* out, long out_stride,
+                            long n_hops) {
+    if (!p) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null processor");
+    if (n_hops < 1) return set_err(TVOLAP_ERR_INVALID_SIZE, "process() expects at least one hop of input");
+    if (!in || !out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null input or output");
+    const long T = n_hops * p->hop;
+    if (in_stride < T || out_stride < T) return set_err(TVOLAP_ERR_INVALID_SIZE, "lane stride shorter than the call");
+    return guarded([&] {
+        CK(cudaSetDevice(p->device));
+        const long C = p->channels;
+        // device views of the input / output lanes
+        const Mem min = classify(in), mout = classify(out);
+        if ((min != Mem::Device || mout != Mem::Device) && p->io_cap < C * T) {
+            if (p->d_in) CK(cudaFree(p->d_in));
+            if (p->d_out) CK(cudaFree(p->d_out));
+            p->d_in = dalloc<float>(C * T);
+            p->d_out = dalloc<float>(C * T);
+            p->io_cap = C * T;
+        }
+        const float* din = in;
+        long din_stride = in_stride;
+        if (min != Mem::Device) {
+            CK(cudaMemcpy2DAsync(p->d_in, sizeof(float) * T, in, sizeof(float) * in_stride, sizeof(float) * T, C,
+                                 cudaMemcpyHostToDevice, p->stream));
+            din = p->d_in;
+            din_stride = T;
+        }
+        float* dout = mout == Mem::Device ? out : p->d_out;
+        const long dout_stride = mout == Mem::Device ? out_stride : T;
+        if (p->kind == TVOLAP_CMP_TDC || p->kind == TVOLAP_CMP_CF_TDC) {
+            if (p->pending) {  // reference.cpp:72-76 / 137-146: latch at the hop boundary
+                if (p->kind == TVOLAP_CMP_CF_TDC) {
+                    std::swap(p->old_coeffs, p->coeffs);
+                    p->fade_duration = p->pending_duration;
+                    p->fade_shape = p->pending_shape;
+                    p->fade_remaining = p->fade_duration;
+                    p->fade_elapsed = 0;
+                }
+                std::swap(p->coeffs, p->pend_coeffs);
+                p->pending = false;
+            }
+            const long th = p->taps - 1, span = th + T;
+            if (p->xx_cap < C * span) {
+                if (p->xx) CK(cudaFree(p->xx));
+                p->xx = dalloc<float>(C * span);
+                p->xx_cap = C * span;
+            }
+            if (th > 0)
+                CK(cudaMemcpy2DAsync(p->xx, sizeof(float) * span, p->history, sizeof(float) * th, sizeof(float) * th, C,
+                                     cudaMemcpyDeviceToDevice, p->stream));
+            CK(cudaMemcpy2DAsync(p->xx + th, sizeof(float) * span, din, sizeof(float) * din_stride, sizeof(float) * T, C,
+                                 cudaMemcpyDeviceToDevice, p->stream));
+            const long fade_len = p->kind == TVOLAP_CMP_CF_TDC ? std::min(p->fade_remaining, T) : 0;
+            CK(tvb::launch_fir((int)p->taps, C, T, p->xx, span, p->coeffs, p->old_coeffs, dout, dout_stride, fade_len,
+                               p->fade_elapsed, p->fade_duration, p->fade_shape, p->stream));
+            p->fade_elapsed += fade_len;
+            p->fade_remaining -= fade_len;
+            if (th > 0)
+                CK(cudaMemcpy2DAsync(p->history, sizeof(float) * th, p->xx + T, sizeof(float) * span, sizeof(float) * th,
+                                     C, cudaMemcpyDeviceToDevice, p->stream));
+        } else {
+            if (p->spec_staged) {  // the carried tails keep whatever filter produced them
+                std::swap(p->spec, p->spec_pend);
+                p->spec_staged = false;
+            }
+            const long need = C * n_hops * 2 * p->block;
+            if (p->yhat_cap < need) {
+                if (p->yhat) CK(cudaFree(p->yhat));
+                p->yhat = dalloc<float>(need);
+                p->yhat_cap = need;
+            }
+            CK(tvb::launch_fbconv(p->kind, (int)p->block, C, n_hops, din, din_stride, p->prev, p->spec, p->win, p->tw,
+                                  p->pk, p->yhat, dout, dout_stride, p->rem, p->stream));
+        }
+        if (mout != Mem::Device)
+            CK(cudaMemcpy2DAsync(out, sizeof(float) * out_stride, dout, sizeof(float) * T, sizeof(float) * T, C,
+                                 cudaMemcpyDeviceToHost, p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int tvolap_cmp_set_filter(tvolap_cmp* p, const float* ir, long taps, long channels, long ir_stride) {
+    if (!p) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null processor");
+    if (p->kind == TVOLAP_CMP_CF_TDC)  // reference.cpp:134-136: switch with the configured fade
+        return tvolap_cmp_switch_filter(p, ir, taps, channels, ir_stride, p->fade_duration, p->fade_shape);
+    return guarded([&] {
+        cmp_check_filter(p, ir, taps, channels, ir_stride);
+        CK(cudaSetDevice(p->device));
+        if (p->kind == TVOLAP_CMP_TDC) {
+            cmp_upload(p, p->pend_coeffs, ir, ir_stride);
+            p->pending = true;
+        } else {
+            cmp_spectra(p, p->spec_pend, ir, ir_stride);
+            p->spec_staged = true;
+        }
+        CK(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int tvolap_cmp_switch_filter(tvolap_cmp* p, const float* ir, long taps, long channels, long ir_stride,
+                             long fade_duration, int fade_shape) {
+    if (!p) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null processor");
+    return guarded([&] {
+        if (p->kind != TVOLAP_CMP_CF_TDC)
+            throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "switch_filter needs a cf-tdc processor"};
+        if (p->fade_remaining > 0 || p->pending)
+            throw ApiError{TVOLAP_ERR_SWITCH_IN_PROGRESS, "a crossfade is already in progress"};
+        cmp_check_filter(p, ir, taps, channels, ir_stride);
+        if (fade_duration < 1) throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "crossfade duration must be >= 1"};
+        CK(cudaSetDevice(p->device));
+        cmp_upload(p, p->pend_coeffs, ir, ir_stride);
+        p->pending_duration = fade_duration;
+        p->pending_shape = fade_shape;
+        p->pending = true;
+        CK(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int tvolap_cmp_reset(tvolap_cmp* p) {
+    if (!p) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null processor");
+    return guarded([&] {
+        CK(cudaSetDevice(p->device));
+        const long C = p->channels;
+        if (p->history) CK(cudaMemsetAsync(p->history, 0, sizeof(float) * std::max<long>(1, (p->taps - 1) * C), p->stream));
+        if (p->rem)
+            CK(cudaMemsetAsync(p->rem, 0, sizeof(float) * (p->kind == TVOLAP_CMP_WOLA ? 3 * p->hop : p->taps) * C,
+                               p->stream));
+        if (p->prev) CK(cudaMemsetAsync(p->prev, 0, sizeof(float) * p->hop * C, p->stream));
+        p->fade_remaining = 0;
+        p->fade_elapsed = 0;
+        CK(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int tvolap_cmp_geometry(const tvolap_cmp* p, long* out6) {
+    if (!p || !out6) return set_err(TVOLAP_ERR_INVALID_INPUT, "null processor or output");
+    const bool block = p->block > 0;
+    out6[0] = p->hop;
+    out6[1] = p->channels;
+    out6[2] = block ? p->block : 0;
+    out6[3] = p->kind == TVOLAP_CMP_WOLA ? p->block / 2 : 0;
+    out6[4] = p->kind == TVOLAP_CMP_CF_TDC ? p->fade_duration : (p->kind == TVOLAP_CMP_WOLA ? p->block / 2 : 0);
+    out6[5] = p->fade_remaining > 0 ? 1 : 0;
+    return TVOLAP_OK;
+}
+
 }  // extern "C"

@@ -67,4 +67,13 @@ cudaError_t launch_gen_irs(uint64_t seed, long count, const long* lanes, const l
 cudaError_t launch_mix(long sources, long ears, long samples, const float* out, long out_stride, float* mix,
                        long mix_stride, cudaStream_t stream);
 
+// comparison convolvers: OLA / OLS / WOLA block FFT convolution (kind 2/3/4)
+// and the direct-form FIR of "tdc" / "cf-tdc"
+cudaError_t launch_fbconv(int kind, int B, long channels, long n_hops, const float* in, long in_stride, float* prev,
+                          const float2* spec, const float* win, const float2* tw, const float2* pk, float* yhat,
+                          float* out, long out_stride, float* rem, cudaStream_t stream);
+cudaError_t launch_fir(int taps, long channels, long T, const float* xx, long xx_stride, const float* h,
+                       const float* h_old, float* out, long out_stride, long fade_len, long fade_elapsed0,
+                       long fade_duration, int fade_shape, cudaStream_t stream);
+
 }  // namespace tvb

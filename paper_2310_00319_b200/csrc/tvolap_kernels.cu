@@ -1232,6 +1232,162 @@ int grid_for(long work, int threads) {
 
 int fft_threads(int N) { return std::max(32, std::min(256, N / 4)); }
 
+
+// ---------------------------------------------------------------- comparison convolvers (§8f row 4)
+// OLA / OLS / WOLA (reference.cpp:182-320) on the TVOLAP building blocks with M = 1: one CTA per
+// (channel, hop) frames the hop, takes the real 2B transform (B = block = IR length) as a B-point
+// complex Stockham FFT + untangle, multiplies by the channel's filter spectrum (packed bins),
+// tangles and inverse-transforms into a per-hop scratch frame (WOLA: synthesis window applied).
+// Frames depend only on the inputs, so every hop of a call transforms in parallel; the tails are
+// then combined across hops by fbconv_combine_kernel. kind: 2 ola, 3 ols, 4 wola.
+__global__ void __launch_bounds__(256) fbconv_frames_kernel(int kind, int B, int n_hops, const float* __restrict__ in,
+                                                            long in_stride, const float* __restrict__ prev,
+                                                            const float2* __restrict__ spec,
+                                                            const float* __restrict__ win,
+                                                            const float2* __restrict__ tw,
+                                                            const float2* __restrict__ pk, float* __restrict__ yhat) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int N = B;  // complex points of the real 2B transform
+    const int c = blockIdx.y, j = blockIdx.x, tid = threadIdx.x, NT = blockDim.x;
+    const int hop = kind == 4 ? B / 2 : B;
+    float2* s_tw = reinterpret_cast<float2*>(smem);
+    float2* s_pk = s_tw + N;
+    float2* s_a = s_pk + N + 2;
+    float2* s_b = s_a + N;
+    for (int i = tid; i < N; i += NT) s_tw[i] = tw[i];
+    for (int i = tid; i <= N; i += NT) s_pk[i] = pk[i];
+    const float* x = in + (long)c * in_stride + (long)j * hop;  // this hop
+    // the previous hop's input: the call's own previous hop, or the carried state for j = 0
+    const float* xp = j > 0 ? x - hop : prev + (long)c * hop;
+    auto frame = [&](int i) -> float {  // real frame sample i < 2B
+        if (kind == 2) return i < B ? x[i] : 0.f;
+        if (kind == 3) return i < B ? xp[i] : x[i - B];
+        const int h = B / 2;
+        if (i < h) return xp[i] * win[i];
+        return i < B ? x[i - h] * win[i] : 0.f;
+    };
+    for (int k = tid; k < N; k += NT) s_a[k] = make_float2(frame(2 * k), frame(2 * k + 1));
+    __syncthreads();
+    const bool prune = kind != 3;  // OLA and WOLA frames are zero past B
+    const float2* Z = fft_batch<false, 0>(s_a, s_b, N, 1, s_tw, prune, tid, NT);
+    float2* Y = Z == s_a ? s_b : s_a;
+    const float2* H = spec + (long)c * N;
+    for (int k = tid; k < N; k += NT) {
+        const float2 X = untangle_packed(Z, N, k, s_pk);
+        const float2 h = H[k];
+        Y[k] = k == 0 ? make_float2(X.x * h.x, X.y * h.y) : cmul(X, h);  // DC / Nyquist real (packed bin 0)
+    }
+    __syncthreads();
+    float2* T = const_cast<float2*>(Z);
+    for (int k = tid; k < N; k += NT) T[k] = tangle_packed(Y, N, k, s_pk);
+    __syncthreads();
+    const float2* yt = fft_batch<true, 0>(T, Y, N, 1, s_tw, false, tid, NT);
+    const float sc = 1.0f / (float)N;
+    float* o = yhat + ((long)c * n_hops + j) * 2 * B;
+    for (int k = tid; k < N; k += NT) {
+        float a = yt[k].x * sc, b = yt[k].y * sc;
+        if (kind == 4 && 2 * k < B) {  // synthesis window over the block itself (reference.cpp:300-302)
+            a *= win[2 * k];
+            b *= win[2 * k + 1];
+        }
+        o[2 * k] = a;
+        o[2 * k + 1] = b;
+    }
+}
+
+// Tail combination across the hops of a call (one thread per (channel, sample of a hop)) and the
+// carried state: OLA remainder [C][B]; OLS / WOLA previous input hop [C][hop]; WOLA three pending
+// partial sums [C][3][hop] (the 2B accumulator of reference.cpp:304-307 shifted by one hop).
+__global__ void fbconv_combine_kernel(int kind, int B, int channels, int n_hops, const float* __restrict__ in,
+                                      long in_stride, const float* __restrict__ yhat, float* __restrict__ out,
+                                      long out_stride, float* __restrict__ rem, float* __restrict__ prev) {
+    const int hop = kind == 4 ? B / 2 : B;
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)channels * hop) return;
+    const int c = (int)(i / hop), u = (int)(i % hop);
+    const float* y = yhat + (long)c * n_hops * 2 * B;
+    float* o = out + (long)c * out_stride;
+    if (kind == 2) {
+        float r = rem[(long)c * B + u];
+        for (int j = 0; j < n_hops; ++j) {
+            o[(long)j * hop + u] = y[(long)j * 2 * B + u] + r;
+            r = y[(long)j * 2 * B + B + u];
+        }
+        rem[(long)c * B + u] = r;
+    } else if (kind == 3) {
+        for (int j = 0; j < n_hops; ++j) o[(long)j * hop + u] = y[(long)j * 2 * B + B + u];
+    } else {
+        float* A = rem + (long)c * 3 * hop;
+        float a0 = A[u], a1 = A[hop + u], a2 = A[2 * hop + u];
+        for (int j = 0; j < n_hops; ++j) {
+            const float* yj = y + (long)j * 2 * B;
+            o[(long)j * hop + u] = 0.5f * (a0 + yj[u]);
+            a0 = a1 + yj[hop + u];
+            a1 = a2 + yj[2 * hop + u];
+            a2 = yj[3 * hop + u];
+        }
+        A[u] = a0;
+        A[hop + u] = a1;
+        A[2 * hop + u] = a2;
+    }
+    if (kind != 2) prev[(long)c * hop + u] = in[(long)c * in_stride + (long)(n_hops - 1) * hop + u];
+}
+
+// Direct-form FIR for "tdc" / "cf-tdc" (reference.cpp:68-93, 136-172): out[t] = sum_q h[q] xx[t+taps-1-q]
+// over xx = [history (taps-1) | this call's samples]. The first `fade_len` samples of the call blend
+// the old filter's output in with g_new = gain(fade_elapsed0 + t) (Hann-complementary or linear).
+// One CTA = 256 consecutive outputs of one channel; taps are streamed through shared memory in
+// chunks of kFirChunk together with the input span they touch.
+constexpr int kFirTile = 256, kFirChunk = 512;
+__global__ void __launch_bounds__(kFirTile) fir_kernel(int taps, long T, const float* __restrict__ xx, long xx_stride,
+                                                       const float* __restrict__ h, const float* __restrict__ h_old,
+                                                       float* __restrict__ out, long out_stride, long fade_len,
+                                                       long fade_elapsed0, long fade_duration, int fade_shape) {
+    __shared__ float s_h[kFirChunk], s_ho[kFirChunk], s_x[kFirTile + kFirChunk];
+    const int c = blockIdx.y, tid = threadIdx.x;
+    const long t0 = (long)blockIdx.x * kFirTile, t = t0 + tid;
+    const bool blend_cta = t0 < fade_len;
+    const float* xc = xx + (long)c * xx_stride;
+    const float* hc = h + (long)c * taps;
+    const float* hoc = h_old + (long)c * taps;
+    float acc = 0.f, acc_old = 0.f;
+    for (int q0 = 0; q0 < taps; q0 += kFirChunk) {
+        const int qn = min(kFirChunk, taps - q0);
+        __syncthreads();
+        for (int k = tid; k < qn; k += kFirTile) {
+            s_h[k] = hc[q0 + k];
+            if (blend_cta) s_ho[k] = hoc[q0 + k];
+        }
+        // outputs t0 .. t0+255 with taps q0 .. q0+qn-1 read xx[t0 + taps-1-q0-(qn-1) .. t0+255 + taps-1-q0]
+        const long base = t0 + taps - 1 - q0 - (qn - 1);
+        for (int k = tid; k < kFirTile + qn - 1; k += kFirTile) {
+            const long idx = base + k;
+            s_x[k] = idx < T + taps - 1 ? xc[idx] : 0.f;
+        }
+        __syncthreads();
+        if (t < T) {
+            // xx index of (t, q) relative to base: tid + (qn - 1) - (q - q0)
+            for (int k = 0; k < qn; ++k) {
+                const float xv = s_x[tid + qn - 1 - k];
+                acc = fmaf(s_h[k], xv, acc);
+                if (blend_cta) acc_old = fmaf(s_ho[k], xv, acc_old);
+            }
+        }
+    }
+    if (t >= T) return;
+    float y = acc;
+    if (t < fade_len) {
+        const long e = fade_elapsed0 + t;
+        double g = 1.0;
+        if (e < fade_duration && fade_duration != 1) {
+            const double phase = (double)e / (double)fade_duration;
+            g = fade_shape == 1 ? phase : 0.5 * (1.0 - cos(3.14159265358979323846 * phase));
+        }
+        y = (float)(1.0 - g) * acc_old + (float)g * acc;
+    }
+    out[(long)c * out_stride + t] = y;
+}
+
 }  // namespace
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int qm) { return SmemLayout(L, P, E, qm).total; }
@@ -1467,6 +1623,32 @@ cudaError_t launch_mix(long sources, long ears, long samples, const float* out, 
                        long mix_stride, cudaStream_t stream) {
     mix_kernel<<<grid_for(ears * samples, 256), 256, 0, stream>>>(sources, ears, samples, out, out_stride, mix,
                                                                  mix_stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fbconv(int kind, int B, long channels, long n_hops, const float* in, long in_stride, float* prev,
+                          const float2* spec, const float* win, const float2* tw, const float2* pk, float* yhat,
+                          float* out, long out_stride, float* rem, cudaStream_t stream) {
+    const size_t smem = (size_t)(4 * (size_t)B + 2) * sizeof(float2);
+    cudaError_t err = cudaFuncSetAttribute(fbconv_frames_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    fbconv_frames_kernel<<<dim3((unsigned)n_hops, (unsigned)channels), 256, smem, stream>>>(kind, B, (int)n_hops, in,
+                                                                                          in_stride, prev, spec, win, tw,
+                                                                                          pk, yhat);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    const long hop = kind == 4 ? B / 2 : B;
+    fbconv_combine_kernel<<<grid_for(channels * hop, 256), 256, 0, stream>>>(kind, B, (int)channels, (int)n_hops, in,
+                                                                            in_stride, yhat, out, out_stride, rem, prev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fir(int taps, long channels, long T, const float* xx, long xx_stride, const float* h,
+                       const float* h_old, float* out, long out_stride, long fade_len, long fade_elapsed0,
+                       long fade_duration, int fade_shape, cudaStream_t stream) {
+    const dim3 grid((unsigned)((T + kFirTile - 1) / kFirTile), (unsigned)channels);
+    fir_kernel<<<grid, kFirTile, 0, stream>>>(taps, T, xx, xx_stride, h, h_old, out, out_stride, fade_len,
+                                              fade_elapsed0, fade_duration, fade_shape);
     return cudaGetLastError();
 }
 

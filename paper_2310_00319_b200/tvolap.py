@@ -55,6 +55,10 @@ class CudaError(RuntimeError):
     """Device failure (no reference analogue): the engine never falls back to the CPU."""
 
 
+class SwitchInProgressError(RuntimeError):
+    """tvolap::SwitchInProgressError (errors.hpp:46) — a crossfade is already running."""
+
+
 _ERRORS = {
     1: InvalidSizeError,
     2: InvalidInputError,
@@ -62,6 +66,7 @@ _ERRORS = {
     4: IncompatibleFilterError,
     5: InvalidSpectrumError,
     6: CudaError,
+    7: SwitchInProgressError,
 }
 
 _lib = None
@@ -114,6 +119,13 @@ def lib() -> C.CDLL:
             "tvolap_gen_white_device": (ip, [ip, C.c_uint64, lg, lg, lg, lg, fp, lg]),
             "tvolap_gen_irs_device": (ip, [ip, C.c_uint64, lg, fp, fp, fp, fp, C.c_double, lg, fp]),
             "tvolap_mix_device": (ip, [ip, lg, lg, lg, fp, lg, fp, lg, vp]),
+            "tvolap_cmp_create": (ip, [C.POINTER(vp), ip, ip, lg, lg, fp, lg, lg, lg, ip]),
+            "tvolap_cmp_destroy": (ip, [vp]),
+            "tvolap_cmp_process_hops": (ip, [vp, fp, lg, fp, lg, lg]),
+            "tvolap_cmp_set_filter": (ip, [vp, fp, lg, lg, lg]),
+            "tvolap_cmp_switch_filter": (ip, [vp, fp, lg, lg, lg, lg, ip]),
+            "tvolap_cmp_reset": (ip, [vp]),
+            "tvolap_cmp_geometry": (ip, [vp, fp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -130,7 +142,9 @@ EXPORTED_SYMBOLS = (
     "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
     "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_set_block_config tvolap_block_config "
     "tvolap_forward_real tvolap_inverse_real tvolap_mac tvolap_hann_window tvolap_partition "
-    "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device"
+    "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device "
+    "tvolap_cmp_create tvolap_cmp_destroy tvolap_cmp_process_hops tvolap_cmp_set_filter tvolap_cmp_switch_filter "
+    "tvolap_cmp_reset tvolap_cmp_geometry"
 ).split()
 
 
@@ -491,8 +505,167 @@ class TvolapProcessor:
         return self._engine
 
 
-def make_processor(name: str, ir, hop: int, device: int = 0) -> TvolapProcessor:
-    """make_processor (reference.cpp:346-365) — this tier implements the "tvolap" path."""
+# ---------------------------------------------------------------- comparison convolvers (§8f row 4)
+@dataclass
+class CrossfadeConfig:
+    """CrossfadeConfig (reference.hpp:18-22): duration in samples (1 = hard switch), shape."""
+
+    HANN = 0
+    LINEAR = 1
+    duration: int = 1
+    shape: int = 0
+
+
+class _CmpProcessor:
+    """The reference's other streaming convolvers on the GPU (reference.hpp:53-200), through
+    tvolap_cmp_* (include/tvolap_b200.h). process() takes hop() x channels() like the reference;
+    process_hops() takes lanes x (n * hop())."""
+
+    KIND = -1
+    NAME = ""
+
+    def __init__(self, ir, hop: int = 0, fade: Optional[CrossfadeConfig] = None, device: int = 0):
+        h = np.asarray(ir, dtype=np.float64)
+        if h.ndim == 1:
+            h = h[:, None]
+        taps = _f32(h.T) if h.size else np.zeros((max(h.shape[1], 1), 1), np.float32)
+        fade = fade or CrossfadeConfig()
+        self._h = C.c_void_p()
+        _check(lib().tvolap_cmp_create(C.byref(self._h), device, self.KIND, h.shape[0], h.shape[1],
+                                       taps.ctypes.data, max(h.shape[0], 1), hop, fade.duration, fade.shape))
+        self.device = device
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tvolap_cmp_destroy(self._h)
+            self._h = None
+
+    def _geo(self):
+        g = np.zeros(6, dtype=np.int64)
+        _check(lib().tvolap_cmp_geometry(self._h, g.ctypes.data))
+        return g
+
+    def name(self) -> str:
+        return self.NAME
+
+    def hop(self) -> int:
+        return int(self._geo()[0])
+
+    def channels(self) -> int:
+        return int(self._geo()[1])
+
+    def latency(self) -> int:
+        return int(self._geo()[2])
+
+    def stream_delay(self) -> int:
+        return int(self._geo()[3])
+
+    def switching_latency(self) -> int:
+        return int(self._geo()[4])
+
+    def fading(self) -> bool:
+        return bool(self._geo()[5])
+
+    def process_hops(self, x) -> np.ndarray:
+        """lanes x (n * hop) float32 -> same shape (n consecutive process() calls)."""
+        xs = _f32(x)
+        if xs.ndim != 2:
+            raise InvalidInputError("process_hops expects lanes x samples")
+        hop = self.hop()
+        if xs.shape[1] % hop:
+            raise InvalidSizeError("process_hops expects a whole number of hops")
+        out = np.empty_like(xs)
+        _check(lib().tvolap_cmp_process_hops(self._h, xs.ctypes.data, xs.shape[1], out.ctypes.data, out.shape[1],
+                                             xs.shape[1] // hop))
+        return out
+
+    def process(self, input) -> np.ndarray:
+        x = np.asarray(input, dtype=np.float64)
+        if x.ndim == 1:
+            x = x[:, None]
+        if x.shape[0] != self.hop():
+            raise InvalidSizeError("process() expects exactly one hop of input per call")
+        if x.shape[1] != self.channels():
+            raise InvalidInputError("input channel count does not match the filter")
+        return self.process_hops(x.T).T.astype(np.float64)
+
+    def set_filter(self, ir) -> None:
+        h = np.asarray(ir, dtype=np.float64)
+        if h.ndim == 1:
+            h = h[:, None]
+        t = _f32(h.T)
+        _check(lib().tvolap_cmp_set_filter(self._h, t.ctypes.data, h.shape[0], h.shape[1], h.shape[0]))
+
+    def reset(self) -> None:
+        _check(lib().tvolap_cmp_reset(self._h))
+
+
+class DirectProcessor(_CmpProcessor):
+    """DirectProcessor "tdc" (reference.cpp:57-95): direct-form FIR, hard switch at hop boundaries."""
+
+    KIND, NAME = 0, "tdc"
+
+    def __init__(self, ir, hop: int, device: int = 0):
+        super().__init__(ir, hop, device=device)
+
+
+class CfTdcProcessor(_CmpProcessor):
+    """CfTdcProcessor "cf-tdc" (reference.cpp:97-180): direct form, crossfaded filter switch."""
+
+    KIND, NAME = 1, "cf-tdc"
+
+    def __init__(self, ir, hop: int, fade: CrossfadeConfig, device: int = 0):
+        super().__init__(ir, hop, fade=fade, device=device)
+
+    def switch_filter(self, ir, fade: CrossfadeConfig) -> None:
+        h = np.asarray(ir, dtype=np.float64)
+        if h.ndim == 1:
+            h = h[:, None]
+        t = _f32(h.T)
+        _check(lib().tvolap_cmp_switch_filter(self._h, t.ctypes.data, h.shape[0], h.shape[1], h.shape[0],
+                                              fade.duration, fade.shape))
+
+
+class OlaProcessor(_CmpProcessor):
+    """OlaProcessor "ola" (reference.cpp:182-219): block = IR length, hop = block."""
+
+    KIND, NAME = 2, "ola"
+
+    def __init__(self, ir, device: int = 0):
+        super().__init__(ir, 0, device=device)
+
+
+class OlsProcessor(_CmpProcessor):
+    """OlsProcessor "ols" (reference.cpp:221-255): block = IR length, hop = block."""
+
+    KIND, NAME = 3, "ols"
+
+    def __init__(self, ir, device: int = 0):
+        super().__init__(ir, 0, device=device)
+
+
+class WolaProcessor(_CmpProcessor):
+    """WolaProcessor "wola" (reference.cpp:257-315): sqrt-Hann analysis/synthesis, hop = block / 2."""
+
+    KIND, NAME = 4, "wola"
+
+    def __init__(self, ir, device: int = 0):
+        super().__init__(ir, 0, device=device)
+
+
+def make_processor(name: str, ir, hop: int, device: int = 0):
+    """make_processor (reference.cpp:345-363): "tdc", "cf-tdc" (cosine fade over one hop), "ola",
+    "ols", "wola" (block forms ignore `hop`), "tvolap"."""
+    if name == "tdc":
+        return DirectProcessor(ir, hop, device=device)
+    if name == "cf-tdc":
+        return CfTdcProcessor(ir, hop, CrossfadeConfig(hop, CrossfadeConfig.HANN), device=device)
+    if name == "ola":
+        return OlaProcessor(ir, device=device)
+    if name == "ols":
+        return OlsProcessor(ir, device=device)
+    if name == "wola":
+        return WolaProcessor(ir, device=device)
     if name == "tvolap":
         return TvolapProcessor(ir, hop, device=device)
     raise InvalidConfigurationError(f"unknown algorithm: {name}")

@@ -78,6 +78,35 @@ int main() {
         TvolapProcessor proc(delta_ir(0.5, 300), 64);
         Frames y = proc.process(Frames(64, 1, 1.0));
         CHECK(proc.name() == "tvolap" && y.rows() == 64);
+
+        // comparison convolvers through the StreamingProcessor face (reference.hpp:26-226)
+        for (const char* name : {"tdc", "cf-tdc", "ola", "ols", "wola", "tvolap"}) {
+            auto p = make_processor(name, delta_ir(1.0, 128), 32);
+            CHECK(p->name() == name);
+            // identity response: after the stream delay the output reproduces the input
+            const Index h = p->hop(), d = p->stream_delay();
+            std::vector<double> xs, ys;
+            for (Index k = 0; k < 8; ++k) {
+                Frames x(h, 1);
+                for (Index t = 0; t < h; ++t) x(t, 0) = std::sin(0.01 * (double)(k * h + t));
+                Frames o = p->process(x);
+                for (Index t = 0; t < h; ++t) {
+                    xs.push_back(x(t, 0));
+                    ys.push_back(o(t, 0));
+                }
+            }
+            double e = 0.0;
+            for (size_t t = (size_t)d; t < ys.size(); ++t) e = std::max(e, std::fabs(ys[t] - xs[t - (size_t)d]));
+            CHECK(e < 1e-5);
+        }
+        threw = false;
+        try {
+            CfTdcProcessor cf(delta_ir(1.0, 8), 32, CrossfadeConfig{200});
+            cf.process(Frames(32, 1, 1.0));
+            cf.set_filter(delta_ir(0.5, 8));
+            cf.set_filter(delta_ir(0.25, 8));
+        } catch (const SwitchInProgressError&) { threw = true; }
+        CHECK(threw);
     } catch (const CudaError& e) {
         std::printf("NO_GPU %s\n", e.what());
         return 77;

@@ -69,6 +69,14 @@ def test_argument_validation_without_device():
     ir = np.ones(10, np.float32)
     assert T.lib().tvolap_create(ctypes.byref(h), 0, 24, 1, 10, ir.ctypes.data, 1) == 1
     assert T.lib().tvolap_create(ctypes.byref(h), 0, 64, 1, 0, ir.ctypes.data, 1) == 2
+    # comparison convolvers (§8f row 4): the reference's constructor checks, before any device work
+    c = ctypes.c_void_p()
+    assert T.lib().tvolap_cmp_create(ctypes.byref(c), 0, 2, 100, 1, ir.ctypes.data, 100, 0, 1, 0) == 1  # ola: 2^k
+    assert T.lib().tvolap_cmp_create(ctypes.byref(c), 0, 0, 10, 1, ir.ctypes.data, 10, 0, 1, 0) == 3  # tdc: hop < 1
+    assert T.lib().tvolap_cmp_create(ctypes.byref(c), 0, 1, 10, 1, ir.ctypes.data, 10, 8, 0, 0) == 3  # fade < 1
+    assert T.lib().tvolap_cmp_create(ctypes.byref(c), 0, 9, 10, 1, ir.ctypes.data, 10, 8, 1, 0) == 3  # kind
+    with pytest.raises(T.InvalidSizeError):
+        T.OlaProcessor(np.ones(100))
 
 
 @pytest.mark.skipif(gpu_available(), reason="checks the no-GPU behaviour")
