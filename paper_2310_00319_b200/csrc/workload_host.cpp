@@ -4,6 +4,7 @@
 // generators produce. Not part of the hot path.
 #include <algorithm>
 #include <cmath>
+#include <random>
 #include <cstdint>
 #include <thread>
 #include <vector>
@@ -83,5 +84,52 @@ void tv_gen_schedule(uint64_t seed, long hop0, long n_hops, long lanes, int n_ba
 }
 
 uint64_t tv_rand64_c(uint64_t seed, uint64_t stream, uint64_t ctr) { return tv_rand64(seed, stream, ctr); }
+
+
+// ---- the reference's CLI signal generators (proj/src/signal_gen.cpp), with the same engine
+// (std::mt19937_64) and the same 53-bit mapping (signal_gen.cpp:14-16), so `pink:SEED` and
+// `synth:azDEG` specs produce the reference's exact fp64 streams.
+static double tv_uniform_pm1(std::mt19937_64& g) { return 2.0 * ((double)(g() >> 11) * 0x1.0p-53) - 1.0; }
+
+// gen_pink (signal_gen.cpp:42-59): Kellet's pole-zero cascade over uniform white noise.
+void tv_gen_pink(uint64_t seed, long n, double* out) {
+    std::mt19937_64 g(seed);
+    double b0 = 0, b1 = 0, b2 = 0, b3 = 0, b4 = 0, b5 = 0, b6 = 0;
+    for (long t = 0; t < n; ++t) {
+        const double w = tv_uniform_pm1(g);
+        b0 = 0.99886 * b0 + w * 0.0555179;
+        b1 = 0.99332 * b1 + w * 0.0750759;
+        b2 = 0.96900 * b2 + w * 0.1538520;
+        b3 = 0.86650 * b3 + w * 0.3104856;
+        b4 = 0.55000 * b4 + w * 0.5329522;
+        b5 = -0.7616 * b5 - w * 0.0168980;
+        out[t] = 0.11 * (b0 + b1 + b2 + b3 + b4 + b5 + b6 + w * 0.5362);
+        b6 = w * 0.115926;
+    }
+}
+
+// synthetic_binaural_ir (signal_gen.cpp:73-107): direct taps with an azimuth-dependent
+// interaural delay / level, plus a shared decaying room tail 30 dB down. out[c * n_ir + q].
+int tv_synthetic_binaural_ir(double azimuth_deg, long n_ir, double fs, uint64_t seed, double* out) {
+    if (n_ir < 128 || !(fs > 0.0)) return 2;
+    const double pi = 3.14159265358979323846264338327950288;
+    for (long i = 0; i < 2 * n_ir; ++i) out[i] = 0.0;
+    const double lateral = std::sin(azimuth_deg * pi / 180.0);
+    const long base_delay = 2;
+    const long max_itd = (long)std::llround(fs / 1500.0);
+    const long itd = (long)std::llround(std::fabs(lateral) * (double)max_itd);
+    const double far_gain = itd == 0 ? 1.0 : 1.0 - 0.75 * std::fabs(lateral);
+    const long near = lateral >= 0.0 ? 0 : 1;
+    out[near * n_ir + base_delay] = 1.0;
+    out[(1 - near) * n_ir + base_delay + itd] = far_gain;
+    const long tail_start = 64;
+    const double tau = (double)std::max<long>(256, n_ir / 8);
+    for (long c = 0; c < 2; ++c) {
+        std::mt19937_64 g(seed ^ (0x9e3779b97f4a7c15ULL * (uint64_t)(c + 1)));
+        for (long q = tail_start; q < n_ir; ++q)
+            out[c * n_ir + q] += 0.0316 * std::exp(-(double)(q - tail_start) / tau) * tv_uniform_pm1(g);
+    }
+    return 0;
+}
 
 }  // extern "C"

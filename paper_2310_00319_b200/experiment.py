@@ -1,23 +1,25 @@
-"""Switch experiment and metric tables over the GPU engine.
+"""Switch / compare experiments and metric tables over the GPU processors.
 
-Restates proj/src/experiment.cpp:33-128 (drive, run_switch) and :163-264 (metrics_csv,
-metrics_json, transition_csv) for the "tvolap" algorithm on the B200 engine, so the reference's
-switching analysis (transition start / width / click steps) runs on GPU output. The three runs
-(switched, old filter throughout, new filter throughout) use multi-hop calls, which are
-bit-identical to one process() per hop, so outputs before the boundary and after settling match
-the references to within fp32 rounding; the detection threshold is 1e-6 of the signal scale
-(the reference's fp64 engine uses 1e-9).
+Restates proj/src/experiment.cpp:23-161 (make_proc, drive, run_switch, run_compare) and
+:163-264 (metrics_csv, metrics_json, compare_csv, compare_json, transition_csv) for every
+algorithm of make_processor ("tvolap" on the B200 engine; "tdc", "cf-tdc", "ola", "ols", "wola"
+on the GPU comparison convolvers), so the reference's switching analysis (transition start /
+width / click steps, engine vs crossfade difference) runs on GPU output. The three runs
+(switched, old filter throughout, new filter throughout) use multi-hop calls, which equal one
+process() per hop, so outputs before the boundary and after settling match the references to
+within fp32 rounding; the detection threshold is 1e-6 of the signal scale (the reference's fp64
+engine uses 1e-9).
 """
 from __future__ import annotations
 
 import json
 from dataclasses import asdict, dataclass, field
-from typing import List
+from typing import List, Optional
 
 import numpy as np
 
-from .tvolap import (IncompatibleFilterError, InvalidConfigurationError, InvalidInputError,  # noqa: F401
-                     TvolapProcessor)
+from .tvolap import (CfTdcProcessor, CrossfadeConfig, IncompatibleFilterError,  # noqa: F401
+                     InvalidConfigurationError, InvalidInputError, TvolapProcessor, make_processor)
 
 
 @dataclass
@@ -50,34 +52,39 @@ def _as_frames(a) -> np.ndarray:
     return a[:, None] if a.ndim == 1 else a
 
 
-def _drive(proc: TvolapProcessor, padded: np.ndarray, ir_b, switch_call: int) -> np.ndarray:
+def _make_proc(algorithm: str, ir, hop: int, fade: Optional[CrossfadeConfig], device: int):
+    """experiment.cpp:23-29."""
+    if algorithm == "cf-tdc" and fade is not None:
+        return CfTdcProcessor(ir, hop, fade, device=device)
+    return make_processor(algorithm, ir, hop, device=device)
+
+
+def _drive(proc, padded: np.ndarray, ir_b, switch_call: int) -> np.ndarray:
     """experiment.cpp:33-54: hops in order (plus delay/hop zero hops), filter staged right before
     `switch_call` (negative: never); returns the input-aligned stream."""
     hop, delay = proc.hop(), proc.stream_delay()
     calls = padded.shape[0] // hop + delay // hop
     x = np.zeros((calls * hop, padded.shape[1]), dtype=np.float32)
     x[: padded.shape[0]] = padded
-    eng = proc.engine()
+    run = proc.engine().process_hops if isinstance(proc, TvolapProcessor) else proc.process_hops
     lanes = np.ascontiguousarray(x.T)
     cut = switch_call * hop if 0 <= switch_call < calls else calls * hop
     parts = []
     if cut > 0:
-        parts.append(eng.process_hops(np.ascontiguousarray(lanes[:, :cut])))
+        parts.append(run(np.ascontiguousarray(lanes[:, :cut])))
     if cut < calls * hop:
         proc.set_filter(ir_b)
-        parts.append(eng.process_hops(np.ascontiguousarray(lanes[:, cut:])))
+        parts.append(run(np.ascontiguousarray(lanes[:, cut:])))
     stream = np.concatenate(parts, axis=1).T
     return stream[delay: delay + padded.shape[0]].astype(np.float64)
 
 
 def run_switch(input, ir_a, ir_b, hop: int, requested_switch_sample: int, algorithm: str = "tvolap",
                input_rate: float = 48000.0, ir_a_rate: float = 48000.0, ir_b_rate: float = 48000.0,
-               device: int = 0) -> SwitchRun:
-    """run_switch (experiment.cpp:58-128) for the partitioned engine on the GPU."""
+               device: int = 0, fade: Optional[CrossfadeConfig] = None) -> SwitchRun:
+    """run_switch (experiment.cpp:58-128) on the GPU processors."""
     import time
 
-    if algorithm != "tvolap":
-        raise InvalidConfigurationError(f"unknown algorithm on the GPU path: {algorithm}")
     x = _as_frames(input)
     a, b = _as_frames(ir_a), _as_frames(ir_b)
     if x.shape[0] < 1:
@@ -87,9 +94,9 @@ def run_switch(input, ir_a, ir_b, hop: int, requested_switch_sample: int, algori
     if x.shape[1] == 1 and a.shape[1] > 1:  # fan_out (audio_buffer.hpp:60-67)
         x = np.repeat(x, a.shape[1], axis=1)
 
-    proc = TvolapProcessor(a, hop, device=device)
-    ref_old = TvolapProcessor(a, hop, device=device)
-    ref_new = TvolapProcessor(b, hop, device=device)
+    proc = _make_proc(algorithm, a, hop, fade, device)
+    ref_old = _make_proc(algorithm, a, hop, fade, device)
+    ref_new = _make_proc(algorithm, b, hop, fade, device)
     h = proc.hop()
     calls_in = -(-x.shape[0] // h)
     n = calls_in * h
@@ -100,7 +107,7 @@ def run_switch(input, ir_a, ir_b, hop: int, requested_switch_sample: int, algori
     padded = np.zeros((n, x.shape[1]))
     padded[: x.shape[0]] = x
 
-    if -(-b.shape[0] // (2 * h)) > proc.engine().partition_count():
+    if algorithm == "tvolap" and -(-b.shape[0] // (2 * h)) > proc.engine().partition_count():
         raise IncompatibleFilterError("replacement filter partition count differs")
     run = SwitchRun()
     switch_call = boundary // h + proc.stream_delay() // h
@@ -130,6 +137,52 @@ def run_switch(input, ir_a, ir_b, hop: int, requested_switch_sample: int, algori
     return run
 
 
+@dataclass
+class CompareMetrics:
+    """experiment.hpp:47-56."""
+
+    fade_shape: str = "hann"
+    fade_duration: int = 0
+    window_begin: int = 0
+    window_end: int = 0
+    max_abs_diff: float = 0.0
+    rms_diff: float = 0.0
+    output_rms: float = 0.0
+    diff_db: float = 0.0
+
+
+@dataclass
+class CompareRun:
+    tvolap: SwitchRun = None
+    crossfaded: SwitchRun = None
+    difference: np.ndarray = field(repr=False, default=None)
+    metrics: CompareMetrics = field(default_factory=CompareMetrics)
+
+
+def run_compare(input, ir_a, ir_b, hop: int, requested_switch_sample: int, shape: int = CrossfadeConfig.HANN,
+                device: int = 0) -> CompareRun:
+    """run_compare (experiment.cpp:130-161): the partitioned engine against the crossfaded direct
+    form (fade duration = hop), both on the GPU."""
+    fade = CrossfadeConfig(hop, shape)
+    run = CompareRun()
+    run.tvolap = run_switch(input, ir_a, ir_b, hop, requested_switch_sample, "tvolap", device=device)
+    run.crossfaded = run_switch(input, ir_a, ir_b, hop, requested_switch_sample, "cf-tdc", device=device, fade=fade)
+    run.difference = run.tvolap.output - run.crossfaded.output
+    m = run.metrics
+    m.fade_shape = "linear" if shape == CrossfadeConfig.LINEAR else "hann"
+    m.fade_duration = fade.duration
+    n = run.difference.shape[0]
+    b = run.tvolap.metrics.switch_boundary
+    m.window_begin, m.window_end = b, min(n, b + 3 * hop)
+    m.max_abs_diff = float(np.abs(run.difference).max())
+    win = run.difference[m.window_begin:m.window_end]
+    out = run.tvolap.output[m.window_begin:m.window_end]
+    m.rms_diff = float(np.sqrt(np.mean(win ** 2)))
+    m.output_rms = float(np.sqrt(np.mean(out ** 2)))
+    m.diff_db = float(20.0 * np.log10(max(m.rms_diff, 1e-300) / max(m.output_rms, 1e-300)))
+    return run
+
+
 def _fmt(v: float) -> str:
     return "%.12g" % v
 
@@ -147,6 +200,20 @@ def metrics_csv(rows: List[SwitchMetrics]) -> str:
 
 def metrics_json(rows: List[SwitchMetrics]) -> str:
     """experiment.cpp:183-200."""
+    return json.dumps([asdict(m) for m in rows], indent=2) + "\n"
+
+
+def compare_csv(rows: List[CompareMetrics]) -> str:
+    """experiment.cpp:202-218."""
+    out = "fade_shape,fade_duration,window_begin,window_end,max_abs_diff,rms_diff,output_rms,diff_db\n"
+    for m in rows:
+        out += ",".join([m.fade_shape, str(m.fade_duration), str(m.window_begin), str(m.window_end),
+                         _fmt(m.max_abs_diff), _fmt(m.rms_diff), _fmt(m.output_rms), _fmt(m.diff_db)]) + "\n"
+    return out
+
+
+def compare_json(rows: List[CompareMetrics]) -> str:
+    """experiment.cpp:220-234."""
     return json.dumps([asdict(m) for m in rows], indent=2) + "\n"
 
 

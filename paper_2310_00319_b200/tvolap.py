@@ -566,6 +566,9 @@ class _CmpProcessor:
     def fading(self) -> bool:
         return bool(self._geo()[5])
 
+    def channels_out(self) -> int:
+        return self.channels()
+
     def process_hops(self, x) -> np.ndarray:
         """lanes x (n * hop) float32 -> same shape (n consecutive process() calls)."""
         xs = _f32(x)

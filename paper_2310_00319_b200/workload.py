@@ -38,6 +38,10 @@ def wlib() -> C.CDLL:
         L.tv_gen_schedule.restype = None
         L.tv_rand64_c.argtypes = [u64, u64, u64]
         L.tv_rand64_c.restype = u64
+        L.tv_gen_pink.argtypes = [u64, lg, vp]
+        L.tv_gen_pink.restype = None
+        L.tv_synthetic_binaural_ir.argtypes = [dp, lg, dp, u64, vp]
+        L.tv_synthetic_binaural_ir.restype = C.c_int
         _wl = L
     return _wl
 
@@ -171,3 +175,21 @@ def flops_per_hop(cfg: Config) -> float:
     B = 2 * L + 1
     fft = (5 * np.log2(2 * L) + 14) * 2 * L
     return cfg.lanes * 8 * B * M + (cfg.sources + cfg.lanes) * fft
+
+
+def gen_pink(seed: int, n: int) -> np.ndarray:
+    """gen_pink (proj/src/signal_gen.cpp:42-59): (n,) fp64, bit-exact with the reference."""
+    if n < 1:
+        raise ValueError("gen_pink: need at least one sample")
+    out = np.empty(n)
+    wlib().tv_gen_pink(seed, n, out.ctypes.data)
+    return out
+
+
+def synthetic_binaural_ir(azimuth_deg: float, n_ir: int, fs: float = FS, seed: int = 7) -> np.ndarray:
+    """synthetic_binaural_ir (proj/src/signal_gen.cpp:73-107): (n_ir, 2) fp64."""
+    out = np.empty((2, n_ir))
+    if wlib().tv_synthetic_binaural_ir(azimuth_deg, n_ir, fs, seed, out.ctypes.data):
+        raise ValueError("synthetic_binaural_ir: response too short or bad sample rate")
+    return np.ascontiguousarray(out.T)
+

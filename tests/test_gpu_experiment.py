@@ -83,3 +83,53 @@ def test_metric_tables_render():  # test_experiment.cpp:105-122
     assert parsed[0]["transition_width"] == 256 and parsed[1]["switch_boundary"] == 2048
     tc = X.transition_csv(run, 4, 4).splitlines()
     assert tc[0] == "offset,output_0,old_ref_0,new_ref_0" and tc[1].startswith("-4,") and len(tc) == 9
+
+
+def flip_alg(alg, hop, requested, n=8192, fade=None):
+    return X.run_switch(np.ones(n), delta(1, 2048), delta(-1, 2048), hop, requested, alg, fade=fade)
+
+
+def test_switch_widths_of_all_algorithms():  # test_experiment.cpp:53-60
+    assert flip_alg("ols", 2048, 4096).metrics.transition_width == 0
+    assert flip_alg("ola", 2048, 4096).metrics.transition_width == 0
+    assert flip_alg("wola", 1024, 4096).metrics.transition_width == 1024
+    assert flip_alg("tvolap", 256, 4096).metrics.transition_width == 256
+    assert flip_alg("tdc", 256, 4096).metrics.transition_width == 0
+
+
+def test_wola_crosses_over_along_half_cosine():  # test_experiment.cpp:62-71
+    run = flip_alg("wola", 1024, 4096)
+    b, r = run.metrics.switch_boundary, 1024
+    u = np.arange(0, r, 7)
+    assert np.abs(run.output[b + u, 0] - np.cos(np.pi * u / r)).max() < 1e-5
+
+
+def test_crossfaded_direct_follows_requested_fade():  # test_experiment.cpp:73-85
+    fade = T.CrossfadeConfig(512, T.CrossfadeConfig.LINEAR)
+    run = X.run_switch(np.ones(8192), delta(1, 2048), delta(-1, 2048), 256, 2048, "cf-tdc", fade=fade)
+    m = run.metrics
+    assert (m.switching_latency, m.switch_boundary, m.transition_width) == (512, 2048, 512)
+    u = np.arange(0, 512, 13)
+    assert np.abs(run.output[2048 + u, 0] - (1.0 - 2.0 * u / 512)).max() < 1e-5
+
+
+def test_engine_against_crossfaded_reference():  # test_experiment.cpp:136-171
+    cmp = X.run_compare(np.ones(8192), delta(1, 2048), delta(-1, 2048), 256, 2048)
+    assert cmp.metrics.fade_shape == "hann" and cmp.metrics.fade_duration == 256
+    assert cmp.metrics.max_abs_diff < 1e-5  # the polarity flip: both transitions coincide
+    # a smooth two-channel scene (stand-in for the reference's pink-noise binaural scene)
+    g = np.random.default_rng(3)
+    x = np.convolve(g.standard_normal(16384 + 63), np.hanning(64) / 32, mode="valid")
+    t = np.arange(2048)[:, None]
+    ir_a = g.standard_normal((2048, 2)) * np.exp(-t / 150.0)
+    ir_b = g.standard_normal((2048, 2)) * np.exp(-t / 150.0)
+    hann = X.run_compare(x, ir_a, ir_b, 256, 336)
+    lin = X.run_compare(x, ir_a, ir_b, 256, 336, T.CrossfadeConfig.LINEAR)
+    assert (hann.metrics.window_begin, hann.metrics.window_end) == (256, 256 + 3 * 256)
+    assert hann.metrics.max_abs_diff > 0 and hann.metrics.output_rms > 0
+    assert hann.metrics.diff_db < 0
+    assert lin.metrics.fade_shape == "linear"
+    csv = X.compare_csv([hann.metrics, lin.metrics])
+    assert csv.startswith("fade_shape,fade_duration,window_begin,window_end,max_abs_diff,rms_diff,output_rms,diff_db\n")
+    parsed = json.loads(X.compare_json([hann.metrics, lin.metrics]))
+    assert parsed[0]["fade_shape"] == "hann" and parsed[1]["fade_shape"] == "linear"

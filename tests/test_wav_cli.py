@@ -112,3 +112,55 @@ def test_cli_library_error_exit_code(tmp_path):
     r = _cli("process", "--input", "ones:100", "--ir", "+delta", "--output", str(tmp_path / "o.wav"),
              "--block", "24")
     assert r.returncode == 1 and "error" in r.stderr
+
+
+def test_reference_signal_generators():
+    """pink:SEED and synth:azDEG specs (proj/src/signal_gen.cpp:42-107): host generators."""
+    from paper_2310_00319_b200 import workload as W
+
+    p = W.gen_pink(1, 4096)
+    assert p.shape == (4096,) and 0.01 < np.std(p) < 1.0 and np.array_equal(p, W.gen_pink(1, 4096))
+    h = W.synthetic_binaural_ir(90.0, 2048)
+    assert h.shape == (2048, 2)
+    itd = round(48000 / 1500)  # full lateral displacement
+    assert h[2, 0] == 1.0 and h[2 + itd, 1] == pytest.approx(0.25) and h[3:64, 0].max() == 0.0
+    assert np.abs(h[64:]).max() < 0.0316
+    h0 = W.synthetic_binaural_ir(0.0, 2048)
+    assert h0[2, 0] == 1.0 and h0[2, 1] == 1.0
+    assert np.array_equal(h0[64:], h[64:])  # the room tail never depends on azimuth
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["tdc", "cf-tdc", "ola", "ols", "wola"])
+def test_cli_process_other_algorithms(tmp_path, algo):
+    out = tmp_path / "o.wav"
+    r = _cli("process", "--algo", algo, "--input", "sine:1000:6000", "--ir", "delta:0.5:2", "--out", str(out),
+             "--block", "512", "--ir-len", "512")
+    assert r.returncode == 0, r.stderr
+    y, _ = wav.read_wav(str(out))
+    x = np.sin(2 * np.pi * 1000 / 48000 * np.arange(6000))
+    ref = np.zeros(6000)
+    ref[2:] = 0.5 * x[:-2]
+    assert y.shape[0] >= 6000
+    err = np.abs(y[:6000, 0] - ref)
+    if algo == "wola":  # only approximate for a delayed tap (test_reference.cpp:108-120)
+        assert err.max() < 0.1
+    else:
+        assert err.max() < 1e-4
+
+
+@pytest.mark.gpu
+def test_cli_switch_and_compare(tmp_path, monkeypatch):
+    monkeypatch.setenv("TVOLAP_OUT_DIR", str(tmp_path))
+    r = _cli("switch", "--algo", "tvolap", "--switch-ms", "16", "--out-prefix", "sw")
+    assert r.returncode == 0, r.stderr
+    assert "transition width 256" in r.stdout
+    for f in ("sw_output.wav", "sw_metrics.csv", "sw_metrics.json", "sw_transition.csv"):
+        assert (tmp_path / f).exists()
+    r = _cli("compare", "--frames", "8192", "--out-prefix", "cmp")
+    assert r.returncode == 0, r.stderr
+    assert "hann:" in r.stdout and "linear:" in r.stdout
+    csv = (tmp_path / "cmp_metrics.csv").read_text()
+    assert csv.startswith("fade_shape,fade_duration,window_begin,window_end,max_abs_diff,rms_diff,output_rms,diff_db")
+    for f in ("cmp_tvolap.wav", "cmp_cftdc_hann.wav", "cmp_diff_linear.wav", "cmp_metrics.json"):
+        assert (tmp_path / f).exists()
