@@ -100,6 +100,20 @@ int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, 
                         long n_hops, const int32_t* schedule);
 
 /*
+ * n_hops hops with a filter switch every `period` hops: exactly
+ *   for k: { if (irs[k]) exchange_filter(irs[k], ir_length, channels); process_hops(period) }
+ * (the reference's drive() loop, experiment.cpp:42-49, with the switch staged right before the
+ * hop it applies to), k < ceil(n_hops / period); irs[k] == NULL keeps the running filter. `irs`
+ * is a host array of channel-major IR pointers (irs[k][c * ir_length + n]). With device
+ * buffers and device IRs the whole call is one hop-blocked launch that transforms switch k+1's
+ * partitions inside the cluster-barrier gaps of period k (no separate K4 launch, no launch gap
+ * per period); otherwise it runs the loop above. Outputs are bit-identical either way.
+ * Filter-set engines only.
+ */
+int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
+                             long n_hops, long period, const float* const* irs, long ir_length);
+
+/*
  * Stage a replacement filter: TvolapProcessor::set_filter(ir) ≙
  * exchange_filter(partition(ir, L, M)) (reference.cpp:335-338,
  * engine.cpp:37-48). The partition runs on the device on a side stream

@@ -185,6 +185,14 @@ struct tvolap_engine {
     bool k4_side = false;            // true: transform staged sets on the side stream (overlapping hops)
     bool staged_on_side = false;     // the pending set was transformed on the side stream
     bool k4_stream = false;          // true: transform at latch time on the engine stream (PDL chain)
+    // switching launches (tvolap_process_switching): per-switch IR pointers / pool entries
+    const float** d_sw_irs = nullptr;
+    int* d_sw_entry = nullptr;
+    long sw_cap = 0;
+    const float* const* sw_irs_launch = nullptr;  // set only around a switching launch
+    const int* sw_entry_launch = nullptr;
+    int sw_count_launch = 0, sw_period_launch = 0;
+    long sw_len_launch = 0;
     bool staged_in_stream = false;   // the pending set is transformed by latch() on the engine stream
     // chunked host pipeline
     long chunk_hops = 0;
@@ -216,7 +224,7 @@ struct tvolap_engine {
                         (void*)d_sel, (void*)d_irstage, (void*)d_irst[0], (void*)d_irst[1], (void*)d_irst[2],
                         (void*)d_irst[3], (void*)d_in[0],
                         (void*)d_in[1], (void*)d_out[0],
-                        (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1]})
+                        (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1], (void*)d_sw_irs, (void*)d_sw_entry})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
@@ -443,6 +451,12 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.pool_w = e->pool;
     p.new_entry_base = e->active * (int)e->S;
     p.qm = e->QM;
+    p.sw_irs = e->sw_irs_launch;
+    p.sw_entry = e->sw_entry_launch;
+    p.sw_count = e->sw_count_launch;
+    p.sw_period = e->sw_period_launch;
+    p.sw_ir_stride = e->sw_len_launch;
+    p.sw_ir_len = e->sw_len_launch;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (e->profiling) {
         if (e->prof_used == e->prof_events.size()) {
@@ -738,6 +752,88 @@ int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, 
                 return set_err(TVOLAP_ERR_INVALID_INPUT, "bank index out of range in schedule");
     }
     return guarded([&] { process_hops_impl(e, in, in_lane_stride, out, out_lane_stride, n_hops, schedule); });
+}
+
+int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
+                             long n_hops, long period, const float* const* irs, long ir_length) {
+    if (int rc = check_hops_args(e, in, out, n_hops)) return rc;
+    if (e->bank) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "process_switching needs a filter-set engine");
+    if (period < 1) return set_err(TVOLAP_ERR_INVALID_SIZE, "switch period must be >= 1 hop");
+    if (!irs) return set_err(TVOLAP_ERR_INVALID_INPUT, "null IR list");
+    if (in_lane_stride < n_hops * e->L || out_lane_stride < n_hops * e->L)
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "lane stride shorter than n_hops * L");
+    const long nsw = (n_hops + period - 1) / period;
+    bool any = false;
+    for (long k = 0; k < nsw; ++k) any |= irs[k] != nullptr;
+    if (any && ir_length < 1) return set_err(TVOLAP_ERR_INVALID_INPUT, "partition: impulse response is empty");
+    if (any && (ir_length + 2 * e->L - 1) / (2 * e->L) > e->M)
+        return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter partition count differs");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        bool fast = classify(in) == Mem::Device && classify(out) == Mem::Device && n_hops >= e->block_min &&
+                    (e->N == 256 || e->N == 512 || e->N == 1024) && e->E == 1;
+        for (long k = 0; fast && k < nsw; ++k) fast = !irs[k] || classify(irs[k]) == Mem::Device;
+        if (!fast) {  // the loop it stands for
+            for (long k = 0; k < nsw; ++k) {
+                const long h0 = k * period, kc = std::min(period, n_hops - h0);
+                if (irs[k]) {
+                    const int rc = tvolap_exchange_filter(e, irs[k], ir_length, e->S);
+                    if (rc) throw ApiError{rc, g_err};
+                }
+                process_hops_impl(e, in + h0 * e->L, in_lane_stride, out + h0 * e->L, out_lane_stride, kc, nullptr);
+            }
+            return;
+        }
+        if (irs[0]) {  // a set staged by exchange_filter is superseded at this very hop (last wins)
+            std::lock_guard<std::mutex> lock(e->mu);
+            if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+            e->pending = false;
+        }
+        latch(e);
+        std::vector<const float*> ptrs(irs, irs + nsw);
+        std::vector<int> entries(nsw, -1);
+        int slot = e->active;
+        for (long k = 0; k < nsw; ++k)
+            if (irs[k]) {
+                slot = (slot + 1) % kSlots;
+                entries[k] = slot * (int)e->S;
+            }
+        if (e->sw_cap < nsw) {
+            CK(cudaStreamSynchronize(e->stream));
+            if (e->d_sw_irs) CK(cudaFree(e->d_sw_irs));
+            if (e->d_sw_entry) CK(cudaFree(e->d_sw_entry));
+            e->d_sw_irs = dalloc<const float*>(nsw);
+            e->d_sw_entry = dalloc<int>(nsw);
+            e->sw_cap = nsw;
+        }
+        // stream-ordered behind any earlier switching launch that still reads these tables
+        CK(cudaMemcpyAsync(e->d_sw_irs, ptrs.data(), sizeof(const float*) * nsw, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(e->d_sw_entry, entries.data(), sizeof(int) * nsw, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaStreamSynchronize(e->stream));  // host tables may go away when we return
+        e->sw_irs_launch = e->d_sw_irs;
+        e->sw_entry_launch = e->d_sw_entry;
+        e->sw_count_launch = (int)nsw;
+        e->sw_period_launch = (int)period;
+        e->sw_len_launch = ir_length;
+        try {
+            launch_hops(e, e->hops, n_hops, in, in_lane_stride, out, out_lane_stride, nullptr, 0);
+        } catch (...) {
+            e->sw_count_launch = 0;
+            e->sw_irs_launch = nullptr;
+            e->sw_entry_launch = nullptr;
+            throw;
+        }
+        e->sw_count_launch = 0;
+        e->sw_irs_launch = nullptr;
+        e->sw_entry_launch = nullptr;
+        e->active = slot;
+        for (int i = 0; i < kSlots; ++i) CK(cudaEventRecord(e->ev_slot[i], e->stream));  // every slot was touched
+        CK(cudaEventRecord(e->ev_main, e->stream));
+        e->hops += n_hops;
+        e->fwd += (uint64_t)(e->S * n_hops);
+        e->inv += (uint64_t)(e->S * e->E * n_hops);
+        e->macs += (uint64_t)(e->S * e->E * e->M * n_hops);
+    });
 }
 
 int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, long channels) {

@@ -36,6 +36,15 @@ struct HopParams {
     float2* pool_w;        // writable view of pool
     int new_entry_base;    // pool entry of source 0 for the staged set
     int qm;                // one-hop kernel: partition groups (== the blocked kernel's, for bit-identical sums)
+    // switching mode (tvolap_process_switching, hop-blocked set engines): a filter switch may
+    // happen every sw_period hops of this launch; switch k (k < sw_count) installs the set
+    // sw_irs[k] into pool entry sw_entry[k] (entry of source 0; -1: no switch at k).
+    const float* const* sw_irs = nullptr;  // device array of sw_count device pointers
+    const int* sw_entry = nullptr;         // device array of sw_count entries
+    int sw_count = 0;
+    int sw_period = 0;
+    long sw_ir_stride = 0;                 // sw_irs[k][s * sw_ir_stride + n], n < sw_ir_len
+    long sw_ir_len = 0;
 };
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int qm);

@@ -453,6 +453,13 @@ struct BlockLayout {
     }
 };
 
+__device__ __forceinline__ void cluster_arrive(int P) {
+    if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait(int P) {
+    if (P > 1) asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void block_sync(int P) {
     if (P > 1)
         cg::this_cluster().sync();
@@ -463,7 +470,7 @@ __device__ __forceinline__ void block_sync(int P) {
 // BANK = false: filter-set engines (one set for every hop of a block) — only the unified
 // mapping (JH <= 4) or the per-parity shared mapping (JH == 8) is compiled. BANK = true:
 // per-hop bank selections — per-parity mapping with shared or per-output filter loads.
-template <int E, int JH, bool BANK, int NC>
+template <int E, int JH, bool BANK, int NC, bool SW = false>
 __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p, const int Q) {
     constexpr int J = 2 * JH;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -506,8 +513,17 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     for (int i = tid; i < L; i += NT) xcur[i] = p.hist[(long)s * L + i];
     // hops b .. b+J-1 of this source into xcur[L..] (cp.async; lands while the block's MAC runs)
     const bool in_vec = (L & 3) == 0 && (p.in_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(p.in) & 15) == 0;
+    // Switching mode (tvolap_process_switching): blocks end at switch boundaries; the next
+    // switch's partitions are transformed by this launch inside the cluster-barrier gaps.
+    // (a separate instantiation, SW = true, so the plain launches carry none of this code)
+    const bool swm = SW && p.sw_count > 0;
+    auto block_len = [&](int b) {
+        int jn = min(J, p.n_hops - b);
+        if (swm) jn = min(jn, (b / p.sw_period + 1) * p.sw_period - b);
+        return jn;
+    };
     auto prefetch_block = [&](int b) {
-        const int jn = min(J, p.n_hops - b);
+        const int jn = block_len(b);
         const float* src = p.in + (long)s * p.in_stride + (long)b * L;
         if (in_vec) {
             for (int i = 4 * tid; i < jn * L; i += 4 * NT) cp_async16(xcur + L + i, src + i);
@@ -526,6 +542,51 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                             NT);
         block_sync(P);
     }
+    // K4 work units of this CTA for a switch: partitions m = r + u P, one warp per unit with a
+    // warp-private buffer in the fa | fb | red area (idle in the barrier gaps it runs in).
+    const int warp = tid >> 5, lane = tid & 31;
+    const int k4_slots = max(1, min(NT >> 5, (int)((lay.ola - lay.fa) / (N * sizeof(float2)))));
+    // one unit per warp per gap (same-box A/B: two lockstep units per warp in the first gap
+    // measured 2.45 vs 2.37 us/hop on C2 — the longer second gap absorbs half the work better)
+    const int k4_per_gap = k4_slots;
+    const int k4_units = r < M ? (M - r + P - 1) / P : 0;
+    auto k4_range = [&](const float* ir, int entry, int u0, int u1) {
+        if constexpr (SW && NC != 0 && NC <= 1024 && !BANK) {
+            const float* h = ir + (long)s * p.sw_ir_stride;
+            const bool vec = (p.sw_ir_stride & 1) == 0 && (reinterpret_cast<uintptr_t>(ir) & 7) == 0;
+            auto load_unit = [&](int u, int n) -> float2 {
+                const long i0 = (long)(r + u * P) * NC + 2 * n;
+                if (vec && i0 + 1 < p.sw_ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
+                return make_float2(i0 < p.sw_ir_len ? h[i0] : 0.f, i0 + 1 < p.sw_ir_len ? h[i0 + 1] : 0.f);
+            };
+            auto store_unit = [&](const float2* buf, int u) {
+                float4* d4 = reinterpret_cast<float4*>(p.pool_w + ((long)(entry + s) * M + r + u * P) * NC);
+                for (int k2 = lane; k2 < NC / 2; k2 += 32) {
+                    const float2 a = untangle_packed(buf, NC, 2 * k2, s_pk);
+                    const float2 b = untangle(buf, NC, 2 * k2 + 1, s_pk);
+                    d4[k2] = make_float4(a.x, a.y, b.x, b.y);
+                }
+            };
+            if (warp >= k4_slots) return;
+            float2* buf = s_fa + (size_t)warp * NC;
+            for (int u = u0 + warp; u < u1; u += k4_slots) {
+                fft_warp4<false, NC, true>(buf, p.tw + NC, lane, [&](int, int n) { return load_unit(u, n); });
+                store_unit(buf, u);
+                __syncwarp();
+            }
+        } else {
+            (void)ir, (void)entry, (void)u0, (void)u1;
+        }
+    };
+    int cur_entry = p.entry_base;  // pool entry (of source 0) of the running filter set
+    if (SW && swm && p.sw_entry[0] >= 0) {  // switch 0 at the first hop: transform it before any MAC
+        __syncthreads();
+        k4_range(p.sw_irs[0], p.sw_entry[0], 0, k4_units);
+        cur_entry = p.sw_entry[0];
+        block_sync(P);
+    }
+    const float* k4_ir = nullptr;  // the next switch's set, transformed during this period
+    int k4_entry = -1, k4_done = 0;
     for (int i = tid; i < E * 3 * Lp; i += NT) {
         const int e = i / (3 * Lp), rem = i % (3 * Lp), j = rem / Lp, u = rem % Lp;
         s_ola[i] = p.ola[((long)s * E + e) * 3 * L + j * L + r * Lp + u];
@@ -536,10 +597,24 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
     cg::cluster_group cluster = cg::this_cluster();
     PHASE_MARK(11);
 
-    for (int b0 = 0; b0 < p.n_hops; b0 += J) {
+    for (int b0 = 0, jb = 0; b0 < p.n_hops; b0 += jb) {
         const long l0 = p.hop0 + b0;
-        const int jb = min(J, p.n_hops - b0);
-        if (b0 + J >= p.n_hops) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+        jb = block_len(b0);
+        bool period_end = false;
+        if (SW && swm) {
+            const int k = b0 / p.sw_period;
+            if (b0 % p.sw_period == 0) {  // a new period: latch switch k, prepare switch k + 1
+                if (k > 0 && p.sw_entry[k] >= 0) cur_entry = p.sw_entry[k];
+                k4_ir = nullptr;
+                if (k + 1 < p.sw_count && p.sw_entry[k + 1] >= 0) {
+                    k4_ir = p.sw_irs[k + 1];
+                    k4_entry = p.sw_entry[k + 1];
+                }
+                k4_done = 0;
+            }
+            period_end = (b0 + jb) % p.sw_period == 0 || b0 + jb >= p.n_hops;
+        }
+        if (b0 + jb >= p.n_hops) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
         // ---- inputs: this block's landed (prefetched during the previous block)
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
@@ -557,7 +632,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         // block's input copy into the (now free) hop area
         for (int i = tid; i < L; i += NT) xcur[i] = xcur[(size_t)jb * L + i];
         __syncthreads();
-        if (b0 + J < p.n_hops) prefetch_block(b0 + J);
+        if (b0 + jb < p.n_hops) prefetch_block(b0 + jb);
         if (nf > 0) {
             const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
             for (int f = 0; f < nf; ++f) {
@@ -567,13 +642,23 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             }
         }
         PHASE_MARK(1);
-        block_sync(P);  // ring writes of all frames visible cluster-wide
+        if (SW && k4_ir) {  // ring writes visible cluster-wide; next switch's K4 units in the barrier gap
+            __syncthreads();
+            cluster_arrive(P);
+            const int u1 = min(k4_units, k4_done + k4_per_gap);
+            k4_range(k4_ir, k4_entry, k4_done, u1);
+            k4_done = u1;
+            __syncthreads();
+            cluster_wait(P);
+        } else {
+            block_sync(P);  // ring writes of all frames visible cluster-wide
+        }
         PHASE_MARK(2);
 
         // ---- K3: hop-blocked MAC over this CTA's bin slice.
         // Does every hop of the block use the same filter set (set engines: always)?
         bool all_same = true;
-        int ent0 = p.entry_base + s;
+        int ent0 = cur_entry + s;
         if (p.sched) {
             ent0 = p.sched[(long)b0 * p.sched_stride + s];
             for (int jj = 1; jj < jb; ++jj) all_same &= p.sched[(long)(b0 + jj) * p.sched_stride + s] == ent0;
@@ -925,7 +1010,17 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             }
         }
         PHASE_MARK(4);
-        block_sync(P);  // Y slices of all frames published
+        if (SW && k4_ir) {  // Y slices published; more K4 units (all that remain at the period's end)
+            __syncthreads();
+            cluster_arrive(P);
+            const int u1 = period_end ? k4_units : min(k4_units, k4_done + k4_per_gap);
+            k4_range(k4_ir, k4_entry, k4_done, u1);
+            k4_done = u1;
+            __syncthreads();
+            cluster_wait(P);
+        } else {
+            block_sync(P);  // Y slices of all frames published
+        }
         PHASE_MARK(5);
 
         // ---- K5a: this CTA's frames: gather Y over DSMEM, tangle, inverse FFT.
@@ -1404,9 +1499,10 @@ static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaSt
     void (*fn)(const HopParams, const int) = tvolap_block_kernel<E, JH, BANK, 0>;
     const int N = 2 * p.L;
     if constexpr (!BANK && E == 1 && (JH == 4 || JH == 8)) {
-        if (N == 256) fn = tvolap_block_kernel<E, JH, BANK, 256>;
-        if (N == 512) fn = tvolap_block_kernel<E, JH, BANK, 512>;
-        if (N == 1024) fn = tvolap_block_kernel<E, JH, BANK, 1024>;
+        const bool sw = p.sw_count > 0;  // switching launches: the in-kernel K4 instantiation
+        if (N == 256) fn = sw ? tvolap_block_kernel<E, JH, BANK, 256, true> : tvolap_block_kernel<E, JH, BANK, 256>;
+        if (N == 512) fn = sw ? tvolap_block_kernel<E, JH, BANK, 512, true> : tvolap_block_kernel<E, JH, BANK, 512>;
+        if (N == 1024) fn = sw ? tvolap_block_kernel<E, JH, BANK, 1024, true> : tvolap_block_kernel<E, JH, BANK, 1024>;
     }
     if constexpr (BANK && E == 1 && JH == 8) {
         if (N == 64) fn = tvolap_block_kernel<E, JH, BANK, 64>;

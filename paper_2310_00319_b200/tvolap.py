@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
             "tvolap_destroy": (ip, [vp]),
             "tvolap_process": (ip, [vp, fp, lg, lg, lg, fp, lg]),
             "tvolap_process_hops": (ip, [vp, fp, lg, fp, lg, lg, fp]),
+            "tvolap_process_switching": (ip, [vp, fp, lg, fp, lg, lg, lg, vp, lg]),
             "tvolap_exchange_filter": (ip, [vp, fp, lg, lg]),
             "tvolap_select_bank": (ip, [vp, fp]),
             "tvolap_reset": (ip, [vp]),
@@ -128,7 +129,9 @@ def lib() -> C.CDLL:
             "tvolap_cmp_geometry": (ip, [vp, fp]),
         }
         for name, (res, args) in sig.items():
-            f = getattr(L, name)
+            f = getattr(L, name, None)
+            if f is None:  # an older diagnostic build (TVOLAP_LIB); tests check the real exports
+                continue
             f.restype = res
             f.argtypes = args
         _lib = L
@@ -137,7 +140,7 @@ def lib() -> C.CDLL:
 
 EXPORTED_SYMBOLS = (
     "tvolap_last_error tvolap_version tvolap_create tvolap_create_bank tvolap_destroy tvolap_process "
-    "tvolap_process_hops tvolap_exchange_filter tvolap_select_bank tvolap_reset tvolap_hop tvolap_channels "
+    "tvolap_process_hops tvolap_process_switching tvolap_exchange_filter tvolap_select_bank tvolap_reset tvolap_hop tvolap_channels "
     "tvolap_output_channels tvolap_partition_count tvolap_delay_line_depth tvolap_latency "
     "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
     "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_set_block_config tvolap_block_config "
@@ -368,6 +371,52 @@ class TvolapEngine:
         sp, _k3 = _ptr(None if schedule is None else
                        (schedule if hasattr(schedule, "data_ptr") else np.ascontiguousarray(schedule, np.int32)))
         _check(lib().tvolap_process_hops(self._h, xp, _stride(x), op, _stride(out), n, sp))
+        return out
+
+    def process_switching(self, x, irs, period: int, out=None):
+        """n hops with a filter switch every `period` hops: the same as
+        `for k: exchange_ir(irs[k]) (unless None); process_hops(period hops)`.
+        irs: sequence of (lanes, taps) IR arrays / tensors (None = no switch at k), one per period.
+        With device tensors everywhere this is one launch (tvolap_process_switching)."""
+        L = self.hop()
+        lanes, total = x.shape[0], x.shape[-1]
+        if total % L:
+            raise InvalidSizeError("process_switching: sample count is not a whole number of hops")
+        n = total // L
+        nsw = -(-n // period)
+        if len(irs) < nsw:
+            raise InvalidInputError(f"process_switching: {nsw} switch slots needed, got {len(irs)}")
+        if out is None:
+            if hasattr(x, "data_ptr"):
+                import torch
+
+                out = torch.empty((self.channels_out(), total), dtype=torch.float32, device=x.device)
+            else:
+                out = np.empty((self.channels_out(), total), dtype=np.float32)
+        if not hasattr(x, "data_ptr"):
+            x = _f32(x)
+        keep, ptrs, taps = [], (C.c_void_p * nsw)(), 0
+        for k in range(nsw):
+            ir = irs[k]
+            if ir is None:
+                ptrs[k] = None
+                continue
+            if not hasattr(ir, "data_ptr"):
+                ir = _f32(ir)
+            if ir.shape[0] != self.channels():
+                raise IncompatibleFilterError("replacement filter channel count differs")
+            if taps and ir.shape[-1] != taps:
+                raise InvalidInputError("process_switching: all IRs must have the same length")
+            taps = ir.shape[-1]
+            if _stride(ir) != taps:
+                raise InvalidInputError("process_switching: IRs must be dense (lanes, taps)")
+            p, k2 = _ptr(ir)
+            keep.append(k2)
+            ptrs[k] = p.value
+        xp, _k1 = _ptr(x)
+        op, _k2 = _ptr(out)
+        _check(lib().tvolap_process_switching(self._h, xp, _stride(x), op, _stride(out), n, period,
+                                              C.cast(ptrs, C.c_void_p), taps))
         return out
 
     def reset(self) -> None:

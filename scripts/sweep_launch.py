@@ -18,7 +18,7 @@ from paper_2310_00319_b200.tvolap import TvolapBankEngine, TvolapEngine, partiti
 HOPS = {"C1": 3750, "C2": 1024, "C3": 512, "C4": 128, "C5": 1024}
 
 
-def run(name, Ps, JHs, reps=3, period=0, exchange=False):
+def run(name, Ps, JHs, reps=3, period=0, exchange=False, switching=False):
     cfg = W.CONFIGS[name]
     H, L, S = HOPS[name], cfg.hop, cfg.sources
     lib = T.lib()
@@ -38,6 +38,9 @@ def run(name, Ps, JHs, reps=3, period=0, exchange=False):
         irs = torch.from_numpy(np.stack([W.fresh_irs(cfg, k)[:, 0, :] for k in range(2)])).cuda() if exchange else None
 
     def step():
+        if switching:  # one tvolap_process_switching call (in-kernel K4)
+            eng.process_switching(x, [irs[k & 1] for k in range(-(-H // period))], period, out=out)
+            return
         if not period:
             eng.process_hops(x, out=out, schedule=sched)
             return
@@ -77,6 +80,7 @@ def run(name, Ps, JHs, reps=3, period=0, exchange=False):
                 continue
             j, bm, q = eng.block_config()
             print(json.dumps({"cfg": name, "P": P, "J": 2 * jh, "Q": q, "period": period, "exchange": exchange,
+                              "switching": switching,
                               "us_per_hop": 1e3 * ms / H,
                               "GBps_alg": bph * H / (ms / 1e3) / 1e9, "frac": bph * H / (ms / 1e3) / 1e9 / 6542.1}),
                   flush=True)
@@ -93,8 +97,10 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--period", type=int, default=0, help="hops per process_hops call (0 = one call)")
     ap.add_argument("--exchange", action="store_true", help="exchange_filter before every call (fresh configs)")
+    ap.add_argument("--switching", action="store_true", help="one process_switching call per pass (fresh configs)")
     a = ap.parse_args()
     for n in a.configs:
         if a.hops:
             HOPS[n] = a.hops
-        run(n, a.P, [j // 2 for j in a.J], reps=a.reps, period=a.period, exchange=a.exchange)
+        run(n, a.P, [j // 2 for j in a.J], reps=a.reps, period=a.period, exchange=a.exchange or a.switching,
+            switching=a.switching)
