@@ -242,10 +242,9 @@ def main():
     def step(e, xs, outs, ir_set, sch):
         e.reset()
         if cfg.mode == "fresh":
-            for k in range(n_sw):
-                e.exchange_ir(ir_set[k % n_pool])
-                sl = slice(k * cfg.period * L, min(H, (k + 1) * cfg.period) * L)
-                e.process_hops(xs[:, sl], out=outs[:, sl])
+            # the drive() loop (exchange before every period's hops) as one call:
+            # device-resident -> one hop-blocked launch with in-kernel K4; host -> the loop itself
+            e.process_switching(xs, [ir_set[k % n_pool] for k in range(n_sw)], cfg.period, out=outs)
         else:
             e.process_hops(xs, out=outs, schedule=sch)
             if mix is not None and outs.is_cuda:
@@ -315,7 +314,8 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": f"tvolap_hop_kernel (K1+K2+K3+K5 fused), {hops_per_launch:g} hops x {S} sources per launch",
+                "kernel": f"tvolap_block_kernel (K1-K5 fused{', K4 for the next switch in the barrier gaps' if cfg.mode == 'fresh' else ''}), "
+                          f"{hops_per_launch:g} hops x {S} sources per launch",
                 "avg_launch_ms": avg_launch_ms, "launches": kern_n, "bytes_per_hop": bytes_hop,
                 "bytes_per_launch": bytes_launch, "distinct_filters_per_hop": distinct,
                 "kernel_share_of_step": kern_ms / prof_elapsed if prof_elapsed else None,

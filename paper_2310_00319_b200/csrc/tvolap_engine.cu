@@ -770,8 +770,14 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter partition count differs");
     return guarded([&] {
         CK(cudaSetDevice(e->device));
+        // In-kernel K4 pays off when a CTA's share of one switch's partitions fits the barrier gaps
+        // of a period (2 gaps per block, one partition per warp each): C2 16 partitions per CTA in
+        // one 16-hop block -> 2.37 vs 2.83 us/hop; C4 (2048-point, 32 per CTA per 8-hop period)
+        // is faster as the loop with the in-stream K4 launch.
+        const long J = 2L * e->JH, blocks = (period + J - 1) / J;
+        const long units = (e->M + e->PB - 1) / e->PB, warps = e->NTB / 32;
         bool fast = classify(in) == Mem::Device && classify(out) == Mem::Device && n_hops >= e->block_min &&
-                    (e->N == 256 || e->N == 512 || e->N == 1024) && e->E == 1;
+                    (e->N == 256 || e->N == 512) && e->E == 1 && units <= 2 * warps * blocks;
         for (long k = 0; fast && k < nsw; ++k) fast = !irs[k] || classify(irs[k]) == Mem::Device;
         if (!fast) {  // the loop it stands for
             for (long k = 0; k < nsw; ++k) {
