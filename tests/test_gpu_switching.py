@@ -64,13 +64,17 @@ def test_switching_host_buffers_fall_back_to_the_loop():
     b = T.TvolapEngine(T.partition(ir0, hop))
     ya = a.process_switching(x.cpu().numpy(), [None if d is None else d.cpu().numpy() for d in dirs], period)
     yb = _loop(b, x, dirs, period, hop)
+    b.synchronize()  # device calls are asynchronous on the engine's stream
     assert np.array_equal(ya, yb.cpu().numpy())
 
 
 def test_switching_matches_oracle():
     hop, S, taps, n, period = 256, 2, 2048, 50, 16
     ir0, x, dirs = _case(hop, S, taps, n, period)
-    y = T.TvolapEngine(T.partition(ir0, hop)).process_switching(x, dirs, period).cpu().numpy()
+    eng_g = T.TvolapEngine(T.partition(ir0, hop))
+    y = eng_g.process_switching(x, dirs, period)
+    eng_g.synchronize()
+    y = y.cpu().numpy()
     xs = x.cpu().numpy().astype(np.float64)
     eng = O.Engine(O.partition(ir0.astype(np.float32).astype(np.float64), hop))
     ref = []
