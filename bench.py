@@ -309,7 +309,10 @@ def main():
     summ = ROOT / "profiles" / f"ncu_summary_{cfg.name}.json"
     if summ.exists():
         try:
-            traffic = json.loads(summ.read_text()).get("dram_bytes_per_launch")
+            sj = json.loads(summ.read_text())
+            # per hop when the capture records it (its launch length may differ from this run's)
+            traffic = sj["dram_bytes_per_hop"] * hops_per_launch if sj.get("dram_bytes_per_hop") \
+                else sj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

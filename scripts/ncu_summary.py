@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--kernel", required=True, help="description of the captured kernel / geometry")
     ap.add_argument("--source", required=True, help="the command the capture ran")
     ap.add_argument("--alg-bytes", type=float, default=None, help="SURVEY 8(d) algorithmic bytes per launch")
+    ap.add_argument("--hops-per-launch", type=float, default=None,
+                    help="hops one captured launch processes (bench.py scales traffic per hop by its own launches)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.rep, "--page", "raw", "--csv"], check=True, capture_output=True,
@@ -54,6 +56,8 @@ def main():
            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
            "l2_bytes_per_launch": 32 * mean("lts__t_sectors.sum") if "lts__t_sectors.sum" in hdr else None,
            "algorithmic_bytes_per_launch_8d": a.alg_bytes,
+           "hops_per_launch": a.hops_per_launch,
+           "dram_bytes_per_hop": (rd + wr) / a.hops_per_launch if a.hops_per_launch else None,
            "note": "ncu flushes caches before each replay (cold); in the timed bench the C1/C2 delay line and "
                    "filter pool are L2-resident",
            "per_launch": launches}
