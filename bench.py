@@ -211,6 +211,13 @@ def main():
                                            ka.ctypes.data, ta.ctypes.data, W.FS, cfg.ir_length,
                                            ctypes.c_void_p(dst.data_ptr())))
 
+    def fit_block(e):
+        """Blocks never span a filter switch, so a block longer than the switch period would
+        load each delay-line / filter slice for fewer hops: cap it at the period (C4: 8)."""
+        j, _, _ = e.block_config()
+        if cfg.period < j:
+            e.set_block_config(max(2, 1 << (cfg.period.bit_length() - 1)))
+
     sched = mix = irs = None
     n_pool = n_sw  # distinct IR sets held in HBM (and pinned host memory for e2e)
     if cfg.mode == "fresh":
@@ -221,6 +228,7 @@ def main():
         gen_irs([(lane0 + s, 0, k) for k in range(n_pool) for s in range(S)], irs)
         ir0 = W.fresh_irs(cfg, 0, lane0, S)[:, 0, :]
         eng = TvolapEngine(partition(ir0.T, L, M), device=local)
+        fit_block(eng)
         distinct = S
     else:
         bank = torch.empty((cfg.n_bank, cfg.ears, cfg.ir_length), dtype=torch.float32, device=dev)
@@ -337,6 +345,7 @@ def main():
             irh = torch.empty(irs.shape, dtype=torch.float32, pin_memory=True)
             irh.copy_(irs)
             eng2 = TvolapEngine(partition(ir0.T, L, M), device=local)
+            fit_block(eng2)
             h2d += n_sw * S * cfg.ir_length * 4  # one whole set uploaded per switch
             schh = None
         else:
