@@ -1181,6 +1181,7 @@ __global__ void __launch_bounds__(256) partition_kernel(int L, int M, long rows,
 // K4, one warp per partition (N <= 1024): no CTA barriers, a warp-private 8N-byte buffer, IR
 // slices read straight into the first FFT stage's registers. Bit-identical to partition_kernel.
 template <int NC>
+// (same-box A/B for N = 1024: one CTA per SM without spills 248 us per C4 switch vs 225 us here)
 __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows, const float* __restrict__ ir,
                                                              long ir_stride, long ir_len, float2* __restrict__ pool,
                                                              long row0, const float2* __restrict__ tw,

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--hops", type=int, default=512)
     ap.add_argument("--period", type=int, default=0)
     ap.add_argument("--exchange", action="store_true")
+    ap.add_argument("--switching", action="store_true", help="one process_switching call (in-kernel K4)")
     a = ap.parse_args()
     path = _build.build_variant("prof", ["TVOLAP_PHASE_PROF"])
     if a.build:
@@ -52,6 +53,9 @@ def main():
     period = a.period or H
 
     def step():
+        if a.switching:
+            eng.process_switching(x, [irs[k & 1] for k in range(-(-H // period))], period, out=out)
+            return
         for h0 in range(0, H, period):
             if a.exchange:
                 eng.exchange_ir(irs[(h0 // period) & 1])
