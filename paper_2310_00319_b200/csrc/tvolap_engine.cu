@@ -193,6 +193,9 @@ struct tvolap_engine {
     const int* sw_entry_launch = nullptr;
     int sw_count_launch = 0, sw_period_launch = 0;
     long sw_len_launch = 0;
+    // pinned-host switching pipeline: double-buffered device staging of hops, sets and outputs
+    float *swh_x[2] = {}, *swh_y[2] = {}, *swh_ir[2] = {};
+    long swh_cap_x = 0, swh_cap_ir = 0;
     bool staged_in_stream = false;   // the pending set is transformed by latch() on the engine stream
     // chunked host pipeline
     long chunk_hops = 0;
@@ -224,7 +227,9 @@ struct tvolap_engine {
                         (void*)d_sel, (void*)d_irstage, (void*)d_irst[0], (void*)d_irst[1], (void*)d_irst[2],
                         (void*)d_irst[3], (void*)d_in[0],
                         (void*)d_in[1], (void*)d_out[0],
-                        (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1], (void*)d_sw_irs, (void*)d_sw_entry})
+                        (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1], (void*)d_sw_irs, (void*)d_sw_entry,
+                        (void*)swh_x[0], (void*)swh_x[1], (void*)swh_y[0], (void*)swh_y[1], (void*)swh_ir[0],
+                        (void*)swh_ir[1]})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
@@ -776,10 +781,19 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         // is faster as the loop with the in-stream K4 launch.
         const long J = 2L * e->JH, blocks = (period + J - 1) / J;
         const long units = (e->M + e->PB - 1) / e->PB, warps = e->NTB / 32;
-        bool fast = classify(in) == Mem::Device && classify(out) == Mem::Device && n_hops >= e->block_min &&
-                    (e->N == 256 || e->N == 512) && e->E == 1 && units <= 2 * warps * blocks;
-        for (long k = 0; fast && k < nsw; ++k) fast = !irs[k] || classify(irs[k]) == Mem::Device;
-        if (!fast) {  // the loop it stands for
+        const bool kernel_ok = (e->N == 256 || e->N == 512) && e->E == 1 && units <= 2 * warps * blocks;
+        const Mem min = classify(in), mout = classify(out);
+        bool dev = kernel_ok && min == Mem::Device && mout == Mem::Device && n_hops >= e->block_min;
+        // (every chunk launch must take the hop-blocked kernel: full periods, and a last one of
+        // at least block_min hops)
+        bool pinned = kernel_ok && min == Mem::Pinned && mout == Mem::Pinned && period >= e->block_min &&
+                      n_hops - (nsw - 1) * period >= e->block_min;
+        for (long k = 0; k < nsw; ++k) {
+            const Mem mk = irs[k] ? classify(irs[k]) : (dev ? Mem::Device : Mem::Pinned);
+            dev = dev && mk == Mem::Device;
+            pinned = pinned && mk == Mem::Pinned;
+        }
+        if (!dev && !pinned) {  // the loop it stands for
             for (long k = 0; k < nsw; ++k) {
                 const long h0 = k * period, kc = std::min(period, n_hops - h0);
                 if (irs[k]) {
@@ -796,14 +810,44 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             e->pending = false;
         }
         latch(e);
-        std::vector<const float*> ptrs(irs, irs + nsw);
+        const long S = e->S, L = e->L;
+        // Host pipeline (pinned buffers): chunks of Kp periods staged through two device buffers;
+        // H2D of chunk c+1 and D2H of chunk c-1 overlap the launch of chunk c, every copy large.
+        long Kp = nsw;
+        if (pinned) {
+            const long per = S * period * L * 4 * 2 + (ir_length > 0 ? S * ir_length * 4 : 0);
+            Kp = std::max<long>(1, std::min<long>(nsw, (64L << 20) / per));
+        }
+        std::vector<const float*> ptrs(nsw);
         std::vector<int> entries(nsw, -1);
         int slot = e->active;
-        for (long k = 0; k < nsw; ++k)
+        for (long k = 0; k < nsw; ++k) {
+            ptrs[k] = irs[k];
+            if (pinned && irs[k])  // the device staging copy of this set
+                ptrs[k] = nullptr;  // filled below once the staging buffers exist
             if (irs[k]) {
                 slot = (slot + 1) % kSlots;
-                entries[k] = slot * (int)e->S;
+                entries[k] = slot * (int)S;
             }
+        }
+        if (pinned) {
+            const long need_x = S * Kp * period * L, need_ir = Kp * S * std::max<long>(ir_length, 1);
+            if (e->swh_cap_x < need_x || e->swh_cap_ir < need_ir) {
+                CK(cudaDeviceSynchronize());
+                for (int b = 0; b < 2; ++b) {
+                    if (e->swh_x[b]) CK(cudaFree(e->swh_x[b]));
+                    if (e->swh_y[b]) CK(cudaFree(e->swh_y[b]));
+                    if (e->swh_ir[b]) CK(cudaFree(e->swh_ir[b]));
+                    e->swh_x[b] = dalloc<float>(need_x);
+                    e->swh_y[b] = dalloc<float>(need_x);
+                    e->swh_ir[b] = dalloc<float>(need_ir);
+                }
+                e->swh_cap_x = need_x;
+                e->swh_cap_ir = need_ir;
+            }
+            for (long k = 0; k < nsw; ++k)
+                if (irs[k]) ptrs[k] = e->swh_ir[(k / Kp) & 1] + (k % Kp) * S * ir_length;
+        }
         if (e->sw_cap < nsw) {
             CK(cudaStreamSynchronize(e->stream));
             if (e->d_sw_irs) CK(cudaFree(e->d_sw_irs));
@@ -816,29 +860,63 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         CK(cudaMemcpyAsync(e->d_sw_irs, ptrs.data(), sizeof(const float*) * nsw, cudaMemcpyHostToDevice, e->stream));
         CK(cudaMemcpyAsync(e->d_sw_entry, entries.data(), sizeof(int) * nsw, cudaMemcpyHostToDevice, e->stream));
         CK(cudaStreamSynchronize(e->stream));  // host tables may go away when we return
-        e->sw_irs_launch = e->d_sw_irs;
-        e->sw_entry_launch = e->d_sw_entry;
-        e->sw_count_launch = (int)nsw;
-        e->sw_period_launch = (int)period;
-        e->sw_len_launch = ir_length;
-        try {
-            launch_hops(e, e->hops, n_hops, in, in_lane_stride, out, out_lane_stride, nullptr, 0);
-        } catch (...) {
+        auto launch = [&](long k0, long nk, long hops, const float* din, long din_stride, float* dout, long dout_stride) {
+            e->sw_irs_launch = e->d_sw_irs + k0;
+            e->sw_entry_launch = e->d_sw_entry + k0;
+            e->sw_count_launch = (int)nk;
+            e->sw_period_launch = (int)period;
+            e->sw_len_launch = ir_length;
+            try {
+                launch_hops(e, e->hops, hops, din, din_stride, dout, dout_stride, nullptr, 0);
+            } catch (...) {
+                e->sw_count_launch = 0;
+                e->sw_irs_launch = nullptr;
+                e->sw_entry_launch = nullptr;
+                throw;
+            }
             e->sw_count_launch = 0;
             e->sw_irs_launch = nullptr;
             e->sw_entry_launch = nullptr;
-            throw;
+            e->hops += hops;
+        };
+        if (!pinned) {
+            launch(0, nsw, n_hops, in, in_lane_stride, out, out_lane_stride);
+        } else {
+            CK(cudaEventRecord(e->ev_start, e->stream));
+            CK(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
+            CK(cudaStreamWaitEvent(e->d2h, e->ev_start, 0));
+            for (long c = 0, k0 = 0; k0 < nsw; ++c, k0 += Kp) {
+                const int b = (int)(c & 1);
+                const long nk = std::min(Kp, nsw - k0), h0 = k0 * period;
+                const long hops = std::min(nk * period, n_hops - h0), w = Kp * period * L;
+                // H2D: the chunk's hops and sets, after the launch that last read buffer b
+                if (c >= 2) CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
+                CK(cudaMemcpy2DAsync(e->swh_x[b], w * sizeof(float), in + h0 * L, in_lane_stride * sizeof(float),
+                                     hops * L * sizeof(float), S, cudaMemcpyHostToDevice, e->h2d));
+                for (long k = k0; k < k0 + nk; ++k)
+                    if (irs[k])
+                        CK(cudaMemcpyAsync(const_cast<float*>(ptrs[k]), irs[k], sizeof(float) * S * ir_length,
+                                           cudaMemcpyHostToDevice, e->h2d));
+                CK(cudaEventRecord(e->ev_in[b], e->h2d));
+                CK(cudaStreamWaitEvent(e->stream, e->ev_in[b], 0));
+                if (c >= 2) CK(cudaStreamWaitEvent(e->stream, e->ev_o[b], 0));  // D2H of chunk c-2 done
+                launch(k0, nk, hops, e->swh_x[b], w, e->swh_y[b], w);
+                CK(cudaEventRecord(e->ev_k[b], e->stream));
+                CK(cudaStreamWaitEvent(e->d2h, e->ev_k[b], 0));
+                CK(cudaMemcpy2DAsync(out + h0 * L, out_lane_stride * sizeof(float), e->swh_y[b], w * sizeof(float),
+                                     hops * L * sizeof(float), S, cudaMemcpyDeviceToHost, e->d2h));
+                CK(cudaEventRecord(e->ev_o[b], e->d2h));
+            }
+            CK(cudaEventRecord(e->ev_start, e->d2h));  // later work on the engine stream sees the outputs
+            CK(cudaStreamWaitEvent(e->stream, e->ev_start, 0));
         }
-        e->sw_count_launch = 0;
-        e->sw_irs_launch = nullptr;
-        e->sw_entry_launch = nullptr;
         e->active = slot;
         for (int i = 0; i < kSlots; ++i) CK(cudaEventRecord(e->ev_slot[i], e->stream));  // every slot was touched
         CK(cudaEventRecord(e->ev_main, e->stream));
-        e->hops += n_hops;
-        e->fwd += (uint64_t)(e->S * n_hops);
-        e->inv += (uint64_t)(e->S * e->E * n_hops);
-        e->macs += (uint64_t)(e->S * e->E * e->M * n_hops);
+        e->fwd += (uint64_t)(S * n_hops);
+        e->inv += (uint64_t)(S * e->E * n_hops);
+        e->macs += (uint64_t)(S * e->E * e->M * n_hops);
+        if (pinned && !e->host_async) CK(cudaStreamSynchronize(e->stream));
     });
 }
 

@@ -99,3 +99,22 @@ def test_switching_validation():
     big = torch.zeros((2, 64 * 2 * 9), device="cuda")
     with pytest.raises(T.IncompatibleFilterError):
         eng.process_switching(x, [big] * 2, 4)
+
+
+@pytest.mark.parametrize("n_hops,period", [(16 * 9 + 5, 16), (64, 16), (90, 10)])
+def test_switching_pinned_host_pipeline(n_hops, period):
+    """Pinned host buffers: chunked H2D / launch / D2H pipeline, bit-identical to the device call."""
+    import torch
+
+    hop, S, taps = 256, 4, 4096
+    ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at=(1,))
+    xh = x.cpu().pin_memory()
+    irh = [None if d is None else d.cpu().pin_memory() for d in dirs]
+    yh = torch.empty(xh.shape, dtype=torch.float32).pin_memory()
+    a = T.TvolapEngine(T.partition(ir0, hop))
+    b = T.TvolapEngine(T.partition(ir0, hop))
+    a.process_switching(xh, irh, period, out=yh)
+    a.synchronize()
+    yd = b.process_switching(x, dirs, period)
+    b.synchronize()
+    assert np.array_equal(yh.numpy(), yd.cpu().numpy())
