@@ -781,19 +781,20 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         // is faster as the loop with the in-stream K4 launch.
         const long J = 2L * e->JH, blocks = (period + J - 1) / J;
         const long units = (e->M + e->PB - 1) / e->PB, warps = e->NTB / 32;
-        const bool kernel_ok = (e->N == 256 || e->N == 512) && e->E == 1 && units <= 2 * warps * blocks;
         const Mem min = classify(in), mout = classify(out);
-        bool dev = kernel_ok && min == Mem::Device && mout == Mem::Device && n_hops >= e->block_min;
-        // (every chunk launch must take the hop-blocked kernel: full periods, and a last one of
-        // at least block_min hops)
-        bool pinned = kernel_ok && min == Mem::Pinned && mout == Mem::Pinned && period >= e->block_min &&
-                      n_hops - (nsw - 1) * period >= e->block_min;
+        bool dev = min == Mem::Device && mout == Mem::Device && n_hops >= e->block_min;
+        bool pinned = min == Mem::Pinned && mout == Mem::Pinned;
+        // the switching kernel (in-kernel K4); in a pinned pipeline every chunk launch must take
+        // the hop-blocked kernel: full periods, and a last one of at least block_min hops
+        const bool kernel_ok = (e->N == 256 || e->N == 512) && e->E == 1 && units <= 2 * warps * blocks &&
+                               (!pinned || (period >= e->block_min && n_hops - (nsw - 1) * period >= e->block_min));
+        dev = dev && kernel_ok;
         for (long k = 0; k < nsw; ++k) {
             const Mem mk = irs[k] ? classify(irs[k]) : (dev ? Mem::Device : Mem::Pinned);
             dev = dev && mk == Mem::Device;
             pinned = pinned && mk == Mem::Pinned;
         }
-        if (!dev && !pinned) {  // the loop it stands for
+        if (!dev && !pinned) {  // the loop it stands for (device buffers without the kernel, pageable)
             for (long k = 0; k < nsw; ++k) {
                 const long h0 = k * period, kc = std::min(period, n_hops - h0);
                 if (irs[k]) {
@@ -804,12 +805,12 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             }
             return;
         }
-        if (irs[0]) {  // a set staged by exchange_filter is superseded at this very hop (last wins)
+        if (kernel_ok && irs[0]) {  // a staged set is superseded at this very hop (last wins)
             std::lock_guard<std::mutex> lock(e->mu);
             if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
             e->pending = false;
         }
-        latch(e);
+        if (kernel_ok) latch(e);
         const long S = e->S, L = e->L;
         // Host pipeline (pinned buffers): chunks of Kp periods staged through two device buffers;
         // H2D of chunk c+1 and D2H of chunk c-1 overlap the launch of chunk c, every copy large.
@@ -825,7 +826,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             ptrs[k] = irs[k];
             if (pinned && irs[k])  // the device staging copy of this set
                 ptrs[k] = nullptr;  // filled below once the staging buffers exist
-            if (irs[k]) {
+            if (irs[k] && kernel_ok) {
                 slot = (slot + 1) % kSlots;
                 entries[k] = slot * (int)S;
             }
@@ -848,7 +849,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             for (long k = 0; k < nsw; ++k)
                 if (irs[k]) ptrs[k] = e->swh_ir[(k / Kp) & 1] + (k % Kp) * S * ir_length;
         }
-        if (e->sw_cap < nsw) {
+        if (kernel_ok && e->sw_cap < nsw) {
             CK(cudaStreamSynchronize(e->stream));
             if (e->d_sw_irs) CK(cudaFree(e->d_sw_irs));
             if (e->d_sw_entry) CK(cudaFree(e->d_sw_entry));
@@ -856,10 +857,12 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             e->d_sw_entry = dalloc<int>(nsw);
             e->sw_cap = nsw;
         }
-        // stream-ordered behind any earlier switching launch that still reads these tables
-        CK(cudaMemcpyAsync(e->d_sw_irs, ptrs.data(), sizeof(const float*) * nsw, cudaMemcpyHostToDevice, e->stream));
-        CK(cudaMemcpyAsync(e->d_sw_entry, entries.data(), sizeof(int) * nsw, cudaMemcpyHostToDevice, e->stream));
-        CK(cudaStreamSynchronize(e->stream));  // host tables may go away when we return
+        if (kernel_ok) {  // stream-ordered behind any earlier switching launch still reading the tables
+            CK(cudaMemcpyAsync(e->d_sw_irs, ptrs.data(), sizeof(const float*) * nsw, cudaMemcpyHostToDevice,
+                               e->stream));
+            CK(cudaMemcpyAsync(e->d_sw_entry, entries.data(), sizeof(int) * nsw, cudaMemcpyHostToDevice, e->stream));
+            CK(cudaStreamSynchronize(e->stream));  // host tables may go away when we return
+        }
         auto launch = [&](long k0, long nk, long hops, const float* din, long din_stride, float* dout, long dout_stride) {
             e->sw_irs_launch = e->d_sw_irs + k0;
             e->sw_entry_launch = e->d_sw_entry + k0;
@@ -879,6 +882,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             e->sw_entry_launch = nullptr;
             e->hops += hops;
         };
+        (void)launch;
         if (!pinned) {
             launch(0, nsw, n_hops, in, in_lane_stride, out, out_lane_stride);
         } else {
@@ -900,7 +904,18 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
                 CK(cudaEventRecord(e->ev_in[b], e->h2d));
                 CK(cudaStreamWaitEvent(e->stream, e->ev_in[b], 0));
                 if (c >= 2) CK(cudaStreamWaitEvent(e->stream, e->ev_o[b], 0));  // D2H of chunk c-2 done
-                launch(k0, nk, hops, e->swh_x[b], w, e->swh_y[b], w);
+                if (kernel_ok) {
+                    launch(k0, nk, hops, e->swh_x[b], w, e->swh_y[b], w);
+                } else {  // the loop on device-resident staging (in-stream K4 launches)
+                    for (long k = k0; k < k0 + nk; ++k) {
+                        const long r0 = (k - k0) * period, kc = std::min(period, hops - r0);
+                        if (irs[k]) {
+                            const int rc = tvolap_exchange_filter(e, ptrs[k], ir_length, S);
+                            if (rc) throw ApiError{rc, g_err};
+                        }
+                        process_hops_impl(e, e->swh_x[b] + r0 * L, w, e->swh_y[b] + r0 * L, w, kc, nullptr);
+                    }
+                }
                 CK(cudaEventRecord(e->ev_k[b], e->stream));
                 CK(cudaStreamWaitEvent(e->d2h, e->ev_k[b], 0));
                 CK(cudaMemcpy2DAsync(out + h0 * L, out_lane_stride * sizeof(float), e->swh_y[b], w * sizeof(float),
@@ -910,12 +925,14 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
             CK(cudaEventRecord(e->ev_start, e->d2h));  // later work on the engine stream sees the outputs
             CK(cudaStreamWaitEvent(e->stream, e->ev_start, 0));
         }
-        e->active = slot;
-        for (int i = 0; i < kSlots; ++i) CK(cudaEventRecord(e->ev_slot[i], e->stream));  // every slot was touched
-        CK(cudaEventRecord(e->ev_main, e->stream));
-        e->fwd += (uint64_t)(S * n_hops);
-        e->inv += (uint64_t)(S * e->E * n_hops);
-        e->macs += (uint64_t)(S * e->E * e->M * n_hops);
+        if (kernel_ok) {  // (the loop path keeps its own slot rotation and counts)
+            e->active = slot;
+            for (int i = 0; i < kSlots; ++i) CK(cudaEventRecord(e->ev_slot[i], e->stream));  // every slot touched
+            CK(cudaEventRecord(e->ev_main, e->stream));
+            e->fwd += (uint64_t)(S * n_hops);
+            e->inv += (uint64_t)(S * e->E * n_hops);
+            e->macs += (uint64_t)(S * e->E * e->M * n_hops);
+        }
         if (pinned && !e->host_async) CK(cudaStreamSynchronize(e->stream));
     });
 }

@@ -101,12 +101,14 @@ def test_switching_validation():
         eng.process_switching(x, [big] * 2, 4)
 
 
-@pytest.mark.parametrize("n_hops,period", [(16 * 9 + 5, 16), (64, 16), (90, 10)])
-def test_switching_pinned_host_pipeline(n_hops, period):
-    """Pinned host buffers: chunked H2D / launch / D2H pipeline, bit-identical to the device call."""
+@pytest.mark.parametrize("n_hops,period,hop", [(16 * 9 + 5, 16, 256), (64, 16, 256), (90, 10, 256), (40, 8, 512),
+                                              (50, 16, 256)])
+def test_switching_pinned_host_pipeline(n_hops, period, hop):
+    """Pinned host buffers: chunked H2D / launch / D2H pipeline (switching kernel, or the loop on
+    device staging for 2048-point transforms), bit-identical to the device call."""
     import torch
 
-    hop, S, taps = 256, 4, 4096
+    S, taps = 4, 4096
     ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at=(1,))
     xh = x.cpu().pin_memory()
     irh = [None if d is None else d.cpu().pin_memory() for d in dirs]
