@@ -419,7 +419,7 @@ enum MacMap { kUni4, kUni2, kParity };
 __host__ __device__ constexpr MacMap mac_map(bool bank, int J) { return bank ? kParity : (J <= 8 ? kUni4 : kUni2); }
 
 struct BlockLayout {
-    size_t tw, pk, win, xin, yb, fa, fb, red, stg, ola, total;
+    size_t tw, pk, win, xin, yb, fa, fb, red, stg, ola, tdr, total;
     // fa | fb (FFT ping-pong) are idle during the MAC: the unified MAC's per-thread staging ring
     // and the partition-group partial sums (red) alias them; red is written only after every
     // thread has drained its ring, and is consumed before the inverse FFT reuses fa.
@@ -445,11 +445,11 @@ struct BlockLayout {
         size_t end = fb + fpc * E * N * sizeof(float2);
         if (red + red_bytes > end) end = red + red_bytes;
         if (stg + stg_bytes > end) end = stg + stg_bytes;
-        // the fused K4 prologue runs two partitions per warp in lockstep (warp-private buffers)
-        const size_t k4_bytes = N <= 512 ? 2 * (size_t)(threads / 32) * N * sizeof(float2) : 0;
-        if (!bank && fa + k4_bytes > end) end = fa + k4_bytes;
         ola = align16(end);
-        total = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
+        // time-domain receive buffer: the 4 quarter-slices of every frame of the block at this
+        // CTA's output samples, pushed by the frame owners over DSMEM [J][E][4][L/P]
+        tdr = align16(ola + (size_t)E * 3 * (L / P) * sizeof(float));
+        total = align16(tdr + (size_t)J * E * 4 * (L / P) * sizeof(float));
     }
 };
 
@@ -1044,16 +1044,45 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         // the result buffer depends only on the stage count (same in every CTA of the cluster)
         const int stages = fft_stage_count(N);
         const float* ytd = reinterpret_cast<const float*>((stages & 1) ? s_fa : s_fb);
-        // time-domain frame (f, e) of this CTA = ytd[(f * E + e) * 2N ...] (unscaled)
+        // time-domain frame (f, e) of this CTA = ytd[(f * E + e) * 2N ...] (unscaled); push each
+        // frame's quarter-slices, scaled, to the CTAs that emit those output samples (DSMEM
+        // stores: the OLA then reads only local shared memory, and no barrier has to protect
+        // ytd from remote readers)
+        float* s_tdr = reinterpret_cast<float*>(smem + lay.tdr);
+        {
+            const float sc = 1.0f / (float)N;
+            if ((Lp & 3) == 0) {
+                const int L4 = L >> 2, lgL4 = lgL - 2;
+                for (int i = tid; i < nt * 4 * L4; i += NT) {  // (transform t, quarter d, float4 v)
+                    const int v = i & (L4 - 1), td = i >> lgL4, d = td & 3, t = td >> 2;
+                    const int f = t / E, e = t - f * E;
+                    float4 y4 = reinterpret_cast<const float4*>(ytd + (size_t)t * 2 * N + (size_t)d * L)[v];
+                    y4 = make_float4(y4.x * sc, y4.y * sc, y4.z * sc, y4.w * sc);
+                    const int smp = 4 * v, q = smp >> lgLp, u = smp & (Lp - 1);
+                    const int jj = r + f * P;
+                    float* dst = s_tdr + ((size_t)(jj * E + e) * 4 + d) * Lp + u;
+                    if (q != r) dst = cluster.map_shared_rank(dst, q);
+                    *reinterpret_cast<float4*>(dst) = y4;
+                }
+            } else {
+                for (int i = tid; i < nt * 4 * L; i += NT) {
+                    const int smp = i & (L - 1), td = i >> lgL, d = td & 3, t = td >> 2;
+                    const int f = t / E, e = t - f * E;
+                    const float y = ytd[(size_t)t * 2 * N + (size_t)d * L + smp] * sc;
+                    const int q = smp >> lgLp, u = smp & (Lp - 1);
+                    const int jj = r + f * P;
+                    float* dst = s_tdr + ((size_t)(jj * E + e) * 4 + d) * Lp + u;
+                    if (q != r) dst = cluster.map_shared_rank(dst, q);
+                    *dst = y;
+                }
+            }
+        }
         PHASE_MARK(6);
-        block_sync(P);  // all frames' time-domain blocks ready
+        block_sync(P);  // all frames' time-domain slices delivered
         PHASE_MARK(7);
 
-        // ---- K5b: hop-2 overlap-add for this CTA's sample slice, all frames of the block.
-        // Both ping-pong buffers hold the same transform count, so the result buffer
-        // offset is identical in every CTA of the cluster.
-        const size_t ytd_off = (size_t)((const unsigned char*)ytd - smem);
-        const float sc = 1.0f / (float)N;
+        // ---- K5b: hop-2 overlap-add for this CTA's sample slice, all frames of the block
+        // (from the local receive buffer).
         for (int i = tid; i < E * Lp; i += NT) {
             const int e = i >> lgLp, u = i & (Lp - 1);
             const int ug = r * Lp + u;
@@ -1069,12 +1098,9 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                 for (int jc = 0; jc < JC; ++jc) {
                     const int jj = j0 + jc;
                     if (jj < jb) {
-                        const int owner = jj & (P - 1), f = jj >> lgP;
-                        const float* base = reinterpret_cast<const float*>(smem + ytd_off);
-                        if (owner != r) base = cluster.map_shared_rank(base, owner);
-                        const float* yf = base + ((size_t)f * E + e) * 2 * N;
+                        const float* yf = s_tdr + (size_t)(jj * E + e) * 4 * Lp + u;
 #pragma unroll
-                        for (int d = 0; d < 4; ++d) y[jc][d] = yf[d * L + ug] * sc;
+                        for (int d = 0; d < 4; ++d) y[jc][d] = yf[d * Lp];
                     } else {
 #pragma unroll
                         for (int d = 0; d < 4; ++d) y[jc][d] = 0.f;
@@ -1097,12 +1123,17 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         }
         PHASE_MARK(8);
         PHASE_MARK(9);
-        block_sync(P);  // peers done reading this CTA's Y slices / time-domain frames
+        // No cluster barrier here: peers read nothing of this CTA after the time-domain barrier
+        // (its Y slices are protected by the next block's first barrier, which peers reach only
+        // after their gather), and the next block's pushes into s_tdr come after its Y barrier,
+        // which this CTA reaches only after the overlap-add above. (Intra-CTA, the next block
+        // starts with __syncthreads; the write-back below has its own.)
         PHASE_MARK(10);
 #ifdef TVOLAP_PHASE_PROF
         if (tid == 0) atomicAdd(&g_phase[12], 1ull);
 #endif
     }
+    __syncthreads();  // the OLA threads' last s_ola updates before the state write-back
     asm volatile("cp.async.wait_all;\n" ::);
     if (r == 0)
         for (int i = tid; i < L; i += NT) p.hist[(long)s * L + i] = xcur[i];
