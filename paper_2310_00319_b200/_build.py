@@ -45,7 +45,9 @@ def build(force: bool = False, verbose: bool = False) -> None:
         # --fmad=false: no implicit multiply-add contraction, so the one-hop and hop-blocked
         # kernels (same operations, different code around them) round identically; every
         # intended FMA is an explicit fmaf().
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+        # host-only calls from device code compile to traps: make them errors
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Werror", "cross-execution-space-call",
+               "-Xcompiler", "-fPIC", "-shared",
                "-I", INCLUDE, "-o", LIB_CUDA, *CUDA_SOURCES]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -68,7 +70,8 @@ def build_variant(name: str, defines, verbose: bool = False) -> Path:
     out = LIB / name / "libtvolap_b200.so"
     out.parent.mkdir(parents=True, exist_ok=True)
     if _stale(out, CUDA_DEPS):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Werror", "cross-execution-space-call",
+              "-Xcompiler", "-fPIC", "-shared",
               *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", out, *CUDA_SOURCES])
     return out
 
