@@ -615,6 +615,14 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             period_end = (b0 + jb) % p.sw_period == 0 || b0 + jb >= p.n_hops;
         }
         if (b0 + jb >= p.n_hops) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+        // delay-line slots: hop l0 + k lives in slot ((l0 + k) >> 1) mod D of parity (l0 + k) & 1;
+        // one 64-bit modulo per block, then small int offsets with a single wrap
+        const int sl0 = (int)((l0 >> 1) % D), odd0 = (int)(l0 & 1);
+        auto slot_of = [&](int k) {
+            const int sl = sl0 + ((odd0 + k) >> 1);
+            return sl >= D ? sl - D : sl;
+        };
+        auto wrapD = [&](int x) { return x < 0 ? x + D : (x >= D ? x - D : x); };
         // ---- inputs: this block's landed (prefetched during the previous block)
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
@@ -636,8 +644,8 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         if (nf > 0) {
             const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
             for (int f = 0; f < nf; ++f) {
-                const long h = l0 + r + f * P;
-                float2* ringw = p.ring + (((long)s * 2 + (h & 1)) * D + (h >> 1) % D) * N;
+                const int k = r + f * P;
+                float2* ringw = p.ring + (((long)s * 2 + ((odd0 + k) & 1)) * D + slot_of(k)) * N;
                 untangle_store<NC>(Z + (size_t)f * N, N, s_pk, ringw, tid, NT);
             }
         }
@@ -674,22 +682,19 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
             constexpr int JU = JH <= 4 ? JH : 1;
             for (int f = (V >= NT ? tid : tid % V); f < V; f += (V >= NT ? NT : V)) {
                 const float4* xr[2];
-                long sbp[2];
+                int sbp[2];
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
-                    const long hbg = l0 + g;
-                    xr[g] = ring4 + (((long)s * 2 + (hbg & 1)) * D) * spec4 + (long)r * V + f;
-                    sbp[g] = hbg >> 1;
+                    xr[g] = ring4 + (((long)s * 2 + ((odd0 + g) & 1)) * D) * spec4 + (long)r * V + f;
+                    sbp[g] = slot_of(g);
                 }
-                auto xs = [&](int g, long t) -> const float4* {  // window init only
-                    long sl = (sbp[g] + t) % D;
-                    if (sl < 0) sl += D;
-                    return xr[g] + sl * spec4;
+                auto xs = [&](int g, int t) -> const float4* {  // window init only
+                    return xr[g] + (long)wrapD(sbp[g] + t) * spec4;
                 };
                 // slot cursors for the next delay-line load (t = -m-1), decremented per partition
                 int cur[2];
 #pragma unroll
-                for (int g = 0; g < 2; ++g) cur[g] = (int)(((sbp[g] - mu0 - 1) % D + D) % D);
+                for (int g = 0; g < 2; ++g) cur[g] = wrapD(sbp[g] - mu0 - 1);
                 const float4* hb4[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) hb4[e] = pool4 + (((long)ent0 * E + e) * M) * spec4 + (long)r * V + f;
@@ -792,14 +797,13 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                 auto mac = [&](auto pk_tag) {
                     constexpr bool PK = decltype(pk_tag)::value;
                     const float2* xr[2];
-                    long sbp[2];
+                    int sbp[2];
                     int cur[2];
 #pragma unroll
                     for (int g = 0; g < 2; ++g) {
-                        const long hbg = l0 + g;
-                        xr[g] = ring2 + (((long)s * 2 + (hbg & 1)) * D) * N + (long)r * Np + f;
-                        sbp[g] = hbg >> 1;
-                        cur[g] = (int)(((sbp[g] - mu0 - 1) % D + D) % D);
+                        xr[g] = ring2 + (((long)s * 2 + ((odd0 + g) & 1)) * D) * N + (long)r * Np + f;
+                        sbp[g] = slot_of(g);
+                        cur[g] = wrapD(sbp[g] - mu0 - 1);
                     }
                     const float2* hb = pool2 + ((long)ent0 * M) * N + (long)r * Np + f;
                     float2 acc[2][JH];
@@ -811,9 +815,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                         for (int i = 0; i < JH; ++i) {
                             acc[g][i] = make_float2(0.f, 0.f);
                             if constexpr (PK) aux[g][i] = 0.f;
-                            long sl = (sbp[g] + i - mu0) % D;
-                            if (sl < 0) sl += D;
-                            win[g][i] = __ldcg(xr[g] + sl * N);
+                            win[g][i] = __ldcg(xr[g] + (long)wrapD(sbp[g] + i - mu0) * N);
                         }
                     auto mac_step = [&](const float2 (&xn)[2], const float2 h) {
 #pragma unroll
@@ -888,17 +890,14 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
         // Per-parity mapping (W >= NT: threads stride over the work items; W < NT: Qeff groups of W).
         for (int w = (W >= NT ? tid : tid % W); w < W; w += (W >= NT ? NT : W)) {
             const int g = w / V, f = w - g * V;
-            const long hb = l0 + g;
-            const int par = (int)(hb & 1);
-            const long sb = hb >> 1;
+            const int par = (odd0 + g) & 1;
+            const int sb = slot_of(g);
             const int ni = jb > g ? (jb - g + 1) / 2 : 0;  // outputs of this parity group
             const float4* xr = ring4 + (((long)s * 2 + par) * D) * spec4 + (long)r * V + f;
-            auto xslot = [&](long t) -> const float4* {  // window init only
-                long sl = (sb + t) % D;
-                if (sl < 0) sl += D;
-                return xr + sl * spec4;
+            auto xslot = [&](int t) -> const float4* {  // window init only
+                return xr + (long)wrapD(sb + t) * spec4;
             };
-            int cur = (int)(((sb - m0 - 1) % D + D) % D);  // slot of the next load (t = -m-1)
+            int cur = wrapD(sb - m0 - 1);  // slot of the next load (t = -m-1)
             auto xnext = [&]() -> float4 {
                 const float4 v = __ldcg(xr + (long)cur * spec4);
                 cur = cur == 0 ? D - 1 : cur - 1;
