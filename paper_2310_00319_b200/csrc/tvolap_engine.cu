@@ -294,7 +294,7 @@ void pick_block_geometry(tvolap_engine* e) {
         if (ej > 0) e->JH = ej;
     }
     const long W = e->N / e->PB;
-    e->NTB = 256;
+    e->NTB = std::max(32, std::min(256, env_int("TVOLAP_NTB", 256)));  // A/B knob; 256 measured best
     e->QB = 1;
     if (W < e->NTB) {
         e->QB = (int)(e->NTB / W);
@@ -786,7 +786,8 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         bool pinned = min == Mem::Pinned && mout == Mem::Pinned;
         // the switching kernel (in-kernel K4); in a pinned pipeline every chunk launch must take
         // the hop-blocked kernel: full periods, and a last one of at least block_min hops
-        const bool kernel_ok = (e->N == 256 || e->N == 512) && e->E == 1 && units <= 2 * warps * blocks &&
+        const long gap_units = 2 * warps * blocks * env_int("TVOLAP_K4_GAP_MULT", 1);
+        const bool kernel_ok = (e->N == 256 || e->N == 512) && e->E == 1 && units <= gap_units &&
                                (!pinned || (period >= e->block_min && n_hops - (nsw - 1) * period >= e->block_min));
         dev = dev && kernel_ok;
         for (long k = 0; k < nsw; ++k) {

@@ -163,14 +163,7 @@ __device__ void fused_partition(const HopParams& p, int s, int r, int P, float2*
                 return make_float2(i0 < p.new_ir_len ? h[i0] : 0.f, i0 + 1 < p.new_ir_len ? h[i0 + 1] : 0.f);
             };
         };
-        auto store = [&](const float2* buf, int m) {
-            float4* d4 = reinterpret_cast<float4*>(dst + (long)m * NC);
-            for (int k2 = lane; k2 < NC / 2; k2 += 32) {
-                const float2 a = untangle_packed(buf, NC, 2 * k2, pk);
-                const float2 b = untangle(buf, NC, 2 * k2 + 1, pk);
-                d4[k2] = make_float4(a.x, a.y, b.x, b.y);
-            }
-        };
+        auto store = [&](const float2* buf, int m) { untangle_pairs_warp(buf, NC, pk, dst + (long)m * NC, lane); };
         if (slots >= 2 * (NT >> 5) && NC <= 512) {
             float2* buf = fa + (size_t)warp * 2 * NC;
             const int nw = NT >> 5;
@@ -560,12 +553,7 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                 return make_float2(i0 < p.sw_ir_len ? h[i0] : 0.f, i0 + 1 < p.sw_ir_len ? h[i0 + 1] : 0.f);
             };
             auto store_unit = [&](const float2* buf, int u) {
-                float4* d4 = reinterpret_cast<float4*>(p.pool_w + ((long)(entry + s) * M + r + u * P) * NC);
-                for (int k2 = lane; k2 < NC / 2; k2 += 32) {
-                    const float2 a = untangle_packed(buf, NC, 2 * k2, s_pk);
-                    const float2 b = untangle(buf, NC, 2 * k2 + 1, s_pk);
-                    d4[k2] = make_float4(a.x, a.y, b.x, b.y);
-                }
+                untangle_pairs_warp(buf, NC, s_pk, p.pool_w + ((long)(entry + s) * M + r + u * P) * NC, lane);
             };
             if (warp >= k4_slots) return;
             float2* buf = s_fa + (size_t)warp * NC;
@@ -1243,12 +1231,7 @@ __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows
             return make_float2(i0 < ir_len ? h[i0] : 0.f, i0 + 1 < ir_len ? h[i0 + 1] : 0.f);
         };
         fft_warp4<false, N, true>(buf, tw + N, lane, load0);
-        float4* d4 = reinterpret_cast<float4*>(pool + ((row0 + row) * M + m) * N);
-        for (int k2 = lane; k2 < N / 2; k2 += 32) {
-            const float2 a = untangle_packed(buf, N, 2 * k2, s_pk);
-            const float2 b = untangle(buf, N, 2 * k2 + 1, s_pk);
-            d4[k2] = make_float4(a.x, a.y, b.x, b.y);
-        }
+        untangle_pairs_warp(buf, N, s_pk, pool + ((row0 + row) * M + m) * N, lane);
         __syncwarp();
     }
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
