@@ -787,7 +787,8 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         // the switching kernel (in-kernel K4); in a pinned pipeline every chunk launch must take
         // the hop-blocked kernel: full periods, and a last one of at least block_min hops
         const long gap_units = 2 * warps * blocks * env_int("TVOLAP_K4_GAP_MULT", 1);
-        const bool kernel_ok = (e->N == 256 || e->N == 512) && e->E == 1 && units <= gap_units &&
+        const bool n_ok = e->N == 256 || e->N == 512 || (e->N == 1024 && env_int("TVOLAP_SW_1024", 0));
+        const bool kernel_ok = n_ok && e->E == 1 && units <= gap_units &&
                                (!pinned || (period >= e->block_min && n_hops - (nsw - 1) * period >= e->block_min));
         dev = dev && kernel_ok;
         for (long k = 0; k < nsw; ++k) {
