@@ -19,7 +19,7 @@ INCLUDE = ROOT / "include"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CUDA_SOURCES = [CSRC / "tvolap_kernels.cu", CSRC / "tvolap_engine.cu"]
+CUDA_SOURCES = [CSRC / "tvolap_kernels.cu", CSRC / "tvolap_wide.cu", CSRC / "tvolap_engine.cu"]
 CUDA_DEPS = CUDA_SOURCES + [CSRC / "tvolap_fft.cuh", CSRC / "tvolap_internal.cuh", CSRC / "workload.h",
                             INCLUDE / "tvolap_b200.h"]
 

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/tvolap_b200.h"
@@ -197,6 +198,15 @@ struct tvolap_engine {
     float *swh_x[2] = {}, *swh_y[2] = {}, *swh_ir[2] = {};
     long swh_cap_x = 0, swh_cap_ir = 0;
     bool staged_in_stream = false;   // the pending set is transformed by latch() on the engine stream
+    // time-parallel pass (tvolap_wide.cu): extended spectra, the call's filter sets, tile tables
+    float2 *wide_xe = nullptr, *wide_pool = nullptr;
+    float *wide_state = nullptr, *wide_head = nullptr;
+    const float2** d_wide_fset = nullptr;
+    const float** d_wide_irs = nullptr;
+    int* d_wide_tile0 = nullptr;
+    size_t wide_xe_cap = 0, wide_pool_cap = 0, wide_tile_cap = 0, wide_fset_cap = 0, wide_sw_cap = 0;
+    size_t wide_state_cap = 0, wide_head_cap = 0;
+    int wide_mode = 1;               // TVOLAP_WIDE: 0 off, 1 auto, 2 whenever supported
     // chunked host pipeline
     long chunk_hops = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
@@ -229,7 +239,8 @@ struct tvolap_engine {
                         (void*)d_in[1], (void*)d_out[0],
                         (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1], (void*)d_sw_irs, (void*)d_sw_entry,
                         (void*)swh_x[0], (void*)swh_x[1], (void*)swh_y[0], (void*)swh_y[1], (void*)swh_ir[0],
-                        (void*)swh_ir[1]})
+                        (void*)swh_ir[1], (void*)wide_xe, (void*)wide_pool, (void*)wide_state, (void*)wide_head,
+                        (void*)d_wide_fset, (void*)d_wide_irs, (void*)d_wide_tile0})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
@@ -264,6 +275,7 @@ void pick_launch_config(tvolap_engine* e) {
     // in-stream K4 chained by PDL 2.53 (profiles/r01_ab_pdl.txt)
     e->k4_stream = env_int("TVOLAP_K4_STREAM", 1) != 0;
     e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 1)));
+    e->wide_mode = env_int("TVOLAP_WIDE", 1);
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -759,6 +771,165 @@ int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, 
     return guarded([&] { process_hops_impl(e, in, in_lane_stride, out, out_lane_stride, n_hops, schedule); });
 }
 
+// ---- time-parallel pass (tvolap_wide.cu) for device-resident switching calls
+extern "C++" {
+namespace {
+
+bool wide_eligible(const tvolap_engine* e, long n_hops, long period) {
+    if (e->wide_mode == 0 || e->bank || e->E != 1 || !tvb::wide_supported((int)e->L)) return false;
+    if (period < 3 || n_hops < period || n_hops < 16) return false;
+    // auto: only where the hop-blocked kernel leaves most of the GPU idle (lanes x cluster CTAs
+    // below two per SM, e.g. C1/C2); there the hop axis is the parallelism
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * 148) return false;
+    return true;
+}
+
+void prof_pair(tvolap_engine* e, cudaEvent_t* t0, cudaEvent_t* t1) {
+    *t0 = *t1 = nullptr;
+    if (!e->profiling) return;
+    if (e->prof_used == e->prof_events.size()) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        e->prof_events.emplace_back(a, b);
+    }
+    *t0 = e->prof_events[e->prof_used].first;
+    *t1 = e->prof_events[e->prof_used].second;
+    ++e->prof_used;
+}
+
+template <class T>
+void ensure_dev(T*& p, size_t& cap, size_t count) {
+    if (cap >= count) return;
+    if (p) CK(cudaFree((void*)p));
+    p = dalloc<std::remove_const_t<T>>(count);
+    cap = count;
+}
+
+// The call as time-parallel passes (chunks of periods whose new sets fit the pool budget): K4
+// of the chunk's sets, K1 of all its hops, then (lane, tile) CTAs for K3+K5 and the OLA fix-up.
+// Same results, bit for bit, as the switching / hop-blocked launches.
+void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n_hops,
+              long period, const float* const* irs, long ir_length) {
+    const long S = e->S, M = e->M, N = e->N, L = e->L;
+    const long nsw = (n_hops + period - 1) / period;
+    const long last = n_hops - (nsw - 1) * period;
+    const long nsw_w = last >= 3 ? nsw : nsw - 1;  // a 1-2 hop final period runs on the blocked path
+    const long n_w = last >= 3 ? n_hops : (nsw - 1) * period;
+    if (irs[0]) {  // a staged set is superseded at this very hop (last wins)
+        std::lock_guard<std::mutex> lock(e->mu);
+        if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+        e->pending = false;
+    }
+    latch(e);
+    int JH = 8;
+    if (tvb::wide_mac_smem_bytes((int)L, JH) > 227 * 1024) JH = 4;
+    const long Jmax = 2 * JH;
+    const size_t set_elems = (size_t)S * M * N;
+    const long budget_mb = env_int("TVOLAP_WIDE_POOL_MB", 8192);
+    const long cap_sets = std::max<long>(1, (long)((budget_mb << 20) / (long)(set_elems * sizeof(float2))));
+    const float2* cur_set = e->pool + (size_t)e->active * set_elems;
+    for (long k0 = 0; k0 < nsw_w;) {
+        long k1 = k0, nsets = 0;
+        while (k1 < nsw_w && (!irs[k1] || nsets < cap_sets)) nsets += irs[k1++] ? 1 : 0;
+        const long h0 = k0 * period, nh = std::min(k1 * period, n_w) - h0;
+        // K4 for the chunk's sets
+        std::vector<const float*> tab;
+        for (long k = k0; k < k1; ++k)
+            if (irs[k]) tab.push_back(irs[k]);
+        if (nsets) {
+            ensure_dev(e->wide_pool, e->wide_pool_cap, (size_t)nsets * set_elems);
+            ensure_dev(e->d_wide_irs, e->wide_sw_cap, (size_t)nsets);
+            CK(cudaMemcpyAsync(e->d_wide_irs, tab.data(), sizeof(const float*) * nsets, cudaMemcpyHostToDevice,
+                               e->stream));
+            CK(tvb::launch_partition_multi((int)L, (int)M, (int)S, nsets * S, e->d_wide_irs, ir_length, e->wide_pool,
+                                           e->tw, e->pk, e->stream));
+            ++e->launches;
+        }
+        // tiles: each period split into balanced tiles of <= 2 JH hops (>= 3 each: OLA fix-up)
+        std::vector<int> t0;
+        std::vector<const float2*> fs;
+        long idx = 0;
+        for (long k = k0; k < k1; ++k) {
+            if (irs[k]) cur_set = e->wide_pool + (size_t)(idx++) * set_elems;
+            const long plen = std::min(period, n_w - k * period);
+            const long tp = (plen + Jmax - 1) / Jmax, base = plen / tp, rem = plen % tp;
+            long st = k * period - h0;
+            for (long w = 0; w < tp; ++w) {
+                t0.push_back((int)st);
+                fs.push_back(cur_set);
+                st += base + (w < rem ? 1 : 0);
+            }
+        }
+        t0.push_back((int)nh);
+        const long ntiles = (long)fs.size();
+        ensure_dev(e->d_wide_fset, e->wide_fset_cap, (size_t)ntiles);
+        ensure_dev(e->d_wide_tile0, e->wide_tile_cap, (size_t)ntiles + 1);
+        CK(cudaMemcpyAsync(e->d_wide_fset, fs.data(), sizeof(const float2*) * ntiles, cudaMemcpyHostToDevice,
+                           e->stream));
+        CK(cudaMemcpyAsync(e->d_wide_tile0, t0.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice, e->stream));
+        // carry and head terms per tile, extended spectra
+        ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * ntiles * 3 * L);
+        ensure_dev(e->wide_head, e->wide_head_cap, (size_t)S * ntiles * 6 * L);
+        const long T = (nh + 1) / 2 + M + JH + 4;
+        ensure_dev(e->wide_xe, e->wide_xe_cap, (size_t)S * 2 * T * N);
+        tvb::WideParams p{};
+        p.L = (int)L;
+        p.M = (int)M;
+        p.D = (int)e->D;
+        p.S = (int)S;
+        p.Q = e->QM;
+        p.hop0 = e->hops;
+        p.n = (int)nh;
+        p.in = in + h0 * L;
+        p.in_stride = in_stride;
+        p.out = out + h0 * L;
+        p.out_stride = out_stride;
+        p.ring = e->ring;
+        p.xe = e->wide_xe;
+        p.T = T;
+        p.tbase = (e->hops >> 1) - M;
+        p.hist = e->hist;
+        p.ola = e->ola;
+        p.tw = e->tw;
+        p.pk = e->pk;
+        p.win = e->win;
+        p.fset = e->d_wide_fset;
+        p.tile0 = e->d_wide_tile0;
+        p.ntiles = (int)ntiles;
+        p.tstate = e->wide_state;
+        p.thead = e->wide_head;
+        cudaEvent_t ev0, ev1;
+        prof_pair(e, &ev0, &ev1);
+        CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
+        e->launches += 4;
+        e->hops += nh;
+        if (nsets) {  // the chunk's last set becomes the engine's active set (a pool slot)
+            const int slot = (e->active + 1) % kSlots;
+            float2* dst = e->pool + (size_t)slot * set_elems;
+            CK(cudaMemcpyAsync(dst, cur_set, set_elems * sizeof(float2), cudaMemcpyDeviceToDevice, e->stream));
+            e->active = slot;
+            cur_set = dst;
+        }
+        k0 = k1;
+    }
+    for (int i = 0; i < kSlots; ++i) CK(cudaEventRecord(e->ev_slot[i], e->stream));
+    CK(cudaEventRecord(e->ev_main, e->stream));
+    e->fwd += (uint64_t)(S * n_w);
+    e->inv += (uint64_t)(S * n_w);
+    e->macs += (uint64_t)(S * M * n_w);
+    if (n_w < n_hops) {  // final 1-2 hop period: the blocked path with its set
+        if (irs[nsw - 1]) {
+            const int rc = tvolap_exchange_filter(e, irs[nsw - 1], ir_length, S);
+            if (rc) throw ApiError{rc, g_err};
+        }
+        process_hops_impl(e, in + n_w * L, in_stride, out + n_w * L, out_stride, n_hops - n_w, nullptr);
+    }
+}
+
+}  // namespace
+}  // extern "C++"
+
 int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
                              long n_hops, long period, const float* const* irs, long ir_length) {
     if (int rc = check_hops_args(e, in, out, n_hops)) return rc;
@@ -775,6 +946,14 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter partition count differs");
     return guarded([&] {
         CK(cudaSetDevice(e->device));
+        {  // device-resident call with enough hops: the time-parallel pass
+            bool wide = classify(in) == Mem::Device && classify(out) == Mem::Device && wide_eligible(e, n_hops, period);
+            for (long k = 0; wide && k < nsw; ++k) wide = !irs[k] || classify(irs[k]) == Mem::Device;
+            if (wide) {
+                run_wide(e, in, in_lane_stride, out, out_lane_stride, n_hops, period, irs, ir_length);
+                return;
+            }
+        }
         // In-kernel K4 pays off when a CTA's share of one switch's partitions fits the barrier gaps
         // of a period (2 gaps per block, one partition per warp each): C2 16 partitions per CTA in
         // one 16-hop block -> 2.37 vs 2.83 us/hop; C4 (2048-point, 32 per CTA per 8-hop period)

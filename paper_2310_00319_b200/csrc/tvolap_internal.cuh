@@ -47,6 +47,38 @@ struct HopParams {
     long sw_ir_len = 0;
 };
 
+// Time-parallel pass (tvolap_wide.cu) over n hops of a device-resident call.
+struct WideParams {
+    int L, M, D, S, Q;     // Q: partition groups (the blocked kernel's, for bit-identical sums)
+    long hop0;             // global index of the pass's first hop
+    int n;                 // hops in the pass
+    const float* in;       // in[s * in_stride + k * L + t], k < n
+    long in_stride;
+    float* out;            // out[s * out_stride + k * L + t]
+    long out_stride;
+    float2* ring;          // delay line [S][2][D][2L]: read before the pass, its last 2D hops written
+    float2* xe;            // extended spectra [S][2][T][2L]: slot t of parity p = hop 2 (t + tbase) + p
+    long T;
+    long tbase;            // (hop0 >> 1) - M
+    float* hist;           // [S][L]
+    float* ola;            // [S][3L]
+    const float2* tw;
+    const float2* pk;
+    const float* win;
+    const float2* const* fset;  // per tile: filter set [S][M][2L]
+    const int* tile0;           // tile k = hops tile0[k] .. tile0[k+1] of the pass (>= 3 hops each)
+    int ntiles;
+    float* tstate;              // overlap-add carry after each tile [S][ntiles][3][L]
+    float* thead;               // first-three-output terms of each tile [S][ntiles][6][L]
+};
+bool wide_supported(int L);
+size_t wide_mac_smem_bytes(int L, int JH);
+// parts: 1 = head copy + forward FFTs, 2 = MAC/inverse tiles (+ fix-up); events bracket the tiles
+cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1, int parts);
+// K4 for rows = sets * S IRs: irs[row / S] + (row % S) * ir_len -> pool[(row * M + m) * 2L]
+cudaError_t launch_partition_multi(int L, int M, int S, long rows, const float* const* irs, long ir_len, float2* pool,
+                                   const float2* tw, const float2* pk, cudaStream_t stream);
+
 size_t hop_kernel_smem_bytes(int L, int P, int E, int qm);
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
 

@@ -1,0 +1,466 @@
+// Time-parallel ("wide") pass of the TVOLAP engine for long device-resident calls.
+//
+// A call that carries all of its hops (tvolap_process_switching on device buffers) fixes every
+// input frame and every filter set up front, so nothing in the per-hop pipeline of
+// proj/src/engine.cpp:60-106 is sequential across hops except the hop-2 overlap-add carry
+// (engine.cpp:97-102), which is a 3-value linear recurrence per output sample. The hop-blocked
+// kernel walks the hops of a lane in order (parallelism = lanes x cluster CTAs: 256 CTAs for
+// C2); here the hop axis is parallel too:
+//   wide_head_kernel     the spectra of hops before the call (still needed by its first
+//                        outputs) from the delay line into the extended spectra buffer Xe,
+//   wide_forward_kernel  K1 for every hop of the call at once (window + pruned Stockham FFT +
+//                        untangle), into Xe; the last 2D hops also into the delay line,
+//   partition_multi      K4 for every filter set the call installs (one warp per partition),
+//   wide_mac_kernel      one CTA per (lane, tile of <= 16 hops inside one filter period): K3
+//                        over Xe with a sliding register window, then K5 (tangle + inverse FFT)
+//                        and the overlap-add of the tile's outputs from its 4th hop on,
+//   wide_fixup_kernel    the first three outputs of every tile from the carry of the tile
+//                        before it (and the engine's carry / history for the next call).
+// Every arithmetic operation and its order per output equal the hop-blocked kernel's (same FFT
+// code, same partition groups summed in the same order, same OLA recurrence), so the outputs
+// are bit-identical to tvolap_block_kernel's (tests/test_gpu_wide.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "tvolap_fft.cuh"
+#include "tvolap_internal.cuh"
+
+namespace tvb {
+namespace {
+
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Delay-line history of the call: Xe[s][parity][t] holds the spectrum of hop j with
+// j & 1 == parity and t = (j >> 1) - tbase, for every hop the call's outputs read.
+__global__ void wide_head_kernel(const WideParams p) {
+    const int N = 2 * p.L, V = N / 2;
+    const int nh = p.M + 2;  // slots per parity that can precede hop0
+    const long total = (long)p.S * 2 * nh * V;
+    const float4* ring4 = reinterpret_cast<const float4*>(p.ring);
+    float4* xe4 = reinterpret_cast<float4*>(p.xe);
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const int v = (int)(i % V);
+        const long r = i / V;
+        const int t = (int)(r % nh);
+        const int par = (int)((r / nh) & 1);
+        const long s = r / (2 * nh);
+        const long j = 2 * (t + p.tbase) + par;  // hop held in this slot
+        if (j >= p.hop0) continue;               // written by wide_forward_kernel
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j >= 0) {
+            const long slot = (j >> 1) % p.D;
+            val = ring4[((s * 2 + par) * p.D + slot) * V + v];
+        }
+        xe4[((s * 2 + par) * p.T + t) * V + v] = val;
+    }
+}
+
+// K1 for frames hop0 + blockIdx.x * F + f of lane blockIdx.y (engine.cpp:77-82): the operations
+// of the hop-blocked kernel's forward phase (window products, fft_batch, untangle_store).
+template <int NC>
+__global__ void __launch_bounds__(256) wide_forward_kernel(const WideParams p, int F) {
+    constexpr int N = NC, L = NC / 2;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* s_tw = reinterpret_cast<float2*>(smem);
+    float2* s_pk = reinterpret_cast<float2*>(smem + a16(N * sizeof(float2)));
+    float* s_win = reinterpret_cast<float*>(smem + a16(N * sizeof(float2)) + a16((N + 2) * sizeof(float2)));
+    float2* s_fa = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(s_win) + a16(N * sizeof(float)));
+    float2* s_fb = s_fa + (size_t)F * N;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const long s = blockIdx.y;
+    const int j0 = blockIdx.x * F;
+    const int nf = min(F, p.n - j0);
+    for (int i = tid; i < N; i += NT) {
+        s_tw[i] = p.tw[i];
+        s_win[i] = p.win[i];
+    }
+    for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    __syncthreads();  // the window products below read other threads' table entries
+    const float* xin = p.in + s * p.in_stride;
+    const float* hist = p.hist + s * L;
+    for (int i = tid; i < nf * L; i += NT) {
+        const int f = i / L, jj = i - f * L;
+        const int r = j0 + f;  // hop of the call; frame = (hop r - 1 | hop r)
+        const int e = 2 * jj;  // e, e + 1 lie in the same half (L even)
+        float x0, x1;
+        if (e < L) {
+            const float* prev = r == 0 ? hist : xin + (long)(r - 1) * L;
+            x0 = prev[e];
+            x1 = prev[e + 1];
+        } else {
+            const float* cur = xin + (long)r * L;
+            x0 = cur[e - L];
+            x1 = cur[e + 1 - L];
+        }
+        s_fa[(size_t)f * N + jj] = make_float2(x0 * s_win[e], x1 * s_win[e + 1]);
+    }
+    __syncthreads();
+    if (nf <= 0) return;
+    const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
+    const long ring_from = p.hop0 + p.n - 2L * p.D;  // these hops stay in the delay line after the call
+    for (int f = 0; f < nf; ++f) {
+        const long j = p.hop0 + j0 + f;
+        const int par = (int)(j & 1);
+        float2* dst = p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N;
+        untangle_store<NC>(Z + (size_t)f * N, N, s_pk, dst, tid, NT);
+        if (j >= ring_from)
+            untangle_store<NC>(Z + (size_t)f * N, N, s_pk, p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N, tid,
+                               NT);
+    }
+}
+
+// K4 for the sets a call installs: row r = k * S + s transforms irs[k] + s * ir_len into
+// pool[(r * M + m) * N] (partition.cpp:20-51). Same warp transform as partition_warp_kernel.
+template <int NC>
+__global__ void __launch_bounds__(256, 2) partition_multi_kernel(int M, int S, long rows,
+                                                                 const float* const* __restrict__ irs, long ir_len,
+                                                                 float2* __restrict__ pool,
+                                                                 const float2* __restrict__ tw,
+                                                                 const float2* __restrict__ pk) {
+    constexpr int N = NC;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* s_pk = reinterpret_cast<float2*>(smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    float2* buf = reinterpret_cast<float2*>(smem + a16((N + 2) * sizeof(float2))) + (size_t)warp * N;
+    for (int i = tid; i <= N; i += blockDim.x) s_pk[i] = pk[i];
+    __syncthreads();
+    const long tasks = rows * M;
+    for (long t = (long)blockIdx.x * nw + warp; t < tasks; t += (long)gridDim.x * nw) {
+        const long row = t / M;
+        const int m = (int)(t - row * M);
+        const float* h = irs[row / S] + (row % S) * ir_len;
+        const bool vec = (ir_len & 1) == 0 && (reinterpret_cast<uintptr_t>(h) & 7) == 0;
+        const long base = (long)m * N;
+        auto load0 = [&](int, int n) -> float2 {
+            const long i0 = base + 2 * n;
+            if (vec && i0 + 1 < ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
+            return make_float2(i0 < ir_len ? h[i0] : 0.f, i0 + 1 < ir_len ? h[i0 + 1] : 0.f);
+        };
+        fft_warp4<false, N, true>(buf, tw + N, lane, load0);
+        untangle_pairs_warp(buf, N, s_pk, pool + (row * M + m) * N, lane);
+        __syncwarp();
+    }
+}
+
+constexpr int kWideFB = 4;  // frames per inverse-FFT batch
+
+struct WideLayout {
+    size_t tw, pk, y, fa, fb, total;
+    __host__ __device__ WideLayout(int N, int J) {
+        tw = 0;
+        pk = a16(tw + N * sizeof(float2));
+        y = a16(pk + (N + 2) * sizeof(float2));
+        fa = a16(y + (size_t)J * N * sizeof(float2));
+        fb = a16(fa + (size_t)kWideFB * N * sizeof(float2));
+        total = a16(fb + (size_t)kWideFB * N * sizeof(float2));
+    }
+};
+
+// K3 + K5 for one tile (lane blockIdx.y, hops tile0[x] .. tile0[x+1] of the call, one filter set):
+//   Y_l = sum_m H[m] X_{l-2m} (engine.cpp:85-92) for every packed bin, the partitions in Q
+//   contiguous groups summed in group order (the blocked kernel's grouping), then the inverse
+//   real FFT (spectral.cpp:127-158) and the hop-2 overlap-add (engine.cpp:94-102).
+template <int NC, int JH>
+__global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
+    constexpr int N = NC, L = NC / 2, J = 2 * JH;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const WideLayout lay(N, J);
+    float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
+    float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
+    float2* s_y = reinterpret_cast<float2*>(smem + lay.y);
+    float2* s_fa = reinterpret_cast<float2*>(smem + lay.fa);
+    float2* s_fb = reinterpret_cast<float2*>(smem + lay.fb);
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int tile = blockIdx.x;
+    const long s = blockIdx.y;
+    const int l0r = p.tile0[tile], jt = p.tile0[tile + 1] - l0r;
+    const long l0 = p.hop0 + l0r;
+    const int M = p.M, Q = p.Q;
+    for (int i = tid; i < N; i += NT) s_tw[i] = p.tw[i];
+    for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+
+    // ---- K3: thread per packed bin k, both parity groups (outputs l0 + g + 2i), JH each
+    const float2* H = p.fset[tile] + s * M * N;
+    const float2* X[2];
+    long bse[2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        X[g] = p.xe + (s * 2 + ((l0 + g) & 1)) * p.T * N;
+        bse[g] = ((l0 + g) >> 1) - p.tbase;  // t of output i = bse + i, of its partition-m input bse + i - m
+    }
+    for (int k = tid; k < N; k += NT) {
+        const bool pkw = __any_sync(0xffffffffu, k == 0);
+        auto mac = [&](auto pk_tag) {
+            constexpr bool PK = decltype(pk_tag)::value;
+            for (int qq = 0; qq < Q; ++qq) {
+                const int mu0 = (int)((long)qq * M / Q), mu1 = (int)((long)(qq + 1) * M / Q);
+                float2 acc[2][JH];
+                float aux[2][PK ? JH : 1];
+                float2 win[2][JH];
+                long cur[2];
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    cur[g] = bse[g] - mu0 - 1;
+#pragma unroll
+                    for (int i = 0; i < JH; ++i) {
+                        acc[g][i] = make_float2(0.f, 0.f);
+                        if constexpr (PK) aux[g][i] = 0.f;
+                        win[g][i] = __ldcg(X[g] + (bse[g] + i - mu0) * N + k);
+                    }
+                }
+                auto mac_step = [&](const float2 (&xn)[2], const float2 h) {
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+#pragma unroll
+                        for (int i = 0; i < JH; ++i) {
+                            float2& a = acc[g][i];
+                            const float2 x = win[g][i];
+                            a.x = fmaf(h.x, x.x, a.x);
+                            a.x = fmaf(-h.y, x.y, a.x);
+                            a.y = fmaf(h.x, x.y, a.y);
+                            a.y = fmaf(h.y, x.x, a.y);
+                            if constexpr (PK) aux[g][i] = fmaf(h.y, x.y, aux[g][i]);
+                        }
+#pragma unroll
+                        for (int i = JH - 1; i > 0; --i) win[g][i] = win[g][i - 1];
+                        win[g][0] = xn[g];
+                    }
+                };
+                int m = mu0;
+                constexpr int U = 4;
+                for (; m + U <= mu1; m += U) {
+                    float2 xn[U][2], hh[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) xn[u][g] = __ldcg(X[g] + (cur[g] - u) * N + k);
+                        hh[u] = __ldcg(H + (long)(m + u) * N + k);
+                    }
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) cur[g] -= U;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) mac_step(xn[u], hh[u]);
+                }
+                for (; m < mu1; ++m) {
+                    float2 xn[2];
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) xn[g] = __ldcg(X[g] + (cur[g]--) * N + k);
+                    mac_step(xn, __ldcg(H + (long)m * N + k));
+                }
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int i = 0; i < JH; ++i) {
+                        const int jj = g + 2 * i;
+                        if (jj >= jt) continue;
+                        float2 a = acc[g][i];
+                        if constexpr (PK) {
+                            if (k == 0) {  // packed bin 0: two real products
+                                a.x += aux[g][i];
+                                a.y = aux[g][i];
+                            }
+                        }
+                        float2* y = s_y + (size_t)jj * N + k;
+                        if (qq == 0) {
+                            *y = a;
+                        } else {
+                            const float2 t = *y;
+                            *y = make_float2(t.x + a.x, t.y + a.y);
+                        }
+                    }
+            }
+        };
+        if (pkw)
+            mac(std::true_type{});
+        else
+            mac(std::false_type{});
+    }
+    __syncthreads();
+
+    // ---- K5: tangle + inverse FFT in batches of kWideFB frames, overlap-add per output sample
+    constexpr int UPT = (L + 255) / 256;  // samples per thread (NT = 256)
+    float st[UPT][3];
+#pragma unroll
+    for (int c = 0; c < UPT; ++c) st[c][0] = st[c][1] = st[c][2] = 0.f;
+    const float sc = 1.0f / (float)N;
+    float* head = p.thead + (s * p.ntiles + tile) * 6 * L;
+    float* outp = p.out + s * p.out_stride + (long)l0r * L;
+    for (int f0 = 0; f0 < jt; f0 += kWideFB) {
+        const int nb = min(kWideFB, jt - f0);
+        for (int i = tid; i < nb * N; i += NT) {
+            const int fi = i / N, kk = i - fi * N;
+            s_fb[(size_t)fi * N + kk] = tangle_packed(s_y + (size_t)(f0 + fi) * N, N, kk, s_pk);
+        }
+        __syncthreads();
+        const float* ytd = reinterpret_cast<const float*>(fft_batch<true, NC>(s_fb, s_fa, N, nb, s_tw, false, tid, NT));
+#pragma unroll
+        for (int c = 0; c < UPT; ++c) {
+            const int u = tid + c * 256;
+            if (u >= L || tid >= NT) continue;
+            for (int fi = 0; fi < nb; ++fi) {
+                const int jj = f0 + fi;
+                const float* yf = ytd + (size_t)fi * 2 * N + u;
+                const float y0 = yf[0] * sc, y1 = yf[L] * sc, y2 = yf[2 * L] * sc, y3 = yf[3 * L] * sc;
+                const float o = 0.5f * (y0 + st[c][0]);
+                st[c][0] = st[c][1] + y1;
+                st[c][1] = st[c][2] + y2;
+                st[c][2] = y3;
+                if (jj >= 3) {
+                    outp[(long)jj * L + u] = o;
+                } else if (jj == 0) {
+                    head[0 * L + u] = y0;
+                    head[1 * L + u] = y1;
+                    head[2 * L + u] = y2;
+                } else if (jj == 1) {
+                    head[3 * L + u] = y0;
+                    head[4 * L + u] = y1;
+                } else {
+                    head[5 * L + u] = y0;
+                }
+            }
+        }
+        __syncthreads();  // ytd / s_fb free for the next batch
+    }
+    float* stt = p.tstate + (s * p.ntiles + tile) * 3 * L;
+#pragma unroll
+    for (int c = 0; c < UPT; ++c) {
+        const int u = tid + c * 256;
+        if (u >= L) continue;
+        stt[u] = st[c][0];
+        stt[L + u] = st[c][1];
+        stt[2 * L + u] = st[c][2];
+    }
+}
+
+// First three outputs of every tile: the overlap-add recurrence of engine.cpp:97-102 continued
+// from the carry after the previous tile (tile 0: the engine's carry from the previous call),
+// in the order the sequential kernels evaluate it. Tile 0's threads also hand the last tile's
+// carry and the last input hop (history) to the next call.
+__global__ void wide_fixup_kernel(const WideParams p) {
+    const int L = p.L;
+    const long total = (long)p.S * p.ntiles * L;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const int u = (int)(i % L);
+        const int tile = (int)((i / L) % p.ntiles);
+        const long s = i / ((long)L * p.ntiles);
+        const float* A = tile == 0 ? p.ola + s * 3 * L : p.tstate + (s * p.ntiles + tile - 1) * 3 * L;
+        const float A0 = A[u], A1 = A[L + u], A2 = A[2 * L + u];
+        const float* h = p.thead + (s * p.ntiles + tile) * 6 * L;
+        const float o0 = 0.5f * (h[u] + A0);
+        const float b0 = A1 + h[L + u];
+        const float b1 = A2 + h[2 * L + u];
+        const float o1 = 0.5f * (h[3 * L + u] + b0);
+        const float c0 = b1 + h[4 * L + u];
+        const float o2 = 0.5f * (h[5 * L + u] + c0);
+        float* o = p.out + s * p.out_stride + (long)p.tile0[tile] * L + u;
+        o[0] = o0;
+        o[L] = o1;
+        o[2 * L] = o2;
+        if (tile == 0) {
+            const float* last = p.tstate + (s * p.ntiles + p.ntiles - 1) * 3 * L;
+            float* C = p.ola + s * 3 * L;
+            C[u] = last[u];
+            C[L + u] = last[L + u];
+            C[2 * L + u] = last[2 * L + u];
+            p.hist[s * L + u] = p.in[s * p.in_stride + (long)(p.n - 1) * L + u];
+        }
+    }
+}
+
+int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+int grid_cap(long work, int threads) {
+    const long g = (work + threads - 1) / threads;
+    return (int)std::max<long>(1, std::min<long>(g, (long)sm_count() * 16));
+}
+
+template <int NC>
+cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1,
+                          int parts) {
+    cudaError_t err;
+    if (parts & 1) {
+        wide_head_kernel<<<grid_cap((long)p.S * 2 * (p.M + 2) * (NC / 2), 256), 256, 0, stream>>>(p);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        static const int f_env = [] { const char* v = std::getenv("TVOLAP_WIDE_F"); return v ? std::atoi(v) : 0; }();
+        const int F = f_env > 0 ? f_env : std::max(1, std::min(8, 4096 / NC));
+        const size_t smem = a16(NC * sizeof(float2)) + a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) +
+                            2 * (size_t)F * NC * sizeof(float2);
+        if ((err = cudaFuncSetAttribute(wide_forward_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem)) != cudaSuccess)
+            return err;
+        wide_forward_kernel<NC><<<dim3((unsigned)((p.n + F - 1) / F), (unsigned)p.S), 256, smem, stream>>>(p, F);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    if (parts & 2) {
+        auto kern = JH == 8 ? wide_mac_kernel<NC, 8> : wide_mac_kernel<NC, 4>;
+        const size_t smem = WideLayout(NC, 2 * JH).total;
+        if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+            return err;
+        if (t0) cudaEventRecord(t0, stream);
+        kern<<<dim3((unsigned)p.ntiles, (unsigned)p.S), 256, smem, stream>>>(p);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (t1) cudaEventRecord(t1, stream);
+        wide_fixup_kernel<<<grid_cap((long)p.S * p.ntiles * p.L, 256), 256, 0, stream>>>(p);
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    return cudaSuccess;
+}
+
+template <int NC>
+cudaError_t launch_partition_multi_t(int M, int S, long rows, const float* const* irs, long ir_len, float2* pool,
+                                     const float2* tw, const float2* pk, cudaStream_t stream) {
+    constexpr int kWarps = 8;
+    const size_t smem = a16((NC + 2) * sizeof(float2)) + (size_t)kWarps * NC * sizeof(float2);
+    cudaError_t err = cudaFuncSetAttribute(partition_multi_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+    if (err != cudaSuccess) return err;
+    int per_sm = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, partition_multi_kernel<NC>, 32 * kWarps, smem);
+    if (err != cudaSuccess) return err;
+    const long tasks = rows * M;
+    const long grid = std::max<long>(1, std::min<long>((tasks + kWarps - 1) / kWarps,
+                                                       (long)sm_count() * std::max(1, per_sm)));
+    partition_multi_kernel<NC><<<(unsigned)grid, 32 * kWarps, smem, stream>>>(M, S, rows, irs, ir_len, pool, tw, pk);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool wide_supported(int L) {
+    const int N = 2 * L;
+    return N == 64 || N == 128 || N == 256 || N == 512 || N == 1024;
+}
+
+size_t wide_mac_smem_bytes(int L, int JH) { return WideLayout(2 * L, 2 * JH).total; }
+
+cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1, int parts) {
+    switch (2 * p.L) {
+        case 64: return launch_wide_t<64>(p, JH, stream, t0, t1, parts);
+        case 128: return launch_wide_t<128>(p, JH, stream, t0, t1, parts);
+        case 256: return launch_wide_t<256>(p, JH, stream, t0, t1, parts);
+        case 512: return launch_wide_t<512>(p, JH, stream, t0, t1, parts);
+        case 1024: return launch_wide_t<1024>(p, JH, stream, t0, t1, parts);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_partition_multi(int L, int M, int S, long rows, const float* const* irs, long ir_len, float2* pool,
+                                   const float2* tw, const float2* pk, cudaStream_t stream) {
+    switch (2 * L) {
+        case 64: return launch_partition_multi_t<64>(M, S, rows, irs, ir_len, pool, tw, pk, stream);
+        case 128: return launch_partition_multi_t<128>(M, S, rows, irs, ir_len, pool, tw, pk, stream);
+        case 256: return launch_partition_multi_t<256>(M, S, rows, irs, ir_len, pool, tw, pk, stream);
+        case 512: return launch_partition_multi_t<512>(M, S, rows, irs, ir_len, pool, tw, pk, stream);
+        case 1024: return launch_partition_multi_t<1024>(M, S, rows, irs, ir_len, pool, tw, pk, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace tvb

@@ -1,0 +1,122 @@
+"""Time-parallel pass (csrc/tvolap_wide.cu): a device-resident tvolap_process_switching call run
+as K4-for-all-sets + K1-for-all-hops + (lane, tile) MAC/inverse CTAs + OLA fix-up must equal the
+exchange_filter + process_hops loop it stands for (hop-blocked kernel), bit for bit, and leave the
+engine in the same state (delay line, carry, history, active set)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2310_00319_b200 import tvolap as T
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(hop, S, taps, n_hops, period, none_at=(), seed=0):
+    import torch
+
+    g = np.random.default_rng(seed)
+    nsw = -(-n_hops // period)
+    irs = [None if k in none_at else g.standard_normal((S, taps)).astype(np.float32) * 0.05 for k in range(nsw)]
+    ir0 = g.standard_normal((taps, S)) * 0.05
+    x = torch.from_numpy(g.uniform(-1, 1, (S, n_hops * hop)).astype(np.float32)).cuda()
+    dirs = [None if ir is None else torch.from_numpy(ir).cuda() for ir in irs]
+    return ir0, x, dirs
+
+
+def _loop(eng, x, dirs, period, hop):
+    import torch
+
+    n = x.shape[1] // hop
+    out = torch.empty_like(x)
+    for k in range(-(-n // period)):
+        if dirs[k] is not None:
+            eng.exchange_ir(dirs[k])
+        sl = slice(k * period * hop, min(n, (k + 1) * period) * hop)
+        eng.process_hops(x[:, sl], out=out[:, sl])
+    return out
+
+
+def _engines(monkeypatch, ir0, hop):
+    monkeypatch.setenv("TVOLAP_WIDE", "2")
+    a = T.TvolapEngine(T.partition(ir0, hop))
+    monkeypatch.setenv("TVOLAP_WIDE", "0")
+    b = T.TvolapEngine(T.partition(ir0, hop))
+    monkeypatch.delenv("TVOLAP_WIDE")
+    return a, b
+
+
+@pytest.mark.parametrize("hop,S,taps,n_hops,period,none_at,pre", [
+    (256, 5, 4096, 16 * 9, 16, (2,), 3),      # C2 geometry, odd start hop, one period without a switch
+    (256, 3, 4096, 16 * 6 + 7, 16, (), 0),    # ragged final period (7 hops), first call
+    (256, 3, 3000, 61, 10, (), 5),            # final period of 1 hop -> hop-blocked tail
+    (256, 2, 4096, 100, 40, (1,), 2),         # 40-hop periods -> three tiles each
+    (256, 2, 4096, 45, 3, (), 1),             # 3-hop periods (shortest tile)
+    (128, 4, 2048, 150, 64, (), 4),           # N = 256, C1-like period
+    (512, 2, 8192, 48, 8, (0,), 3),           # N = 1024, no switch at the first hop
+    (32, 6, 1024, 90, 17, (), 2),             # N = 64, M = 16
+    (64, 3, 8192, 70, 16, (), 1),             # N = 128, M = 64 (long history: ring wraps)
+])
+def test_wide_equals_exchange_loop(monkeypatch, hop, S, taps, n_hops, period, none_at, pre):
+    ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at)
+    a, b = _engines(monkeypatch, ir0, hop)
+    if pre:
+        a.process_hops(x[:, : pre * hop])
+        b.process_hops(x[:, : pre * hop])
+    ya = a.process_switching(x, dirs, period)
+    yb = _loop(b, x, dirs, period, hop)
+    a.synchronize()
+    b.synchronize()
+    assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+    # state handed to the next calls: delay line, carry, history and the active set
+    za, zb = a.process_hops(x[:, : 40 * hop]), b.process_hops(x[:, : 40 * hop])
+    a.synchronize()
+    b.synchronize()
+    assert np.array_equal(za.cpu().numpy(), zb.cpu().numpy())
+    assert a.op_counts() == b.op_counts()
+
+
+def test_wide_chunked_pool(monkeypatch):
+    """A pool budget of one set per chunk: every period is its own pass."""
+    hop, S, taps, n, period = 256, 4, 4096, 16 * 7 + 5, 16
+    ir0, x, dirs = _case(hop, S, taps, n, period, none_at=(3,))
+    a, b = _engines(monkeypatch, ir0, hop)
+    monkeypatch.setenv("TVOLAP_WIDE_POOL_MB", "1")
+    ya = a.process_switching(x, dirs, period)
+    yb = _loop(b, x, dirs, period, hop)
+    a.synchronize()
+    b.synchronize()
+    assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+
+
+def test_wide_back_to_back_calls(monkeypatch):
+    """Consecutive switching calls (the bench's step loop) hand the state over bit-exactly."""
+    hop, S, taps, n, period = 256, 3, 4096, 64, 16
+    ir0, x, dirs = _case(hop, S, taps, n, period)
+    a, b = _engines(monkeypatch, ir0, hop)
+    for _ in range(3):
+        ya = a.process_switching(x, dirs, period)
+        yb = _loop(b, x, dirs, period, hop)
+        a.synchronize()
+        b.synchronize()
+        assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+
+
+def test_wide_matches_oracle(monkeypatch):
+    hop, S, taps, n, period = 128, 2, 4096, 80, 16
+    ir0, x, dirs = _case(hop, S, taps, n, period)
+    monkeypatch.setenv("TVOLAP_WIDE", "2")
+    eng_g = T.TvolapEngine(T.partition(ir0, hop))
+    y = eng_g.process_switching(x, dirs, period)
+    eng_g.synchronize()
+    y = y.cpu().numpy()
+    xs = x.cpu().numpy().astype(np.float64)
+    eng = O.Engine(O.partition(ir0.astype(np.float32).astype(np.float64), hop))
+    ref = []
+    for h in range(n):
+        if h % period == 0 and dirs[h // period] is not None:
+            eng.exchange_filter(O.partition(dirs[h // period].cpu().numpy().T.astype(np.float64), hop,
+                                            eng.partition_count()))
+        ref.append(eng.process(xs[:, h * hop:(h + 1) * hop].T))
+    ref = np.concatenate(ref).T
+    err = np.max(np.abs(y - ref)) / np.max(np.abs(ref))
+    assert err <= 1e-4, err  # north-star tolerance (fp32 vs the fp64 reference algorithm)
