@@ -680,8 +680,8 @@ int tvolap_create(tvolap_engine** out, int device, long hop, long channels, long
         try {
             init_common(e, device, hop, channels, 1, M);
             const size_t slot = (size_t)channels * M * e->N;
-            e->pool = dalloc<float2>(kSlots * slot);
-            CK(cudaMemsetAsync(e->pool, 0, kSlots * slot * sizeof(float2), e->stream));
+            e->pool = dalloc<float2>(kSlots * slot + (size_t)tvb::kWideTail * e->N);  // + rows read by wide prefetches
+            CK(cudaMemsetAsync(e->pool, 0, (kSlots * slot + (size_t)tvb::kWideTail * e->N) * sizeof(float2), e->stream));
             const float* src = stage_ir(e, ir, (size_t)channels * ir_length, e->stream);
             CK(tvb::launch_partition((int)hop, (int)M, channels, src, ir_length, ir_length, e->pool, 0, e->tw, e->pk,
                                      e->stream));
@@ -823,7 +823,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     }
     latch(e);
     int JH = 8;
-    if (tvb::wide_mac_smem_bytes((int)L, JH) > 227 * 1024) JH = 4;
+    if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
     const long Jmax = 2 * JH;
     const size_t set_elems = (size_t)S * M * N;
     const long budget_mb = env_int("TVOLAP_WIDE_POOL_MB", 8192);
@@ -838,7 +838,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         for (long k = k0; k < k1; ++k)
             if (irs[k]) tab.push_back(irs[k]);
         if (nsets) {
-            ensure_dev(e->wide_pool, e->wide_pool_cap, (size_t)nsets * set_elems);
+            ensure_dev(e->wide_pool, e->wide_pool_cap, (size_t)nsets * set_elems + (size_t)tvb::kWideTail * N);
             ensure_dev(e->d_wide_irs, e->wide_sw_cap, (size_t)nsets);
             CK(cudaMemcpyAsync(e->d_wide_irs, tab.data(), sizeof(const float*) * nsets, cudaMemcpyHostToDevice,
                                e->stream));
@@ -871,7 +871,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         // carry and head terms per tile, extended spectra
         ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * ntiles * 3 * L);
         ensure_dev(e->wide_head, e->wide_head_cap, (size_t)S * ntiles * 6 * L);
-        const long T = (nh + 1) / 2 + M + JH + 4;
+        const long T = (nh + 1) / 2 + M + tvb::kWideFront + JH + 4;
         ensure_dev(e->wide_xe, e->wide_xe_cap, (size_t)S * 2 * T * N);
         tvb::WideParams p{};
         p.L = (int)L;
@@ -888,7 +888,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         p.ring = e->ring;
         p.xe = e->wide_xe;
         p.T = T;
-        p.tbase = (e->hops >> 1) - M;
+        p.tbase = (e->hops >> 1) - M - tvb::kWideFront;
         p.hist = e->hist;
         p.ola = e->ola;
         p.tw = e->tw;

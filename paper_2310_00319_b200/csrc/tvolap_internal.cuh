@@ -59,7 +59,7 @@ struct WideParams {
     float2* ring;          // delay line [S][2][D][2L]: read before the pass, its last 2D hops written
     float2* xe;            // extended spectra [S][2][T][2L]: slot t of parity p = hop 2 (t + tbase) + p
     long T;
-    long tbase;            // (hop0 >> 1) - M
+    long tbase;            // (hop0 >> 1) - M - kWideFront
     float* hist;           // [S][L]
     float* ola;            // [S][3L]
     const float2* tw;
@@ -72,7 +72,9 @@ struct WideParams {
     float* thead;               // first-three-output terms of each tile [S][ntiles][6][L]
 };
 bool wide_supported(int L);
-size_t wide_mac_smem_bytes(int L, int JH);
+size_t wide_mac_smem_bytes(int L, int JH, int M, int Q);
+constexpr int kWideFront = 8;   // Xe front padding slots per parity (tbase = (hop0 >> 1) - M - kWideFront)
+constexpr int kWideTail = 8;    // spectra rows readable past the end of every filter set (prefetch)
 // parts: 1 = head copy + forward FFTs, 2 = MAC/inverse tiles (+ fix-up); events bracket the tiles
 cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1, int parts);
 // K4 for rows = sets * S IRs: irs[row / S] + (row % S) * ir_len -> pool[(row * M + m) * 2L]

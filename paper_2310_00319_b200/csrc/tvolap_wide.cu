@@ -32,11 +32,12 @@ namespace {
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
+
 // Delay-line history of the call: Xe[s][parity][t] holds the spectrum of hop j with
 // j & 1 == parity and t = (j >> 1) - tbase, for every hop the call's outputs read.
 __global__ void wide_head_kernel(const WideParams p) {
     const int N = 2 * p.L, V = N / 2;
-    const int nh = p.M + 2;  // slots per parity that can precede hop0
+    const int nh = p.M + 2 + kWideFront;  // slots per parity that can precede hop0
     const long total = (long)p.S * 2 * nh * V;
     const float4* ring4 = reinterpret_cast<const float4*>(p.ring);
     float4* xe4 = reinterpret_cast<float4*>(p.xe);
@@ -146,15 +147,21 @@ __global__ void __launch_bounds__(256, 2) partition_multi_kernel(int M, int S, l
 
 constexpr int kWideFB = 4;  // frames per inverse-FFT batch
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+}
+
 struct WideLayout {
-    size_t tw, pk, y, fa, fb, total;
-    __host__ __device__ WideLayout(int N, int J) {
+    size_t tw, pk, y, fa, fb, aux, total;
+    __host__ __device__ WideLayout(int N, int J, int M, int Q) {
         tw = 0;
         pk = a16(tw + N * sizeof(float2));
         y = a16(pk + (N + 2) * sizeof(float2));
         fa = a16(y + (size_t)J * N * sizeof(float2));
         fb = a16(fa + (size_t)kWideFB * N * sizeof(float2));
-        total = a16(fb + (size_t)kWideFB * N * sizeof(float2));
+        aux = a16(fb + (size_t)kWideFB * N * sizeof(float2));  // bin-0 Nyquist chains (K3)
+        total = a16(aux + (size_t)(3 * M + J + Q * J) * sizeof(float));
     }
 };
 
@@ -166,7 +173,7 @@ template <int NC, int JH>
 __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     constexpr int N = NC, L = NC / 2, J = 2 * JH;
     extern __shared__ __align__(16) unsigned char smem[];
-    const WideLayout lay(N, J);
+    const WideLayout lay(N, J, p.M, p.Q);
     float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
     float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
     float2* s_y = reinterpret_cast<float2*>(smem + lay.y);
@@ -181,7 +188,11 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     for (int i = tid; i < N; i += NT) s_tw[i] = p.tw[i];
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
 
-    // ---- K3: thread per packed bin k, both parity groups (outputs l0 + g + 2i), JH each
+    // ---- K3: thread per packed bin k, both parity groups (outputs l0 + g + 2i), JH each.
+    // The m loop is unrolled by JH so the sliding window rotates by register renaming (output i
+    // at unrolled step u reads win[(i - u) mod JH]); loads run kPf steps ahead in registers.
+    // Partition-group partials accumulate in the thread's own column of s_y (rows = outputs).
+    constexpr int kPf = 2;  // divides JH
     const float2* H = p.fset[tile] + s * M * N;
     const float2* X[2];
     long bse[2];
@@ -190,92 +201,129 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
         X[g] = p.xe + (s * 2 + ((l0 + g) & 1)) * p.T * N;
         bse[g] = ((l0 + g) >> 1) - p.tbase;  // t of output i = bse + i, of its partition-m input bse + i - m
     }
+    // Packed bin 0 = (Re X_0, Re X_N) also needs the Nyquist products sum_m Im H . Im X (the hop
+    // kernels' aux chain beside the complex one): warp 0 stages Im H[m][0] and Im X[g][t][0] in
+    // shared memory and runs the Q x 2 x JH sequential fmaf chains, one per lane.
+    float* s_auxh = reinterpret_cast<float*>(smem + lay.aux);
+    float* s_auxx = s_auxh + M;                 // [2][M + JH]: t = bse - M + j
+    float* s_auxr = s_auxx + 2 * (M + JH);      // [Q][2][JH]
+    if (tid < 32) {
+        for (int j = tid; j < M; j += 32) s_auxh[j] = __ldcg(H + (long)j * N).y;
+        for (int j = tid; j < 2 * (M + JH); j += 32) {
+            const int g = j >= M + JH, jj = j - g * (M + JH);
+            s_auxx[j] = __ldcg((g ? X[1] + (bse[1] - M) * N : X[0] + (bse[0] - M) * N) + (long)jj * N).y;
+        }
+        __syncwarp();
+        for (int c = tid; c < Q * 2 * JH; c += 32) {
+            const int qq = c / (2 * JH), g = (c / JH) & 1, i = c % JH;
+            const int mu0 = (int)((long)qq * M / Q), mu1 = (int)((long)(qq + 1) * M / Q);
+            float aux = 0.f;
+            for (int mm = mu0; mm < mu1; ++mm) aux = fmaf(s_auxh[mm], s_auxx[g * (M + JH) + M + i - mm], aux);
+            s_auxr[c] = aux;
+        }
+        __syncwarp();
+    }
     for (int k = tid; k < N; k += NT) {
-        const bool pkw = __any_sync(0xffffffffu, k == 0);
-        auto mac = [&](auto pk_tag) {
-            constexpr bool PK = decltype(pk_tag)::value;
-            for (int qq = 0; qq < Q; ++qq) {
-                const int mu0 = (int)((long)qq * M / Q), mu1 = (int)((long)(qq + 1) * M / Q);
-                float2 acc[2][JH];
-                float aux[2][PK ? JH : 1];
-                float2 win[2][JH];
-                long cur[2];
+        float2* col = s_y + k;  // this bin's outputs (rows jj), partition-group partials first
+        for (int qq = 0; qq < Q; ++qq) {
+            const int mu0 = (int)((long)qq * M / Q), mu1 = (int)((long)(qq + 1) * M / Q);
+            float2 acc[2][JH];
+            float2 win[2][JH];
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int i = 0; i < JH; ++i) {
+                    acc[g][i] = make_float2(0.f, 0.f);
+                    win[g][i] = __ldcg(X[g] + (bse[g] + i - mu0) * N + k);
+                }
+            // step m reads X[g][bse - m - 1] (the window's next entry) and H[m]; prefetches past
+            // mu1 read padding (Xe front slots, pool tail rows) and are never used
+            const float2* px0 = X[0] + (bse[0] - mu0 - 1) * N + k;
+            const float2* px1 = X[1] + (bse[1] - mu0 - 1) * N + k;
+            const float2* ph = H + (long)mu0 * N + k;
+            float2 f0[kPf], f1[kPf], fh[kPf];
+#pragma unroll
+            for (int u = 0; u < kPf; ++u) {
+                f0[u] = __ldcg(px0 - (long)u * N);
+                f1[u] = __ldcg(px1 - (long)u * N);
+                fh[u] = __ldcg(ph + (long)u * N);
+            }
+            px0 -= (long)kPf * N;
+            px1 -= (long)kPf * N;
+            ph += (long)kPf * N;
+            auto step = [&](auto u_tag) {
+                constexpr int u = decltype(u_tag)::value;
+                constexpr int sl = u % kPf;
+                const float2 x0 = f0[sl], x1 = f1[sl], h = fh[sl];
+                f0[sl] = __ldcg(px0);
+                f1[sl] = __ldcg(px1);
+                fh[sl] = __ldcg(ph);
+                px0 -= N;
+                px1 -= N;
+                ph += N;
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
-                    cur[g] = bse[g] - mu0 - 1;
 #pragma unroll
                     for (int i = 0; i < JH; ++i) {
-                        acc[g][i] = make_float2(0.f, 0.f);
-                        if constexpr (PK) aux[g][i] = 0.f;
-                        win[g][i] = __ldcg(X[g] + (bse[g] + i - mu0) * N + k);
+                        float2& a = acc[g][i];
+                        const float2 x = win[g][(i - u) & (JH - 1)];
+                        a.x = fmaf(h.x, x.x, a.x);
+                        a.x = fmaf(-h.y, x.y, a.x);
+                        a.y = fmaf(h.x, x.y, a.y);
+                        a.y = fmaf(h.y, x.x, a.y);
                     }
                 }
-                auto mac_step = [&](const float2 (&xn)[2], const float2 h) {
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) {
-#pragma unroll
-                        for (int i = 0; i < JH; ++i) {
-                            float2& a = acc[g][i];
-                            const float2 x = win[g][i];
-                            a.x = fmaf(h.x, x.x, a.x);
-                            a.x = fmaf(-h.y, x.y, a.x);
-                            a.y = fmaf(h.x, x.y, a.y);
-                            a.y = fmaf(h.y, x.x, a.y);
-                            if constexpr (PK) aux[g][i] = fmaf(h.y, x.y, aux[g][i]);
-                        }
-#pragma unroll
-                        for (int i = JH - 1; i > 0; --i) win[g][i] = win[g][i - 1];
-                        win[g][0] = xn[g];
-                    }
-                };
-                int m = mu0;
-                constexpr int U = 4;
-                for (; m + U <= mu1; m += U) {
-                    float2 xn[U][2], hh[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-#pragma unroll
-                        for (int g = 0; g < 2; ++g) xn[u][g] = __ldcg(X[g] + (cur[g] - u) * N + k);
-                        hh[u] = __ldcg(H + (long)(m + u) * N + k);
-                    }
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) cur[g] -= U;
-#pragma unroll
-                    for (int u = 0; u < U; ++u) mac_step(xn[u], hh[u]);
+                win[0][(JH - 1 - u) & (JH - 1)] = x0;  // replaces the entry output JH-1 just used
+                win[1][(JH - 1 - u) & (JH - 1)] = x1;
+            };
+            int m = mu0;
+            for (; m + JH <= mu1; m += JH) {
+                step(std::integral_constant<int, 0>{});
+                step(std::integral_constant<int, 1>{});
+                step(std::integral_constant<int, 2>{});
+                step(std::integral_constant<int, 3>{});
+                if constexpr (JH == 8) {
+                    step(std::integral_constant<int, 4>{});
+                    step(std::integral_constant<int, 5>{});
+                    step(std::integral_constant<int, 6>{});
+                    step(std::integral_constant<int, 7>{});
                 }
-                for (; m < mu1; ++m) {
-                    float2 xn[2];
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) xn[g] = __ldcg(X[g] + (cur[g]--) * N + k);
-                    mac_step(xn, __ldcg(H + (long)m * N + k));
-                }
+            }
+            const int rem = mu1 - m;  // < JH: the same unrolled steps, cut short
+            if (rem > 0) step(std::integral_constant<int, 0>{});
+            if (rem > 1) step(std::integral_constant<int, 1>{});
+            if (rem > 2) step(std::integral_constant<int, 2>{});
+            if constexpr (JH == 8) {
+                if (rem > 3) step(std::integral_constant<int, 3>{});
+                if (rem > 4) step(std::integral_constant<int, 4>{});
+                if (rem > 5) step(std::integral_constant<int, 5>{});
+                if (rem > 6) step(std::integral_constant<int, 6>{});
+            }
+            if (k == 0) {  // packed bin 0: two real products
 #pragma unroll
                 for (int g = 0; g < 2; ++g)
 #pragma unroll
                     for (int i = 0; i < JH; ++i) {
-                        const int jj = g + 2 * i;
-                        if (jj >= jt) continue;
-                        float2 a = acc[g][i];
-                        if constexpr (PK) {
-                            if (k == 0) {  // packed bin 0: two real products
-                                a.x += aux[g][i];
-                                a.y = aux[g][i];
-                            }
-                        }
-                        float2* y = s_y + (size_t)jj * N + k;
-                        if (qq == 0) {
-                            *y = a;
-                        } else {
-                            const float2 t = *y;
-                            *y = make_float2(t.x + a.x, t.y + a.y);
-                        }
+                        const float a = s_auxr[(qq * 2 + g) * JH + i];
+                        acc[g][i].x += a;
+                        acc[g][i].y = a;
                     }
             }
-        };
-        if (pkw)
-            mac(std::true_type{});
-        else
-            mac(std::false_type{});
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int i = 0; i < JH; ++i) {
+                    const int jj = g + 2 * i;
+                    if (jj >= jt) continue;
+                    float2* y = col + (size_t)jj * N;
+                    if (qq == 0) {
+                        *y = acc[g][i];
+                    } else {
+                        const float2 t = *y;
+                        *y = make_float2(t.x + acc[g][i].x, t.y + acc[g][i].y);
+                    }
+                }
+        }
     }
     __syncthreads();
 
@@ -400,7 +448,7 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
     }
     if (parts & 2) {
         auto kern = JH == 8 ? wide_mac_kernel<NC, 8> : wide_mac_kernel<NC, 4>;
-        const size_t smem = WideLayout(NC, 2 * JH).total;
+        const size_t smem = WideLayout(NC, 2 * JH, p.M, p.Q).total;
         if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
             return err;
         if (t0) cudaEventRecord(t0, stream);
@@ -438,7 +486,7 @@ bool wide_supported(int L) {
     return N == 64 || N == 128 || N == 256 || N == 512 || N == 1024;
 }
 
-size_t wide_mac_smem_bytes(int L, int JH) { return WideLayout(2 * L, 2 * JH).total; }
+size_t wide_mac_smem_bytes(int L, int JH, int M, int Q) { return WideLayout(2 * L, 2 * JH, M, Q).total; }
 
 cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1, int parts) {
     switch (2 * p.L) {
