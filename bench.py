@@ -4,8 +4,10 @@
 metric: convolved channel-samples/s. Workload: BASELINE config C2 (configs[1]):
 64 independent channels, fp32, L=256, M=64 (IR 32768 taps), each channel
 switching to a freshly seeded IR every 16 blocks, 30 s of white noise per
-channel = 5625 hops. One step = one full 30 s pass from zero state: 352
-exchange_filter + process_hops(16 hops) calls on device-resident inputs.
+channel = 5625 hops. One step = one full 30 s pass from zero state: the 352
+exchange_filter + process_hops(16 hops) drive() loop as one tvolap_process_switching
+call on device-resident inputs (run as a time-parallel pass: K4 of all 352 sets,
+K1 of all hops, one MAC/inverse CTA per (channel, 16-hop period)).
 Multi-GPU (torchrun): one process per GPU, each rank runs its own 64 channels
 (lanes rank*64 ..), no data-path collective — weak scaling; time = max over
 ranks of CUDA-event time.
@@ -251,7 +253,8 @@ def main():
         e.reset()
         if cfg.mode == "fresh":
             # the drive() loop (exchange before every period's hops) as one call:
-            # device-resident -> one hop-blocked launch with in-kernel K4; host -> the loop itself
+            # device-resident -> the time-parallel pass (few channels) or one hop-blocked launch with
+            # in-kernel K4; pinned host buffers -> the chunked H2D / launch / D2H pipeline
             e.process_switching(xs, [ir_set[k % n_pool] for k in range(n_sw)], cfg.period, out=outs)
         else:
             e.process_hops(xs, out=outs, schedule=sch)
@@ -273,6 +276,7 @@ def main():
         step(eng, x, out, irs, sched)
     barrier()
     launches0 = eng.kernel_launches()
+    wide0 = eng.wide_passes() if hasattr(eng, "wide_passes") else 0
     clocks = Clocks(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -283,6 +287,7 @@ def main():
     clk = clocks.stop()
     elapsed = ev0.elapsed_time(ev1)
     gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
+    wide = (eng.wide_passes() - wide0 if hasattr(eng, "wide_passes") else 0) > 0
     # Per-launch kernel durations: a second pass of the same steps with CUDA events around every
     # hop launch on the engine stream. Timing events serialise the programmatic-dependent-launch
     # chain (K4 -> hop launch overlap), so they stay out of the timed region above.
@@ -323,16 +328,27 @@ def main():
                 else sj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    if wide:  # time-parallel pass: the MAC/inverse launch dominates; K4 and K1 are separate launches
+        kname = (f"wide_mac_kernel (K3+K5+OLA, one CTA per (channel, <=16-hop tile)), {hops_per_launch:g} hops x {S} "
+                 "sources per launch; K4 of all the pass's sets (partition_multi_kernel) and K1 of all its hops "
+                 "(wide_forward_kernel) run as separate launches outside this kernel's time")
+    else:
+        kname = (f"tvolap_block_kernel (K1-K5 fused{', K4 for the next switch in the barrier gaps' if cfg.mode == 'fresh' else ''}), "
+                 f"{hops_per_launch:g} hops x {S} sources per launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "peak_source": peak_src,
-                "kernel": f"tvolap_block_kernel (K1-K5 fused{', K4 for the next switch in the barrier gaps' if cfg.mode == 'fresh' else ''}), "
-                          f"{hops_per_launch:g} hops x {S} sources per launch",
+                "kernel": kname,
+                "pass_achieved": bytes_hop * H / (ms_per_step / 1e3) / 1e9,
                 "avg_launch_ms": avg_launch_ms, "launches": kern_n, "bytes_per_hop": bytes_hop,
                 "bytes_per_launch": bytes_launch, "distinct_filters_per_hop": distinct,
                 "kernel_share_of_step": kern_ms / prof_elapsed if prof_elapsed else None,
                 "timing": f"avg launch from a separate event-instrumented pass of {prof_steps} step(s) "
                           "(share = kernel time / that pass's elapsed)"}
-    if cfg.name in ("C1", "C2"):
+    if wide:
+        roofline["note"] = ("algorithmic bytes (SURVEY 8d: every output re-reads M delay-line spectra and M filter "
+                            "spectra) over the MAC launch's time; the kernel reads each spectrum once per 16-hop tile, "
+                            "so frac can exceed 1; pass_achieved = the same bytes over the whole step (all launches)")
+    elif cfg.name in ("C1", "C2"):
         roofline["note"] = "delay line + filter pool are L2-resident in this config, so frac vs HBM can exceed 1"
 
     # ---- e2e through the public API with pinned host buffers (H2D inputs [+ IRs], D2H outputs)

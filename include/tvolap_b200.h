@@ -192,6 +192,12 @@ int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block
 /* Number of kernels this engine has launched since creation. */
 uint64_t tvolap_kernel_launches(const tvolap_engine* e);
 
+/* Time-parallel passes run so far: device-resident tvolap_process_switching calls executed as
+   K4-for-all-sets + K1-for-all-hops + (lane, hop-tile) MAC/inverse CTAs (a diagnostic of which
+   path a call took; outputs equal the hop-blocked path bit for bit). TVOLAP_WIDE=0 disables it,
+   TVOLAP_WIDE=2 forces it wherever it is supported. */
+uint64_t tvolap_wide_passes(const tvolap_engine* e);
+
 /* ------------------------------------------------------ spectral primitives */
 /* Batched K1/K5 building blocks, exposed so the reference's spectral tests
  * (proj/tests/test_spectral.cpp) run against the device FFT. */

@@ -207,6 +207,7 @@ struct tvolap_engine {
     size_t wide_xe_cap = 0, wide_pool_cap = 0, wide_tile_cap = 0, wide_fset_cap = 0, wide_sw_cap = 0;
     size_t wide_state_cap = 0, wide_head_cap = 0;
     int wide_mode = 1;               // TVOLAP_WIDE: 0 off, 1 auto, 2 whenever supported
+    uint64_t wide_passes = 0;
     // chunked host pipeline
     long chunk_hops = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
@@ -903,6 +904,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         prof_pair(e, &ev0, &ev1);
         CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
         e->launches += 4;
+        ++e->wide_passes;
         e->hops += nh;
         if (nsets) {  // the chunk's last set becomes the engine's active set (a pool slot)
             const int slot = (e->active + 1) % kSlots;
@@ -1316,6 +1318,8 @@ int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block
 }
 
 uint64_t tvolap_kernel_launches(const tvolap_engine* e) { return e ? e->launches : 0; }
+
+uint64_t tvolap_wide_passes(const tvolap_engine* e) { return e ? e->wide_passes : 0; }
 
 // ------------------------------------------------------------------ spectral primitives
 namespace {

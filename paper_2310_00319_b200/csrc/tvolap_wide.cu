@@ -58,64 +58,81 @@ __global__ void wide_head_kernel(const WideParams p) {
     }
 }
 
-// K1 for frames hop0 + blockIdx.x * F + f of lane blockIdx.y (engine.cpp:77-82): the operations
-// of the hop-blocked kernel's forward phase (window products, fft_batch, untangle_store).
+// K1 for every hop of the pass (engine.cpp:77-82): the operations of the hop-blocked kernel's
+// forward phase (window products, fft_batch, untangle_store). Persistent CTAs walk work items
+// (lane, kFwdF consecutive frames); the raw input of the next item (kFwdF + 1 hops, the first
+// one being the previous hop) is loaded into registers while the current item's FFTs run.
+constexpr int kFwdF = 4;
+
 template <int NC>
-__global__ void __launch_bounds__(256) wide_forward_kernel(const WideParams p, int F) {
-    constexpr int N = NC, L = NC / 2;
+__global__ void __launch_bounds__(256) wide_forward_kernel(const WideParams p) {
+    constexpr int N = NC, L = NC / 2, F = kFwdF, SPAN = (F + 1) * L, PER = (SPAN + 255) / 256;
     extern __shared__ __align__(16) unsigned char smem[];
     float2* s_tw = reinterpret_cast<float2*>(smem);
     float2* s_pk = reinterpret_cast<float2*>(smem + a16(N * sizeof(float2)));
     float* s_win = reinterpret_cast<float*>(smem + a16(N * sizeof(float2)) + a16((N + 2) * sizeof(float2)));
-    float2* s_fa = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(s_win) + a16(N * sizeof(float)));
+    float* s_x = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(s_win) + a16(N * sizeof(float)));
+    float2* s_fa = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(s_x) + a16(SPAN * sizeof(float)));
     float2* s_fb = s_fa + (size_t)F * N;
-    const int tid = threadIdx.x, NT = blockDim.x;
-    const long s = blockIdx.y;
-    const int j0 = blockIdx.x * F;
-    const int nf = min(F, p.n - j0);
+    const int tid = threadIdx.x, NT = 256;
     for (int i = tid; i < N; i += NT) {
         s_tw[i] = p.tw[i];
         s_win[i] = p.win[i];
     }
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
-    __syncthreads();  // the window products below read other threads' table entries
-    const float* xin = p.in + s * p.in_stride;
-    const float* hist = p.hist + s * L;
-    for (int i = tid; i < nf * L; i += NT) {
-        const int f = i / L, jj = i - f * L;
-        const int r = j0 + f;  // hop of the call; frame = (hop r - 1 | hop r)
-        const int e = 2 * jj;  // e, e + 1 lie in the same half (L even)
-        float x0, x1;
-        if (e < L) {
-            const float* prev = r == 0 ? hist : xin + (long)(r - 1) * L;
-            x0 = prev[e];
-            x1 = prev[e + 1];
-        } else {
-            const float* cur = xin + (long)r * L;
-            x0 = cur[e - L];
-            x1 = cur[e + 1 - L];
+    const int chunks = (p.n + F - 1) / F;
+    const long items = (long)p.S * chunks;
+    // raw samples of item w: hops r0 - 1 .. r0 + F - 1 (hop -1 of the pass = the history)
+    auto load = [&](long w, float (&v)[PER]) {
+        const long s = w / chunks;
+        const int r0 = (int)(w - s * chunks) * F;
+        const float* xin = p.in + s * p.in_stride;
+#pragma unroll
+        for (int c = 0; c < PER; ++c) {
+            const int i = tid + c * NT;
+            const int r = r0 - 1 + i / L;  // hop of the pass
+            float val = 0.f;
+            if (i < SPAN && r < p.n) val = r < 0 ? p.hist[s * L + (i % L)] : __ldcs(xin + (long)r * L + (i % L));
+            v[c] = val;
         }
-        s_fa[(size_t)f * N + jj] = make_float2(x0 * s_win[e], x1 * s_win[e + 1]);
-    }
-    __syncthreads();
-    if (nf <= 0) return;
-    const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
+    };
+    float v[PER];
+    long w = blockIdx.x;
+    if (w < items) load(w, v);
     const long ring_from = p.hop0 + p.n - 2L * p.D;  // these hops stay in the delay line after the call
-    for (int f = 0; f < nf; ++f) {
-        const long j = p.hop0 + j0 + f;
-        const int par = (int)(j & 1);
-        float2* dst = p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N;
-        untangle_store<NC>(Z + (size_t)f * N, N, s_pk, dst, tid, NT);
-        if (j >= ring_from)
-            untangle_store<NC>(Z + (size_t)f * N, N, s_pk, p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N, tid,
-                               NT);
+    for (; w < items; w += gridDim.x) {
+        const long s = w / chunks;
+        const int r0 = (int)(w - s * chunks) * F;
+        const int nf = min(F, p.n - r0);
+        __syncthreads();  // previous item's FFT buffers and s_x are free (and the tables loaded)
+#pragma unroll
+        for (int c = 0; c < PER; ++c)
+            if (tid + c * NT < SPAN) s_x[tid + c * NT] = v[c];
+        if (w + gridDim.x < items) load(w + gridDim.x, v);  // in flight during this item's FFTs
+        __syncthreads();
+        for (int i = tid; i < nf * L; i += NT) {
+            const int f = i / L, jj = i - f * L;
+            const float* xs = s_x + f * L;  // (hop r0 + f - 1 | hop r0 + f)
+            s_fa[(size_t)f * N + jj] = make_float2(xs[2 * jj] * s_win[2 * jj], xs[2 * jj + 1] * s_win[2 * jj + 1]);
+        }
+        __syncthreads();
+        const float2* Z = fft_batch<false, NC>(s_fa, s_fb, N, nf, s_tw, true, tid, NT);
+        for (int f = 0; f < nf; ++f) {
+            const long j = p.hop0 + r0 + f;
+            const int par = (int)(j & 1);
+            float2* dst = p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N;
+            untangle_store<NC>(Z + (size_t)f * N, N, s_pk, dst, tid, NT);
+            if (j >= ring_from)
+                untangle_store<NC>(Z + (size_t)f * N, N, s_pk, p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N,
+                                   tid, NT);
+        }
     }
 }
 
 // K4 for the sets a call installs: row r = k * S + s transforms irs[k] + s * ir_len into
 // pool[(r * M + m) * N] (partition.cpp:20-51). Same warp transform as partition_warp_kernel.
 template <int NC>
-__global__ void __launch_bounds__(256, 2) partition_multi_kernel(int M, int S, long rows,
+__global__ void __launch_bounds__(256, NC >= 1024 ? 2 : 3) partition_multi_kernel(int M, int S, long rows,
                                                                  const float* const* __restrict__ irs, long ir_len,
                                                                  float2* __restrict__ pool,
                                                                  const float2* __restrict__ tw,
@@ -436,14 +453,19 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
     if (parts & 1) {
         wide_head_kernel<<<grid_cap((long)p.S * 2 * (p.M + 2) * (NC / 2), 256), 256, 0, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
-        static const int f_env = [] { const char* v = std::getenv("TVOLAP_WIDE_F"); return v ? std::atoi(v) : 0; }();
-        const int F = f_env > 0 ? f_env : std::max(1, std::min(8, 4096 / NC));
+        constexpr int F = kFwdF;
         const size_t smem = a16(NC * sizeof(float2)) + a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) +
-                            2 * (size_t)F * NC * sizeof(float2);
+                            a16((F + 1) * (NC / 2) * sizeof(float)) + 2 * (size_t)F * NC * sizeof(float2);
         if ((err = cudaFuncSetAttribute(wide_forward_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem)) != cudaSuccess)
             return err;
-        wide_forward_kernel<NC><<<dim3((unsigned)((p.n + F - 1) / F), (unsigned)p.S), 256, smem, stream>>>(p, F);
+        int per_sm = 0;
+        if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_forward_kernel<NC>, 256, smem)) !=
+            cudaSuccess)
+            return err;
+        const long items = (long)p.S * ((p.n + F - 1) / F);
+        const long grid = std::max<long>(1, std::min<long>(items, (long)sm_count() * std::max(1, per_sm)));
+        wide_forward_kernel<NC><<<(unsigned)grid, 256, smem, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
     if (parts & 2) {

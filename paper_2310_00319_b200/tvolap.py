@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
             "tvolap_launch_config": (ip, [vp, fp, fp]),
             "tvolap_set_launch_config": (ip, [vp, ip, ip]),
             "tvolap_kernel_launches": (C.c_uint64, [vp]),
+            "tvolap_wide_passes": (C.c_uint64, [vp]),
             "tvolap_set_block_config": (ip, [vp, ip, lg]),
             "tvolap_block_config": (ip, [vp, fp, fp, fp]),
             "tvolap_forward_real": (ip, [ip, lg, lg, fp, fp]),
@@ -143,7 +144,7 @@ EXPORTED_SYMBOLS = (
     "tvolap_process_hops tvolap_process_switching tvolap_exchange_filter tvolap_select_bank tvolap_reset tvolap_hop tvolap_channels "
     "tvolap_output_channels tvolap_partition_count tvolap_delay_line_depth tvolap_latency "
     "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
-    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_set_block_config tvolap_block_config "
+    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_wide_passes tvolap_set_block_config tvolap_block_config "
     "tvolap_forward_real tvolap_inverse_real tvolap_mac tvolap_hann_window tvolap_partition "
     "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device "
     "tvolap_cmp_create tvolap_cmp_destroy tvolap_cmp_process_hops tvolap_cmp_set_filter tvolap_cmp_switch_filter "
@@ -467,6 +468,10 @@ class TvolapEngine:
 
     def kernel_launches(self) -> int:
         return lib().tvolap_kernel_launches(self._h)
+
+    def wide_passes(self) -> int:
+        """Time-parallel passes run (device-resident switching calls, csrc/tvolap_wide.cu)."""
+        return lib().tvolap_wide_passes(self._h)
 
 
 @dataclass
