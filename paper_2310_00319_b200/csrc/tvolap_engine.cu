@@ -206,6 +206,10 @@ struct tvolap_engine {
     int* d_wide_tile0 = nullptr;
     size_t wide_xe_cap = 0, wide_pool_cap = 0, wide_tile_cap = 0, wide_fset_cap = 0, wide_sw_cap = 0;
     size_t wide_state_cap = 0, wide_head_cap = 0;
+    float2* wide_scratch = nullptr;      // fused K4: one set per resident MAC CTA
+    unsigned* wide_lock = nullptr;
+    const float** d_wide_tile_ir = nullptr;
+    size_t wide_scratch_cap = 0, wide_lock_cap = 0, wide_tile_ir_cap = 0;
     int wide_mode = 1;               // TVOLAP_WIDE: 0 off, 1 auto, 2 whenever supported
     uint64_t wide_passes = 0;
     // chunked host pipeline
@@ -241,7 +245,8 @@ struct tvolap_engine {
                         (void*)d_out[1], (void*)d_sch[0], (void*)d_sch[1], (void*)d_sw_irs, (void*)d_sw_entry,
                         (void*)swh_x[0], (void*)swh_x[1], (void*)swh_y[0], (void*)swh_y[1], (void*)swh_ir[0],
                         (void*)swh_ir[1], (void*)wide_xe, (void*)wide_pool, (void*)wide_state, (void*)wide_head,
-                        (void*)d_wide_fset, (void*)d_wide_irs, (void*)d_wide_tile0})
+                        (void*)d_wide_fset, (void*)d_wide_irs, (void*)d_wide_tile0, (void*)wide_scratch,
+                        (void*)wide_lock, (void*)d_wide_tile_ir})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
@@ -776,6 +781,12 @@ int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, 
 extern "C++" {
 namespace {
 
+int sm_count_of(int device) {
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    return sms;
+}
+
 bool wide_eligible(const tvolap_engine* e, long n_hops, long period) {
     if (e->wide_mode == 0 || e->bank || e->E != 1 || !tvb::wide_supported((int)e->L)) return false;
     if (period < 3 || n_hops < period || n_hops < 16) return false;
@@ -830,9 +841,28 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     const long budget_mb = env_int("TVOLAP_WIDE_POOL_MB", 8192);
     const long cap_sets = std::max<long>(1, (long)((budget_mb << 20) / (long)(set_elems * sizeof(float2))));
     const float2* cur_set = e->pool + (size_t)e->active * set_elems;
+    // Fused K4: when every period is one tile, each tile transforms its own set into an
+    // L2-resident scratch slot (no set spectra through HBM); TVOLAP_WIDE_FUSE=0 disables.
+    const bool fuse = env_int("TVOLAP_WIDE_FUSE", 1) != 0 && period <= Jmax && period >= 3;
+    int nslots = 0;
+    if (fuse) {
+        nslots = tvb::wide_mac_ctas_per_sm((int)L, JH, (int)M, e->QM) * sm_count_of(e->device);
+        if (nslots <= 0) throw ApiError{TVOLAP_ERR_CUDA, "wide pass: no resident CTA for the MAC kernel"};
+        ensure_dev(e->wide_scratch, e->wide_scratch_cap, (size_t)nslots * (M + tvb::kWideTail) * N);
+        if (e->wide_lock_cap < (size_t)nslots) {
+            ensure_dev(e->wide_lock, e->wide_lock_cap, (size_t)nslots);
+            CK(cudaMemsetAsync(e->wide_lock, 0, sizeof(unsigned) * nslots, e->stream));
+        }
+    }
+    const float* cur_ir = nullptr;  // fused: the IR set in effect (null: the engine's active set)
+    const float* last_ir = nullptr;
     for (long k0 = 0; k0 < nsw_w;) {
         long k1 = k0, nsets = 0;
-        while (k1 < nsw_w && (!irs[k1] || nsets < cap_sets)) nsets += irs[k1++] ? 1 : 0;
+        if (fuse) {
+            k1 = nsw_w;
+        } else {
+            while (k1 < nsw_w && (!irs[k1] || nsets < cap_sets)) nsets += irs[k1++] ? 1 : 0;
+        }
         const long h0 = k0 * period, nh = std::min(k1 * period, n_w) - h0;
         // K4 for the chunk's sets
         std::vector<const float*> tab;
@@ -850,9 +880,12 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         // tiles: each period split into balanced tiles of <= 2 JH hops (>= 3 each: OLA fix-up)
         std::vector<int> t0;
         std::vector<const float2*> fs;
+        std::vector<const float*> tirs;
         long idx = 0;
         for (long k = k0; k < k1; ++k) {
-            if (irs[k]) cur_set = e->wide_pool + (size_t)(idx++) * set_elems;
+            if (irs[k] && !fuse) cur_set = e->wide_pool + (size_t)(idx++) * set_elems;
+            if (irs[k] && fuse) cur_ir = last_ir = irs[k];
+            tirs.push_back(cur_ir);
             const long plen = std::min(period, n_w - k * period);
             const long tp = (plen + Jmax - 1) / Jmax, base = plen / tp, rem = plen % tp;
             long st = k * period - h0;
@@ -869,6 +902,12 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         CK(cudaMemcpyAsync(e->d_wide_fset, fs.data(), sizeof(const float2*) * ntiles, cudaMemcpyHostToDevice,
                            e->stream));
         CK(cudaMemcpyAsync(e->d_wide_tile0, t0.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice, e->stream));
+        if (fuse) {
+            if ((long)tirs.size() != ntiles) throw ApiError{TVOLAP_ERR_CUDA, "wide pass: fused K4 needs one tile per period"};
+            ensure_dev(e->d_wide_tile_ir, e->wide_tile_ir_cap, (size_t)ntiles);
+            CK(cudaMemcpyAsync(e->d_wide_tile_ir, tirs.data(), sizeof(const float*) * ntiles, cudaMemcpyHostToDevice,
+                               e->stream));
+        }
         // carry and head terms per tile, extended spectra
         ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * ntiles * 3 * L);
         ensure_dev(e->wide_head, e->wide_head_cap, (size_t)S * ntiles * 6 * L);
@@ -900,12 +939,25 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         p.ntiles = (int)ntiles;
         p.tstate = e->wide_state;
         p.thead = e->wide_head;
+        p.tile_ir = fuse ? e->d_wide_tile_ir : nullptr;
+        p.ir_len = ir_length;
+        p.scratch = e->wide_scratch;
+        p.slot_lock = e->wide_lock;
+        p.nslots = nslots;
         cudaEvent_t ev0, ev1;
         prof_pair(e, &ev0, &ev1);
         CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
         e->launches += 4;
         ++e->wide_passes;
         e->hops += nh;
+        if (fuse && last_ir) {  // the pass's last set becomes the engine's active set (K4 into a pool slot)
+            const int slot = (e->active + 1) % kSlots;
+            CK(tvb::launch_partition((int)L, (int)M, S, last_ir, ir_length, ir_length, e->pool, (long)slot * S, e->tw,
+                                     e->pk, e->stream));
+            ++e->launches;
+            e->active = slot;
+            cur_set = e->pool + (size_t)slot * set_elems;
+        }
         if (nsets) {  // the chunk's last set becomes the engine's active set (a pool slot)
             const int slot = (e->active + 1) % kSlots;
             float2* dst = e->pool + (size_t)slot * set_elems;

@@ -70,7 +70,15 @@ struct WideParams {
     int ntiles;
     float* tstate;              // overlap-add carry after each tile [S][ntiles][3][L]
     float* thead;               // first-three-output terms of each tile [S][ntiles][6][L]
+    // fused K4 (one tile per period): tile_ir[tile] = the IR set in effect (null: use fset),
+    // transformed by the tile into scratch slot [nslots][M + kWideTail][2L] (slot_lock: 0 = free)
+    const float* const* tile_ir;
+    long ir_len;
+    float2* scratch;
+    unsigned* slot_lock;
+    int nslots;
 };
+int wide_mac_ctas_per_sm(int L, int JH, int M, int Q);
 bool wide_supported(int L);
 size_t wide_mac_smem_bytes(int L, int JH, int M, int Q);
 constexpr int kWideFront = 8;   // Xe front padding slots per parity (tbase = (hop0 >> 1) - M - kWideFront)

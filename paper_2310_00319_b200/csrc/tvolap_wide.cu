@@ -205,12 +205,51 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     for (int i = tid; i < N; i += NT) s_tw[i] = p.tw[i];
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
 
+    // ---- K4 fused (passes with one tile per filter period): the tile transforms its own set
+    // (one warp per partition, the warp transform of partition_warp_kernel, bit-identical) into
+    // a scratch slot held by this CTA; the slot stays in L2 and the MAC reads it straight back,
+    // so the set's spectra never go to HBM. Slots: one per resident CTA, taken by atomicCAS.
+    const float* tir = p.tile_ir ? p.tile_ir[tile] : nullptr;
+    __shared__ int s_slot;
+    int slot = -1;
+    const float2* H = nullptr;
+    if (tir) {
+        if (tid == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            int sl = (int)((sm * 2u) % (unsigned)p.nslots);
+            while (atomicCAS(p.slot_lock + sl, 0u, 1u) != 0u) sl = sl + 1 == p.nslots ? 0 : sl + 1;
+            s_slot = sl;
+        }
+        __syncthreads();  // slot chosen, tables loaded
+        slot = s_slot;
+        float2* Hs = p.scratch + (size_t)slot * (M + kWideTail) * N;
+        const float* h = tir + s * p.ir_len;
+        const bool vec = (p.ir_len & 1) == 0 && (reinterpret_cast<uintptr_t>(h) & 7) == 0;
+        const int lane = tid & 31;
+        float2* buf = s_y + (size_t)(tid >> 5) * N;  // warp buffers (s_y is idle until the MAC's group ends)
+        for (int m = tid >> 5; m < M; m += NT >> 5) {
+            const long base = (long)m * N;
+            auto load0 = [&](int, int n) -> float2 {
+                const long i0 = base + 2 * n;
+                if (vec && i0 + 1 < p.ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
+                return make_float2(i0 < p.ir_len ? h[i0] : 0.f, i0 + 1 < p.ir_len ? h[i0 + 1] : 0.f);
+            };
+            fft_warp4<false, N, true>(buf, p.tw + N, lane, load0);
+            untangle_pairs_warp(buf, N, s_pk, Hs + base, lane);
+            __syncwarp();
+        }
+        __syncthreads();  // the set's spectra (global, this CTA's writes) visible to all its threads
+        H = Hs;
+    } else {
+        H = p.fset[tile] + s * M * N;
+    }
+
     // ---- K3: thread per packed bin k, both parity groups (outputs l0 + g + 2i), JH each.
     // The m loop is unrolled by JH so the sliding window rotates by register renaming (output i
     // at unrolled step u reads win[(i - u) mod JH]); loads run kPf steps ahead in registers.
     // Partition-group partials accumulate in the thread's own column of s_y (rows = outputs).
     constexpr int kPf = 2;  // divides JH
-    const float2* H = p.fset[tile] + s * M * N;
     const float2* X[2];
     long bse[2];
 #pragma unroll
@@ -343,6 +382,17 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
         }
     }
     __syncthreads();
+    if (slot >= 0) {  // every read of the scratch set is done: drop its L2 lines unwritten, hand the slot on
+        const char* sb = reinterpret_cast<const char*>(p.scratch + (size_t)slot * (M + kWideTail) * N);
+        const size_t bytes = (size_t)M * N * sizeof(float2);
+        for (size_t off = (size_t)tid * 128; off + 128 <= bytes; off += (size_t)NT * 128)
+            asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(sb + off) : "memory");
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicExch(p.slot_lock + slot, 0u);
+        }
+    }
 
     // ---- K5: tangle + inverse FFT in batches of kWideFB frames, overlap-add per output sample
     constexpr int UPT = (L + 255) / 256;  // samples per thread (NT = 256)
@@ -502,6 +552,21 @@ cudaError_t launch_partition_multi_t(int M, int S, long rows, const float* const
 }
 
 }  // namespace
+
+int wide_mac_ctas_per_sm(int L, int JH, int M, int Q) {
+    const int N = 2 * L;
+    const size_t smem = WideLayout(N, 2 * JH, M, Q).total;
+    void (*fn)(const WideParams) = nullptr;
+#define TVB_WK(n)                                                      \
+    if (N == n) fn = JH == 8 ? wide_mac_kernel<n, 8> : wide_mac_kernel<n, 4>;
+    TVB_WK(64) TVB_WK(128) TVB_WK(256) TVB_WK(512) TVB_WK(1024)
+#undef TVB_WK
+    if (!fn) return 0;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess) return 0;
+    return per_sm;
+}
 
 bool wide_supported(int L) {
     const int N = 2 * L;
