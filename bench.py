@@ -329,9 +329,9 @@ def main():
         except Exception:
             traffic = None
     if wide:  # time-parallel pass: the MAC/inverse launch dominates; K4 and K1 are separate launches
-        kname = (f"wide_mac_kernel (K3+K5+OLA, one CTA per (channel, <=16-hop tile)), {hops_per_launch:g} hops x {S} "
-                 "sources per launch; K4 of all the pass's sets (partition_multi_kernel) and K1 of all its hops "
-                 "(wide_forward_kernel) run as separate launches outside this kernel's time")
+        kname = (f"wide_mac_kernel (K4 of the tile's filter set into an L2 scratch slot + K3 + K5 + OLA, one CTA "
+                 f"per (channel, filter period <= 16 hops)), {hops_per_launch:g} hops x {S} sources per launch; K1 of "
+                 "all hops (wide_forward_kernel, ~13% of the step) is a separate launch outside this kernel's time")
     else:
         kname = (f"tvolap_block_kernel (K1-K5 fused{', K4 for the next switch in the barrier gaps' if cfg.mode == 'fresh' else ''}), "
                  f"{hops_per_launch:g} hops x {S} sources per launch")
