@@ -834,7 +834,9 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         e->pending = false;
     }
     latch(e);
-    int JH = 8;
+    // 16-hop tiles, or 8-hop tiles when no period needs more (8-hop periods would leave half of a
+    // 16-hop tile's MAC outputs unused) or the 16-hop tile's shared memory does not fit
+    int JH = period <= 8 ? 4 : 8;
     if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
     const long Jmax = 2 * JH;
     const size_t set_elems = (size_t)S * M * N;

@@ -164,10 +164,6 @@ __global__ void __launch_bounds__(256, NC >= 1024 ? 2 : 3) partition_multi_kerne
 
 constexpr int kWideFB = 4;  // frames per inverse-FFT batch
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
-}
 
 struct WideLayout {
     size_t tw, pk, y, fa, fb, aux, total;
@@ -226,17 +222,21 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
         float2* Hs = p.scratch + (size_t)slot * (M + kWideTail) * N;
         const float* h = tir + s * p.ir_len;
         const bool vec = (p.ir_len & 1) == 0 && (reinterpret_cast<uintptr_t>(h) & 7) == 0;
-        const int lane = tid & 31;
-        float2* buf = s_y + (size_t)(tid >> 5) * N;  // warp buffers (s_y is idle until the MAC's group ends)
-        for (int m = tid >> 5; m < M; m += NT >> 5) {
-            const long base = (long)m * N;
-            auto load0 = [&](int, int n) -> float2 {
-                const long i0 = base + 2 * n;
+        const int lane = tid & 31, warp = tid >> 5, nw = NT >> 5;
+        auto loader = [&](int m) {
+            return [&, m](int, int n) -> float2 {
+                const long i0 = (long)m * N + 2 * n;
+                if (m >= M) return make_float2(0.f, 0.f);
                 if (vec && i0 + 1 < p.ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
                 return make_float2(i0 < p.ir_len ? h[i0] : 0.f, i0 + 1 < p.ir_len ? h[i0 + 1] : 0.f);
             };
-            fft_warp4<false, N, true>(buf, p.tw + N, lane, load0);
-            untangle_pairs_warp(buf, N, s_pk, Hs + base, lane);
+        };
+        // warp buffers in s_y (idle until the MAC's first group ends); same-box A/B: two partitions
+        // per warp in lockstep (fft_warp4 NB = 2) spills and measured 6.24 vs 5.83 ms per C2 pass
+        float2* buf = s_y + (size_t)warp * N;
+        for (int m = warp; m < M; m += nw) {
+            fft_warp4<false, N, true>(buf, p.tw + N, lane, loader(m));
+            untangle_pairs_warp(buf, N, s_pk, Hs + (long)m * N, lane);
             __syncwarp();
         }
         __syncthreads();  // the set's spectra (global, this CTA's writes) visible to all its threads
