@@ -858,13 +858,15 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     }
     const float* cur_ir = nullptr;  // fused: the IR set in effect (null: the engine's active set)
     const float* last_ir = nullptr;
+    // periods per pass: the extended spectra (and per-tile carries) of a pass stay within
+    // TVOLAP_WIDE_XE_MB (default 4 GB), the sets of an unfused pass within TVOLAP_WIDE_POOL_MB
+    const long xe_mb = env_int("TVOLAP_WIDE_XE_MB", 4096);
+    const long per_period = (long)(S * N * sizeof(float2) * period + S * 9 * L * sizeof(float));
+    const long cap_periods = std::max<long>(1, (xe_mb << 20) / std::max<long>(1, per_period) - (M + 32) / period);
     for (long k0 = 0; k0 < nsw_w;) {
         long k1 = k0, nsets = 0;
-        if (fuse) {
-            k1 = nsw_w;
-        } else {
-            while (k1 < nsw_w && (!irs[k1] || nsets < cap_sets)) nsets += irs[k1++] ? 1 : 0;
-        }
+        while (k1 < nsw_w && k1 - k0 < cap_periods && (fuse || !irs[k1] || nsets < cap_sets))
+            nsets += (irs[k1++] && !fuse) ? 1 : 0;
         const long h0 = k0 * period, nh = std::min(k1 * period, n_w) - h0;
         // K4 for the chunk's sets
         std::vector<const float*> tab;

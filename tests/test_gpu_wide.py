@@ -66,6 +66,7 @@ def test_wide_equals_exchange_loop(monkeypatch, hop, S, taps, n_hops, period, no
     yb = _loop(b, x, dirs, period, hop)
     a.synchronize()
     b.synchronize()
+    assert a.wide_passes() >= 1 and b.wide_passes() == 0
     assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
     # state handed to the next calls: delay line, carry, history and the active set
     za, zb = a.process_hops(x[:, : 40 * hop]), b.process_hops(x[:, : 40 * hop])
@@ -86,6 +87,24 @@ def test_wide_chunked_pool(monkeypatch):
     a.synchronize()
     b.synchronize()
     assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+
+
+@pytest.mark.parametrize("period,none_at", [(16, (0, 3)), (8, (2,)), (24, (1,))])
+def test_wide_chunked_passes(monkeypatch, period, none_at):
+    """A 1 MB extended-spectra budget: the call runs as several passes (fused K4 for periods of
+    <= 16 hops, a partition_multi launch per pass otherwise); the set in effect crosses passes."""
+    hop, S, taps, n = 256, 4, 4096, period * 9 + 5
+    ir0, x, dirs = _case(hop, S, taps, n, period, none_at=none_at)
+    a, b = _engines(monkeypatch, ir0, hop)
+    monkeypatch.setenv("TVOLAP_WIDE_XE_MB", "1")
+    ya = a.process_switching(x, dirs, period)
+    yb = _loop(b, x, dirs, period, hop)
+    a.synchronize()
+    b.synchronize()
+    assert a.wide_passes() > 1
+    assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+    za, zb = a.process_hops(x[:, : 20 * hop]), b.process_hops(x[:, : 20 * hop])
+    assert np.array_equal(za.cpu().numpy(), zb.cpu().numpy())
 
 
 def test_wide_back_to_back_calls(monkeypatch):
