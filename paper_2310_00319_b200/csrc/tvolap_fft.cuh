@@ -286,15 +286,50 @@ __device__ __forceinline__ float2 w32c(int j) {
 }
 
 // In-register DFT of R = 1..32 points, natural order in and out (sign -1 forward, +1 inverse).
-// 16 = 4 x 4 and 32 = 8 x 4 four-step splits with compile-time twiddles.
-template <bool INV, int R>
+// 16 = 4 x 4 and 32 = 8 x 4 four-step splits with compile-time twiddles. HALF: the upper half
+// of the input is zero (pruned transforms): the first butterfly level keeps x +- 0 = x (equal
+// values; only the sign of a zero can differ) instead of adding zeros.
+template <bool INV, int R, bool HALF = false>
 __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
     if constexpr (R == 2) {
-        const float2 t0 = cadd(v[0], v[1]), t1 = csub(v[0], v[1]);
+        const float2 t0 = HALF ? v[0] : cadd(v[0], v[1]), t1 = HALF ? v[0] : csub(v[0], v[1]);
         v[0] = t0;
         v[1] = t1;
+    } else if constexpr (R == 4 && HALF) {
+        const float2 a0 = v[0], a2 = v[1];  // dft4 with v2 = v3 = 0: a1 = a0, a3 = a2
+        v[0] = cadd(a0, a2);
+        v[2] = csub(a0, a2);
+        if (INV) {
+            v[1] = make_float2(a0.x - a2.y, a0.y + a2.x);
+            v[3] = make_float2(a0.x + a2.y, a0.y - a2.x);
+        } else {
+            v[1] = make_float2(a0.x + a2.y, a0.y - a2.x);
+            v[3] = make_float2(a0.x - a2.y, a0.y + a2.x);
+        }
     } else if constexpr (R == 4) {
         dft4<INV>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8 && HALF) {
+        // dft8 with v4..v7 = 0: b[n] = b[n + 4] = v[n]
+        constexpr float c = 0.70710678118654752440f;
+        float2 b[8];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) b[n] = b[n + 4] = v[n];
+        if (INV) {
+            b[5] = make_float2((b[5].x - b[5].y) * c, (b[5].x + b[5].y) * c);
+            b[6] = make_float2(-b[6].y, b[6].x);
+            b[7] = make_float2(-(b[7].x + b[7].y) * c, (b[7].x - b[7].y) * c);
+        } else {
+            b[5] = make_float2((b[5].x + b[5].y) * c, (b[5].y - b[5].x) * c);
+            b[6] = make_float2(b[6].y, -b[6].x);
+            b[7] = make_float2((b[7].y - b[7].x) * c, -(b[7].x + b[7].y) * c);
+        }
+        dft4<INV>(b[0], b[1], b[2], b[3]);
+        dft4<INV>(b[4], b[5], b[6], b[7]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[2 * k] = b[k];
+            v[2 * k + 1] = b[k + 4];
+        }
     } else if constexpr (R == 8) {
         dft8<INV>(v);
     } else if constexpr (R == 16 || R == 32) {
@@ -304,7 +339,7 @@ __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
         for (int b = 0; b < 4; ++b) {
 #pragma unroll
             for (int a = 0; a < A; ++a) y[b][a] = v[4 * a + b];
-            dft_reg<INV, A>(y[b]);
+            dft_reg<INV, A, HALF>(y[b]);  // HALF: v[4a + b] = 0 for a >= A / 2
 #pragma unroll
             for (int ka = 1; ka < A; ++ka)
                 if (b > 0) y[b][ka] = twmul<INV>(y[b][ka], w32c((32 / R) * b * ka));
@@ -364,7 +399,7 @@ __device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict_
             v[t][n1] = (PRUNE && n1 >= N1 / 2) ? make_float2(0.f, 0.f) : load(t, 32 * n1 + lane);
 #pragma unroll
     for (int t = 0; t < NB; ++t) {
-        dft_reg<INV, N1>(v[t]);
+        dft_reg<INV, N1, PRUNE>(v[t]);
 #pragma unroll
         for (int k1 = 1; k1 < N1; ++k1) v[t][k1] = twmul<INV>(v[t][k1], tw4[k1 * 32 + lane]);
 #pragma unroll
@@ -398,7 +433,9 @@ __device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict_
                     float2 o;
                     o.x = __shfl_xor_sync(0xffffffffu, v[t][c].x, hs);
                     o.y = __shfl_xor_sync(0xffffffffu, v[t][c].y, hs);
-                    v[t][c] = upper ? twmul<INV>(csub(o, v[t][c]), w) : cadd(v[t][c], o);
+                    // the last level (hs = 1) multiplies by W^0 = 1: skipped (equal values)
+                    v[t][c] = upper ? (hs == 1 ? csub(o, v[t][c]) : twmul<INV>(csub(o, v[t][c]), w))
+                                    : cadd(v[t][c], o);
                 }
         }
     }
