@@ -212,6 +212,7 @@ struct tvolap_engine {
     size_t wide_scratch_cap = 0, wide_lock_cap = 0, wide_tile_ir_cap = 0;
     int wide_mode = 1;               // TVOLAP_WIDE: 0 off, 1 auto, 2 whenever supported
     uint64_t wide_passes = 0;
+    int wide_warp_fft = 1;           // TVOLAP_WIDE_WARPFFT: 1 warp FFTs for K1/K5 (0: bit-identical Stockham)
     // chunked host pipeline
     long chunk_hops = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
@@ -282,6 +283,7 @@ void pick_launch_config(tvolap_engine* e) {
     e->k4_stream = env_int("TVOLAP_K4_STREAM", 1) != 0;
     e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 1)));
     e->wide_mode = env_int("TVOLAP_WIDE", 1);
+    e->wide_warp_fft = env_int("TVOLAP_WIDE_WARPFFT", 1);
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -948,6 +950,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         p.scratch = e->wide_scratch;
         p.slot_lock = e->wide_lock;
         p.nslots = nslots;
+        p.warp_fft = e->wide_warp_fft;
         cudaEvent_t ev0, ev1;
         prof_pair(e, &ev0, &ev1);
         CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));

@@ -77,6 +77,8 @@ struct WideParams {
     float2* scratch;
     unsigned* slot_lock;
     int nslots;
+    int warp_fft;               // K1 / K5 with one warp per frame (warp four-step FFT) instead of the
+                                // hop kernels' CTA Stockham (equal to fp32 rounding, not bit-identical)
 };
 int wide_mac_ctas_per_sm(int L, int JH, int M, int Q);
 bool wide_supported(int L);

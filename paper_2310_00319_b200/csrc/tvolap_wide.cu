@@ -129,6 +129,43 @@ __global__ void __launch_bounds__(256) wide_forward_kernel(const WideParams p) {
     }
 }
 
+// K1 with one warp per frame (warp four-step FFT, no CTA barriers): frame f = (lane f / n,
+// hop f mod n), lane-major so consecutive warps share input hops. Same values as the Stockham
+// K1 up to fp32 rounding (a different factorisation).
+template <int NC>
+__global__ void __launch_bounds__(256) wide_forward_warp_kernel(const WideParams p) {
+    constexpr int N = NC, L = NC / 2;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* s_pk = reinterpret_cast<float2*>(smem);
+    float* s_win = reinterpret_cast<float*>(smem + a16((N + 2) * sizeof(float2)));
+    float2* bufs = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(s_win) + a16(N * sizeof(float)));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int i = tid; i < N; i += blockDim.x) s_win[i] = p.win[i];
+    for (int i = tid; i <= N; i += blockDim.x) s_pk[i] = p.pk[i];
+    __syncthreads();
+    float2* buf = bufs + (size_t)warp * N;
+    const long frames = (long)p.S * p.n;
+    const long ring_from = p.hop0 + p.n - 2L * p.D;
+    for (long f = (long)blockIdx.x * nw + warp; f < frames; f += (long)gridDim.x * nw) {
+        const long s = f / p.n;
+        const int r = (int)(f - s * p.n);
+        const float* prev = r == 0 ? p.hist + s * L : p.in + s * p.in_stride + (long)(r - 1) * L;
+        const float* cur = p.in + s * p.in_stride + (long)r * L;
+        auto load0 = [&](int, int n) -> float2 {  // z_n = (x[2n] w[2n], x[2n+1] w[2n+1]), n < L
+            const int e = 2 * n;
+            const float* src = e < L ? prev + e : cur + (e - L);
+            return make_float2(src[0] * s_win[e], src[1] * s_win[e + 1]);
+        };
+        fft_warp4<false, N, true>(buf, p.tw + N, lane, load0);
+        const long j = p.hop0 + r;
+        const int par = (int)(j & 1);
+        untangle_pairs_warp(buf, N, s_pk, p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N, lane);
+        if (j >= ring_from)
+            untangle_pairs_warp(buf, N, s_pk, p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N, lane);
+        __syncwarp();
+    }
+}
+
 // K4 for the sets a call installs: row r = k * S + s transforms irs[k] + s * ir_len into
 // pool[(r * M + m) * N] (partition.cpp:20-51). Same warp transform as partition_warp_kernel.
 template <int NC>
@@ -402,21 +439,16 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     const float sc = 1.0f / (float)N;
     float* head = p.thead + (s * p.ntiles + tile) * 6 * L;
     float* outp = p.out + s * p.out_stride + (long)l0r * L;
-    for (int f0 = 0; f0 < jt; f0 += kWideFB) {
-        const int nb = min(kWideFB, jt - f0);
-        for (int i = tid; i < nb * N; i += NT) {
-            const int fi = i / N, kk = i - fi * N;
-            s_fb[(size_t)fi * N + kk] = tangle_packed(s_y + (size_t)(f0 + fi) * N, N, kk, s_pk);
-        }
-        __syncthreads();
-        const float* ytd = reinterpret_cast<const float*>(fft_batch<true, NC>(s_fb, s_fa, N, nb, s_tw, false, tid, NT));
+    // overlap-add of frames f0 .. f0 + nb - 1 whose time-domain samples (unscaled, 2N floats per
+    // frame at stride fstride floats) start at ytd
+    auto ola = [&](const float* ytd, size_t fstride, int f0, int nb) {
 #pragma unroll
         for (int c = 0; c < UPT; ++c) {
             const int u = tid + c * 256;
             if (u >= L || tid >= NT) continue;
             for (int fi = 0; fi < nb; ++fi) {
                 const int jj = f0 + fi;
-                const float* yf = ytd + (size_t)fi * 2 * N + u;
+                const float* yf = ytd + (size_t)fi * fstride + u;
                 const float y0 = yf[0] * sc, y1 = yf[L] * sc, y2 = yf[2 * L] * sc, y3 = yf[3 * L] * sc;
                 const float o = 0.5f * (y0 + st[c][0]);
                 st[c][0] = st[c][1] + y1;
@@ -436,7 +468,35 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
                 }
             }
         }
-        __syncthreads();  // ytd / s_fb free for the next batch
+    };
+    if (p.warp_fft && N >= 64 && N <= 1024 && 8 * N <= kWideFB * 2 * N) {
+        // one warp per frame, no CTA barriers: tangle into the warp's buffer (K5 buffers), then
+        // the warp four-step inverse FFT writes the time-domain frame over its own Y row
+        // (only this warp reads that row)
+        const int warp = tid >> 5, lane = tid & 31;
+        float2* wb = s_fa + (size_t)warp * N;
+        for (int jj = warp; jj < jt; jj += NT >> 5) {
+            float2* yrow = s_y + (size_t)jj * N;
+            for (int kk = lane; kk < N; kk += 32) wb[kk] = tangle_packed(yrow, N, kk, s_pk);
+            __syncwarp();
+            if constexpr (N >= 64 && N <= 1024)
+                fft_warp4<true, N, false>(yrow, p.tw + N, lane, [&](int, int n) { return wb[n]; });
+            __syncwarp();
+        }
+        __syncthreads();
+        ola(reinterpret_cast<const float*>(s_y), 2 * (size_t)N, 0, jt);
+    } else {
+        for (int f0 = 0; f0 < jt; f0 += kWideFB) {
+            const int nb = min(kWideFB, jt - f0);
+            for (int i = tid; i < nb * N; i += NT) {
+                const int fi = i / N, kk = i - fi * N;
+                s_fb[(size_t)fi * N + kk] = tangle_packed(s_y + (size_t)(f0 + fi) * N, N, kk, s_pk);
+            }
+            __syncthreads();
+            ola(reinterpret_cast<const float*>(fft_batch<true, NC>(s_fb, s_fa, N, nb, s_tw, false, tid, NT)),
+                2 * (size_t)N, f0, nb);
+            __syncthreads();  // ytd / s_fb free for the next batch
+        }
     }
     float* stt = p.tstate + (s * p.ntiles + tile) * 3 * L;
 #pragma unroll
@@ -503,6 +563,21 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
     if (parts & 1) {
         wide_head_kernel<<<grid_cap((long)p.S * 2 * (p.M + 2) * (NC / 2), 256), 256, 0, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (p.warp_fft && NC >= 64 && NC <= 1024) {
+            const size_t smem = a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) + 8 * (size_t)NC * sizeof(float2);
+            if ((err = cudaFuncSetAttribute(wide_forward_warp_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem)) != cudaSuccess)
+                return err;
+            int per_sm = 0;
+            if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_forward_warp_kernel<NC>, 256, smem)) !=
+                cudaSuccess)
+                return err;
+            const long frames = (long)p.S * p.n;
+            const long grid = std::max<long>(1, std::min<long>((frames + 7) / 8, (long)sm_count() * std::max(1, per_sm)));
+            wide_forward_warp_kernel<NC><<<(unsigned)grid, 256, smem, stream>>>(p);
+            if ((err = cudaGetLastError()) != cudaSuccess) return err;
+            return launch_wide_t<NC>(p, JH, stream, t0, t1, parts & ~1);
+        }
         constexpr int F = kFwdF;
         const size_t smem = a16(NC * sizeof(float2)) + a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) +
                             a16((F + 1) * (NC / 2) * sizeof(float)) + 2 * (size_t)F * NC * sizeof(float2);

@@ -41,7 +41,8 @@ def _loop(eng, x, dirs, period, hop):
     (128, 4, 2048, 70, 16, ()),             # N = 256
     (512, 2, 8192, 48, 8, (0,)),            # N = 1024, no switch at the first hop
 ])
-def test_switching_equals_exchange_loop(hop, S, taps, n_hops, period, none_at):
+def test_switching_equals_exchange_loop(monkeypatch, hop, S, taps, n_hops, period, none_at):
+    monkeypatch.setenv("TVOLAP_WIDE", "0")  # the hop-blocked switching launch (the pass: test_gpu_wide.py)
     ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at)
     a = T.TvolapEngine(T.partition(ir0, hop))
     b = T.TvolapEngine(T.partition(ir0, hop))
@@ -103,11 +104,12 @@ def test_switching_validation():
 
 @pytest.mark.parametrize("n_hops,period,hop", [(16 * 9 + 5, 16, 256), (64, 16, 256), (90, 10, 256), (40, 8, 512),
                                               (50, 16, 256)])
-def test_switching_pinned_host_pipeline(n_hops, period, hop):
+def test_switching_pinned_host_pipeline(monkeypatch, n_hops, period, hop):
     """Pinned host buffers: chunked H2D / launch / D2H pipeline (switching kernel, or the loop on
     device staging for 2048-point transforms), bit-identical to the device call."""
     import torch
 
+    monkeypatch.setenv("TVOLAP_WIDE", "0")  # device reference = the switching launch the pipeline runs
     S, taps = 4, 4096
     ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at=(1,))
     xh = x.cpu().pin_memory()

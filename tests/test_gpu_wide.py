@@ -1,7 +1,8 @@
 """Time-parallel pass (csrc/tvolap_wide.cu): a device-resident tvolap_process_switching call run
 as K4-for-all-sets + K1-for-all-hops + (lane, tile) MAC/inverse CTAs + OLA fix-up must equal the
-exchange_filter + process_hops loop it stands for (hop-blocked kernel), bit for bit, and leave the
-engine in the same state (delay line, carry, history, active set)."""
+exchange_filter + process_hops loop it stands for (hop-blocked kernel) and leave the engine in the
+same state (delay line, carry, history, active set): bit for bit with the hop kernels' Stockham
+transforms (TVOLAP_WIDE_WARPFFT=0), to fp32 rounding with the default warp-per-frame transforms."""
 import numpy as np
 import pytest
 
@@ -36,13 +37,20 @@ def _loop(eng, x, dirs, period, hop):
     return out
 
 
-def _engines(monkeypatch, ir0, hop):
+def _engines(monkeypatch, ir0, hop, warp_fft=False):
     monkeypatch.setenv("TVOLAP_WIDE", "2")
+    monkeypatch.setenv("TVOLAP_WIDE_WARPFFT", "1" if warp_fft else "0")
     a = T.TvolapEngine(T.partition(ir0, hop))
     monkeypatch.setenv("TVOLAP_WIDE", "0")
     b = T.TvolapEngine(T.partition(ir0, hop))
     monkeypatch.delenv("TVOLAP_WIDE")
+    monkeypatch.delenv("TVOLAP_WIDE_WARPFFT")
     return a, b
+
+
+def _close(ya, yb, rel=2e-6):
+    ya, yb = ya.cpu().numpy(), yb.cpu().numpy()
+    return np.abs(ya - yb).max() <= rel * np.abs(yb).max()
 
 
 @pytest.mark.parametrize("hop,S,taps,n_hops,period,none_at,pre", [
@@ -74,6 +82,35 @@ def test_wide_equals_exchange_loop(monkeypatch, hop, S, taps, n_hops, period, no
     b.synchronize()
     assert np.array_equal(za.cpu().numpy(), zb.cpu().numpy())
     assert a.op_counts() == b.op_counts()
+
+
+@pytest.mark.parametrize("hop,S,taps,n_hops,period,none_at,pre", [
+    (256, 5, 4096, 16 * 9, 16, (2,), 3),
+    (256, 3, 3000, 61, 10, (), 5),
+    (256, 2, 4096, 100, 40, (1,), 2),
+    (128, 4, 2048, 150, 64, (), 4),
+    (512, 2, 8192, 48, 8, (0,), 3),
+    (32, 6, 1024, 90, 17, (), 2),
+    (64, 3, 8192, 70, 16, (), 1),
+])
+def test_wide_warp_fft_matches_loop(monkeypatch, hop, S, taps, n_hops, period, none_at, pre):
+    """Default mode (warp-per-frame K1/K5 transforms): the loop's outputs to fp32 rounding, and
+    the state it hands on (delay line from the warp K1) keeps later calls within rounding."""
+    ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at)
+    a, b = _engines(monkeypatch, ir0, hop, warp_fft=True)
+    if pre:
+        a.process_hops(x[:, : pre * hop])
+        b.process_hops(x[:, : pre * hop])
+    ya = a.process_switching(x, dirs, period)
+    yb = _loop(b, x, dirs, period, hop)
+    a.synchronize()
+    b.synchronize()
+    assert a.wide_passes() >= 1
+    assert _close(ya, yb)
+    za, zb = a.process_hops(x[:, : 40 * hop]), b.process_hops(x[:, : 40 * hop])
+    a.synchronize()
+    b.synchronize()
+    assert _close(za, zb)
 
 
 def test_wide_chunked_pool(monkeypatch):
