@@ -105,10 +105,13 @@ int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, 
  * (the reference's drive() loop, experiment.cpp:42-49, with the switch staged right before the
  * hop it applies to), k < ceil(n_hops / period); irs[k] == NULL keeps the running filter. `irs`
  * is a host array of channel-major IR pointers (irs[k][c * ir_length + n]). With device
- * buffers and device IRs the whole call is one hop-blocked launch that transforms switch k+1's
- * partitions inside the cluster-barrier gaps of period k (no separate K4 launch, no launch gap
- * per period); otherwise it runs the loop above. Outputs are bit-identical either way.
- * Filter-set engines only.
+ * buffers and device IRs the call runs as a time-parallel pass when the engine has few channels
+ * (forward FFTs of every hop at once, then one CTA per (channel, period) that transforms its
+ * period's set in-CTA and runs MAC + inverse + overlap-add; tvolap_wide_passes counts them), or
+ * as one hop-blocked launch that transforms switch k+1's partitions inside the cluster-barrier
+ * gaps of period k; otherwise it runs the loop above. The hop-blocked forms are bit-identical to
+ * the loop; the time-parallel pass is too with TVOLAP_WIDE_WARPFFT=0, and by default (warp
+ * per-frame transforms) equal to fp32 rounding. Filter-set engines only.
  */
 int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
                              long n_hops, long period, const float* const* irs, long ir_length);
@@ -193,9 +196,8 @@ int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block
 uint64_t tvolap_kernel_launches(const tvolap_engine* e);
 
 /* Time-parallel passes run so far: device-resident tvolap_process_switching calls executed as
-   K4-for-all-sets + K1-for-all-hops + (lane, hop-tile) MAC/inverse CTAs (a diagnostic of which
-   path a call took; outputs equal the hop-blocked path bit for bit). TVOLAP_WIDE=0 disables it,
-   TVOLAP_WIDE=2 forces it wherever it is supported. */
+   K1-for-all-hops + (lane, hop-tile) K4/MAC/inverse CTAs (a diagnostic of which path a call
+   took). TVOLAP_WIDE=0 disables the pass, TVOLAP_WIDE=2 forces it wherever it is supported. */
 uint64_t tvolap_wide_passes(const tvolap_engine* e);
 
 /* ------------------------------------------------------ spectral primitives */
