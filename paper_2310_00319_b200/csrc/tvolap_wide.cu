@@ -6,19 +6,22 @@
 // (engine.cpp:97-102), which is a 3-value linear recurrence per output sample. The hop-blocked
 // kernel walks the hops of a lane in order (parallelism = lanes x cluster CTAs: 256 CTAs for
 // C2); here the hop axis is parallel too:
-//   wide_head_kernel     the spectra of hops before the call (still needed by its first
-//                        outputs) from the delay line into the extended spectra buffer Xe,
-//   wide_forward_kernel  K1 for every hop of the call at once (window + pruned Stockham FFT +
-//                        untangle), into Xe; the last 2D hops also into the delay line,
-//   partition_multi      K4 for every filter set the call installs (one warp per partition),
-//   wide_mac_kernel      one CTA per (lane, tile of <= 16 hops inside one filter period): K3
-//                        over Xe with a sliding register window, then K5 (tangle + inverse FFT)
-//                        and the overlap-add of the tile's outputs from its 4th hop on,
-//   wide_fixup_kernel    the first three outputs of every tile from the carry of the tile
-//                        before it (and the engine's carry / history for the next call).
-// Every arithmetic operation and its order per output equal the hop-blocked kernel's (same FFT
-// code, same partition groups summed in the same order, same OLA recurrence), so the outputs
-// are bit-identical to tvolap_block_kernel's (tests/test_gpu_wide.py).
+//   wide_head_kernel          the spectra of hops before the call (still needed by its first
+//                             outputs) from the delay line into the extended spectra buffer Xe,
+//   wide_forward[_warp]_kernel K1 for every hop of the call at once (window + pruned FFT +
+//                             untangle), into Xe; the last 2D hops also into the delay line,
+//   partition_multi_kernel    K4 for every filter set of the call (periods longer than a tile),
+//   wide_mac_kernel           one CTA per (lane, tile of <= 16 hops inside one filter period):
+//                             K4 of the period's set into an L2 scratch slot (periods of one
+//                             tile), K3 over Xe with a sliding register window, then K5 (tangle
+//                             + inverse FFT) and the overlap-add of the tile's outputs from its
+//                             4th hop on,
+//   wide_fixup_kernel         the first three outputs of every tile from the carry of the tile
+//                             before it (and the engine's carry / history for the next call).
+// The MAC sums the partition groups in the hop-blocked kernel's order and the OLA recurrence runs
+// in the sequential order. With the hop kernels' CTA Stockham transforms for K1/K5
+// (TVOLAP_WIDE_WARPFFT=0) the outputs are bit-identical to tvolap_block_kernel's; the default
+// warp-per-frame transforms (fft_warp4) equal them to fp32 rounding (tests/test_gpu_wide.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
             }
         }
     };
-    if (p.warp_fft && N >= 64 && N <= 1024 && 8 * N <= kWideFB * 2 * N) {
+    if (p.warp_fft && N >= 64 && N <= 1024) {  // 8 warp buffers of N = the two K5 buffers
         // one warp per frame, no CTA barriers: tangle into the warp's buffer (K5 buffers), then
         // the warp four-step inverse FFT writes the time-domain frame over its own Y row
         // (only this warp reads that row)
