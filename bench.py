@@ -72,32 +72,39 @@ def config_block(cfg, n_hops, world):
 
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
+    """nvidia-smi sampled every 20 ms from before the warm-up on; a reader thread stamps each line
+    on arrival, and stop(t0, t1) summarises the samples that arrived inside the timed region
+    (falling back to warm-up + timed region when the region is shorter than the sampling)."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
+        import threading
+
         self.proc = None
         self.idx = gpu_index
+        self.lines = []
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
 
-    def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out, _ = self.proc.communicate()
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.time(), line))
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    @staticmethod
+    def summarise(lines):
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for _, line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -111,6 +118,26 @@ class Clocks:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+    def stop(self, t0=None, t1=None):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=5)
+        lines = list(self.lines)
+        if t0 is not None:
+            inside = [(t, l) for t, l in lines if t0 <= t <= t1 + 0.03]
+            out = self.summarise(inside)
+            if out["samples"]:
+                out["window"] = "timed region"
+                return out
+        out = self.summarise(lines)
+        out["window"] = "warm-up + timed region (timed region shorter than the 20 ms sampling)"
+        return out
 
 
 # ----------------------------------------------------------------------------- CPU legs
@@ -272,19 +299,21 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         step(eng, x, out, irs, sched)
     barrier()
     launches0 = eng.kernel_launches()
     wide0 = eng.wide_passes() if hasattr(eng, "wide_passes") else 0
-    clocks = Clocks(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
         step(eng, x, out, irs, sched)
     ev1.record(stream)
     barrier()
-    clk = clocks.stop()
+    t_end = time.time()
+    clk = clocks.stop(t_start, t_end)
     elapsed = ev0.elapsed_time(ev1)
     gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
     wide = (eng.wide_passes() - wide0 if hasattr(eng, "wide_passes") else 0) > 0
