@@ -951,6 +951,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         p.slot_lock = e->wide_lock;
         p.nslots = nslots;
         p.warp_fft = e->wide_warp_fft;
+        p.stage_ir = env_int("TVOLAP_WIDE_STAGE", 1);
         cudaEvent_t ev0, ev1;
         prof_pair(e, &ev0, &ev1);
         CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));

@@ -77,6 +77,7 @@ struct WideParams {
     float2* scratch;
     unsigned* slot_lock;
     int nslots;
+    int stage_ir;               // fused K4: IR slices through a cp.async double buffer in shared memory
     int warp_fft;               // K1 / K5 with one warp per frame (warp four-step FFT) instead of the
                                 // hop kernels' CTA Stockham (equal to fp32 rounding, not bit-identical)
 };

@@ -274,10 +274,40 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
         // warp buffers in s_y (idle until the MAC's first group ends); same-box A/B: two partitions
         // per warp in lockstep (fft_warp4 NB = 2) spills and measured 6.24 vs 5.83 ms per C2 pass
         float2* buf = s_y + (size_t)warp * N;
-        for (int m = warp; m < M; m += nw) {
-            fft_warp4<false, N, true>(buf, p.tw + N, lane, loader(m));
-            untangle_pairs_warp(buf, N, s_pk, Hs + (long)m * N, lane);
-            __syncwarp();
+        const bool staged = p.stage_ir && J >= 16 && p.ir_len >= (long)M * N && (p.ir_len & 3) == 0 &&
+                            (reinterpret_cast<uintptr_t>(h) & 15) == 0;
+        if (staged) {
+            // IR slices (N floats) through a per-warp double buffer in rows 8..15 of s_y, one
+            // partition ahead with 16-byte cp.async: the transform's loads hit shared memory
+            float* pb = reinterpret_cast<float*>(s_y + (size_t)8 * N) + (size_t)warp * 2 * N;
+            auto issue = [&](int m, int b) {
+                if (m < M)
+                    for (int i = 4 * lane; i < N; i += 128) {
+                        const unsigned sa = (unsigned)__cvta_generic_to_shared(pb + (size_t)b * N + i);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(h + (long)m * N + i)
+                                     : "memory");
+                    }
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            };
+            int b = 0;
+            issue(warp, 0);
+            for (int m = warp; m < M; m += nw, b ^= 1) {
+                issue(m + nw, b ^ 1);
+                asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                __syncwarp();
+                const float* cur = pb + (size_t)b * N;
+                fft_warp4<false, N, true>(buf, p.tw + N, lane,
+                                          [&](int, int n) { return make_float2(cur[2 * n], cur[2 * n + 1]); });
+                untangle_pairs_warp(buf, N, s_pk, Hs + (long)m * N, lane);
+                __syncwarp();
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+        } else {
+            for (int m = warp; m < M; m += nw) {
+                fft_warp4<false, N, true>(buf, p.tw + N, lane, loader(m));
+                untangle_pairs_warp(buf, N, s_pk, Hs + (long)m * N, lane);
+                __syncwarp();
+            }
         }
         __syncthreads();  // the set's spectra (global, this CTA's writes) visible to all its threads
         H = Hs;
