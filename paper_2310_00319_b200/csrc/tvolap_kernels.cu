@@ -1203,7 +1203,7 @@ template <int NC>
 __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows, const float* __restrict__ ir,
                                                              long ir_stride, long ir_len, float2* __restrict__ pool,
                                                              long row0, const float2* __restrict__ tw,
-                                                             const float2* __restrict__ pk) {
+                                                             const float2* __restrict__ pk, int k4_prefetch) {
     constexpr int N = NC;
     extern __shared__ __align__(16) unsigned char smem[];
     float2* s_tw = reinterpret_cast<float2*>(smem);
@@ -1225,6 +1225,18 @@ __global__ void __launch_bounds__(256, 2) partition_warp_kernel(int M, long rows
         const int m = (int)(t - row * M);
         const float* h = ir + row * ir_stride;
         const long base = (long)m * N;  // partition m = IR samples [m N, (m + 1) N), N = 2L
+        if (lane == 0 && k4_prefetch) {  // the warp's next slice on its way into L2 (TMA bulk prefetch)
+            const long tn = t + (long)gridDim.x * nw;
+            if (tn < tasks) {
+                const long rn = tn / M;
+                const long i0 = (tn - rn * M) * N, i1 = min(i0 + N, ir_len);
+                const uintptr_t a = (reinterpret_cast<uintptr_t>(ir + rn * ir_stride + i0) + 15) & ~uintptr_t(15);
+                const uintptr_t e = reinterpret_cast<uintptr_t>(ir + rn * ir_stride + i1) & ~uintptr_t(15);
+                if (e > a)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"((unsigned)(e - a))
+                                 : "memory");
+            }
+        }
         auto load0 = [&](int, int n) -> float2 {  // z_n = (h[2n], h[2n+1])
             const long i0 = base + 2 * n;
             if (vec && i0 + 1 < ir_len) return __ldcs(reinterpret_cast<const float2*>(h + i0));
@@ -1643,7 +1655,12 @@ static cudaError_t launch_partition_warp(int M, long rows, const float* ir, long
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, partition_warp_kernel<NC>, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk);
+    static const int k4_prefetch = [] {  // TVOLAP_K4_PREFETCH=0 disables the per-slice L2 prefetch (A/B)
+        const char* v = std::getenv("TVOLAP_K4_PREFETCH");
+        return v ? std::atoi(v) : 1;
+    }();
+    return cudaLaunchKernelEx(&cfg, partition_warp_kernel<NC>, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk,
+                              k4_prefetch);
 }
 
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
