@@ -348,6 +348,7 @@ def main():
     avg_launch_ms = kern_ms / kern_n if kern_n else float("nan")
     achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
     traffic = None
+    ncu_view = None
     summ = ROOT / "profiles" / f"ncu_summary_{cfg.name}.json"
     if summ.exists():
         try:
@@ -355,6 +356,17 @@ def main():
             # per hop when the capture records it (its launch length may differ from this run's)
             traffic = sj["dram_bytes_per_hop"] * hops_per_launch if sj.get("dram_bytes_per_hop") \
                 else sj.get("dram_bytes_per_launch")
+            # what actually bounds the captured kernel (committed capture, cold caches)
+            k = next((l for l in sj.get("per_launch", []) if "wide_mac" in l.get("name", "")),
+                     (sj.get("per_launch") or [{}])[0])
+            us = k.get("gpu__time_duration.sum")
+            dram = (k.get("dram__bytes_read.sum") or 0) + (k.get("dram__bytes_write.sum") or 0)
+            ncu_view = {"kernel": k.get("name", "")[:60], "source": f"profiles/{summ.name}",
+                        "dram_gbs": dram / (us * 1e-6) / 1e9 if us else None,
+                        "dram_frac": dram / (us * 1e-6) / 1e9 / hbm if us else None,
+                        "fma_pipe_pct": k.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                        "warps_active_pct": k.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                        "top_stalls": k.get("top_stalls")}
         except Exception:
             traffic = None
     if wide:  # time-parallel pass: the MAC/inverse launch dominates; K4 and K1 are separate launches
@@ -368,6 +380,7 @@ def main():
                 "traffic": traffic, "peak_source": peak_src,
                 "kernel": kname,
                 "pass_achieved": bytes_hop * H / (ms_per_step / 1e3) / 1e9,
+                "ncu": ncu_view,
                 "avg_launch_ms": avg_launch_ms, "launches": kern_n, "bytes_per_hop": bytes_hop,
                 "bytes_per_launch": bytes_launch, "distinct_filters_per_hop": distinct,
                 "kernel_share_of_step": kern_ms / prof_elapsed if prof_elapsed else None,
