@@ -212,6 +212,7 @@ struct tvolap_engine {
     size_t wide_scratch_cap = 0, wide_lock_cap = 0, wide_tile_ir_cap = 0;
     int wide_mode = 1;               // TVOLAP_WIDE: 0 off, 1 auto, 2 whenever supported
     uint64_t wide_passes = 0;
+    int pipe_merge = 1;              // TVOLAP_PIPE_MERGE: one H2D copy per run of host-contiguous sets
     int wide_warp_fft = 1;           // TVOLAP_WIDE_WARPFFT: 1 warp FFTs for K1/K5 (0: bit-identical Stockham)
     // chunked host pipeline
     long chunk_hops = 0;
@@ -284,6 +285,7 @@ void pick_launch_config(tvolap_engine* e) {
     e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 1)));
     e->wide_mode = env_int("TVOLAP_WIDE", 1);
     e->wide_warp_fft = env_int("TVOLAP_WIDE_WARPFFT", 1);
+    e->pipe_merge = env_int("TVOLAP_PIPE_MERGE", 1);
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -1060,7 +1062,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         long Kp = nsw;
         if (pinned) {
             const long per = S * period * L * 4 * 2 + (ir_length > 0 ? S * ir_length * 4 : 0);
-            Kp = std::max<long>(1, std::min<long>(nsw, (64L << 20) / per));
+            Kp = std::max<long>(1, std::min<long>(nsw, ((long)env_int("TVOLAP_PIPE_MB", 64) << 20) / per));
         }
         std::vector<const float*> ptrs(nsw);
         std::vector<int> entries(nsw, -1);
@@ -1140,10 +1142,28 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
                 if (c >= 2) CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
                 CK(cudaMemcpy2DAsync(e->swh_x[b], w * sizeof(float), in + h0 * L, in_lane_stride * sizeof(float),
                                      hops * L * sizeof(float), S, cudaMemcpyHostToDevice, e->h2d));
-                for (long k = k0; k < k0 + nk; ++k)
-                    if (irs[k])
-                        CK(cudaMemcpyAsync(const_cast<float*>(ptrs[k]), irs[k], sizeof(float) * S * ir_length,
-                                           cudaMemcpyHostToDevice, e->h2d));
+                // the chunk's sets; runs of sets that are consecutive in host memory (and so in the
+                // staging buffer) go as one copy when they lie in one pinned allocation (the
+                // runtime rejects a range spanning two: then one copy per set)
+                for (long k = k0; k < k0 + nk;) {
+                    if (!irs[k]) {
+                        ++k;
+                        continue;
+                    }
+                    long k2 = k + 1;
+                    while (e->pipe_merge && k2 < k0 + nk && irs[k2] && irs[k2] == irs[k2 - 1] + S * ir_length &&
+                           ptrs[k2] == ptrs[k2 - 1] + S * ir_length)
+                        ++k2;
+                    const size_t set_bytes = sizeof(float) * S * ir_length;
+                    if (cudaMemcpyAsync(const_cast<float*>(ptrs[k]), irs[k], set_bytes * (k2 - k),
+                                        cudaMemcpyHostToDevice, e->h2d) != cudaSuccess) {
+                        (void)cudaGetLastError();  // not sticky: an argument error
+                        for (long kk = k; kk < k2; ++kk)
+                            CK(cudaMemcpyAsync(const_cast<float*>(ptrs[kk]), irs[kk], set_bytes, cudaMemcpyHostToDevice,
+                                               e->h2d));
+                    }
+                    k = k2;
+                }
                 CK(cudaEventRecord(e->ev_in[b], e->h2d));
                 CK(cudaStreamWaitEvent(e->stream, e->ev_in[b], 0));
                 if (c >= 2) CK(cudaStreamWaitEvent(e->stream, e->ev_o[b], 0));  // D2H of chunk c-2 done
