@@ -176,3 +176,25 @@ def test_wide_matches_oracle(monkeypatch):
     ref = np.concatenate(ref).T
     err = np.max(np.abs(y - ref)) / np.max(np.abs(ref))
     assert err <= 1e-4, err  # north-star tolerance (fp32 vs the fp64 reference algorithm)
+
+
+@pytest.mark.parametrize("first_switch", [False, True])
+def test_wide_after_staged_exchange(monkeypatch, first_switch):
+    """A filter staged with exchange_filter before the call is latched at its first hop (irs[0] is
+    None), or superseded when irs[0] names a set (last staged wins, engine.cpp:47)."""
+    hop, S, taps, n, period = 256, 3, 4096, 16 * 5, 16
+    ir0, x, dirs = _case(hop, S, taps, n, period, none_at=() if first_switch else (0,))
+    import torch
+
+    staged = torch.from_numpy(np.random.default_rng(9).standard_normal((S, taps)).astype(np.float32) * 0.05).cuda()
+    a, b = _engines(monkeypatch, ir0, hop)
+    a.process_hops(x[:, : 2 * hop])
+    b.process_hops(x[:, : 2 * hop])
+    a.exchange_ir(staged)
+    b.exchange_ir(staged)
+    ya = a.process_switching(x, dirs, period)
+    yb = _loop(b, x, dirs, period, hop)
+    a.synchronize()
+    b.synchronize()
+    assert a.wide_passes() >= 1
+    assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
