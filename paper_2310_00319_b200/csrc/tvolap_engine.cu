@@ -538,6 +538,9 @@ void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
     }
 }
 
+bool run_wide_bank(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
+                   const int* sched);
+
 void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
                        const int* sched) {
     CK(cudaSetDevice(e->device));
@@ -545,6 +548,10 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
     const long L = e->L, S = e->S, E = e->E;
     const Mem min = classify(in), mout = classify(out);
     const Mem msch = sched ? classify(sched) : Mem::Device;
+    if (min == Mem::Device && mout == Mem::Device && sched && e->bank &&
+        run_wide_bank(e, in, in_stride, out, out_stride, n, sched)) {
+        return;  // a piecewise-constant bank schedule on device buffers: time-parallel passes
+    }
     if (min == Mem::Device && mout == Mem::Device && msch == Mem::Device) {
         launch_hops(e, e->hops, n, in, in_stride, out, out_stride, sched, sched ? S : 0);
     } else {
@@ -728,7 +735,7 @@ int tvolap_create_bank(tvolap_engine** out, int device, long hop, long sources, 
             e->n_bank = n_bank;
             pick_block_geometry(e);
             const long rows = n_bank * ears;
-            e->pool = dalloc<float2>((size_t)rows * M * e->N);
+            e->pool = dalloc<float2>((size_t)rows * M * e->N + (size_t)tvb::kWideTail * e->N);  // + rows read by wide prefetches
             const float* src = stage_ir(e, bank_ir, (size_t)rows * ir_length, e->stream);
             CK(tvb::launch_partition((int)hop, (int)M, rows, src, ir_length, ir_length, e->pool, 0, e->tw, e->pk,
                                      e->stream));
@@ -822,6 +829,71 @@ void ensure_dev(T*& p, size_t& cap, size_t count) {
     cap = count;
 }
 
+// One time-parallel pass over nh hops starting at the engine's current hop: tiles t0 (starts,
+// nh appended), filter sets fs per tile (base of [S][M][2L]) or, with per_lane, per (tile, lane)
+// (base of [M][2L]); tirs (optional): per tile the IR set the tile transforms itself (fused K4).
+void wide_pass(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long nh,
+               const std::vector<int>& t0, const std::vector<const float2*>& fs, bool per_lane,
+               const std::vector<const float*>* tirs, long ir_length, int JH, int nslots, int warp_fft) {
+    const long S = e->S, M = e->M, N = e->N, L = e->L;
+    const long ntiles = (long)t0.size() - 1;
+    ensure_dev(e->d_wide_fset, e->wide_fset_cap, fs.size());
+    ensure_dev(e->d_wide_tile0, e->wide_tile_cap, (size_t)ntiles + 1);
+    CK(cudaMemcpyAsync(e->d_wide_fset, fs.data(), sizeof(const float2*) * fs.size(), cudaMemcpyHostToDevice,
+                       e->stream));
+    CK(cudaMemcpyAsync(e->d_wide_tile0, t0.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice, e->stream));
+    if (tirs) {
+        ensure_dev(e->d_wide_tile_ir, e->wide_tile_ir_cap, (size_t)ntiles);
+        CK(cudaMemcpyAsync(e->d_wide_tile_ir, tirs->data(), sizeof(const float*) * ntiles, cudaMemcpyHostToDevice,
+                           e->stream));
+    }
+    // carry and head terms per tile, extended spectra
+    ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * ntiles * 3 * L);
+    ensure_dev(e->wide_head, e->wide_head_cap, (size_t)S * ntiles * 6 * L);
+    const long T = (nh + 1) / 2 + M + tvb::kWideFront + JH + 4;
+    ensure_dev(e->wide_xe, e->wide_xe_cap, (size_t)S * 2 * T * N);
+    tvb::WideParams p{};
+    p.L = (int)L;
+    p.M = (int)M;
+    p.D = (int)e->D;
+    p.S = (int)S;
+    p.Q = e->QM;
+    p.hop0 = e->hops;
+    p.n = (int)nh;
+    p.in = in;
+    p.in_stride = in_stride;
+    p.out = out;
+    p.out_stride = out_stride;
+    p.ring = e->ring;
+    p.xe = e->wide_xe;
+    p.T = T;
+    p.tbase = (e->hops >> 1) - M - tvb::kWideFront;
+    p.hist = e->hist;
+    p.ola = e->ola;
+    p.tw = e->tw;
+    p.pk = e->pk;
+    p.win = e->win;
+    p.fset = e->d_wide_fset;
+    p.fset_per_lane = per_lane ? 1 : 0;
+    p.tile0 = e->d_wide_tile0;
+    p.ntiles = (int)ntiles;
+    p.tstate = e->wide_state;
+    p.thead = e->wide_head;
+    p.tile_ir = tirs ? e->d_wide_tile_ir : nullptr;
+    p.ir_len = ir_length;
+    p.scratch = e->wide_scratch;
+    p.slot_lock = e->wide_lock;
+    p.nslots = nslots;
+    p.warp_fft = warp_fft;
+    p.stage_ir = env_int("TVOLAP_WIDE_STAGE", 1);
+    cudaEvent_t ev0, ev1;
+    prof_pair(e, &ev0, &ev1);
+    CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
+    e->launches += 4;
+    ++e->wide_passes;
+    e->hops += nh;
+}
+
 // The call as time-parallel passes (chunks of periods whose new sets fit the pool budget): K4
 // of the chunk's sets, K1 of all its hops, then (lane, tile) CTAs for K3+K5 and the OLA fix-up.
 // Same results, bit for bit, as the switching / hop-blocked launches.
@@ -904,62 +976,10 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
             }
         }
         t0.push_back((int)nh);
-        const long ntiles = (long)fs.size();
-        ensure_dev(e->d_wide_fset, e->wide_fset_cap, (size_t)ntiles);
-        ensure_dev(e->d_wide_tile0, e->wide_tile_cap, (size_t)ntiles + 1);
-        CK(cudaMemcpyAsync(e->d_wide_fset, fs.data(), sizeof(const float2*) * ntiles, cudaMemcpyHostToDevice,
-                           e->stream));
-        CK(cudaMemcpyAsync(e->d_wide_tile0, t0.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice, e->stream));
-        if (fuse) {
-            if ((long)tirs.size() != ntiles) throw ApiError{TVOLAP_ERR_CUDA, "wide pass: fused K4 needs one tile per period"};
-            ensure_dev(e->d_wide_tile_ir, e->wide_tile_ir_cap, (size_t)ntiles);
-            CK(cudaMemcpyAsync(e->d_wide_tile_ir, tirs.data(), sizeof(const float*) * ntiles, cudaMemcpyHostToDevice,
-                               e->stream));
-        }
-        // carry and head terms per tile, extended spectra
-        ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * ntiles * 3 * L);
-        ensure_dev(e->wide_head, e->wide_head_cap, (size_t)S * ntiles * 6 * L);
-        const long T = (nh + 1) / 2 + M + tvb::kWideFront + JH + 4;
-        ensure_dev(e->wide_xe, e->wide_xe_cap, (size_t)S * 2 * T * N);
-        tvb::WideParams p{};
-        p.L = (int)L;
-        p.M = (int)M;
-        p.D = (int)e->D;
-        p.S = (int)S;
-        p.Q = e->QM;
-        p.hop0 = e->hops;
-        p.n = (int)nh;
-        p.in = in + h0 * L;
-        p.in_stride = in_stride;
-        p.out = out + h0 * L;
-        p.out_stride = out_stride;
-        p.ring = e->ring;
-        p.xe = e->wide_xe;
-        p.T = T;
-        p.tbase = (e->hops >> 1) - M - tvb::kWideFront;
-        p.hist = e->hist;
-        p.ola = e->ola;
-        p.tw = e->tw;
-        p.pk = e->pk;
-        p.win = e->win;
-        p.fset = e->d_wide_fset;
-        p.tile0 = e->d_wide_tile0;
-        p.ntiles = (int)ntiles;
-        p.tstate = e->wide_state;
-        p.thead = e->wide_head;
-        p.tile_ir = fuse ? e->d_wide_tile_ir : nullptr;
-        p.ir_len = ir_length;
-        p.scratch = e->wide_scratch;
-        p.slot_lock = e->wide_lock;
-        p.nslots = nslots;
-        p.warp_fft = e->wide_warp_fft;
-        p.stage_ir = env_int("TVOLAP_WIDE_STAGE", 1);
-        cudaEvent_t ev0, ev1;
-        prof_pair(e, &ev0, &ev1);
-        CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
-        e->launches += 4;
-        ++e->wide_passes;
-        e->hops += nh;
+        if (fuse && tirs.size() != fs.size())
+            throw ApiError{TVOLAP_ERR_CUDA, "wide pass: fused K4 needs one tile per period"};
+        wide_pass(e, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, false, fuse ? &tirs : nullptr,
+                  ir_length, JH, nslots, e->wide_warp_fft);
         if (fuse && last_ir) {  // the pass's last set becomes the engine's active set (K4 into a pool slot)
             const int slot = (e->active + 1) % kSlots;
             CK(tvb::launch_partition((int)L, (int)M, S, last_ir, ir_length, ir_length, e->pool, (long)slot * S, e->tw,
@@ -991,6 +1011,68 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     }
 }
 
+
+// Bank engines with a per-hop schedule that changes rarely (C1: two IRs alternating every 64
+// hops) on device buffers: time-parallel passes with tiles that never straddle a change of any
+// lane's entry, each tile reading its lanes' bank entries in place. The hop kernels' Stockham
+// transforms keep it bit-identical to the hop-blocked launch (process_hops == process()).
+// Returns false (nothing done) when the engine or schedule does not qualify.
+bool run_wide_bank(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
+                   const int* sched) {
+    const long S = e->S, M = e->M, N = e->N, L = e->L;
+    if (e->wide_mode == 0 || e->E != 1 || !tvb::wide_supported((int)L) || n < 16) return false;
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * 148) return false;
+    std::vector<int> h((size_t)n * S);
+    if (classify(sched) == Mem::Device) {
+        CK(cudaMemcpyAsync(h.data(), sched, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    } else {
+        std::memcpy(h.data(), sched, sizeof(int) * h.size());
+    }
+    // segments: maximal hop ranges over which no lane changes its entry; all >= 3 hops
+    std::vector<long> seg{0};
+    for (long k = 1; k < n; ++k)
+        if (std::memcmp(&h[(size_t)k * S], &h[(size_t)(k - 1) * S], sizeof(int) * S) != 0) seg.push_back(k);
+    seg.push_back(n);
+    long longest = 0;
+    for (size_t i = 0; i + 1 < seg.size(); ++i) {
+        if (seg[i + 1] - seg[i] < 3) return false;
+        longest = std::max(longest, seg[i + 1] - seg[i]);
+    }
+    for (int v : h)
+        if (v < 0 || v >= e->n_bank) return false;  // validated by the caller; never read outside the bank
+    int JH = longest <= 8 ? 4 : 8;
+    if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
+    const long Jmax = 2 * JH;
+    const long xe_mb = env_int("TVOLAP_WIDE_XE_MB", 4096);
+    const long max_hops = std::max<long>(Jmax, (xe_mb << 20) / (long)(S * N * sizeof(float2)) - 2 * (M + 32));
+    const size_t entry_elems = (size_t)e->E * M * N;
+    for (size_t i0 = 0; i0 + 1 < seg.size();) {  // passes of whole segments
+        size_t i1 = i0 + 1;
+        while (i1 + 1 < seg.size() && seg[i1 + 1] - seg[i0] <= max_hops) ++i1;
+        const long h0 = seg[i0], nh = seg[i1] - h0;
+        std::vector<int> t0;
+        std::vector<const float2*> fs;
+        for (size_t i = i0; i < i1; ++i) {
+            const long plen = seg[i + 1] - seg[i];
+            const long tp = (plen + Jmax - 1) / Jmax, base = plen / tp, rem = plen % tp;
+            long st = seg[i] - h0;
+            for (long w = 0; w < tp; ++w) {
+                t0.push_back((int)st);
+                for (long s = 0; s < S; ++s) fs.push_back(e->pool + (size_t)h[(size_t)seg[i] * S + s] * entry_elems);
+                st += base + (w < rem ? 1 : 0);
+            }
+        }
+        t0.push_back((int)nh);
+        wide_pass(e, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, true, nullptr, 0, JH, 0, 0);
+        i0 = i1;
+    }
+    CK(cudaEventRecord(e->ev_main, e->stream));
+    e->fwd += (uint64_t)(S * n);
+    e->inv += (uint64_t)(S * e->E * n);
+    e->macs += (uint64_t)(S * e->E * M * n);
+    return true;
+}
 }  // namespace
 }  // extern "C++"
 

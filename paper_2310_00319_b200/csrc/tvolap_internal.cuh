@@ -65,7 +65,8 @@ struct WideParams {
     const float2* tw;
     const float2* pk;
     const float* win;
-    const float2* const* fset;  // per tile: filter set [S][M][2L]
+    const float2* const* fset;  // per tile: filter set [S][M][2L]; fset_per_lane: per (tile, lane) [M][2L]
+    int fset_per_lane;
     const int* tile0;           // tile k = hops tile0[k] .. tile0[k+1] of the pass (>= 3 hops each)
     int ntiles;
     float* tstate;              // overlap-add carry after each tile [S][ntiles][3][L]

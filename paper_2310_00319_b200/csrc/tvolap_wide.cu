@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
         __syncthreads();  // the set's spectra (global, this CTA's writes) visible to all its threads
         H = Hs;
     } else {
-        H = p.fset[tile] + s * M * N;
+        H = p.fset_per_lane ? p.fset[(long)tile * p.S + s] : p.fset[tile] + s * M * N;
     }
 
     // ---- K3: thread per packed bin k, both parity groups (outputs l0 + g + 2i), JH each.

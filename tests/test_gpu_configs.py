@@ -190,3 +190,21 @@ def test_c2_full_pass_exact_scaling():
     assert torch.isfinite(y1).all() and y1.abs().max().item() > 0
     assert torch.equal(y2, 2 * y1)
     assert torch.equal(y3, y1)
+
+
+def test_c1_device_path_matches_oracle():
+    """C1 on device buffers (bench path: bank schedule alternating every 64 hops -> time-parallel
+    passes), all 3750 hops against the fp64 oracle."""
+    import torch
+
+    cfg = W.CONFIGS["C1"]
+    n, L = cfg.hops, cfg.hop
+    eng = drive.make_engine(cfg)
+    x = torch.from_numpy(W.white(cfg, 0, cfg.sources, 0, n * L)).cuda()
+    sched = torch.from_numpy(W.schedule(cfg, 0, n)).cuda()
+    torch.cuda.synchronize()
+    y = eng.process_hops(x, schedule=sched)
+    eng.synchronize()
+    assert eng.wide_passes() >= 1
+    ref = oracle_config(cfg, n)
+    assert rel_err(y.cpu().numpy(), ref) <= TOL

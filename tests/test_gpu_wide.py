@@ -198,3 +198,60 @@ def test_wide_after_staged_exchange(monkeypatch, first_switch):
     b.synchronize()
     assert a.wide_passes() >= 1
     assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+
+
+def _bank_engines(monkeypatch, bank, hop, S):
+    monkeypatch.setenv("TVOLAP_WIDE", "2")
+    a = T.TvolapBankEngine(bank, hop, S)
+    monkeypatch.setenv("TVOLAP_WIDE", "0")
+    b = T.TvolapBankEngine(bank, hop, S)
+    monkeypatch.delenv("TVOLAP_WIDE")
+    return a, b
+
+
+@pytest.mark.parametrize("hop,S,taps,n_hops,seg", [
+    (128, 1, 4096, 200, 64),   # C1 shape: one lane, two entries alternating every 64 hops
+    (256, 3, 4096, 120, 20),   # several lanes changing together every 20 hops
+    (64, 2, 2048, 90, 7),      # short segments (7-hop tiles), N = 128
+])
+def test_wide_bank_schedule_equals_blocked(monkeypatch, hop, S, taps, n_hops, seg):
+    """Bank engines on device buffers with a piecewise-constant schedule: time-parallel passes
+    (Stockham transforms) == the hop-blocked launch bit for bit, state included."""
+    import torch
+
+    g = np.random.default_rng(3)
+    n_bank = 3
+    bank = (g.standard_normal((n_bank, 1, taps)) * 0.05).astype(np.float32)
+    x = torch.from_numpy(g.uniform(-1, 1, (S, n_hops * hop)).astype(np.float32)).cuda()
+    h = np.arange(n_hops)
+    sched = np.stack([((h // seg) + s) % n_bank for s in range(S)], 1).astype(np.int32)
+    sched_d = torch.from_numpy(sched).cuda()
+    a, b = _bank_engines(monkeypatch, bank, hop, S)
+    a.process_hops(x[:, : 3 * hop], schedule=sched_d[:3])  # (short call: hop-blocked in both)
+    b.process_hops(x[:, : 3 * hop], schedule=sched_d[:3])
+    ya = a.process_hops(x, schedule=sched_d)
+    yb = b.process_hops(x, schedule=sched_d)
+    a.synchronize()
+    b.synchronize()
+    assert a.wide_passes() >= 1 and b.wide_passes() == 0
+    assert np.array_equal(ya.cpu().numpy(), yb.cpu().numpy())
+    za = a.process_hops(x[:, : 20 * hop], schedule=sched_d[:20])
+    zb = b.process_hops(x[:, : 20 * hop], schedule=sched_d[:20])
+    a.synchronize()
+    b.synchronize()
+    assert np.array_equal(za.cpu().numpy(), zb.cpu().numpy())
+    assert a.op_counts() == b.op_counts()
+
+
+def test_wide_bank_random_schedule_stays_blocked(monkeypatch):
+    """A schedule that changes every hop (C3/C5) has no >= 3-hop segments: no pass is taken."""
+    import torch
+
+    g = np.random.default_rng(4)
+    bank = (g.standard_normal((4, 1, 2048)) * 0.05).astype(np.float32)
+    a, _ = _bank_engines(monkeypatch, bank, 128, 2)
+    x = torch.from_numpy(g.uniform(-1, 1, (2, 64 * 128)).astype(np.float32)).cuda()
+    sched = torch.from_numpy(g.integers(0, 4, (64, 2)).astype(np.int32)).cuda()
+    a.process_hops(x, schedule=sched)
+    a.synchronize()
+    assert a.wide_passes() == 0
