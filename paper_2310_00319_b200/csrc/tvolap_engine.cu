@@ -538,7 +538,7 @@ void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
     }
 }
 
-bool run_wide_bank(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
+bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n,
                    const int* sched);
 
 void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
@@ -548,12 +548,14 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
     const long L = e->L, S = e->S, E = e->E;
     const Mem min = classify(in), mout = classify(out);
     const Mem msch = sched ? classify(sched) : Mem::Device;
-    if (min == Mem::Device && mout == Mem::Device && sched && e->bank &&
-        run_wide_bank(e, in, in_stride, out, out_stride, n, sched)) {
-        return;  // a piecewise-constant bank schedule on device buffers: time-parallel passes
-    }
+    // a bank schedule that changes rarely (C1): time-parallel passes instead of the hop-blocked launch
+    auto hops_launch = [&](long hop0, long kc, const float* ip, long is, float* op, long os, const int* sch_launch,
+                           const int* sch_hops) {
+        if (!(sched && e->bank && run_wide_bank(e, hop0, ip, is, op, os, kc, sch_hops)))
+            launch_hops(e, hop0, kc, ip, is, op, os, sch_launch, sched ? S : 0);
+    };
     if (min == Mem::Device && mout == Mem::Device && msch == Mem::Device) {
-        launch_hops(e, e->hops, n, in, in_stride, out, out_stride, sched, sched ? S : 0);
+        hops_launch(e->hops, n, in, in_stride, out, out_stride, sched, sched);
     } else {
         const long per_hop = S * L * (1 + E);
         const long kc_max = std::max<long>(1, std::min<long>(n, (1L << 22) / per_hop));
@@ -619,7 +621,7 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
                 out_ptr = e->d_out[b];
                 out_s = Kc * L;
             }
-            launch_hops(e, e->hops + h0, kc, in_ptr, in_s, out_ptr, out_s, sch_ptr, sched ? S : 0);
+            hops_launch(e->hops + h0, kc, in_ptr, in_s, out_ptr, out_s, sch_ptr, sched ? sched + h0 * S : nullptr);
             CK(cudaEventRecord(e->ev_k[b], e->stream));
             if (mout != Mem::Device) {
                 CK(cudaStreamWaitEvent(e->d2h, e->ev_k[b], 0));
@@ -832,7 +834,7 @@ void ensure_dev(T*& p, size_t& cap, size_t count) {
 // One time-parallel pass over nh hops starting at the engine's current hop: tiles t0 (starts,
 // nh appended), filter sets fs per tile (base of [S][M][2L]) or, with per_lane, per (tile, lane)
 // (base of [M][2L]); tirs (optional): per tile the IR set the tile transforms itself (fused K4).
-void wide_pass(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long nh,
+void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long nh,
                const std::vector<int>& t0, const std::vector<const float2*>& fs, bool per_lane,
                const std::vector<const float*>* tirs, long ir_length, int JH, int nslots, int warp_fft) {
     const long S = e->S, M = e->M, N = e->N, L = e->L;
@@ -858,7 +860,7 @@ void wide_pass(tvolap_engine* e, const float* in, long in_stride, float* out, lo
     p.D = (int)e->D;
     p.S = (int)S;
     p.Q = e->QM;
-    p.hop0 = e->hops;
+    p.hop0 = hop0;
     p.n = (int)nh;
     p.in = in;
     p.in_stride = in_stride;
@@ -867,7 +869,7 @@ void wide_pass(tvolap_engine* e, const float* in, long in_stride, float* out, lo
     p.ring = e->ring;
     p.xe = e->wide_xe;
     p.T = T;
-    p.tbase = (e->hops >> 1) - M - tvb::kWideFront;
+    p.tbase = (hop0 >> 1) - M - tvb::kWideFront;
     p.hist = e->hist;
     p.ola = e->ola;
     p.tw = e->tw;
@@ -891,7 +893,6 @@ void wide_pass(tvolap_engine* e, const float* in, long in_stride, float* out, lo
     CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
     e->launches += 4;
     ++e->wide_passes;
-    e->hops += nh;
 }
 
 // The call as time-parallel passes (chunks of periods whose new sets fit the pool budget): K4
@@ -978,8 +979,9 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         t0.push_back((int)nh);
         if (fuse && tirs.size() != fs.size())
             throw ApiError{TVOLAP_ERR_CUDA, "wide pass: fused K4 needs one tile per period"};
-        wide_pass(e, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, false, fuse ? &tirs : nullptr,
-                  ir_length, JH, nslots, e->wide_warp_fft);
+        wide_pass(e, e->hops, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, false,
+                  fuse ? &tirs : nullptr, ir_length, JH, nslots, e->wide_warp_fft);
+        e->hops += nh;
         if (fuse && last_ir) {  // the pass's last set becomes the engine's active set (K4 into a pool slot)
             const int slot = (e->active + 1) % kSlots;
             CK(tvb::launch_partition((int)L, (int)M, S, last_ir, ir_length, ir_length, e->pool, (long)slot * S, e->tw,
@@ -1016,8 +1018,9 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
 // hops) on device buffers: time-parallel passes with tiles that never straddle a change of any
 // lane's entry, each tile reading its lanes' bank entries in place. The hop kernels' Stockham
 // transforms keep it bit-identical to the hop-blocked launch (process_hops == process()).
-// Returns false (nothing done) when the engine or schedule does not qualify.
-bool run_wide_bank(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
+// Returns false (nothing done) when the engine or schedule does not qualify. `sched` may be host or
+// device memory; hop0 is the global index of the call's first hop.
+bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n,
                    const int* sched) {
     const long S = e->S, M = e->M, N = e->N, L = e->L;
     if (e->wide_mode == 0 || e->E != 1 || !tvb::wide_supported((int)L) || n < 16) return false;
@@ -1064,14 +1067,11 @@ bool run_wide_bank(tvolap_engine* e, const float* in, long in_stride, float* out
             }
         }
         t0.push_back((int)nh);
-        wide_pass(e, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, true, nullptr, 0, JH, 0, 0);
+        wide_pass(e, hop0 + h0, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, true, nullptr, 0, JH, 0,
+                  0);
         i0 = i1;
     }
-    CK(cudaEventRecord(e->ev_main, e->stream));
-    e->fwd += (uint64_t)(S * n);
-    e->inv += (uint64_t)(S * e->E * n);
-    e->macs += (uint64_t)(S * e->E * M * n);
-    return true;
+    return true;  // (the caller accounts hops, counts and the latched selection)
 }
 }  // namespace
 }  // extern "C++"

@@ -240,7 +240,33 @@ def test_wide_bank_schedule_equals_blocked(monkeypatch, hop, S, taps, n_hops, se
     a.synchronize()
     b.synchronize()
     assert np.array_equal(za.cpu().numpy(), zb.cpu().numpy())
+    # the schedule's last row stays latched for later process() calls (no schedule)
+    xs = x.cpu().numpy()
+    for k in range(3):
+        blk = np.ascontiguousarray(xs[:, k * hop:(k + 1) * hop].T)
+        assert np.array_equal(a.process(blk), b.process(blk))
     assert a.op_counts() == b.op_counts()
+
+
+def test_wide_bank_pinned_host_pipeline(monkeypatch):
+    """Pinned host buffers + host schedule (the C1 e2e path): each pipeline chunk runs as a
+    time-parallel pass; equal bit for bit to the device call on the hop-blocked launch."""
+    import torch
+
+    g = np.random.default_rng(5)
+    hop, S, taps, n = 128, 1, 8192, 300
+    bank = (g.standard_normal((2, 1, taps)) * 0.05).astype(np.float32)
+    xs = g.uniform(-1, 1, (S, n * hop)).astype(np.float32)
+    sched = ((np.arange(n) // 64) % 2).astype(np.int32)[:, None]
+    a, b = _bank_engines(monkeypatch, bank, hop, S)
+    xh = torch.from_numpy(xs).pin_memory()
+    yh = torch.empty(xh.shape, dtype=torch.float32).pin_memory()
+    a.process_hops(xh, out=yh, schedule=sched)
+    a.synchronize()
+    yd = b.process_hops(torch.from_numpy(xs).cuda(), schedule=torch.from_numpy(sched).cuda())
+    b.synchronize()
+    assert a.wide_passes() >= 1
+    assert np.array_equal(yh.numpy(), yd.cpu().numpy())
 
 
 def test_wide_bank_random_schedule_stays_blocked(monkeypatch):
