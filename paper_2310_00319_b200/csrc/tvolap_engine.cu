@@ -540,6 +540,7 @@ void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
 
 bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n,
                    const int* sched);
+bool run_wide_set(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n);
 
 void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
                        const int* sched) {
@@ -551,8 +552,9 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
     // a bank schedule that changes rarely (C1): time-parallel passes instead of the hop-blocked launch
     auto hops_launch = [&](long hop0, long kc, const float* ip, long is, float* op, long os, const int* sch_launch,
                            const int* sch_hops) {
-        if (!(sched && e->bank && run_wide_bank(e, hop0, ip, is, op, os, kc, sch_hops)))
-            launch_hops(e, hop0, kc, ip, is, op, os, sch_launch, sched ? S : 0);
+        if (sched && e->bank && run_wide_bank(e, hop0, ip, is, op, os, kc, sch_hops)) return;
+        if (!sched && !e->bank && run_wide_set(e, hop0, ip, is, op, os, kc)) return;
+        launch_hops(e, hop0, kc, ip, is, op, os, sch_launch, sched ? S : 0);
     };
     if (min == Mem::Device && mout == Mem::Device && msch == Mem::Device) {
         hops_launch(e->hops, n, in, in_stride, out, out_stride, sched, sched);
@@ -1072,6 +1074,41 @@ bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride,
         i0 = i1;
     }
     return true;  // (the caller accounts hops, counts and the latched selection)
+}
+
+// Filter-set engines: a process_hops call (one filter for all its hops) on device buffers or a
+// pinned-pipeline chunk as one time-parallel pass over the active set, with the hop kernels'
+// Stockham transforms (bit-identical to the hop-blocked launch). False when not eligible.
+bool run_wide_set(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n) {
+    const long S = e->S, M = e->M, N = e->N, L = e->L;
+    if (e->wide_mode == 0 || e->E != 1 || !tvb::wide_supported((int)L) || n < 32) return false;
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * 148) return false;
+    if (e->launch_new_ir) return false;  // a staged set the first hop launch transforms (K4 fused mode)
+    int JH = 8;
+    if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
+    const long Jmax = 2 * JH;
+    const long xe_mb = env_int("TVOLAP_WIDE_XE_MB", 4096);
+    const long max_hops = std::max<long>(Jmax, (xe_mb << 20) / (long)(S * N * sizeof(float2)) - 2 * (M + 32));
+    const float2* set = e->pool + (size_t)e->active * S * M * N;
+    for (long h0 = 0; h0 < n;) {
+        long nh = std::min(max_hops, n - h0);
+        if (n - h0 - nh > 0 && n - h0 - nh < 3) nh -= 3;  // no 1-2 hop pass at the end
+        const long tp = (nh + Jmax - 1) / Jmax, base = nh / tp, rem = nh % tp;
+        std::vector<int> t0;
+        std::vector<const float2*> fs;
+        long st = 0;
+        for (long w = 0; w < tp; ++w) {
+            t0.push_back((int)st);
+            fs.push_back(set);
+            st += base + (w < rem ? 1 : 0);
+        }
+        t0.push_back((int)nh);
+        wide_pass(e, hop0 + h0, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, false, nullptr, 0, JH, 0,
+                  0);
+        h0 += nh;
+    }
+    CK(cudaEventRecord(e->ev_slot[e->active], e->stream));  // the last reader of the active slot
+    return true;
 }
 }  // namespace
 }  // extern "C++"

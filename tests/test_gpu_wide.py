@@ -281,3 +281,26 @@ def test_wide_bank_random_schedule_stays_blocked(monkeypatch):
     a.process_hops(x, schedule=sched)
     a.synchronize()
     assert a.wide_passes() == 0
+
+
+@pytest.mark.parametrize("hop,S,taps,n_hops", [(256, 2, 4096, 200), (128, 1, 8192, 97), (512, 3, 16384, 64)])
+def test_wide_set_process_hops_equals_one_hop(monkeypatch, hop, S, taps, n_hops):
+    """Filter-set engines: a device-resident process_hops call runs as a time-parallel pass and
+    equals hop-by-hop process() bit for bit (and the state it leaves behind)."""
+    import torch
+
+    g = np.random.default_rng(6)
+    ir = g.standard_normal((taps, S)) * 0.05
+    monkeypatch.setenv("TVOLAP_WIDE", "2")
+    a = T.TvolapEngine(T.partition(ir, hop))
+    monkeypatch.delenv("TVOLAP_WIDE")
+    b = T.TvolapEngine(T.partition(ir, hop))
+    xs = g.uniform(-1, 1, (S, (n_hops + 5) * hop)).astype(np.float32)
+    ya = a.process_hops(torch.from_numpy(np.ascontiguousarray(xs[:, : n_hops * hop])).cuda())
+    a.synchronize()
+    assert a.wide_passes() >= 1
+    yb = np.concatenate([b.process(np.ascontiguousarray(xs[:, k * hop:(k + 1) * hop].T)).T for k in range(n_hops)], 1)
+    assert np.array_equal(ya.cpu().numpy(), yb)
+    for k in range(n_hops, n_hops + 5):  # the carry, history and delay line handed on
+        blk = np.ascontiguousarray(xs[:, k * hop:(k + 1) * hop].T)
+        assert np.array_equal(a.process(blk), b.process(blk))
