@@ -94,7 +94,11 @@ int tvolap_process(tvolap_engine* e, const float* in, long in_lane_stride, long 
  * samples per lane. schedule (bank engines only, may be NULL) gives the bank
  * entry of every (hop, source): schedule[h * sources + s]; when NULL the
  * current selection holds for all hops. Host pointers are streamed through
- * pinned staging buffers with copies overlapping the kernels.
+ * pinned staging buffers with copies overlapping the kernels. With few channels
+ * (channels x cluster CTAs <= 2 per SM) the hops run as time-parallel passes
+ * (filter-set engines: calls of >= 32 hops; bank engines: schedules that only
+ * change every >= 3 hops), bit-identical to the hop-blocked launch and to
+ * process(); tvolap_wide_passes counts them.
  */
 int tvolap_process_hops(tvolap_engine* e, const float* in, long in_lane_stride, float* out, long out_lane_stride,
                         long n_hops, const int32_t* schedule);
