@@ -560,7 +560,7 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
         hops_launch(e->hops, n, in, in_stride, out, out_stride, sched, sched);
     } else {
         const long per_hop = S * L * (1 + E);
-        const long kc_max = std::max<long>(1, std::min<long>(n, (1L << 22) / per_hop));
+        const long kc_max = std::max<long>(1, std::min<long>(n, (1L << env_int("TVOLAP_PIPE_LOG2", 25)) / per_hop));
         ensure_pipeline(e, kc_max, sched && msch != Mem::Device);
         const long Kc = e->chunk_hops;
         CK(cudaEventRecord(e->ev_start, e->stream));
