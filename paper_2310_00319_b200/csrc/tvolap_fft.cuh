@@ -384,8 +384,9 @@ __host__ __device__ constexpr int bitrev_c(int x, int bits) {
 // DFT across those lanes with shuffles. The result is left in natural order in buf[0 .. N).
 // tw4 = the four-step tables (fft_warp_twiddles). Roughly half the instructions of the
 // radix-8 Stockham passes and no CTA barriers.
-template <bool INV, int N, bool PRUNE, int NB = 1, class LOAD>
+template <bool INV, int N, bool PRUNE, int NB = 1, class LOAD, bool INPLACE = false>
 __device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict__ tw4, int lane, const LOAD& load) {
+    // INPLACE: `load` may read `buf` (every lane's inputs are loaded before any lane stores)
     // NB transforms in lockstep (independent instruction streams for ILP): transform t uses
     // buf + t N and reads its input through load(t, n).
     static_assert(N >= 64 && N <= 1024, "warp FFT covers 64..1024 points");
@@ -397,6 +398,7 @@ __device__ __forceinline__ void fft_warp4(float2* buf, const float2* __restrict_
 #pragma unroll
         for (int n1 = 0; n1 < N1; ++n1)
             v[t][n1] = (PRUNE && n1 >= N1 / 2) ? make_float2(0.f, 0.f) : load(t, 32 * n1 + lane);
+    if constexpr (INPLACE) __syncwarp();
 #pragma unroll
     for (int t = 0; t < NB; ++t) {
         dft_reg<INV, N1, PRUNE>(v[t]);

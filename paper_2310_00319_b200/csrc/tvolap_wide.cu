@@ -507,14 +507,25 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
         // the warp four-step inverse FFT writes the time-domain frame over its own Y row
         // (only this warp reads that row)
         const int warp = tid >> 5, lane = tid & 31;
-        float2* wb = s_fa + (size_t)warp * N;
-        for (int jj = warp; jj < jt; jj += NT >> 5) {
-            float2* yrow = s_y + (size_t)jj * N;
-            for (int kk = lane; kk < N; kk += 32) wb[kk] = tangle_packed(yrow, N, kk, s_pk);
-            __syncwarp();
-            if constexpr (N >= 64 && N <= 1024)
-                fft_warp4<true, N, false>(yrow, p.tw + N, lane, [&](int, int n) { return wb[n]; });
-            __syncwarp();
+        if constexpr (N >= 64 && N <= 512 && J == 16) {
+            // two frames per warp in lockstep (rows 2w, 2w + 1 are contiguous), the tangle computed
+            // in the transform's loads, results written over the two Y rows (in place)
+            const int jj = 2 * warp;
+            if (jj < jt) {
+                float2* rows = s_y + (size_t)jj * N;
+                auto ld = [&](int t, int n) { return tangle_packed(rows + (size_t)t * N, N, n, s_pk); };
+                fft_warp4<true, N, false, 2, decltype(ld), true>(rows, p.tw + N, lane, ld);
+            }
+        } else {
+            float2* wb = s_fa + (size_t)warp * N;
+            for (int jj = warp; jj < jt; jj += NT >> 5) {
+                float2* yrow = s_y + (size_t)jj * N;
+                for (int kk = lane; kk < N; kk += 32) wb[kk] = tangle_packed(yrow, N, kk, s_pk);
+                __syncwarp();
+                if constexpr (N >= 64 && N <= 1024)
+                    fft_warp4<true, N, false>(yrow, p.tw + N, lane, [&](int, int n) { return wb[n]; });
+                __syncwarp();
+            }
         }
         __syncthreads();
         ola(reinterpret_cast<const float*>(s_y), 2 * (size_t)N, 0, jt);
