@@ -146,25 +146,43 @@ __global__ void __launch_bounds__(256) wide_forward_warp_kernel(const WideParams
     for (int i = tid; i < N; i += blockDim.x) s_win[i] = p.win[i];
     for (int i = tid; i <= N; i += blockDim.x) s_pk[i] = p.pk[i];
     __syncthreads();
-    float2* buf = bufs + (size_t)warp * N;
+    // two frames per warp in lockstep (independent FFT chains): pairs (2q, 2q + 1) of the
+    // lane-major frame order; a lone last frame is computed twice and stored once
+    float2* buf = bufs + (size_t)warp * 2 * N;
     const long frames = (long)p.S * p.n;
+    const long pairs = (frames + 1) / 2;
     const long ring_from = p.hop0 + p.n - 2L * p.D;
-    for (long f = (long)blockIdx.x * nw + warp; f < frames; f += (long)gridDim.x * nw) {
-        const long s = f / p.n;
-        const int r = (int)(f - s * p.n);
-        const float* prev = r == 0 ? p.hist + s * L : p.in + s * p.in_stride + (long)(r - 1) * L;
-        const float* cur = p.in + s * p.in_stride + (long)r * L;
-        auto load0 = [&](int, int n) -> float2 {  // z_n = (x[2n] w[2n], x[2n+1] w[2n+1]), n < L
+    for (long q = (long)blockIdx.x * nw + warp; q < pairs; q += (long)gridDim.x * nw) {
+        const float* prev[2];
+        const float* cur[2];
+        long sf[2], jf[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const long f = min(2 * q + t, frames - 1);
+            const long s = f / p.n;
+            const int r = (int)(f - s * p.n);
+            prev[t] = r == 0 ? p.hist + s * L : p.in + s * p.in_stride + (long)(r - 1) * L;
+            cur[t] = p.in + s * p.in_stride + (long)r * L;
+            sf[t] = s;
+            jf[t] = p.hop0 + r;
+        }
+        auto load2 = [&](int t, int n) -> float2 {  // z_n = (x[2n] w[2n], x[2n+1] w[2n+1]), n < L
             const int e = 2 * n;
-            const float* src = e < L ? prev + e : cur + (e - L);
+            const float* src = e < L ? prev[t] + e : cur[t] + (e - L);
             return make_float2(src[0] * s_win[e], src[1] * s_win[e + 1]);
         };
-        fft_warp4<false, N, true>(buf, p.tw + N, lane, load0);
-        const long j = p.hop0 + r;
-        const int par = (int)(j & 1);
-        untangle_pairs_warp(buf, N, s_pk, p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N, lane);
-        if (j >= ring_from)
-            untangle_pairs_warp(buf, N, s_pk, p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N, lane);
+        fft_warp4<false, N, true, 2>(buf, p.tw + N, lane, load2);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (2 * q + t >= frames) break;
+            const long j = jf[t], s = sf[t];
+            const int par = (int)(j & 1);
+            untangle_pairs_warp(buf + (size_t)t * N, N, s_pk, p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N,
+                                lane);
+            if (j >= ring_from)
+                untangle_pairs_warp(buf + (size_t)t * N, N, s_pk,
+                                    p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N, lane);
+        }
         __syncwarp();
     }
 }
@@ -608,7 +626,7 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
         wide_head_kernel<<<grid_cap((long)p.S * 2 * (p.M + 2) * (NC / 2), 256), 256, 0, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         if (p.warp_fft && NC >= 64 && NC <= 1024) {
-            const size_t smem = a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) + 8 * (size_t)NC * sizeof(float2);
+            const size_t smem = a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) + 16 * (size_t)NC * sizeof(float2);
             if ((err = cudaFuncSetAttribute(wide_forward_warp_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem)) != cudaSuccess)
                 return err;
@@ -616,8 +634,8 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
             if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_forward_warp_kernel<NC>, 256, smem)) !=
                 cudaSuccess)
                 return err;
-            const long frames = (long)p.S * p.n;
-            const long grid = std::max<long>(1, std::min<long>((frames + 7) / 8, (long)sm_count() * std::max(1, per_sm)));
+            const long pairs = ((long)p.S * p.n + 1) / 2;
+            const long grid = std::max<long>(1, std::min<long>((pairs + 7) / 8, (long)sm_count() * std::max(1, per_sm)));
             wide_forward_warp_kernel<NC><<<(unsigned)grid, 256, smem, stream>>>(p);
             if ((err = cudaGetLastError()) != cudaSuccess) return err;
             return launch_wide_t<NC>(p, JH, stream, t0, t1, parts & ~1);
