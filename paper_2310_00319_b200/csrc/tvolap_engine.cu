@@ -732,6 +732,9 @@ int tvolap_create_bank(tvolap_engine** out, int device, long hop, long sources, 
         require_device(device);
         const long slice = 2 * hop;
         const long M = std::max((ir_length + slice - 1) / slice, std::max<long>(min_partitions, 1));
+        // the bank kernels address the spectra with 32-bit float4 offsets (<= 64 GB of spectra)
+        if ((double)n_bank * ears * M * hop >= 4294967296.0)
+            throw ApiError{TVOLAP_ERR_INVALID_CONFIGURATION, "bank too large (over 2^32 float4 of spectra)"};
         e = new tvolap_engine();
         try {
             init_common(e, device, hop, sources, ears, M);
