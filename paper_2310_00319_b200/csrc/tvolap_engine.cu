@@ -864,7 +864,9 @@ void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, flo
     p.M = (int)M;
     p.D = (int)e->D;
     p.S = (int)S;
-    p.Q = e->QM;
+    // partition groups: the hop-blocked kernel's (bit-identical sums) with its Stockham transforms;
+    // one chain with the warp transforms (equal to fp32 rounding anyway; TVOLAP_WIDE_Q overrides)
+    p.Q = env_int("TVOLAP_WIDE_Q", warp_fft ? 1 : e->QM);
     p.hop0 = hop0;
     p.n = (int)nh;
     p.in = in;
@@ -930,7 +932,8 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     const bool fuse = env_int("TVOLAP_WIDE_FUSE", 1) != 0 && period <= Jmax && period >= 3;
     int nslots = 0;
     if (fuse) {
-        nslots = tvb::wide_mac_ctas_per_sm((int)L, JH, (int)M, e->QM) * sm_count_of(e->device);
+        const int q_launch = env_int("TVOLAP_WIDE_Q", e->wide_warp_fft ? 1 : e->QM);  // as wide_pass sets it
+        nslots = tvb::wide_mac_ctas_per_sm((int)L, JH, (int)M, q_launch) * sm_count_of(e->device);
         if (nslots <= 0) throw ApiError{TVOLAP_ERR_CUDA, "wide pass: no resident CTA for the MAC kernel"};
         ensure_dev(e->wide_scratch, e->wide_scratch_cap, (size_t)nslots * (M + tvb::kWideTail) * N);
         if (e->wide_lock_cap < (size_t)nslots) {
