@@ -337,7 +337,10 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     // The m loop is unrolled by JH so the sliding window rotates by register renaming (output i
     // at unrolled step u reads win[(i - u) mod JH]); loads run kPf steps ahead in registers.
     // Partition-group partials accumulate in the thread's own column of s_y (rows = outputs).
-    constexpr int kPf = 2;  // divides JH
+#ifndef TVOLAP_WIDE_KPF
+#define TVOLAP_WIDE_KPF 2  // (diagnostic builds: _build.build_variant(..., ["TVOLAP_WIDE_KPF=4"]))
+#endif
+    constexpr int kPf = TVOLAP_WIDE_KPF;  // divides JH
     const float2* X[2];
     long bse[2];
 #pragma unroll
