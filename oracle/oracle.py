@@ -4,18 +4,28 @@ The oracle restates the reference hot path (proj/src/spectral.cpp, partition.cpp
 engine.cpp) in plain C++; see oracle/tvolap_oracle.cpp for the line citations.
 Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs import this
 module. The product package never does.
+
+`using("ref")` switches the same API onto oracle/_ref/libtvolap_ref.so: the
+reference's OWN spectral/partition/engine sources compiled unmodified against a
+minimal Eigen stand-in (oracle/Makefile `ref`, oracle/ref_harness.cpp). That is
+what pins the restatement (tests/test_ref_pin.py) and what bench.py's reference
+arm times. The comparison convolvers and direct_convolve exist only in the port.
 """
 from __future__ import annotations
 
 import ctypes as C
 import subprocess
+from contextlib import contextmanager
 from pathlib import Path
 
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
 _SO = HERE / "liboracle.so"
-_lib = None
+_REF_SO = HERE / "_ref" / "libtvolap_ref.so"
+_libs = {}
+_which = "port"
+_lib = None  # the port, once loaded (kept for the __del__ guards below)
 
 
 class OracleError(ValueError):
@@ -28,12 +38,31 @@ def build() -> None:
     subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
 
 
+def ref_available() -> bool:
+    """oracle/_ref/libtvolap_ref.so exists (built here from /root/reference, shipped to the box)."""
+    return _REF_SO.exists()
+
+
+@contextmanager
+def using(which):
+    """Run the enclosed oracle calls on "port" (the restatement) or "ref" (the reference itself)."""
+    global _which
+    prev, _which = _which, which
+    try:
+        yield
+    finally:
+        _which = prev
+
+
 def lib():
     global _lib
-    if _lib is None:
-        if not _SO.exists():
+    if _which not in _libs:
+        path = _SO if _which == "port" else _REF_SO
+        if _which == "port" and not _SO.exists():
             build()
-        L = C.CDLL(str(_SO))
+        if not path.exists():
+            raise OracleError(3, f"{path} not built (oracle/Makefile target `ref` needs /root/reference)")
+        L = C.CDLL(str(path))
         vp, lg, ip = C.c_void_p, C.c_long, C.c_int
         L.orc_last_error.restype = C.c_char_p
         L.orc_forward_real.argtypes = [lg, vp, vp]
@@ -58,17 +87,20 @@ def lib():
         L.orc_engine_reset.argtypes = [vp]
         L.orc_engine_geometry.argtypes = [vp, vp]
         L.orc_engine_op_counts.argtypes = [vp, vp]
-        L.orc_direct_convolve.argtypes = [vp, lg, vp, lg, vp]
+        if hasattr(L, "orc_direct_convolve"):
+            L.orc_direct_convolve.argtypes = [vp, lg, vp, lg, vp]
         L.orc_run_workload.argtypes = [lg, lg, lg, lg, lg, vp, lg, ip, vp, lg, lg, lg, vp, vp, vp, lg, ip,
                                        C.POINTER(ip)]
         L.orc_run_workload.restype = C.c_double
-        _lib = L
-    return _lib
+        _libs[_which] = L
+        if _which == "port":
+            _lib = L
+    return _libs[_which]
 
 
-def _chk(rc):
+def _chk(rc, L=None):
     if rc:
-        raise OracleError(rc, lib().orc_last_error().decode())
+        raise OracleError(rc, (L or lib()).orc_last_error().decode())
 
 
 def _d(x):
@@ -117,33 +149,34 @@ class FilterSet:
         taps = np.ascontiguousarray(h.T)
         st = C.c_int()
         ptr = taps.ctypes.data if taps.size else None
-        self._h = lib().orc_partition(ptr, h.shape[0], h.shape[1] if h.ndim == 2 else 0, hop, min_partitions,
-                                      C.byref(st))
-        _chk(st.value)
+        self._L = lib()
+        self._h = self._L.orc_partition(ptr, h.shape[0], h.shape[1] if h.ndim == 2 else 0, hop, min_partitions,
+                                        C.byref(st))
+        _chk(st.value, self._L)
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib is not None:
-            _lib.orc_set_free(self._h)
+        if getattr(self, "_h", None):
+            self._L.orc_set_free(self._h)
 
     @property
     def partition_count(self):
-        return lib().orc_set_partition_count(self._h)
+        return self._L.orc_set_partition_count(self._h)
 
     @property
     def channels(self):
-        return lib().orc_set_channels(self._h)
+        return self._L.orc_set_channels(self._h)
 
     @property
     def hop(self):
-        return lib().orc_set_hop(self._h)
+        return self._L.orc_set_hop(self._h)
 
     @property
     def source_length(self):
-        return lib().orc_set_source_length(self._h)
+        return self._L.orc_set_source_length(self._h)
 
     @property
     def normalization_gain(self):
-        return lib().orc_set_gain(self._h)
+        return self._L.orc_set_gain(self._h)
 
     def transform_length(self):
         return 4 * self.hop
@@ -153,12 +186,12 @@ class FilterSet:
 
     def spectra(self):
         out = np.empty((self.channels, self.partition_count, 2 * self.hop + 1, 2))
-        lib().orc_set_spectra(self._h, out.ctypes.data)
+        self._L.orc_set_spectra(self._h, out.ctypes.data)
         return out[..., 0] + 1j * out[..., 1]
 
     def reassemble(self):
         out = np.empty((self.channels, 2 * self.hop * self.partition_count))
-        _chk(lib().orc_reassemble(self._h, out.ctypes.data))
+        _chk(self._L.orc_reassemble(self._h, out.ctypes.data), self._L)
         return out.T.copy()  # (taps, channels), like ImpulseResponse
 
 
@@ -172,16 +205,17 @@ class Engine:
     def __init__(self, filter_set):
         st = C.c_int()
         self._set = filter_set
-        self._h = lib().orc_engine_create(filter_set._h if filter_set is not None else None, C.byref(st))
-        _chk(st.value)
+        self._L = lib()
+        self._h = self._L.orc_engine_create(filter_set._h if filter_set is not None else None, C.byref(st))
+        _chk(st.value, self._L)
 
     def __del__(self):
-        if getattr(self, "_h", None) and _lib is not None:
-            _lib.orc_engine_free(self._h)
+        if getattr(self, "_h", None):
+            self._L.orc_engine_free(self._h)
 
     def _geo(self):
         g = np.empty(7, dtype=np.int64)
-        lib().orc_engine_geometry(self._h, g.ctypes.data)
+        self._L.orc_engine_geometry(self._h, g.ctypes.data)
         return g
 
     def hop(self):
@@ -212,20 +246,20 @@ class Engine:
         rows, cols = x.shape
         xf = np.ascontiguousarray(x.T)
         out = np.empty((max(cols, 1), max(rows, 1)))
-        _chk(lib().orc_engine_process(self._h, xf.ctypes.data if xf.size else None, max(rows, 1), rows, cols,
-                                      out.ctypes.data, max(rows, 1)))
+        _chk(self._L.orc_engine_process(self._h, xf.ctypes.data if xf.size else None, max(rows, 1), rows, cols,
+                                        out.ctypes.data, max(rows, 1)), self._L)
         return out.T.copy()
 
     def exchange_filter(self, filter_set):
         self._next = filter_set
-        _chk(lib().orc_engine_exchange(self._h, filter_set._h if filter_set is not None else None))
+        _chk(self._L.orc_engine_exchange(self._h, filter_set._h if filter_set is not None else None), self._L)
 
     def reset(self):
-        lib().orc_engine_reset(self._h)
+        self._L.orc_engine_reset(self._h)
 
     def op_counts(self):
         c = np.empty(3, dtype=np.uint64)
-        lib().orc_engine_op_counts(self._h, c.ctypes.data)
+        self._L.orc_engine_op_counts(self._h, c.ctypes.data)
         return tuple(int(v) for v in c)
 
 

@@ -76,12 +76,19 @@ def build_variant(name: str, defines, verbose: bool = False) -> Path:
     return out
 
 
+REFERENCE = Path("/root/reference/proj")
+
+
 def build_oracle(force: bool = False) -> None:
-    """TEST INFRASTRUCTURE: the fp64 CPU oracle (oracle/Makefile)."""
+    """TEST INFRASTRUCTURE: the fp64 CPU oracle (oracle/Makefile) and, where /root/reference
+    exists (this container, not the GPU box, which uses the prebuilt file), oracle/_ref: the
+    reference's own hot-path sources compiled unmodified against the Eigen stand-in."""
     args = ["make", "-s", "-C", ROOT / "oracle"]
     if force:
         args.insert(2, "-B")
     _run(args)
+    if (REFERENCE / "src" / "engine.cpp").exists():
+        _run(args + ["ref"])
 
 
 if __name__ == "__main__":

@@ -10,8 +10,23 @@ from paper_2310_00319_b200 import workload as W
 
 
 def oracle_config(cfg: W.Config, n_hops: int, lane0: int = 0, sources: Optional[int] = None,
-                  subset: Optional[Sequence[int]] = None, threads: Optional[int] = None):
-    """Oracle outputs (len(subset)*ears, n_hops*L) for sources lane0+subset[i]; fp32-rounded inputs/IRs."""
+                  subset: Optional[Sequence[int]] = None, threads: Optional[int] = None,
+                  which: Optional[str] = None):
+    """Oracle outputs (len(subset)*ears, n_hops*L) for sources lane0+subset[i]; fp32-rounded inputs/IRs.
+
+    which="ref" runs the reference's own engine (oracle/_ref, see oracle/oracle.py), "port" the
+    restatement; default: the reference itself when its library is present (tests/test_ref_pin.py
+    proves the two bit-identical)."""
+    with O.using(which or best_oracle()):
+        return _oracle_config(cfg, n_hops, lane0, sources, subset, threads)
+
+
+def best_oracle() -> str:
+    """"ref" (the reference's own sources, oracle/_ref) when built, else "port"."""
+    return "ref" if O.ref_available() else "port"
+
+
+def _oracle_config(cfg, n_hops, lane0, sources, subset, threads):
     sources = cfg.sources if sources is None else sources
     subset = list(range(sources)) if subset is None else list(subset)
     L = cfg.hop
