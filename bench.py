@@ -1,26 +1,38 @@
 #!/usr/bin/env python
 """Benchmark of the TVOLAP hot path on B200 (BASELINE.json metric).
 
-metric: convolved channel-samples/s. Workload: BASELINE config C2 (configs[1]):
-64 independent channels, fp32, L=256, M=64 (IR 32768 taps), each channel
-switching to a freshly seeded IR every 16 blocks, 30 s of white noise per
-channel = 5625 hops. One step = one full 30 s pass from zero state: the 352
-exchange_filter + process_hops(16 hops) drive() loop as one tvolap_process_switching
-call on device-resident inputs (run as a time-parallel pass: K4 of all 352 sets,
-K1 of all hops, one MAC/inverse CTA per (channel, 16-hop period)).
-Multi-GPU (torchrun): one process per GPU, each rank runs its own 64 channels
-(lanes rank*64 ..), no data-path collective — weak scaling; time = max over
-ranks of CUDA-event time.
+metric: convolved channel-samples/s (lanes x hops x L / time), at 1/2/4/8 GPUs, next to the
+reference's CPU path on the box's host cores.
 
-Prints ONE JSON line on rank 0. `--impl reference` times the reference
-algorithm's CPU path (the fp64 oracle port; the C++ reference itself needs
-Eigen and cannot be built here) on the box's host cores instead.
+Default workload: BASELINE config C5 (configs[4]) — the largest single-GPU config: 4096
+channels, fp32, L=32 (4L=128 FFT), M=512 partitions (IR 32768 taps), every channel picking a
+seeded-random entry of a 1024-IR bank (T60 0.4 s) every block, 10 s of white noise = 15000 hops.
+One step = one full 10-s pass from zero state: tvolap_process_hops with the per-hop bank schedule
+on device-resident inputs (run as bank passes: K1 of every hop, the MAC over (tile, channel,
+partition group) CTAs, K5 + overlap-add per (tile, channel)). `--config C1..C4` runs the others.
+
+Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run, one process per GPU, NCCL);
+channels are sharded across ranks (`--scaling strong`, default: the config's channels split N
+ways; `weak`: every rank runs a whole config). No data-path collective except C3's stereo mix,
+reduced with NCCL (tvolap_mix_allreduce). Time = max over ranks of CUDA-event time.
+
+JSON line keys beyond the base contract:
+  roofline   measured sides of the dominant kernel: HBM (ncu DRAM bytes), L2 (ncu L2->SM bytes)
+             and FP32 (reference cost model flops), each over the live per-launch time; `bound`
+             names the binding side; the SURVEY §8(d) algorithmic bytes are reported separately
+  latency    p50/p99 per-hop GPU latency of the streaming process() API (one hop per call)
+  cpu_baseline / parity   the reference (oracle/_ref: the reference's own engine sources) on a
+             bounded sample of the same workload on all host cores, and max|y_gpu - y_ref| /
+             max|y_ref| of the bench's own outputs on that sample
+`--impl reference` times the same sample on the reference's CPU path (rank 0 only).
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,6 +48,7 @@ from paper_2310_00319_b200 import workload as W  # noqa: E402
 
 METRIC = "convolved channel-samples/s"
 UNIT = "channel-samples/s"
+DEFAULT_CONFIG = "C5"
 
 
 def log(*a):
@@ -43,29 +56,34 @@ def log(*a):
 
 
 def peaks():
-    try:
-        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        return {}
+    out = {}
+    for f in (ROOT / "MEASURED_PEAKS.json", ROOT / "profiles" / "l2_peak.json"):
+        try:
+            out.update(json.loads(f.read_text()))
+        except Exception:
+            pass
+    return out
 
 
-def config_block(cfg, n_hops, world):
+def config_block(cfg, n_hops, world, lanes_per_rank, scaling):
     if cfg.mode == "fresh":
         sw = f"fresh seeded IR per channel every {cfg.period} blocks, T60~U[{cfg.t60[0]},{cfg.t60[1]}] s"
     else:
         sw = (f"bank of {cfg.n_bank} x {cfg.ears}-ear decaying-noise IRs (T60 {cfg.t60[0]} s), "
               + ("alternating every %d blocks" % cfg.period if cfg.n_bank == 2 else "seeded random choice per block"))
+    total = cfg.sources * (world if scaling == "weak" else 1)
     return {
-        "workload": f"{cfg.name}: {cfg.sources} source(s) x {cfg.ears} ear(s) per GPU, fp32, L={cfg.hop} "
+        "workload": f"{cfg.name}: {total} source(s) x {cfg.ears} ear(s), fp32, L={cfg.hop} "
                     f"(4L={4 * cfg.hop} FFT), M={cfg.partitions} (IR {cfg.ir_length} taps), {sw}, "
                     f"{cfg.seconds:g} s white noise" + (", summed into a stereo mix" if cfg.mix else ""),
-        "channels_per_gpu": cfg.lanes,
+        "channels_total": total * cfg.ears,
+        "sources_per_gpu": lanes_per_rank,
         "hop": cfg.hop,
         "partitions": cfg.partitions,
         "hops_per_step": n_hops,
-        "l2": f"inputs larger than L2: {cfg.sources * n_hops * cfg.hop * 4 / 1e6:.1f} MB input + "
-              f"{cfg.lanes * n_hops * cfg.hop * 4 / 1e6:.1f} MB output streamed per step per GPU",
-        "parallelism": f"lanes sharded, {world} GPU(s), "
+        "l2": f"inputs larger than L2: {total * n_hops * cfg.hop * 4 / 1e6:.0f} MB input + "
+              f"{total * cfg.ears * n_hops * cfg.hop * 4 / 1e6:.0f} MB output per step",
+        "parallelism": f"{scaling} channel sharding over {world} GPU(s), "
                        + ("NCCL all-reduce of the stereo mix" if cfg.mix and world > 1 else "no collective"),
     }
 
@@ -83,7 +101,6 @@ class Clocks:
         import threading
 
         self.proc = None
-        self.idx = gpu_index
         self.lines = []
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.FIELDS}",
@@ -141,70 +158,169 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def cpu_sample(cfg, lanes, n_hops, threads, want_output=False):
-    """The reference algorithm (fp64 oracle port) over a bounded sample of the workload."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import oracle as O  # bench's cpu_baseline / reference leg: the checker, never the product
+def cpu_sample_plan(cfg, max_hops=None):
+    """The bounded sample of the workload the CPU legs run: strided sources x >= 2(2M-1) hops
+    (the delay line wraps), sized for ~1-2 s on a 16-core host."""
+    hops = min(cfg.hops, max(2 * (2 * cfg.partitions - 1), 64)) if max_hops is None else min(max_hops, cfg.hops)
+    per_lane_hop = cfg.partitions * (2 * cfg.hop + 1) * cfg.ears  # MAC complex products (cost proxy)
+    lanes = int(max(1, min(cfg.sources, 64, 4.2e9 / (per_lane_hop * hops))))
+    stride = max(1, cfg.sources // lanes)
+    return list(range(0, stride * lanes, stride)), hops
 
-    x = W.white(cfg, 0, lanes, 0, n_hops * cfg.hop, dtype=np.float64)
-    n_sw = -(-n_hops // cfg.period)
-    irs = np.stack([W.fresh_irs(cfg, k, 0, lanes, dtype=np.float64) for k in range(n_sw)])
-    secs, y = O.run_workload(cfg.hop, cfg.partitions, lanes, 1, n_hops, x, 0, fresh_ir=irs, period=cfg.period,
-                             want_output=want_output, threads=threads)
-    return secs, y
+
+def cpu_run(cfg, subset, n_hops, threads, want_output=True):
+    """The reference's CPU path (oracle/_ref = the reference's own engine sources when built;
+    else the restated oracle) over the sample: the bench's CPU baseline / reference arm and the
+    checker of the GPU outputs — never the measured GPU path."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+
+    kind = "reference" if O.ref_available() else "port"
+    L = cfg.hop
+    x = np.stack([W.white(cfg, s, 1, 0, n_hops * L, dtype=np.float64)[0] for s in subset])
+    with O.using("ref" if kind == "reference" else "port"):
+        if cfg.mode == "bank":
+            bank = W.bank_irs(cfg, dtype=np.float64)
+            sched = np.ascontiguousarray(W.schedule(cfg, 0, n_hops, 0, cfg.sources)[:, subset])
+            secs, y = O.run_workload(L, cfg.partitions, len(subset), cfg.ears, n_hops, x, 1, bank_ir=bank,
+                                     schedule=sched, threads=threads, want_output=want_output)
+        else:
+            n_sw = -(-n_hops // cfg.period)
+            irs = np.stack([W.ir_items(cfg, [(s, e, k) for s in subset for e in range(cfg.ears)], dtype=np.float64)
+                            .reshape(len(subset), cfg.ears, cfg.ir_length) for k in range(n_sw)])
+            secs, y = O.run_workload(L, cfg.partitions, len(subset), cfg.ears, n_hops, x, 0, fresh_ir=irs,
+                                     period=cfg.period, threads=threads, want_output=want_output)
+    return secs, y, kind
+
+
+def cpu_note(kind):
+    if kind == "reference":
+        return ("the reference's own proj/src/{spectral,partition,engine}.cpp compiled unmodified (-O3 -DNDEBUG, "
+                "proj/CMakeLists.txt:8-10) against a minimal Eigen stand-in (oracle/_ref); lanes partitioned over "
+                "std::threads (SPEC.md:221); timed region = process + partition like experiment.cpp:42-52")
+    return ("fp64 C++ restatement of proj/src/{spectral,partition,engine}.cpp (oracle/, bit-identical to the "
+            "reference on every config: tests/test_ref_pin.py); lanes over std::threads; timed region = process + "
+            "partition like experiment.cpp:42-52")
 
 
 def run_reference(args, cfg, rank):
-    if rank != 0:
+    if rank != 0:  # the reference arm runs once, on rank 0
         return
     threads = W.host_threads()
-    lanes, n_hops = cfg.sources, 256
-    used = min(threads, lanes)
-    vals = []
+    subset, n_hops = cpu_sample_plan(cfg, args.cpu_hops or None)
+    vals, kind = [], "port"
     for i in range(args.warmup + args.steps):
-        secs, _ = cpu_sample(cfg, lanes, n_hops, threads)
+        secs, _, kind = cpu_run(cfg, subset, n_hops, threads, want_output=False)
         if i >= args.warmup:
-            vals.append(lanes * n_hops * cfg.hop / secs)
+            vals.append(len(subset) * cfg.ears * n_hops * cfg.hop / secs)
     v = float(statistics.mean(vals))
-    sample = f"{lanes} channels x {n_hops} hops ({n_hops // cfg.period} fresh-IR switches) of {cfg.name} per step"
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    sample = (f"{len(subset)} sources (every {subset[1] - subset[0] if len(subset) > 1 else 1}th) x {cfg.ears} ear(s) "
+              f"x {n_hops} hops of {cfg.name} per step (the same channels, hops, schedule / IRs and inputs as the "
+              "GPU arm's workload)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * lanes * n_hops * cfg.hop / v, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(cfg, n_hops, 1),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "port", "sample": sample,
-                         "note": "fp64 C++ restatement of proj/src/{spectral,partition,engine}.cpp (Eigen "
-                                 "unavailable, reference unbuildable); lanes partitioned over std::threads, "
-                                 "timed region = process + partition like experiment.cpp:42-52"},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * len(subset) * cfg.ears * n_hops * cfg.hop / v,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, cfg.hops, 1, cfg.sources, "strong"),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": min(threads, len(subset)), "kind": kind,
+                         "sample": sample, "note": cpu_note(kind)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "same_config": True,
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- roofline
+def fp32_peak_tflops(sms, mhz):
+    return sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def roofline_block(cfg, summ_path, kern_ms, kern_n, hops_per_launch, distinct, clk, sms, pk, wide):
+    """Measured sides of the dominant kernel's roofline, per launch, over the live launch time."""
+    hbm = pk.get("hbm_gbs") or 6650.0
+    l2pk = pk.get("l2_read_gbs")
+    avg_ms = kern_ms / kern_n if kern_n else float("nan")
+    t = avg_ms / 1e3
+    sides, ncu = {}, None
+    if summ_path.exists():
+        sj = json.loads(summ_path.read_text())
+        ph = sj.get("per_hop", {})
+        ncu = {k: sj.get(k) for k in ("kernel", "source", "hops_per_launch", "duration_us_cold", "per_hop",
+                                      "lts_throughput_pct", "dram_throughput_pct", "l2_hit_pct", "top_stalls")}
+        ncu["file"] = f"profiles/{summ_path.name}"
+        if ph.get("dram_bytes"):
+            a = ph["dram_bytes"] * hops_per_launch / t / 1e9
+            sides["hbm"] = {"achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm,
+                            "bytes_per_hop": ph["dram_bytes"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        if ph.get("l2_read_bytes") and l2pk:
+            a = (ph["l2_read_bytes"] + ph.get("l2_write_bytes", 0.0)) * hops_per_launch / t / 1e9
+            sides["l2"] = {"achieved": a, "peak": l2pk, "unit": "GB/s", "frac": a / l2pk,
+                           "bytes_per_hop": ph["l2_read_bytes"] + ph.get("l2_write_bytes", 0.0),
+                           "peak_source": "profiles/l2_peak.json (scripts/l2_bw.cu, L2-resident reads, this pool)"}
+    flops = W.flops_per_hop(cfg) * hops_per_launch
+    mhz = (clk or {}).get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
+    fpk = fp32_peak_tflops(sms, mhz)
+    sides["fp32"] = {"achieved": flops / t / 1e12, "peak": fpk, "unit": "TFLOP/s", "frac": flops / t / 1e12 / fpk,
+                     "flops_per_hop": W.flops_per_hop(cfg),
+                     "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x {mhz:.0f} MHz (median SM clock under load)"}
+    bound = max(sides, key=lambda k: sides[k]["frac"])
+    b = sides[bound]
+    alg = W.bytes_per_hop(cfg, distinct_filters=distinct)
+    return {
+        "bound": bound, "achieved": b["achieved"], "peak": b["peak"], "unit": b["unit"], "frac": b["frac"],
+        "traffic": (sides["hbm"]["bytes_per_hop"] * hops_per_launch) if "hbm" in sides else None,
+        "sides": sides,
+        "kernel": wide,
+        "avg_launch_ms": avg_ms, "launches": kern_n, "hops_per_launch": hops_per_launch,
+        "algorithmic": {"bytes_per_hop_8d": alg, "gbs": alg * hops_per_launch / t / 1e9,
+                        "distinct_filters_per_hop": distinct,
+                        "note": "SURVEY 8(d) compulsory bytes (every output re-reads M delay-line and M filter "
+                                "spectra) over the launch time; the kernels reuse spectra across hops and channels "
+                                "on chip / in L2, so this exceeds any single memory level's bandwidth"},
+        "ncu": ncu,
+        "timing": "avg launch time from a separate event-instrumented pass (events on the engine stream)",
+    }
+
+
+# ----------------------------------------------------------------------------- launcher
+def spawn(args):
+    """--gpus N without torchrun: re-launch this script under torch.distributed.run, one rank per GPU."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    log("spawning:", " ".join(cmd))
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))
+    return subprocess.call(cmd, env=env)
 
 
 # ----------------------------------------------------------------------------- GPU leg
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--hops", type=int, default=0, help="override hops per step (default: full 30 s)")
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--hops", type=int, default=0, help="override hops per step (default: the config's full length)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-hops", type=int, default=512)
-    ap.add_argument("--latency-hops", type=int, default=0,
-                    help="also time this many single-hop process() calls (pinned host I/O): p50/p99 per-hop latency")
+    ap.add_argument("--cpu-hops", type=int, default=0, help="CPU sample hops (default >= 2(2M-1))")
+    ap.add_argument("--latency-hops", type=int, default=300,
+                    help="single-hop process() calls timed for the p50/p99 per-hop latency (0: skip)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     cfg = W.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
-
-    import ctypes
 
     import torch
 
@@ -219,17 +335,22 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    L, S, M = cfg.hop, cfg.sources, cfg.partitions
+    L, M = cfg.hop, cfg.partitions
     H = args.hops or cfg.hops
     n_sw = -(-H // cfg.period)
-    lane0, _ = shard.weak_lanes(S, rank)
+    if args.scaling == "weak":
+        lane0, S = shard.weak_lanes(cfg.sources, rank)
+    else:
+        lane0, S = shard.strong_lanes(cfg.sources, rank, world)
+    lanes = S * cfg.ears
     lib = T.lib()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
 
-    # ---- inputs resident in HBM (device twins of the seeded generators)
+    # ---- inputs resident in HBM (device twins of the seeded generators), this rank's channels
     t0 = time.time()
     x = torch.empty((S, H * L), dtype=torch.float32, device=dev)
     T._check(lib.tvolap_gen_white_device(local, cfg.seed, lane0, S, 0, H * L, ctypes.c_void_p(x.data_ptr()), H * L))
-    out = torch.empty((cfg.lanes, H * L), dtype=torch.float32, device=dev)
+    out = torch.empty((lanes, H * L), dtype=torch.float32, device=dev)
 
     def gen_irs(items, dst):
         la = np.array([i[0] for i in items], np.int64)
@@ -241,14 +362,13 @@ def main():
                                            ctypes.c_void_p(dst.data_ptr())))
 
     def fit_block(e):
-        """Blocks never span a filter switch, so a block longer than the switch period would
-        load each delay-line / filter slice for fewer hops: cap it at the period (C4: 8)."""
+        """Blocks never span a filter switch: cap the hop block at the period (C4: 8)."""
         j, _, _ = e.block_config()
         if cfg.period < j:
             e.set_block_config(max(2, 1 << (cfg.period.bit_length() - 1)))
 
     sched = mix = irs = None
-    n_pool = n_sw  # distinct IR sets held in HBM (and pinned host memory for e2e)
+    n_pool = n_sw
     if cfg.mode == "fresh":
         # C4's 704 switches x 256 channels x 131072 taps would not fit: cycle through a pool of
         # distinct seeded sets (<= 24 GB); every switch still uploads + transforms a whole set
@@ -269,29 +389,26 @@ def main():
         if cfg.mix:
             mix = torch.empty((cfg.ears, H * L), dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
-    log(f"[rank {rank}] {cfg.name}: generated {x.numel() * 4 / 1e6:.0f} MB input"
+    log(f"[rank {rank}] {cfg.name}: channels {lane0}..{lane0 + S - 1}, generated {x.numel() * 4 / 1e6:.0f} MB input"
         f"{'' if irs is None else f' + {irs.numel() * 4 / 1e9:.2f} GB IRs'} in {time.time() - t0:.1f} s")
     stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream.cuda_stream)
-    P, NT = eng.launch_config()
-    log(f"[rank {rank}] launch config: {P} CTAs/channel (cluster), {NT} threads/CTA")
+    comm = None
+    if mix is not None and world > 1:  # C3: the partial mixes are summed with NCCL through the C-ABI
+        comm = NcclComm(lib, rank, world, local)
 
-    def step(e, xs, outs, ir_set, sch):
+    def step(e, xs, outs, ir_set, sch, mx=None):
         e.reset()
         if cfg.mode == "fresh":
-            # the drive() loop (exchange before every period's hops) as one call:
-            # device-resident -> the time-parallel pass (few channels) or one hop-blocked launch with
-            # in-kernel K4; pinned host buffers -> the chunked H2D / launch / D2H pipeline
+            # the drive() loop (exchange before every period's hops) as one call
             e.process_switching(xs, [ir_set[k % n_pool] for k in range(n_sw)], cfg.period, out=outs)
         else:
             e.process_hops(xs, out=outs, schedule=sch)
-            if mix is not None and outs.is_cuda:
-                T._check(lib.tvolap_mix_device(local, S, cfg.ears, H * L, ctypes.c_void_p(outs.data_ptr()), H * L,
-                                               ctypes.c_void_p(mix.data_ptr()), H * L,
-                                               ctypes.c_void_p(stream.cuda_stream)))
-                if world > 1:
-                    with torch.cuda.stream(stream):
-                        shard.mix_allreduce(mix)
+            if mx is not None and outs.is_cuda:
+                T._check(lib.tvolap_mix_allreduce(local, S, cfg.ears, H * L, ctypes.c_void_p(outs.data_ptr()), H * L,
+                                                  ctypes.c_void_p(mx.data_ptr()), H * L,
+                                                  ctypes.c_void_p(comm.handle if comm else None),
+                                                  ctypes.c_void_p(stream.cuda_stream)))
 
     def barrier():
         torch.cuda.synchronize()
@@ -301,31 +418,30 @@ def main():
 
     clocks = Clocks(local)
     for _ in range(args.warmup):
-        step(eng, x, out, irs, sched)
+        step(eng, x, out, irs, sched, mix)
     barrier()
     launches0 = eng.kernel_launches()
-    wide0 = eng.wide_passes() if hasattr(eng, "wide_passes") else 0
+    wide0 = eng.wide_passes()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
-        step(eng, x, out, irs, sched)
+        step(eng, x, out, irs, sched, mix)
     ev1.record(stream)
     barrier()
     t_end = time.time()
     clk = clocks.stop(t_start, t_end)
     elapsed = ev0.elapsed_time(ev1)
     gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
-    wide = (eng.wide_passes() - wide0 if hasattr(eng, "wide_passes") else 0) > 0
-    # Per-launch kernel durations: a second pass of the same steps with CUDA events around every
-    # hop launch on the engine stream. Timing events serialise the programmatic-dependent-launch
-    # chain (K4 -> hop launch overlap), so they stay out of the timed region above.
-    prof_steps = max(1, min(args.steps, 3))
+    passes = eng.wide_passes() - wide0
+    # Per-launch kernel durations: a separate pass of the same steps with CUDA events around the
+    # dominant launch on the engine stream (kept out of the timed region above).
+    prof_steps = max(1, min(args.steps, 2))
     eng.set_profiling(True)
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev2.record(stream)
     for _ in range(prof_steps):
-        step(eng, x, out, irs, sched)
+        step(eng, x, out, irs, sched, mix)
     ev3.record(stream)
     barrier()
     kern_ms, kern_n = eng.kernel_time()
@@ -333,67 +449,26 @@ def main():
     prof_elapsed = ev2.elapsed_time(ev3)
     elapsed = shard.max_over_ranks(elapsed, dev)
     ms_per_step = elapsed / args.steps
-    samples_per_step = world * cfg.lanes * H * L
+    total_sources = cfg.sources * (world if args.scaling == "weak" else 1)
+    samples_per_step = total_sources * cfg.ears * H * L
     value = samples_per_step / (ms_per_step / 1e3)
 
-    # ---- roofline of the dominant kernel (fused hop kernel), algorithmic bytes per launch
+    # ---- roofline of the dominant kernel
     pk = peaks()
-    hbm = pk.get("hbm_gbs")
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
-    if not hbm:
-        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     hops_per_launch = H * prof_steps / kern_n if kern_n else H
-    bytes_hop = W.bytes_per_hop(cfg, distinct_filters=distinct)
-    bytes_launch = bytes_hop * hops_per_launch
-    avg_launch_ms = kern_ms / kern_n if kern_n else float("nan")
-    achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
-    traffic = None
-    ncu_view = None
-    summ = ROOT / "profiles" / f"ncu_summary_{cfg.name}.json"
-    if summ.exists():
-        try:
-            sj = json.loads(summ.read_text())
-            # per hop when the capture records it (its launch length may differ from this run's)
-            traffic = sj["dram_bytes_per_hop"] * hops_per_launch if sj.get("dram_bytes_per_hop") \
-                else sj.get("dram_bytes_per_launch")
-            # what actually bounds the captured kernel (committed capture, cold caches)
-            k = next((l for l in sj.get("per_launch", []) if "wide_mac" in l.get("name", "")),
-                     (sj.get("per_launch") or [{}])[0])
-            us = k.get("gpu__time_duration.sum")
-            dram = (k.get("dram__bytes_read.sum") or 0) + (k.get("dram__bytes_write.sum") or 0)
-            ncu_view = {"kernel": k.get("name", "")[:60], "source": f"profiles/{summ.name}",
-                        "dram_gbs": dram / (us * 1e-6) / 1e9 if us else None,
-                        "dram_frac": dram / (us * 1e-6) / 1e9 / hbm if us else None,
-                        "fma_pipe_pct": k.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
-                        "warps_active_pct": k.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
-                        "top_stalls": k.get("top_stalls")}
-        except Exception:
-            traffic = None
-    if wide:  # time-parallel pass: the MAC/inverse launch dominates; K4 and K1 are separate launches
-        kname = (f"wide_mac_kernel (K4 of the tile's filter set into an L2 scratch slot + K3 + K5 + OLA, one CTA "
-                 f"per (channel, filter period <= 16 hops)), {hops_per_launch:g} hops x {S} sources per launch; K1 of "
-                 "all hops (wide_forward_kernel, ~13% of the step) is a separate launch outside this kernel's time")
+    if cfg.mode == "bank" and cfg.period == 1 and passes:
+        kname = ("bank_mac_kernel (bank pass K3: one CTA per (hop tile, channel x 32-column chunk, partition group), "
+                 f"{hops_per_launch:.0f} hops x {S} sources per launch; K1 / K5 / head / fix-up are separate launches)")
+    elif passes:
+        kname = (f"wide_mac_kernel (time-parallel pass: K4 of the tile's set + K3 + K5 + OLA per (channel, tile)), "
+                 f"{hops_per_launch:.0f} hops x {S} sources per launch")
     else:
-        kname = (f"tvolap_block_kernel (K1-K5 fused{', K4 for the next switch in the barrier gaps' if cfg.mode == 'fresh' else ''}), "
-                 f"{hops_per_launch:g} hops x {S} sources per launch")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": peak_src,
-                "kernel": kname,
-                "pass_achieved": bytes_hop * H / (ms_per_step / 1e3) / 1e9,
-                "ncu": ncu_view,
-                "avg_launch_ms": avg_launch_ms, "launches": kern_n, "bytes_per_hop": bytes_hop,
-                "bytes_per_launch": bytes_launch, "distinct_filters_per_hop": distinct,
-                "kernel_share_of_step": kern_ms / prof_elapsed if prof_elapsed else None,
-                "timing": f"avg launch from a separate event-instrumented pass of {prof_steps} step(s) "
-                          "(share = kernel time / that pass's elapsed)"}
-    if wide:
-        roofline["note"] = ("algorithmic bytes (SURVEY 8d: every output re-reads M delay-line spectra and M filter "
-                            "spectra) over the MAC launch's time; the kernel reads each spectrum once per 16-hop tile, "
-                            "so frac can exceed 1; pass_achieved = the same bytes over the whole step (all launches)")
-    elif cfg.name in ("C1", "C2"):
-        roofline["note"] = "delay line + filter pool are L2-resident in this config, so frac vs HBM can exceed 1"
+        kname = f"tvolap_block_kernel (K1-K5 fused, hop-blocked), {hops_per_launch:.0f} hops x {S} sources per launch"
+    roofline = roofline_block(cfg, ROOT / "profiles" / f"ncu_summary_{cfg.name}.json", kern_ms, kern_n,
+                              hops_per_launch, distinct * (S / cfg.sources), clk, sms, pk, kname)
+    roofline["kernel_share_of_step"] = kern_ms / prof_elapsed if prof_elapsed else None
 
-    # ---- e2e through the public API with pinned host buffers (H2D inputs [+ IRs], D2H outputs)
+    # ---- e2e through the public API with pinned host buffers (H2D inputs [+ IRs, schedule], D2H outputs)
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
@@ -426,20 +501,24 @@ def main():
         e2e = {"value": samples_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_s * 1e3,
                "timing": "host wall clock around each full pass incl. final synchronize",
-               "matches_device_path": same}
-        del irh
+               "matches_device_path": same,
+               "path": "tvolap_process_hops / process_switching with pinned host buffers: chunked H2D || kernels "
+                       "|| D2H pipeline on three streams"}
+        del irh, eng2
 
+    # ---- p50/p99 per-hop latency of the streaming API (one process() call per hop)
     latency = None
     if args.latency_hops:
         lat_eng = (TvolapBankEngine(bank, L, S, min_partitions=M, device=local) if cfg.mode == "bank"
                    else TvolapEngine(partition(ir0.T, L, M), device=local))
         lat_eng.set_stream(stream.cuda_stream)
         xin = torch.empty((S, L), dtype=torch.float32, pin_memory=True)
-        yout = torch.empty((cfg.lanes, L), dtype=torch.float32, pin_memory=True)
-        xsrc = x[:, : (args.latency_hops + 8) * L].cpu()
+        yout = torch.empty((lanes, L), dtype=torch.float32, pin_memory=True)
+        nl = min(args.latency_hops + 8, H)
+        xsrc = x[:, : nl * L].cpu()
         sch_np = sched.cpu().numpy() if sched is not None else None
         gpu_ms, host_ms = [], []
-        for h in range(args.latency_hops + 8):
+        for h in range(nl):
             xin.copy_(xsrc[:, h * L:(h + 1) * L])
             if sch_np is not None:
                 lat_eng.select_bank(sch_np[h])
@@ -454,42 +533,84 @@ def main():
                 host_ms.append((time.perf_counter() - t0h) * 1e3)
                 gpu_ms.append(a.elapsed_time(b))
         q = lambda v, p: float(np.percentile(v, p))  # noqa: E731
-        latency = {"hops": args.latency_hops, "gpu_ms_p50": q(gpu_ms, 50), "gpu_ms_p99": q(gpu_ms, 99),
+        latency = {"hops": len(gpu_ms), "gpu_ms_p50": q(gpu_ms, 50), "gpu_ms_p99": q(gpu_ms, 99),
                    "host_ms_p50": q(host_ms, 50), "host_ms_p99": q(host_ms, 99),
                    "hop_period_ms": 1e3 * L / W.FS,
-                   "what": "one process() call per hop: pinned H2D of the hop, fused kernel, D2H of the outputs; "
-                           "CUDA events on the engine stream (gpu) and host wall clock (host)"}
+                   "streaming_value": S * cfg.ears * L / (statistics.median(host_ms) / 1e3),
+                   "what": "one tvolap_process() call per hop (the reference's process() API): pinned H2D of the "
+                           "hop, one-hop kernel, D2H of the outputs; CUDA events on the engine stream (gpu) and "
+                           "host wall clock (host); streaming_value = channel-samples/s at the median host time"}
+        del lat_eng
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded white noise + decaying-noise IRs generated on device)",
-        "config": config_block(cfg, H, world), "clocks": clk, "gpu_launches": int(gpu_launches),
+        "config": config_block(cfg, H, world, S, args.scaling), "clocks": clk, "gpu_launches": int(gpu_launches),
         "roofline": roofline, "e2e": e2e, "latency": latency,
         "realtime_factor": (H * L / W.FS) / (ms_per_step / 1e3),
+        "path": {"passes_per_step": passes / args.steps,
+                 "kind": "bank pass" if (cfg.mode == "bank" and cfg.period == 1 and passes) else
+                         ("time-parallel pass" if passes else "hop-blocked launches")},
     }
     if cfg.mode == "fresh" and n_pool < n_sw:
         line["config"]["ir_sets"] = (f"{n_sw} switches per step cycle through {n_pool} distinct seeded IR sets "
                                      "held in HBM (every switch uploads and transforms a whole set)")
 
-    # ---- CPU baseline (rank 0, N=1 only): the reference algorithm on host cores, bounded sample
-    if rank == 0 and world == 1 and not args.no_cpu and cfg.mode == "fresh":
+    # ---- CPU baseline + in-line parity (rank 0, N=1 only): the reference on a bounded sample
+    if rank == 0 and world == 1 and not args.no_cpu:
         threads = W.host_threads()
-        ch = min(args.cpu_hops, H)
-        secs, yref = cpu_sample(cfg, S, ch, threads, want_output=True)
-        y = out[:, : ch * L].double().cpu().numpy()
+        subset, ch = cpu_sample_plan(cfg, args.cpu_hops or None)
+        ch = min(ch, H)
+        secs, yref, kind = cpu_run(cfg, subset, ch, threads, want_output=True)
+        rows = [s * cfg.ears + e for s in subset for e in range(cfg.ears)]
+        y = out[rows, : ch * L].double().cpu().numpy()
         rel = float(np.abs(y - yref).max() / np.abs(yref).max())
-        secs1, _ = cpu_sample(cfg, 4, 64, 1)
+        secs1, _, _ = cpu_run(cfg, subset[:1], min(ch, 256), 1, want_output=False)
+        sample = (f"{len(subset)} sources (every {subset[1] - subset[0] if len(subset) > 1 else 1}th) x "
+                  f"{cfg.ears} ear(s) x {ch} hops of {cfg.name}")
         line["cpu_baseline"] = {
-            "value": S * ch * L / secs, "unit": UNIT, "cores": min(threads, S), "kind": "port",
-            "sample": f"{S} channels x {ch} hops ({ch // cfg.period} fresh-IR switches) of {cfg.name}",
-            "single_thread_value": 4 * 64 * L / secs1,
-            "parity_rel_err_vs_gpu": rel,
+            "value": len(subset) * cfg.ears * ch * L / secs, "unit": UNIT, "cores": min(threads, len(subset)),
+            "kind": kind, "sample": sample, "note": cpu_note(kind),
+            "single_thread_value": cfg.ears * min(ch, 256) * L / secs1,
         }
+        line["parity"] = {"rel_err_vs_reference": rel, "tolerance": 1e-4, "ok": rel <= 1e-4, "sample": sample,
+                          "checked": "the bench's own device-path outputs of the timed pass vs the CPU reference",
+                          "e2e_bit_identical_to_device_path": e2e["matches_device_path"] if e2e else None}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+class NcclComm:
+    """An NCCL communicator made through the C-ABI (tvolap_nccl_*): rank 0's unique id is shared
+    through torch.distributed, so a C++ host does the same with its own transport."""
+
+    def __init__(self, lib, rank, world, device):
+        import torch
+        import torch.distributed as dist
+
+        buf = (ctypes.c_char * 128)()
+        if rank == 0:
+            from paper_2310_00319_b200 import tvolap as T
+
+            T._check(lib.tvolap_nccl_unique_id(buf))
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8, device=f"cuda:{device}")
+        dist.broadcast(t, 0)
+        raw = bytes(t.cpu().tolist())
+        h = ctypes.c_void_p()
+        from paper_2310_00319_b200 import tvolap as T
+
+        T._check(lib.tvolap_nccl_comm_init(ctypes.byref(h), device, world, rank, raw))
+        self.lib, self.handle = lib, h.value
+
+    def close(self):
+        if self.handle:
+            self.lib.tvolap_nccl_comm_destroy(ctypes.c_void_p(self.handle))
+            self.handle = None
 
 
 if __name__ == "__main__":

@@ -45,6 +45,7 @@ extern "C" {
 #define TVOLAP_ERR_CUDA 6                  /* device / driver failure (no reference analogue) */
 
 typedef struct tvolap_engine tvolap_engine;
+typedef struct tvolap_set tvolap_set;
 
 /* Message for the calling thread's most recent failing call. */
 const char* tvolap_last_error(void);
@@ -131,6 +132,32 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
  */
 int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, long channels);
 
+/*
+ * Device-resident filter partition sets: the reference's immutable, shared
+ * FilterPartitionSet (partition.hpp:21-32) held on the GPU.
+ *   tvolap_set_create   ≙ partition(ir, hop, min_partitions) (partition.hpp:38, partition.cpp:20-51):
+ *                         K4 once, on `device`; errors as tvolap_create. Reference-counted: the
+ *                         caller owns one reference (tvolap_set_release); an engine holding the set
+ *                         as its active or staged filter holds another.
+ *   tvolap_create_from_set ≙ TvolapEngine(shared_ptr<const FilterPartitionSet>) (engine.hpp:35):
+ *                         no transform, the engine reads the set's spectra in place.
+ *   tvolap_exchange_set ≙ exchange_filter(shared_ptr<const FilterPartitionSet>) (engine.hpp:55,
+ *                         engine.cpp:37-48): O(1), no K4; validated (INCOMPATIBLE_FILTER on a hop,
+ *                         partition-count, channel-count or device mismatch), latched at the next
+ *                         process call, last staged wins (also against tvolap_exchange_filter).
+ *   tvolap_set_reassemble ≙ reassemble(set) (partition.hpp:43, partition.cpp:53-65):
+ *                         out[c * (2 L M) + n], the response zero-padded to M * 2L taps.
+ *   tvolap_set_spectra:   spectra[((c * M + m) * (2L + 1) + k) * 2 + {re, im}] (as tvolap_partition).
+ */
+int tvolap_set_create(tvolap_set** out, int device, long hop, long channels, long ir_length, const float* ir,
+                      long min_partitions);
+int tvolap_set_release(tvolap_set* s);
+int tvolap_set_geometry(const tvolap_set* s, long* hop, long* partitions, long* channels, long* source_length);
+int tvolap_set_spectra(const tvolap_set* s, float* spectra);
+int tvolap_set_reassemble(const tvolap_set* s, float* out);
+int tvolap_create_from_set(tvolap_engine** out, const tvolap_set* s);
+int tvolap_exchange_set(tvolap_engine* e, const tvolap_set* s);
+
 /* Stage per-source bank selections idx[sources], latched at the next hop. */
 int tvolap_select_bank(tvolap_engine* e, const int32_t* idx);
 
@@ -200,9 +227,25 @@ int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block
 uint64_t tvolap_kernel_launches(const tvolap_engine* e);
 
 /* Time-parallel passes run so far: device-resident tvolap_process_switching calls executed as
-   K1-for-all-hops + (lane, hop-tile) K4/MAC/inverse CTAs (a diagnostic of which path a call
-   took). TVOLAP_WIDE=0 disables the pass, TVOLAP_WIDE=2 forces it wherever it is supported. */
+   K1-for-all-hops + (lane, hop-tile) K4/MAC/inverse CTAs, and bank passes of per-hop bank
+   schedules (a diagnostic of which path a call took; tuning "wide" / "bank_pass" select). */
 uint64_t tvolap_wide_passes(const tvolap_engine* e);
+
+/*
+ * Tuning knobs: every A/B switch of the kernel, geometry and pipeline choices, by name (the
+ * library reads no environment variables). Defaults are the measured-best choices; DESIGN.md §10
+ * documents each key. Engine knobs apply to that engine; "pdl", "k4_warp" and "k4_prefetch" are
+ * process-wide launch knobs. Unknown keys and out-of-range values return INVALID_INPUT; a
+ * geometry that does not fit returns INVALID_CONFIGURATION and keeps the previous value.
+ * tvolap_set_default_tuning sets the value engines created afterwards start with.
+ * No reference counterpart (the reference has no tunables).
+ */
+int tvolap_set_tuning(tvolap_engine* e, const char* key, long value);
+int tvolap_get_tuning(const tvolap_engine* e, const char* key, long* value);
+int tvolap_set_default_tuning(const char* key, long value);
+int tvolap_reset_default_tuning(void);
+/* Comma-separated list of the keys. */
+const char* tvolap_tuning_keys(void);
 
 /* ------------------------------------------------------ spectral primitives */
 /* Batched K1/K5 building blocks, exposed so the reference's spectral tests
@@ -242,6 +285,22 @@ int tvolap_gen_irs_device(int device, uint64_t seed, long count, const long* lan
  * summed in a fixed order (deterministic). Device pointers. */
 int tvolap_mix_device(int device, long sources, long ears, long samples, const float* out, long out_stride,
                       float* mix, long mix_stride, void* stream);
+
+/*
+ * Multi-GPU C3 mix (sources sharded across GPUs, the stereo mix reduced with NCCL
+ * over NVLink): this GPU's partial mix of its own sources (tvolap_mix_device) followed by an
+ * in-place ncclAllReduce(sum) of the ears x samples partial mix over `nccl_comm`, both on `stream`.
+ * nccl_comm == NULL: the single-GPU mix only. `nccl_comm` is an ncclComm_t (void* so this header
+ * does not need nccl.h); NCCL is loaded at first use (libnccl.so.2), so hosts that never mix
+ * carry no NCCL dependency. No reference counterpart (the reference mixes on one CPU thread).
+ */
+int tvolap_mix_allreduce(int device, long sources, long ears, long samples, const float* out, long out_stride,
+                         float* mix, long mix_stride, void* nccl_comm, void* stream);
+/* Communicator helpers for hosts without their own NCCL setup: rank 0 makes the 128-byte unique
+ * id, the host distributes it (any transport), every rank calls tvolap_nccl_comm_init. */
+int tvolap_nccl_unique_id(char id_out[128]);
+int tvolap_nccl_comm_init(void** comm_out, int device, int nranks, int rank, const char id[128]);
+int tvolap_nccl_comm_destroy(void* comm);
 
 
 /* ------------------------------------------------------ comparison convolvers

@@ -97,8 +97,10 @@ struct EngineOpCounts {  // engine.hpp:17-21
     std::uint64_t spectral_macs = 0;
 };
 
-// partition.hpp:21-32. Spectra are computed on the device when an engine takes
-// the set; the set keeps the fp32 taps (channel-major) it was built from.
+// partition.hpp:21-32: immutable, shared via shared_ptr. The partition spectra live on the device
+// (tvolap_set, computed once by partition()); engines take and exchange to them in O(1). The fp32
+// taps it was built from are kept too (TvolapProcessor::set_filter stages taps, whose transform
+// then runs on a device side stream).
 struct FilterPartitionSet {
     Index hop = 0;
     Index partition_count = 0;
@@ -106,15 +108,17 @@ struct FilterPartitionSet {
     Index source_length = 0;
     double normalization_gain = 0.5;
     double sample_rate = 48000.0;
-    std::vector<float> taps;  // taps[c * source_length + n]
+    std::vector<float> taps;             // taps[c * source_length + n]
+    std::shared_ptr<tvolap_set> spectra;  // device-resident partition spectra
+    int device = 0;
     Index transform_length() const { return 4 * hop; }
     Index padded_length() const { return 2 * hop * partition_count; }
 };
 
 inline bool is_power_of_two(Index n) { return n > 0 && (n & (n - 1)) == 0; }
 
-// partition.cpp:20-51 (validation and M; the transform itself runs on the GPU).
-inline FilterPartitionSet partition(const ImpulseResponse& ir, Index hop, Index min_partitions = 1) {
+// partition.cpp:20-51: validation and M on the host, the transforms (K4) on the device.
+inline FilterPartitionSet partition(const ImpulseResponse& ir, Index hop, Index min_partitions = 1, int device = 0) {
     if (ir.length() < 1 || ir.channels() < 1) throw InvalidInputError("partition: impulse response is empty");
     if (hop < 2 || !is_power_of_two(4 * hop))
         throw InvalidSizeError("partition: 4L must be a power of two, got L = " + std::to_string(hop));
@@ -125,23 +129,40 @@ inline FilterPartitionSet partition(const ImpulseResponse& ir, Index hop, Index 
     s.channels = ir.channels();
     s.source_length = ir.length();
     s.sample_rate = ir.sample_rate;
+    s.device = device;
     s.taps.resize((size_t)(s.channels * s.source_length));
     for (Index c = 0; c < s.channels; ++c)
         for (Index n = 0; n < s.source_length; ++n) s.taps[(size_t)(c * s.source_length + n)] = (float)ir.samples(n, c);
+    tvolap_set* h = nullptr;
+    check(tvolap_set_create(&h, device, hop, s.channels, s.source_length, s.taps.data(), s.partition_count));
+    s.spectra.reset(h, [](tvolap_set* p) { tvolap_set_release(p); });
     return s;
+}
+
+// partition.cpp:53-65: the response zero-padded to M * 2L taps, from the device spectra.
+inline ImpulseResponse reassemble(const FilterPartitionSet& set) {
+    const Index len = 2 * set.hop * set.partition_count;
+    std::vector<float> out((size_t)(len * set.channels));
+    check(tvolap_set_reassemble(set.spectra.get(), out.data()));
+    ImpulseResponse ir;
+    ir.sample_rate = set.sample_rate;
+    ir.samples = Frames(len, set.channels);
+    for (Index c = 0; c < set.channels; ++c)
+        for (Index n = 0; n < len; ++n) ir.samples(n, c) = out[(size_t)(c * len + n)];
+    return ir;
 }
 
 class TvolapEngine {
 public:
-    explicit TvolapEngine(std::shared_ptr<const FilterPartitionSet> filter, int device = 0) : filter_(std::move(filter)) {
-        if (!filter_) throw InvalidConfigurationError("engine requires a filter partition set");
+    // engine.hpp:35, engine.cpp:9-32: the engine reads the set's device spectra in place
+    explicit TvolapEngine(std::shared_ptr<const FilterPartitionSet> filter) : filter_(std::move(filter)) {
+        if (!filter_ || !filter_->spectra) throw InvalidConfigurationError("engine requires a filter partition set");
         tvolap_engine* h = nullptr;
-        check(tvolap_create(&h, device, filter_->hop, filter_->channels, filter_->source_length, filter_->taps.data(),
-                            filter_->partition_count));
+        check(tvolap_create_from_set(&h, filter_->spectra.get()));
         h_.reset(h);
     }
-    explicit TvolapEngine(const FilterPartitionSet& filter, int device = 0)
-        : TvolapEngine(std::make_shared<FilterPartitionSet>(filter), device) {}
+    explicit TvolapEngine(const FilterPartitionSet& filter)
+        : TvolapEngine(std::make_shared<FilterPartitionSet>(filter)) {}
 
     Index hop() const { return tvolap_hop(h_.get()); }
     Index channels() const { return tvolap_channels(h_.get()); }
@@ -151,17 +172,23 @@ public:
     Index switching_latency() const { return tvolap_switching_latency(h_.get()); }
     Index stream_delay() const { return tvolap_stream_delay(h_.get()); }
 
-    // engine.cpp:37-48
+    // engine.hpp:55, engine.cpp:37-48: O(1) — validate, stage (last wins), latched at the next process()
     void exchange_filter(std::shared_ptr<const FilterPartitionSet> next) {
         if (!next) throw IncompatibleFilterError("replacement filter is null");
         if (next->hop != hop()) throw IncompatibleFilterError("replacement filter hop differs");
         if (next->partition_count != partition_count())
             throw IncompatibleFilterError("replacement filter partition count differs");
         if (next->channels != channels()) throw IncompatibleFilterError("replacement filter channel count differs");
-        check(tvolap_exchange_filter(h_.get(), next->taps.data(), next->source_length, next->channels));
+        check(tvolap_exchange_set(h_.get(), next->spectra.get()));
         filter_ = std::move(next);
     }
     void exchange_filter(const FilterPartitionSet& next) { exchange_filter(std::make_shared<FilterPartitionSet>(next)); }
+    // TvolapProcessor::set_filter's path: stage time-domain taps; K4 runs on a device side stream
+    void exchange_taps(std::shared_ptr<const FilterPartitionSet> next) {
+        if (!next) throw IncompatibleFilterError("replacement filter is null");
+        check(tvolap_exchange_filter(h_.get(), next->taps.data(), next->source_length, next->channels));
+        filter_ = std::move(next);
+    }
 
     // engine.cpp:60-106: exactly L rows x C cols in, same shape out.
     Frames process(const Frames& input) {
@@ -311,7 +338,7 @@ public:
 class TvolapProcessor : public StreamingProcessor {
 public:
     TvolapProcessor(const ImpulseResponse& ir, Index hop, int device = 0)
-        : engine_(std::make_shared<FilterPartitionSet>(partition(ir, hop)), device) {}
+        : engine_(std::make_shared<FilterPartitionSet>(partition(ir, hop, 1, device))) {}
     std::string name() const override { return "tvolap"; }
     Index hop() const override { return engine_.hop(); }
     Index channels() const override { return engine_.channels(); }
@@ -320,7 +347,19 @@ public:
     Index switching_latency() const override { return engine_.switching_latency(); }
     Frames process(const Frames& input) override { return engine_.process(input); }
     void set_filter(const ImpulseResponse& ir) override {  // reference.cpp:335-338
-        engine_.exchange_filter(std::make_shared<FilterPartitionSet>(partition(ir, engine_.hop(), engine_.partition_count())));
+        // validation / M as partition() (partition.cpp:21-24), the transform on the device side stream
+        if (ir.length() < 1 || ir.channels() < 1) throw InvalidInputError("partition: impulse response is empty");
+        auto s = std::make_shared<FilterPartitionSet>();
+        s->hop = engine_.hop();
+        s->partition_count = std::max((ir.length() + 2 * s->hop - 1) / (2 * s->hop), engine_.partition_count());
+        s->channels = ir.channels();
+        s->source_length = ir.length();
+        s->sample_rate = ir.sample_rate;
+        s->taps.resize((size_t)(s->channels * s->source_length));
+        for (Index c = 0; c < s->channels; ++c)
+            for (Index n = 0; n < s->source_length; ++n)
+                s->taps[(size_t)(c * s->source_length + n)] = (float)ir.samples(n, c);
+        engine_.exchange_taps(std::move(s));
     }
     void reset() override { engine_.reset(); }
     TvolapEngine& engine() { return engine_; }

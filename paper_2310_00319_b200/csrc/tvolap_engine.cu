@@ -15,8 +15,11 @@
 // D2H of consecutive chunks run on three streams so copies overlap compute.
 // Staged filter sets are transformed (K4) on a high-priority side stream.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -146,15 +149,36 @@ constexpr int kSlots = 3;
 // Host-IR upload buffers: uploads run on their own stream up to this many sets ahead.
 constexpr int kIrStage = 4;
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v ? std::atoi(v) : dflt;
-}
 
+}  // namespace
+
+// A device-resident FilterPartitionSet (partition.hpp:21-32): S x M packed partition spectra,
+// computed once by K4 and immutable afterwards; shared by reference count (the engines that
+// hold it as their active or staged filter keep it alive), like the reference's
+// shared_ptr<const FilterPartitionSet>.
+struct tvolap_set {
+    int device = 0;
+    long L = 0, M = 0, S = 0, N = 0, source_length = 0;
+    float2* spec = nullptr;  // [S][M][2L] (+ kWideTail rows)
+    std::atomic<int> refs{1};
+};
+
+namespace {
+void set_retain(const tvolap_set* s) {
+    if (s) const_cast<tvolap_set*>(s)->refs.fetch_add(1);
+}
+void set_release(const tvolap_set* cs) {
+    auto* s = const_cast<tvolap_set*>(cs);
+    if (!s || s->refs.fetch_sub(1) != 1) return;
+    cudaSetDevice(s->device);
+    cudaFree(s->spec);  // implicitly waits for the device work that may still read it
+    delete s;
+}
 }  // namespace
 
 struct tvolap_engine {
     int device = 0;
+    int sms = 148;                   // SM count of the device (queried at creation)
     long L = 0, M = 0, S = 0, E = 1, N = 0;
     bool bank = false;
     long n_bank = 0;
@@ -162,6 +186,10 @@ struct tvolap_engine {
     cudaEvent_t ev_side = nullptr, ev_main = nullptr, ev_start = nullptr;
     cudaEvent_t ev_slot[kSlots] = {};  // last hop kernel that read each filter slot
     float2 *ring = nullptr, *pool = nullptr, *tw = nullptr, *pk = nullptr;
+    // filter held as an external device set (tvolap_create_from_set / tvolap_exchange_set): read in
+    // place, no K4; null = the pool slot `active`
+    const tvolap_set* active_ext = nullptr;
+    const tvolap_set* pending_ext = nullptr;
     float *win = nullptr, *hist = nullptr, *ola = nullptr;
     int* d_sel = nullptr;
     std::vector<int> sel, staged;
@@ -177,15 +205,15 @@ struct tvolap_engine {
     float* d_irst[kIrStage] = {};    // host-IR upload buffers (round robin)
     size_t irst_cap[kIrStage] = {};
     int irst_next = 0;
-    int ir_stages = 1;               // upload buffers in use (<= kIrStage); 1 measured best: uploads
+    long ir_stages = 1;              // upload buffers in use (<= kIrStage); 1 measured best: uploads
                                      // running ahead delay the audio H2D on the critical path
     cudaEvent_t ev_up[kIrStage] = {}, ev_used[kIrStage] = {};  // upload landed / consuming kernel done
     const float* launch_new_ir = nullptr;  // latched: the next launch transforms this set
     long launch_new_len = 0;
     int launch_buf = -1;
-    bool k4_side = false;            // true: transform staged sets on the side stream (overlapping hops)
+    long k4_side = 1;                // 1: transform staged sets on the side stream (overlapping hops)
     bool staged_on_side = false;     // the pending set was transformed on the side stream
-    bool k4_stream = false;          // true: transform at latch time on the engine stream (PDL chain)
+    long k4_stream = 1;              // 1: transform at latch time on the engine stream (PDL chain)
     // switching launches (tvolap_process_switching): per-switch IR pointers / pool entries
     const float** d_sw_irs = nullptr;
     int* d_sw_entry = nullptr;
@@ -210,12 +238,29 @@ struct tvolap_engine {
     unsigned* wide_lock = nullptr;
     const float** d_wide_tile_ir = nullptr;
     size_t wide_scratch_cap = 0, wide_lock_cap = 0, wide_tile_ir_cap = 0;
-    int wide_mode = 1;               // TVOLAP_WIDE: 0 off, 1 auto, 2 whenever supported
+    long wide_mode = 1;              // "wide": 0 off, 1 auto, 2 whenever supported
+    // bank pass (per-hop bank schedules on device-resident hops): MAC partials per partition group
+    float2* bank_yq = nullptr;
+    size_t bank_yq_cap = 0;
+    long bank_pass = 1;              // 0: per-hop schedules stay on the hop-blocked kernel
+    long bank_pass_mb = 32768;       // Xe + partials budget per pass
+    long bank_pass_hops = 0;         // max hops per pass (0: by the budget)
     uint64_t wide_passes = 0;
-    int pipe_merge = 1;              // TVOLAP_PIPE_MERGE: one H2D copy per run of host-contiguous sets
-    int wide_warp_fft = 1;           // TVOLAP_WIDE_WARPFFT: 1 warp FFTs for K1/K5 (0: bit-identical Stockham)
+    long pipe_merge = 1;             // "pipe_merge": one H2D copy per run of host-contiguous sets
+    long wide_warp_fft = 1;          // "wide_warp_fft": 1 warp FFTs for K1/K5 (0: bit-identical Stockham)
+    // further tuning knobs (tvolap_set_tuning; defaults = the measured-best choices)
+    long wide_q = -1;                // wide pass partition groups (-1: auto)
+    long wide_stage = 1;             // fused K4 IR slices through a cp.async double buffer
+    long wide_pool_mb = 8192;        // unfused wide pass: filter-set pool budget
+    long wide_fuse = 1;              // fused K4 in the wide MAC tiles
+    long wide_xe_mb = 4096;          // wide pass: extended-spectra budget
+    long k4_gap_mult = 1;            // switching launch: K4 units per barrier gap (x warps x CTAs)
+    long sw_1024 = 0;                // switching launch also for 1024-point transforms
+    long pipe_mb = 64;               // pinned switching pipeline chunk
+    long pipe_log2 = 25;             // pinned hop pipeline chunk (floats, log2)
+    long fix_p = 0, fix_nt = 0, fix_pb = 0, fix_jh = 0, ntb = 256;  // geometry overrides (0: auto)
     // chunked host pipeline
-    long chunk_hops = 0;
+    long chunk_hops = 0, host_chunk = 0;
     float *d_in[2] = {}, *d_out[2] = {}, *h_in[2] = {}, *h_out[2] = {};
     int* d_sch[2] = {};
     long sch_cap = 0;
@@ -229,7 +274,7 @@ struct tvolap_engine {
     int JH = 4, QB = 1, NTB = 256;   // hop-blocked kernel: 2*JH hops per block, QB partition groups
     int PB = 1;                      // hop-blocked kernel: CTAs (cluster size) per source
     int QM = 1;                      // partition groups of both kernels (bit-identical sums)
-    bool geometry_fixed = false;     // set by tvolap_set_launch_config / set_block_config / env
+    bool geometry_fixed = false;     // set by tvolap_set_launch_config / set_block_config / tuning
     long D = 0;                      // delay-line slots per parity (M + kMaxJH)
     long block_min = 4;              // process_hops calls with >= block_min hops use the blocked kernel
     uint64_t fwd = 0, inv = 0, macs = 0, launches = 0;
@@ -240,6 +285,8 @@ struct tvolap_engine {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
         if (side) cudaStreamSynchronize(side);
+        set_release(active_ext);
+        set_release(pending_ext);
         for (void* p : {(void*)ring, (void*)pool, (void*)tw, (void*)pk, (void*)win, (void*)hist, (void*)ola,
                         (void*)d_sel, (void*)d_irstage, (void*)d_irst[0], (void*)d_irst[1], (void*)d_irst[2],
                         (void*)d_irst[3], (void*)d_in[0],
@@ -248,7 +295,7 @@ struct tvolap_engine {
                         (void*)swh_x[0], (void*)swh_x[1], (void*)swh_y[0], (void*)swh_y[1], (void*)swh_ir[0],
                         (void*)swh_ir[1], (void*)wide_xe, (void*)wide_pool, (void*)wide_state, (void*)wide_head,
                         (void*)d_wide_fset, (void*)d_wide_irs, (void*)d_wide_tile0, (void*)wide_scratch,
-                        (void*)wide_lock, (void*)d_wide_tile_ir})
+                        (void*)wide_lock, (void*)d_wide_tile_ir, (void*)bank_yq})
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
@@ -271,21 +318,13 @@ void pick_launch_config(tvolap_engine* e) {
     // P: CTAs per source. Enough CTAs to cover the 148 SMs, never a slice
     // smaller than one float4 per thread group.
     long p = 1;
-    while (p < 8 && p * 2 <= e->L && e->S * p < 148) p *= 2;
+    while (p < 8 && p * 2 <= e->L && e->S * p < e->sms) p *= 2;
     e->P = (int)p;
     e->NT = 256;
-    const int ep = env_int("TVOLAP_P", 0), et = env_int("TVOLAP_NT", 0);
-    if (ep > 0) e->P = ep;
-    if (et > 0) e->NT = et;
-    e->block_min = env_int("TVOLAP_BLOCK_MIN", 4);
-    e->k4_side = env_int("TVOLAP_K4_SIDE", 1) != 0;
-    // same-box A/B, C2 exchange every 16 hops: side stream 2.82 us/hop, + PDL 2.77,
-    // in-stream K4 chained by PDL 2.53 (profiles/r01_ab_pdl.txt)
-    e->k4_stream = env_int("TVOLAP_K4_STREAM", 1) != 0;
-    e->ir_stages = std::max(1, std::min(kIrStage, env_int("TVOLAP_IR_STAGES", 1)));
-    e->wide_mode = env_int("TVOLAP_WIDE", 1);
-    e->wide_warp_fft = env_int("TVOLAP_WIDE_WARPFFT", 1);
-    e->pipe_merge = env_int("TVOLAP_PIPE_MERGE", 1);
+    if (e->fix_p > 0) e->P = (int)e->fix_p;
+    if (e->fix_nt > 0) e->NT = (int)e->fix_nt;
+    // (same-box A/B, C2 exchange every 16 hops: K4 on a side stream 2.82 us/hop, + PDL 2.77,
+    // in-stream K4 chained by PDL 2.53, profiles/r01_ab_pdl.txt: k4_side = k4_stream = 1)
 }
 
 // Blocked kernel geometry for the current P: W = 2L/P (parity x float4) work items per CTA.
@@ -311,12 +350,11 @@ void pick_block_geometry(tvolap_engine* e) {
             e->JH = 8;
         }
         e->PB = (int)pb;
-        const int eb = env_int("TVOLAP_PB", 0), ej = env_int("TVOLAP_JH", 0);
-        if (eb > 0) e->PB = eb;
-        if (ej > 0) e->JH = ej;
+        if (e->fix_pb > 0) e->PB = (int)e->fix_pb;
+        if (e->fix_jh > 0) e->JH = (int)e->fix_jh;
     }
     const long W = e->N / e->PB;
-    e->NTB = std::max(32, std::min(256, env_int("TVOLAP_NTB", 256)));  // A/B knob; 256 measured best
+    e->NTB = (int)std::max<long>(32, std::min<long>(256, e->ntb));  // A/B knob; 256 measured best
     e->QB = 1;
     if (W < e->NTB) {
         e->QB = (int)(e->NTB / W);
@@ -356,8 +394,11 @@ void validate_launch(const tvolap_engine* e, int P, int NT) {
                            " B of shared memory per CTA (max 227 KB)"};
 }
 
+void apply_default_tuning(tvolap_engine* e);
+
 void init_common(tvolap_engine* e, int device, long hop, long sources, long ears, long partitions) {
     e->device = device;
+    CK(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, device));
     e->L = hop;
     e->N = 2 * hop;
     e->S = sources;
@@ -397,6 +438,7 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     e->staged.assign(e->S, 0);
     e->d_sel = dalloc<int>(e->S);
     CK(cudaMemsetAsync(e->d_sel, 0, sizeof(int) * e->S, e->stream));
+    apply_default_tuning(e);
     pick_launch_config(e);
     validate_launch(e, e->P, e->NT);
     pick_block_geometry(e);
@@ -417,7 +459,14 @@ const float* stage_ir(tvolap_engine* e, const float* ir, size_t count, cudaStrea
 
 void latch(tvolap_engine* e) {  // engine.cpp:54-58
     std::lock_guard<std::mutex> lock(e->mu);
+    if (e->pending_ext) {  // a pre-partitioned device set: O(1), read in place from now on
+        set_release(e->active_ext);
+        e->active_ext = e->pending_ext;
+        e->pending_ext = nullptr;
+    }
     if (e->pending) {
+        set_release(e->active_ext);  // back to the engine's own pool
+        e->active_ext = nullptr;
         if (e->staged_on_side) {  // already transformed on the side stream
             CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
         } else if (e->staged_in_stream) {  // K4 on the engine stream, chained to the hop launches
@@ -443,6 +492,27 @@ void latch(tvolap_engine* e) {  // engine.cpp:54-58
     }
 }
 
+// Paths that install further sets into pool slots mid-call (the switching launch, the wide
+// pass) need the running filter in a pool slot too: copy an external set into the next slot.
+void materialize_ext(tvolap_engine* e) {
+    if (!e->active_ext) return;
+    const int slot = (e->active + 1) % kSlots;
+    const size_t elems = (size_t)e->S * e->M * e->N;
+    CK(cudaMemcpyAsync(e->pool + (size_t)slot * elems, e->active_ext->spec, elems * sizeof(float2),
+                       cudaMemcpyDeviceToDevice, e->stream));
+    e->active = slot;
+    set_release(e->active_ext);
+    e->active_ext = nullptr;
+}
+
+// A replacement staged at the very hop a call starts from supersedes whatever was staged.
+void drop_pending(tvolap_engine* e) {
+    if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+    e->pending = false;
+    set_release(e->pending_ext);
+    e->pending_ext = nullptr;
+}
+
 void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_stride, float* out, long out_stride,
                  const int* sched, long sched_stride) {
     HopParams p;
@@ -459,14 +529,14 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.out = out;
     p.out_stride = out_stride;
     p.ring = e->ring;
-    p.pool = e->pool;
+    p.pool = e->active_ext ? e->active_ext->spec : e->pool;
     if (e->bank && !sched) {  // bank engines without a per-hop schedule: the latched selection
         sched = e->d_sel;
         sched_stride = 0;
     }
     p.sched = sched;
     p.sched_stride = sched_stride;
-    p.entry_base = e->bank ? 0 : e->active * (int)e->S;
+    p.entry_base = (e->bank || e->active_ext) ? 0 : e->active * (int)e->S;
     p.hist = e->hist;
     p.ola = e->ola;
     p.tw = e->tw;
@@ -511,7 +581,7 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     }
 }
 
-void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
+void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched, bool need_host) {
     if (e->chunk_hops < kc) {
         CK(cudaStreamSynchronize(e->stream));
         CK(cudaStreamSynchronize(e->h2d));
@@ -519,14 +589,22 @@ void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
         for (int b = 0; b < 2; ++b) {
             if (e->d_in[b]) CK(cudaFree(e->d_in[b]));
             if (e->d_out[b]) CK(cudaFree(e->d_out[b]));
-            if (e->h_in[b]) CK(cudaFreeHost(e->h_in[b]));
-            if (e->h_out[b]) CK(cudaFreeHost(e->h_out[b]));
             e->d_in[b] = dalloc<float>((size_t)e->S * kc * e->L);
             e->d_out[b] = dalloc<float>((size_t)e->S * e->E * kc * e->L);
-            CK(cudaMallocHost(&e->h_in[b], sizeof(float) * e->S * kc * e->L));
-            CK(cudaMallocHost(&e->h_out[b], sizeof(float) * e->S * e->E * kc * e->L));
         }
         e->chunk_hops = kc;
+    }
+    // pinned host staging only for pageable caller buffers (pinned ones are copied directly)
+    if (need_host && e->host_chunk < e->chunk_hops) {
+        CK(cudaStreamSynchronize(e->h2d));
+        CK(cudaStreamSynchronize(e->d2h));
+        for (int b = 0; b < 2; ++b) {
+            if (e->h_in[b]) CK(cudaFreeHost(e->h_in[b]));
+            if (e->h_out[b]) CK(cudaFreeHost(e->h_out[b]));
+            CK(cudaMallocHost(&e->h_in[b], sizeof(float) * e->S * e->chunk_hops * e->L));
+            CK(cudaMallocHost(&e->h_out[b], sizeof(float) * e->S * e->E * e->chunk_hops * e->L));
+        }
+        e->host_chunk = e->chunk_hops;
     }
     if (need_sched && e->sch_cap < kc) {
         CK(cudaStreamSynchronize(e->stream));
@@ -541,6 +619,8 @@ void ensure_pipeline(tvolap_engine* e, long kc, bool need_sched) {
 bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n,
                    const int* sched);
 bool run_wide_set(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n);
+bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n,
+                   const int* dsched);
 
 void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float* out, long out_stride, long n,
                        const int* sched) {
@@ -553,6 +633,7 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
     auto hops_launch = [&](long hop0, long kc, const float* ip, long is, float* op, long os, const int* sch_launch,
                            const int* sch_hops) {
         if (sched && e->bank && run_wide_bank(e, hop0, ip, is, op, os, kc, sch_hops)) return;
+        if (sched && e->bank && run_bank_pass(e, hop0, ip, is, op, os, kc, sch_launch)) return;
         if (!sched && !e->bank && run_wide_set(e, hop0, ip, is, op, os, kc)) return;
         launch_hops(e, hop0, kc, ip, is, op, os, sch_launch, sched ? S : 0);
     };
@@ -560,8 +641,11 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
         hops_launch(e->hops, n, in, in_stride, out, out_stride, sched, sched);
     } else {
         const long per_hop = S * L * (1 + E);
-        const long kc_max = std::max<long>(1, std::min<long>(n, (1L << env_int("TVOLAP_PIPE_LOG2", 25)) / per_hop));
-        ensure_pipeline(e, kc_max, sched && msch != Mem::Device);
+        long kc_want = (1L << e->pipe_log2) / per_hop;
+        // bank passes re-read M delay-line slots per pass: chunks of >= 8M hops keep that small
+        if (sched && e->bank && e->bank_pass) kc_want = std::max<long>(kc_want, 8 * e->M);
+        const long kc_max = std::max<long>(1, std::min<long>(n, kc_want));
+        ensure_pipeline(e, kc_max, sched && msch != Mem::Device, min == Mem::Pageable || mout == Mem::Pageable);
         const long Kc = e->chunk_hops;
         CK(cudaEventRecord(e->ev_start, e->stream));
         CK(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
@@ -810,7 +894,7 @@ bool wide_eligible(const tvolap_engine* e, long n_hops, long period) {
     if (period < 3 || n_hops < period || n_hops < 16) return false;
     // auto: only where the hop-blocked kernel leaves most of the GPU idle (lanes x cluster CTAs
     // below two per SM, e.g. C1/C2); there the hop axis is the parallelism
-    if (e->wide_mode == 1 && e->S * e->PB > 2 * 148) return false;
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * e->sms) return false;
     return true;
 }
 
@@ -866,7 +950,7 @@ void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, flo
     p.S = (int)S;
     // partition groups: the hop-blocked kernel's (bit-identical sums) with its Stockham transforms;
     // one chain with the warp transforms (equal to fp32 rounding anyway; TVOLAP_WIDE_Q overrides)
-    p.Q = env_int("TVOLAP_WIDE_Q", warp_fft ? 1 : e->QM);
+    p.Q = e->wide_q > 0 ? (int)e->wide_q : (warp_fft ? 1 : e->QM);
     p.hop0 = hop0;
     p.n = (int)nh;
     p.in = in;
@@ -894,7 +978,7 @@ void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, flo
     p.slot_lock = e->wide_lock;
     p.nslots = nslots;
     p.warp_fft = warp_fft;
-    p.stage_ir = env_int("TVOLAP_WIDE_STAGE", 1);
+    p.stage_ir = (int)e->wide_stage;
     cudaEvent_t ev0, ev1;
     prof_pair(e, &ev0, &ev1);
     CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
@@ -914,25 +998,33 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     const long n_w = last >= 3 ? n_hops : (nsw - 1) * period;
     if (irs[0]) {  // a staged set is superseded at this very hop (last wins)
         std::lock_guard<std::mutex> lock(e->mu);
-        if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
-        e->pending = false;
+        drop_pending(e);
     }
     latch(e);
+    materialize_ext(e);
+    if (e->launch_new_ir) {  // a latched set the first hop launch would have transformed (fused-K4 mode)
+        CK(tvb::launch_partition((int)L, (int)M, S, e->launch_new_ir, e->launch_new_len, e->launch_new_len, e->pool,
+                                 (long)e->active * S, e->tw, e->pk, e->stream));
+        ++e->launches;
+        if (e->launch_buf >= 0) CK(cudaEventRecord(e->ev_used[e->launch_buf], e->stream));
+        e->launch_new_ir = nullptr;
+        e->launch_buf = -1;
+    }
     // 16-hop tiles, or 8-hop tiles when no period needs more (8-hop periods would leave half of a
     // 16-hop tile's MAC outputs unused) or the 16-hop tile's shared memory does not fit
     int JH = period <= 8 ? 4 : 8;
     if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
     const long Jmax = 2 * JH;
     const size_t set_elems = (size_t)S * M * N;
-    const long budget_mb = env_int("TVOLAP_WIDE_POOL_MB", 8192);
+    const long budget_mb = e->wide_pool_mb;
     const long cap_sets = std::max<long>(1, (long)((budget_mb << 20) / (long)(set_elems * sizeof(float2))));
     const float2* cur_set = e->pool + (size_t)e->active * set_elems;
     // Fused K4: when every period is one tile, each tile transforms its own set into an
     // L2-resident scratch slot (no set spectra through HBM); TVOLAP_WIDE_FUSE=0 disables.
-    const bool fuse = env_int("TVOLAP_WIDE_FUSE", 1) != 0 && period <= Jmax && period >= 3;
+    const bool fuse = e->wide_fuse != 0 && period <= Jmax && period >= 3;
     int nslots = 0;
     if (fuse) {
-        const int q_launch = env_int("TVOLAP_WIDE_Q", e->wide_warp_fft ? 1 : e->QM);  // as wide_pass sets it
+        const int q_launch = e->wide_q > 0 ? (int)e->wide_q : (e->wide_warp_fft ? 1 : e->QM);  // as wide_pass sets it
         nslots = tvb::wide_mac_ctas_per_sm((int)L, JH, (int)M, q_launch) * sm_count_of(e->device);
         if (nslots <= 0) throw ApiError{TVOLAP_ERR_CUDA, "wide pass: no resident CTA for the MAC kernel"};
         ensure_dev(e->wide_scratch, e->wide_scratch_cap, (size_t)nslots * (M + tvb::kWideTail) * N);
@@ -945,7 +1037,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     const float* last_ir = nullptr;
     // periods per pass: the extended spectra (and per-tile carries) of a pass stay within
     // TVOLAP_WIDE_XE_MB (default 4 GB), the sets of an unfused pass within TVOLAP_WIDE_POOL_MB
-    const long xe_mb = env_int("TVOLAP_WIDE_XE_MB", 4096);
+    const long xe_mb = e->wide_xe_mb;
     const long per_period = (long)(S * N * sizeof(float2) * period + S * 9 * L * sizeof(float));
     const long cap_periods = std::max<long>(1, (xe_mb << 20) / std::max<long>(1, per_period) - (M + 32) / period);
     for (long k0 = 0; k0 < nsw_w;) {
@@ -1032,7 +1124,7 @@ bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride,
                    const int* sched) {
     const long S = e->S, M = e->M, N = e->N, L = e->L;
     if (e->wide_mode == 0 || e->E != 1 || !tvb::wide_supported((int)L) || n < 16) return false;
-    if (e->wide_mode == 1 && e->S * e->PB > 2 * 148) return false;
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * e->sms) return false;
     std::vector<int> h((size_t)n * S);
     if (classify(sched) == Mem::Device) {
         CK(cudaMemcpyAsync(h.data(), sched, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, e->stream));
@@ -1055,7 +1147,7 @@ bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride,
     int JH = longest <= 8 ? 4 : 8;
     if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
     const long Jmax = 2 * JH;
-    const long xe_mb = env_int("TVOLAP_WIDE_XE_MB", 4096);
+    const long xe_mb = e->wide_xe_mb;
     const long max_hops = std::max<long>(Jmax, (xe_mb << 20) / (long)(S * N * sizeof(float2)) - 2 * (M + 32));
     const size_t entry_elems = (size_t)e->E * M * N;
     for (size_t i0 = 0; i0 + 1 < seg.size();) {  // passes of whole segments
@@ -1082,20 +1174,101 @@ bool run_wide_bank(tvolap_engine* e, long hop0, const float* in, long in_stride,
     return true;  // (the caller accounts hops, counts and the latched selection)
 }
 
+// Bank engines with a per-hop schedule that changes every hop (C3, C5) on device-resident hops
+// (the whole call, or one chunk of the pinned-host pipeline): bank passes (tvolap_wide.cu) — K1
+// of every hop into Xe, the MAC over (tile, source, partition group) CTAs with the group as the
+// slowest grid axis (the bank slice each group reads stays L2-resident), K5 + overlap-add per
+// (tile, output lane) and the carry fix-up. `dsched` is device memory (rows of the call's hops).
+// Not bit-identical to the hop-blocked kernel (different partition grouping and transforms);
+// both match the reference within the north-star tolerance. False when not eligible.
+bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n,
+                   const int* dsched) {
+    const long S = e->S, M = e->M, N = e->N, L = e->L, E = e->E;
+    if (!e->bank_pass || !dsched || classify(dsched) != Mem::Device) return false;
+    const int JH = (N <= 128 && E == 1) ? 16 : 8;
+    const long J = 2 * JH;
+    // (any call of >= 3 hops: the same per-output sums whatever the call / chunk boundaries)
+    if (!tvb::bank_pass_supported((int)L, (int)E, JH) || n < 3) return false;
+    // partition groups: the bank slice a group reads stays well inside L2 (<= 40 MB)
+    const double bank_bytes = (double)e->n_bank * E * M * N * sizeof(float2);
+    int Q = 1;
+    while (Q < 64 && 2 * Q <= M && bank_bytes / Q > 40e6) Q *= 2;
+    // hops per pass: extended spectra + partials within the budget
+    const long per_hop = (long)(S * N * sizeof(float2) + (size_t)Q * S * E * N * sizeof(float2));
+    long max_hops = std::max<long>(4 * J, (e->bank_pass_mb << 20) / per_hop);
+    if (e->bank_pass_hops > 0) max_hops = std::max<long>(2 * J, e->bank_pass_hops);
+    for (long h0 = 0; h0 < n;) {
+        long nh = std::min(max_hops, n - h0);
+        if (n - h0 - nh > 0 && n - h0 - nh < 3) nh -= 3;  // no 1-2 hop pass at the end
+        const long tp = (nh + J - 1) / J, base = nh / tp, rem = nh % tp;  // tiles of 3 .. J hops
+        std::vector<int> t0;
+        for (long w = 0, st = 0; w < tp; ++w) {
+            t0.push_back((int)st);
+            st += base + (w < rem ? 1 : 0);
+        }
+        t0.push_back((int)nh);
+        const long ntiles = tp;
+        ensure_dev(e->d_wide_tile0, e->wide_tile_cap, (size_t)ntiles + 1);
+        CK(cudaMemcpyAsync(e->d_wide_tile0, t0.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice, e->stream));
+        ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * E * ntiles * 3 * L);
+        ensure_dev(e->wide_head, e->wide_head_cap, (size_t)S * E * ntiles * 6 * L);
+        const long T = (nh + 1) / 2 + M + tvb::kWideFront + JH + 4;
+        ensure_dev(e->wide_xe, e->wide_xe_cap, (size_t)S * 2 * T * N);
+        ensure_dev(e->bank_yq, e->bank_yq_cap, (size_t)Q * S * E * nh * N);
+        tvb::WideParams p{};
+        p.L = (int)L;
+        p.M = (int)M;
+        p.D = (int)e->D;
+        p.S = (int)S;
+        p.Q = Q;
+        p.E = (int)E;
+        p.hop0 = hop0 + h0;
+        p.n = (int)nh;
+        p.in = in + h0 * L;
+        p.in_stride = in_stride;
+        p.out = out + h0 * L;
+        p.out_stride = out_stride;
+        p.ring = e->ring;
+        p.xe = e->wide_xe;
+        p.T = T;
+        p.tbase = (p.hop0 >> 1) - M - tvb::kWideFront;
+        p.hist = e->hist;
+        p.ola = e->ola;
+        p.tw = e->tw;
+        p.pk = e->pk;
+        p.win = e->win;
+        p.tile0 = e->d_wide_tile0;
+        p.ntiles = (int)ntiles;
+        p.tstate = e->wide_state;
+        p.thead = e->wide_head;
+        p.warp_fft = 1;
+        p.pool = e->pool;
+        p.sched = dsched + h0 * S;
+        p.yq = e->bank_yq;
+        cudaEvent_t ev0, ev1;
+        prof_pair(e, &ev0, &ev1);
+        CK(tvb::launch_bank_pass(p, JH, e->stream, ev0, ev1));
+        e->launches += 5;
+        ++e->wide_passes;
+        h0 += nh;
+    }
+    return true;  // (the caller accounts hops, counts and the latched selection)
+}
+
 // Filter-set engines: a process_hops call (one filter for all its hops) on device buffers or a
 // pinned-pipeline chunk as one time-parallel pass over the active set, with the hop kernels'
 // Stockham transforms (bit-identical to the hop-blocked launch). False when not eligible.
 bool run_wide_set(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long n) {
     const long S = e->S, M = e->M, N = e->N, L = e->L;
     if (e->wide_mode == 0 || e->E != 1 || !tvb::wide_supported((int)L) || n < 32) return false;
-    if (e->wide_mode == 1 && e->S * e->PB > 2 * 148) return false;
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * e->sms) return false;
     if (e->launch_new_ir) return false;  // a staged set the first hop launch transforms (K4 fused mode)
     int JH = 8;
     if (tvb::wide_mac_smem_bytes((int)L, JH, (int)M, e->QM) > 227 * 1024) JH = 4;
     const long Jmax = 2 * JH;
-    const long xe_mb = env_int("TVOLAP_WIDE_XE_MB", 4096);
+    const long xe_mb = e->wide_xe_mb;
     const long max_hops = std::max<long>(Jmax, (xe_mb << 20) / (long)(S * N * sizeof(float2)) - 2 * (M + 32));
-    const float2* set = e->pool + (size_t)e->active * S * M * N;
+    const float2* set = e->active_ext ? e->active_ext->spec : e->pool + (size_t)e->active * S * M * N;
     for (long h0 = 0; h0 < n;) {
         long nh = std::min(max_hops, n - h0);
         if (n - h0 - nh > 0 && n - h0 - nh < 3) nh -= 3;  // no 1-2 hop pass at the end
@@ -1154,8 +1327,8 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         bool pinned = min == Mem::Pinned && mout == Mem::Pinned;
         // the switching kernel (in-kernel K4); in a pinned pipeline every chunk launch must take
         // the hop-blocked kernel: full periods, and a last one of at least block_min hops
-        const long gap_units = 2 * warps * blocks * env_int("TVOLAP_K4_GAP_MULT", 1);
-        const bool n_ok = e->N == 256 || e->N == 512 || (e->N == 1024 && env_int("TVOLAP_SW_1024", 0));
+        const long gap_units = 2 * warps * blocks * e->k4_gap_mult;
+        const bool n_ok = e->N == 256 || e->N == 512 || (e->N == 1024 && e->sw_1024);
         const bool kernel_ok = n_ok && e->E == 1 && units <= gap_units &&
                                (!pinned || (period >= e->block_min && n_hops - (nsw - 1) * period >= e->block_min));
         dev = dev && kernel_ok;
@@ -1177,17 +1350,19 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
         }
         if (kernel_ok && irs[0]) {  // a staged set is superseded at this very hop (last wins)
             std::lock_guard<std::mutex> lock(e->mu);
-            if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
-            e->pending = false;
+            drop_pending(e);
         }
-        if (kernel_ok) latch(e);
+        if (kernel_ok) {
+            latch(e);
+            materialize_ext(e);
+        }
         const long S = e->S, L = e->L;
         // Host pipeline (pinned buffers): chunks of Kp periods staged through two device buffers;
         // H2D of chunk c+1 and D2H of chunk c-1 overlap the launch of chunk c, every copy large.
         long Kp = nsw;
         if (pinned) {
             const long per = S * period * L * 4 * 2 + (ir_length > 0 ? S * ir_length * 4 : 0);
-            Kp = std::max<long>(1, std::min<long>(nsw, ((long)env_int("TVOLAP_PIPE_MB", 64) << 20) / per));
+            Kp = std::max<long>(1, std::min<long>(nsw, (e->pipe_mb << 20) / per));
         }
         std::vector<const float*> ptrs(nsw);
         std::vector<int> entries(nsw, -1);
@@ -1337,6 +1512,12 @@ int tvolap_exchange_filter(tvolap_engine* e, const float* ir, long ir_length, lo
     return guarded([&] {
         CK(cudaSetDevice(e->device));
         std::lock_guard<std::mutex> lock(e->mu);
+        // A set still being transformed on the side stream into the next slot is superseded
+        // (last staged wins): whatever transforms the replacement into the same slot on the
+        // engine stream (at latch, or fused into the first hop launch) must come after it.
+        if (e->pending && e->staged_on_side) CK(cudaStreamWaitEvent(e->stream, e->ev_side, 0));
+        set_release(e->pending_ext);
+        e->pending_ext = nullptr;
         // Stage only: the next process call's first kernel transforms the set (K4 fused).
         // Device IRs are used in place; host IRs are uploaded on the side stream into one of
         // two buffers, after the kernel that consumed that buffer last time.
@@ -1526,6 +1707,140 @@ uint64_t tvolap_kernel_launches(const tvolap_engine* e) { return e ? e->launches
 
 uint64_t tvolap_wide_passes(const tvolap_engine* e) { return e ? e->wide_passes : 0; }
 
+// ------------------------------------------------------------------ tuning knobs
+// Every A/B switch of the kernel, geometry and pipeline choices is a named knob; the defaults are
+// the measured-best choices. Nothing in the library reads the environment.
+extern "C++" {
+namespace {
+struct Knob {
+    const char* key;
+    long tvolap_engine::*field;  // per-engine knob, or
+    long* global;                // process-wide launch knob
+    long lo, hi;
+    int apply;                   // 0: value only, 1: re-derive launch + block geometry
+};
+const Knob kKnobs[] = {
+    {"block_min", &tvolap_engine::block_min, nullptr, 1, 1L << 40, 0},
+    {"k4_side", &tvolap_engine::k4_side, nullptr, 0, 1, 0},
+    {"k4_stream", &tvolap_engine::k4_stream, nullptr, 0, 1, 0},
+    {"ir_stages", &tvolap_engine::ir_stages, nullptr, 1, kIrStage, 0},
+    {"wide", &tvolap_engine::wide_mode, nullptr, 0, 2, 0},
+    {"wide_warp_fft", &tvolap_engine::wide_warp_fft, nullptr, 0, 1, 0},
+    {"wide_q", &tvolap_engine::wide_q, nullptr, -1, 64, 0},
+    {"wide_stage", &tvolap_engine::wide_stage, nullptr, 0, 1, 0},
+    {"wide_pool_mb", &tvolap_engine::wide_pool_mb, nullptr, 1, 1L << 20, 0},
+    {"wide_fuse", &tvolap_engine::wide_fuse, nullptr, 0, 1, 0},
+    {"wide_xe_mb", &tvolap_engine::wide_xe_mb, nullptr, 1, 1L << 20, 0},
+    {"bank_pass", &tvolap_engine::bank_pass, nullptr, 0, 1, 0},
+    {"bank_pass_mb", &tvolap_engine::bank_pass_mb, nullptr, 1, 1L << 20, 0},
+    {"bank_pass_hops", &tvolap_engine::bank_pass_hops, nullptr, 0, 1L << 30, 0},
+    {"pipe_merge", &tvolap_engine::pipe_merge, nullptr, 0, 1, 0},
+    {"pipe_mb", &tvolap_engine::pipe_mb, nullptr, 1, 1L << 20, 0},
+    {"pipe_log2", &tvolap_engine::pipe_log2, nullptr, 10, 34, 0},
+    {"k4_gap_mult", &tvolap_engine::k4_gap_mult, nullptr, 1, 64, 0},
+    {"sw_1024", &tvolap_engine::sw_1024, nullptr, 0, 1, 0},
+    {"p", &tvolap_engine::fix_p, nullptr, 0, 8, 1},
+    {"nt", &tvolap_engine::fix_nt, nullptr, 0, 1024, 1},
+    {"pb", &tvolap_engine::fix_pb, nullptr, 0, 8, 1},
+    {"jh", &tvolap_engine::fix_jh, nullptr, 0, 8, 1},
+    {"ntb", &tvolap_engine::ntb, nullptr, 32, 256, 1},
+    {"pdl", nullptr, &tvb::g_launch_pdl, 0, 1, 0},
+    {"k4_warp", nullptr, &tvb::g_launch_k4_warp, 0, 1, 0},
+    {"k4_prefetch", nullptr, &tvb::g_launch_k4_prefetch, 0, 1, 0},
+};
+std::mutex g_tune_mu;
+std::vector<std::pair<const Knob*, long>> g_default_tuning;  // engine knobs applied at creation
+
+const Knob& find_knob(const char* key) {
+    if (key)
+        for (const Knob& k : kKnobs)
+            if (std::strcmp(k.key, key) == 0) return k;
+    throw ApiError{TVOLAP_ERR_INVALID_INPUT, std::string("unknown tuning key: ") + (key ? key : "(null)")};
+}
+
+void check_range(const Knob& k, long v) {
+    if (v < k.lo || v > k.hi)
+        throw ApiError{TVOLAP_ERR_INVALID_INPUT, std::string("tuning ") + k.key + " must be in [" +
+                                                     std::to_string(k.lo) + ", " + std::to_string(k.hi) + "]"};
+}
+
+void apply_default_tuning(tvolap_engine* e) {
+    std::lock_guard<std::mutex> lock(g_tune_mu);
+    for (const auto& kv : g_default_tuning) e->*(kv.first->field) = kv.second;
+}
+}  // namespace
+}  // extern "C++"
+
+int tvolap_set_tuning(tvolap_engine* e, const char* key, long value) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    return guarded([&] {
+        const Knob& k = find_knob(key);
+        check_range(k, value);
+        if (k.global) {
+            *k.global = value;
+            return;
+        }
+        if (k.apply) {  // validate the resulting geometry before committing it
+            const long old = e->*k.field;
+            e->*k.field = value;
+            try {
+                pick_launch_config(e);
+                validate_launch(e, e->P, e->NT);
+                pick_block_geometry(e);
+            } catch (...) {
+                e->*k.field = old;
+                pick_launch_config(e);
+                pick_block_geometry(e);
+                throw;
+            }
+        } else {
+            e->*k.field = value;
+        }
+    });
+}
+
+int tvolap_get_tuning(const tvolap_engine* e, const char* key, long* value) {
+    if (!e || !value) return set_err(TVOLAP_ERR_INVALID_INPUT, "null engine or output");
+    return guarded([&] {
+        const Knob& k = find_knob(key);
+        *value = k.global ? *k.global : e->*k.field;
+    });
+}
+
+int tvolap_set_default_tuning(const char* key, long value) {
+    return guarded([&] {
+        const Knob& k = find_knob(key);
+        check_range(k, value);
+        if (k.global) {
+            *k.global = value;
+            return;
+        }
+        std::lock_guard<std::mutex> lock(g_tune_mu);
+        for (auto& kv : g_default_tuning)
+            if (kv.first == &k) {
+                kv.second = value;
+                return;
+            }
+        g_default_tuning.emplace_back(&k, value);
+    });
+}
+
+int tvolap_reset_default_tuning(void) {
+    std::lock_guard<std::mutex> lock(g_tune_mu);
+    g_default_tuning.clear();
+    tvb::g_launch_pdl = tvb::g_launch_k4_warp = tvb::g_launch_k4_prefetch = 1;
+    return TVOLAP_OK;
+}
+
+const char* tvolap_tuning_keys(void) {
+    static const std::string keys = [] {
+        std::string out;
+        for (const Knob& k : kKnobs) out += (out.empty() ? "" : ",") + std::string(k.key);
+        return out;
+    }();
+    return keys.c_str();
+}
+
 // ------------------------------------------------------------------ spectral primitives
 namespace {
 
@@ -1702,6 +2017,262 @@ int tvolap_mix_device(int device, long sources, long ears, long samples, const f
         CK(cudaSetDevice(device));
         CK(tvb::launch_mix(sources, ears, samples, out, out_stride, mix, mix_stride, (cudaStream_t)stream));
     });
+}
+
+// ---- device-resident filter partition sets (partition.hpp:21-43)
+int tvolap_set_create(tvolap_set** out, int device, long hop, long channels, long ir_length, const float* ir,
+                      long min_partitions) {
+    if (!out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null output handle");
+    *out = nullptr;
+    if (ir_length < 1 || channels < 1 || !ir)  // partition.cpp:21-24, in the reference's order
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "partition: impulse response is empty");
+    if (hop < 2 || !is_pow2(4 * hop))
+        return set_err(TVOLAP_ERR_INVALID_SIZE, "partition: 4L must be a power of two, got L = " + std::to_string(hop));
+    return guarded([&] {
+        require_device(device);
+        auto* st = new tvolap_set();
+        try {
+            st->device = device;
+            st->L = hop;
+            st->N = 2 * hop;
+            st->S = channels;
+            st->source_length = ir_length;
+            st->M = std::max((ir_length + 2 * hop - 1) / (2 * hop), std::max<long>(min_partitions, 1));
+            const size_t elems = (size_t)channels * st->M * st->N + (size_t)tvb::kWideTail * st->N;
+            st->spec = dalloc<float2>(elems);
+            CK(cudaMemset(st->spec, 0, elems * sizeof(float2)));  // (synchronous: done before the K4 below)
+            Keep k;
+            Tables t(st->N);
+            const float2* tw = (const float2*)dev_in(t.tw.data(), sizeof(float2) * t.tw.size(), k.v);
+            const float2* pk = (const float2*)dev_in(t.pk.data(), sizeof(float2) * t.pk.size(), k.v);
+            const float* dir = (const float*)dev_in(ir, sizeof(float) * channels * ir_length, k.v);
+            cudaStream_t sm = nullptr;  // a private stream: no device-wide synchronisation
+            CK(cudaStreamCreateWithFlags(&sm, cudaStreamNonBlocking));
+            const cudaError_t e1 = tvb::launch_partition((int)hop, (int)st->M, channels, dir, ir_length, ir_length,
+                                                         st->spec, 0, tw, pk, sm);
+            const cudaError_t e2 = cudaStreamSynchronize(sm);
+            cudaStreamDestroy(sm);
+            CK(e1);
+            CK(e2);
+        } catch (...) {
+            set_release(st);
+            throw;
+        }
+        *out = st;
+    });
+}
+
+int tvolap_set_release(tvolap_set* s) {
+    set_release(s);
+    return TVOLAP_OK;
+}
+
+int tvolap_set_geometry(const tvolap_set* s, long* hop, long* partitions, long* channels, long* source_length) {
+    if (!s) return set_err(TVOLAP_ERR_INVALID_INPUT, "null set");
+    if (hop) *hop = s->L;
+    if (partitions) *partitions = s->M;
+    if (channels) *channels = s->S;
+    if (source_length) *source_length = s->source_length;
+    return TVOLAP_OK;
+}
+
+// spectra[((c * M + m) * (2L + 1) + k) * 2 + {re, im}], host or device (tvolap_partition's layout)
+int tvolap_set_spectra(const tvolap_set* s, float* spectra) {
+    if (!s || !spectra) return set_err(TVOLAP_ERR_INVALID_INPUT, "null set or output");
+    return guarded([&] {
+        CK(cudaSetDevice(s->device));
+        const long N = s->N, F = s->S * s->M;
+        std::vector<float2> packed((size_t)F * N);
+        CK(cudaMemcpy(packed.data(), s->spec, sizeof(float2) * packed.size(), cudaMemcpyDeviceToHost));
+        std::vector<float> full((size_t)F * (N + 1) * 2);
+        for (long f = 0; f < F; ++f) {
+            const float2* src = packed.data() + f * N;
+            float* dst = full.data() + f * (N + 1) * 2;
+            dst[0] = src[0].x;
+            dst[1] = 0.f;
+            for (long q = 1; q < N; ++q) {
+                dst[2 * q] = src[q].x;
+                dst[2 * q + 1] = src[q].y;
+            }
+            dst[2 * N] = src[0].y;
+            dst[2 * N + 1] = 0.f;
+        }
+        if (classify(spectra) == Mem::Device)
+            CK(cudaMemcpy(spectra, full.data(), sizeof(float) * full.size(), cudaMemcpyHostToDevice));
+        else
+            std::memcpy(spectra, full.data(), sizeof(float) * full.size());
+    });
+}
+
+// reassemble (partition.cpp:53-65): inverse-transform every partition, keep its first 2L samples,
+// concatenate: out[c * (2 L M) + n] (the source response zero-padded to M * 2L taps)
+int tvolap_set_reassemble(const tvolap_set* s, float* out) {
+    if (!s || !out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null set or output");
+    const long n = 4 * s->L, F = s->S * s->M, slice = 2 * s->L;
+    std::vector<float> bins((size_t)F * (n / 2 + 1) * 2), y((size_t)F * n);
+    if (int rc = tvolap_set_spectra(s, bins.data())) return rc;
+    if (int rc = tvolap_inverse_real(s->device, n, F, bins.data(), y.data())) return rc;
+    return guarded([&] {
+        std::vector<float> res((size_t)F * slice);
+        for (long f = 0; f < F; ++f) std::memcpy(res.data() + f * slice, y.data() + f * n, sizeof(float) * slice);
+        if (classify(out) == Mem::Device) {
+            CK(cudaSetDevice(s->device));
+            CK(cudaMemcpy(out, res.data(), sizeof(float) * res.size(), cudaMemcpyHostToDevice));
+        } else {
+            std::memcpy(out, res.data(), sizeof(float) * res.size());
+        }
+    });
+}
+
+// TvolapEngine(shared_ptr<const FilterPartitionSet>) (engine.hpp:35, engine.cpp:9-32): the engine
+// reads the set's spectra in place (no K4 at construction).
+int tvolap_create_from_set(tvolap_engine** out, const tvolap_set* s) {
+    if (!out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null output handle");
+    *out = nullptr;
+    if (!s) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "engine requires a filter partition set");
+    tvolap_engine* e = nullptr;
+    const int rc = guarded([&] {
+        require_device(s->device);
+        e = new tvolap_engine();
+        try {
+            init_common(e, s->device, s->L, s->S, 1, s->M);
+            const size_t slot = (size_t)s->S * s->M * e->N;
+            e->pool = dalloc<float2>(kSlots * slot + (size_t)tvb::kWideTail * e->N);
+            CK(cudaMemsetAsync(e->pool, 0, (kSlots * slot + (size_t)tvb::kWideTail * e->N) * sizeof(float2), e->stream));
+            set_retain(s);
+            e->active_ext = s;
+            CK(cudaStreamSynchronize(e->stream));
+        } catch (...) {
+            delete e;
+            e = nullptr;
+            throw;
+        }
+    });
+    *out = e;
+    return rc;
+}
+
+// exchange_filter(shared_ptr<const FilterPartitionSet>) (engine.hpp:55, engine.cpp:37-48): O(1) —
+// validate, stage (last wins), latch at the next process call; no transform.
+int tvolap_exchange_set(tvolap_engine* e, const tvolap_set* s) {
+    if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
+    if (e->bank) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "exchange_filter on a bank engine; use select_bank");
+    if (!s) return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter is null");
+    if (s->L != e->L) return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter hop differs");
+    if (s->M != e->M) return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter partition count differs");
+    if (s->S != e->S) return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter channel count differs");
+    if (s->device != e->device)
+        return set_err(TVOLAP_ERR_INCOMPATIBLE_FILTER, "replacement filter lives on another device");
+    return guarded([&] {
+        CK(cudaSetDevice(e->device));
+        std::lock_guard<std::mutex> lock(e->mu);
+        drop_pending(e);  // last staged filter wins
+        set_retain(s);
+        e->pending_ext = s;
+    });
+}
+
+// ---- NCCL (C3's cross-GPU mix), loaded at first use so the library has no link-time dependency
+extern "C++" {
+namespace {
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return a;
+        }
+        auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::decay_t<decltype(f)>>(dlsym(h, name)); };
+        sym(a.get_unique_id, "ncclGetUniqueId");
+        sym(a.comm_init_rank, "ncclCommInitRank");
+        sym(a.all_reduce, "ncclAllReduce");
+        sym(a.comm_destroy, "ncclCommDestroy");
+        sym(a.group_start, "ncclGroupStart");
+        sym(a.group_end, "ncclGroupEnd");
+        sym(a.error_string, "ncclGetErrorString");
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.group_start && a.group_end;
+        if (!a.ok) a.err = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    if (!api.ok) throw ApiError{TVOLAP_ERR_CUDA, "NCCL unavailable: " + api.err};
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const NcclApi& a = nccl();
+        throw ApiError{TVOLAP_ERR_CUDA, std::string(what) + ": " + (a.error_string ? a.error_string(r) : "NCCL error")};
+    }
+}
+}  // namespace
+}  // extern "C++"
+
+int tvolap_mix_allreduce(int device, long sources, long ears, long samples, const float* out, long out_stride,
+                         float* mix, long mix_stride, void* nccl_comm, void* stream) {
+    if (!out || !mix || sources < 1 || ears < 1 || samples < 1 || mix_stride < samples || out_stride < samples)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "mix: bad buffers or sizes");
+    return guarded([&] {
+        CK(cudaSetDevice(device));
+        const cudaStream_t st = (cudaStream_t)stream;
+        CK(tvb::launch_mix(sources, ears, samples, out, out_stride, mix, mix_stride, st));
+        if (!nccl_comm) return;
+        const NcclApi& a = nccl();
+        auto comm = static_cast<ncclComm_t>(nccl_comm);
+        if (mix_stride == samples) {
+            nccl_check(a.all_reduce(mix, mix, (size_t)ears * samples, ncclFloat32, ncclSum, comm, st), "ncclAllReduce");
+        } else {
+            nccl_check(a.group_start(), "ncclGroupStart");
+            for (long e2 = 0; e2 < ears; ++e2)
+                nccl_check(a.all_reduce(mix + e2 * mix_stride, mix + e2 * mix_stride, (size_t)samples, ncclFloat32,
+                                        ncclSum, comm, st),
+                           "ncclAllReduce");
+            nccl_check(a.group_end(), "ncclGroupEnd");
+        }
+    });
+}
+
+int tvolap_nccl_unique_id(char id_out[128]) {
+    if (!id_out) return set_err(TVOLAP_ERR_INVALID_INPUT, "null id buffer");
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+        ncclUniqueId id;
+        nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(id_out, &id, sizeof id);
+    });
+}
+
+int tvolap_nccl_comm_init(void** comm_out, int device, int nranks, int rank, const char id[128]) {
+    if (!comm_out || !id || nranks < 1 || rank < 0 || rank >= nranks)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "nccl comm: bad arguments");
+    *comm_out = nullptr;
+    return guarded([&] {
+        CK(cudaSetDevice(device));
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        ncclComm_t c = nullptr;
+        nccl_check(nccl().comm_init_rank(&c, nranks, uid, rank), "ncclCommInitRank");
+        *comm_out = c;
+    });
+}
+
+int tvolap_nccl_comm_destroy(void* comm) {
+    if (!comm) return TVOLAP_OK;
+    return guarded([&] { nccl_check(nccl().comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy"); });
 }
 
 // ======================================================================= comparison convolvers

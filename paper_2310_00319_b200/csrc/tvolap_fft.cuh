@@ -23,6 +23,24 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
     return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// acc += h * x for two packed bins (one float4 = two complex64), plus the Nyquist product of the
+// first one (only kept for the packed bin 0 = (Re X_0, Re X_N), spectral.cpp:121-123):
+// engine.cpp:85-92 / spectral.cpp:160-166.
+__device__ __forceinline__ void cmac4(float4& acc, float& aux, const float4 h, const float4 x) {
+    acc.x = fmaf(h.x, x.x, acc.x);
+    acc.x = fmaf(-h.y, x.y, acc.x);
+    acc.y = fmaf(h.x, x.y, acc.y);
+    acc.y = fmaf(h.y, x.x, acc.y);
+    acc.z = fmaf(h.z, x.z, acc.z);
+    acc.z = fmaf(-h.w, x.w, acc.z);
+    acc.w = fmaf(h.z, x.w, acc.w);
+    acc.w = fmaf(h.w, x.z, acc.w);
+    aux = fmaf(h.y, x.y, aux);
+}
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
 // Radix of the Stockham stage that starts at sub-transform length Ns: 8 while possible, but a

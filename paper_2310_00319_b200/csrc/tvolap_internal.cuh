@@ -47,6 +47,10 @@ struct HopParams {
     long sw_ir_len = 0;
 };
 
+// Process-wide launch knobs (tvolap_set_default_tuning): programmatic dependent launch of the hop
+// kernels, warp-per-partition K4, its per-slice L2 prefetch.
+extern long g_launch_pdl, g_launch_k4_warp, g_launch_k4_prefetch;
+
 // Time-parallel pass (tvolap_wide.cu) over n hops of a device-resident call.
 struct WideParams {
     int L, M, D, S, Q;     // Q: partition groups (the blocked kernel's, for bit-identical sums)
@@ -81,12 +85,22 @@ struct WideParams {
     int stage_ir;               // fused K4: IR slices through a cp.async double buffer in shared memory
     int warp_fft;               // K1 / K5 with one warp per frame (warp four-step FFT) instead of the
                                 // hop kernels' CTA Stockham (equal to fp32 rounding, not bit-identical)
+    // bank pass (per-hop bank schedules, tvolap_wide.cu bank_mac_kernel / bank_k5_kernel)
+    int E = 1;                  // ears: lanes s * E + e share source s's input spectra
+    const float2* pool = nullptr;  // bank spectra [n_bank][E][M][2L]
+    const int* sched = nullptr;    // bank entry of (pass hop h, source s): sched[h * S + s]
+    float2* yq = nullptr;          // MAC partials per partition group [Q][S * E][n][2L]
 };
 int wide_mac_ctas_per_sm(int L, int JH, int M, int Q);
 bool wide_supported(int L);
 size_t wide_mac_smem_bytes(int L, int JH, int M, int Q);
 constexpr int kWideFront = 8;   // Xe front padding slots per parity (tbase = (hop0 >> 1) - M - kWideFront)
 constexpr int kWideTail = 8;    // spectra rows readable past the end of every filter set (prefetch)
+// Bank pass: K1 as launch_wide part 1, then the per-hop-schedule MAC (tiles of 2 JH hops, JO
+// outputs per thread, p.Q partition groups as the slowest grid axis), K5 + overlap-add per tile,
+// fix-up. Events bracket the MAC launch.
+cudaError_t launch_bank_pass(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1);
+bool bank_pass_supported(int L, int E, int JH);
 // parts: 1 = head copy + forward FFTs, 2 = MAC/inverse tiles (+ fix-up); events bracket the tiles
 cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1, int parts);
 // K4 for rows = sets * S IRs: irs[row / S] + (row % S) * ir_len -> pool[(row * M + m) * 2L]

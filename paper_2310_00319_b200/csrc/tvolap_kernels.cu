@@ -94,6 +94,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 namespace tvb {
+
+// process-wide launch knobs (tvolap_set_default_tuning "pdl", "k4_warp", "k4_prefetch")
+long g_launch_pdl = 1;
+long g_launch_k4_warp = 1;
+long g_launch_k4_prefetch = 1;
+
 namespace {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -116,26 +122,19 @@ struct SmemLayout {
     }
 };
 
-__device__ __forceinline__ void cmac4(float4& acc, float& aux, const float4 h, const float4 x) {
-    acc.x = fmaf(h.x, x.x, acc.x);
-    acc.x = fmaf(-h.y, x.y, acc.x);
-    acc.y = fmaf(h.x, x.y, acc.y);
-    acc.y = fmaf(h.y, x.x, acc.y);
-    acc.z = fmaf(h.z, x.z, acc.z);
-    acc.z = fmaf(-h.w, x.w, acc.z);
-    acc.w = fmaf(h.z, x.w, acc.w);
-    acc.w = fmaf(h.w, x.z, acc.w);
-    aux = fmaf(h.y, x.y, aux);  // Nyquist product, only kept for the packed bin 0
-}
-
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
 }
 
-__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
-    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+// TMA-engine bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16 bytes).
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
+// bank per-output MAC: rows per L2 prefetch and prefetch distance (partitions ahead)
+constexpr int kPfRows = 8;
+constexpr int kPfDist = 2 * kPfRows;
+
 
 // K4 fused into the hop kernels: at the start of the launch that latches a staged
 // filter set, each cluster transforms its own source's new IR (partition.cpp:20-51):
@@ -952,6 +951,49 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
                 // per-output filters (bank switching inside the block). Two ears: 32-bit float4
                 // offsets into the pool, one register each instead of a pointer pair (same-box:
                 // C3 5.08e9 vs 4.78e9); one ear keeps pointers (C5 1.07e9 vs 0.94e9 with offsets)
+                //
+                // L2 bulk prefetch (cp.async.bulk.prefetch.L2, no registers): every per-output
+                // filter row and delay-line row is requested kPfDist partitions ahead by one lane
+                // per (output, ear) and one lane for the delay line, so the 16-byte loads below
+                // find their lines in L2 instead of waiting on HBM; bytes in flight towards HBM no
+                // longer depend on the register budget.
+                const int ln = tid & 31;
+                const int fw = f & ~31;  // this warp's float4 column range [fw, fw + 32) of the slice
+                int pf_ent = -1, pf_e = 0;
+#pragma unroll
+                for (int i = 0; i < JH; ++i)
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+                        if (ln == i * E + e && i < ni) pf_ent = ent[i], pf_e = e;
+                const bool row_whole = V == 32 && P == 1;  // warp slice == whole row: rows contiguous
+                auto prefetch_rows = [&](const float4* base, int rows) {  // rows consecutive rows from base
+                    if (row_whole) {
+                        l2_prefetch(base, (unsigned)rows * 512u);
+                    } else {
+                        for (int k = 0; k < rows; ++k) l2_prefetch(base + (long)k * spec4, 512u);
+                    }
+                };
+                // (only where a warp covers 32 consecutive float4 columns of one parity group)
+                const bool pf_on = (V & 31) == 0;
+                auto prefetch_chunk = [&](int mc) {  // partitions [mc, mc + kPfRows) of this thread's group
+                    const int me = min(mc + kPfRows, m1);
+                    if (!pf_on || mc >= me) return;
+                    if (pf_ent >= 0) {
+                        prefetch_rows(pool4 + (((long)pf_ent * E + pf_e) * M + mc) * spec4 + (long)r * V + fw, me - mc);
+                    } else if (ln == 31) {  // delay line: slots of t = -m-1 run downwards from sb - mc - 1
+                        const int hi = wrapD(sb - mc - 1), lo = wrapD(sb - me);
+                        const float4* xw = xr - f + fw;
+                        if (lo <= hi) {
+                            prefetch_rows(xw + (long)lo * spec4, hi - lo + 1);
+                        } else {
+                            prefetch_rows(xw, hi + 1);
+                            prefetch_rows(xw + (long)lo * spec4, D - lo);
+                        }
+                    }
+                };
+#ifndef TVOLAP_NO_L2PF
+                prefetch_chunk(m0 + kPfRows);
+#endif
                 if constexpr (E == 2) {
                     unsigned hoff[JH][E];
 #pragma unroll
@@ -959,36 +1001,48 @@ __global__ void __launch_bounds__(256, 2) tvolap_block_kernel(const HopParams p,
 #pragma unroll
                         for (int e = 0; e < E; ++e)
                             hoff[i][e] = (unsigned)((((long)ent[i] * E + e) * M) * spec4 + (long)r * V + f);
-                    unsigned mo = (unsigned)((long)m0 * spec4);
+                    for (int mc = m0; mc < m1; mc += kPfRows) {
+#ifndef TVOLAP_NO_L2PF
+                        prefetch_chunk(mc + kPfDist);
+#endif
+                        const int me = min(mc + kPfRows, m1);
+                        unsigned mo = (unsigned)((long)mc * spec4);
 #pragma unroll 2
-                    for (int m = m0; m < m1; ++m, mo += (unsigned)spec4) {
-                        const float4 xn = xnext();
+                        for (int m = mc; m < me; ++m, mo += (unsigned)spec4) {
+                            const float4 xn = xnext();
 #pragma unroll
-                        for (int i = 0; i < JH; ++i)
+                            for (int i = 0; i < JH; ++i)
 #pragma unroll
-                            for (int e = 0; e < E; ++e)
-                                cmac4(acc[i][e], aux[i][e], __ldcg(pool4 + (hoff[i][e] + mo)), win[i]);
+                                for (int e = 0; e < E; ++e)
+                                    cmac4(acc[i][e], aux[i][e], __ldcg(pool4 + (hoff[i][e] + mo)), win[i]);
 #pragma unroll
-                        for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
-                        win[0] = xn;
+                            for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
+                            win[0] = xn;
+                        }
                     }
                 } else {
-                const float4* hbi[JH][E];
-#pragma unroll
-                for (int i = 0; i < JH; ++i)
-#pragma unroll
-                    for (int e = 0; e < E; ++e) hbi[i][e] = pool4 + (((long)ent[i] * E + e) * M) * spec4 + (long)r * V + f;
-#pragma unroll 2
-                for (int m = m0; m < m1; ++m) {
-                    const float4 xn = xnext();
+                    const float4* hbi[JH][E];
 #pragma unroll
                     for (int i = 0; i < JH; ++i)
 #pragma unroll
-                        for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], __ldcg(hbi[i][e] + (long)m * spec4), win[i]);
+                        for (int e = 0; e < E; ++e) hbi[i][e] = pool4 + (((long)ent[i] * E + e) * M) * spec4 + (long)r * V + f;
+                    for (int mc = m0; mc < m1; mc += kPfRows) {
+#ifndef TVOLAP_NO_L2PF
+                        prefetch_chunk(mc + kPfDist);
+#endif
+                        const int me = min(mc + kPfRows, m1);
+#pragma unroll 2
+                        for (int m = mc; m < me; ++m) {
+                            const float4 xn = xnext();
 #pragma unroll
-                    for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
-                    win[0] = xn;
-                }
+                            for (int i = 0; i < JH; ++i)
+#pragma unroll
+                                for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], __ldcg(hbi[i][e] + (long)m * spec4), win[i]);
+#pragma unroll
+                            for (int i = JH - 1; i > 0; --i) win[i] = win[i - 1];
+                            win[0] = xn;
+                        }
+                    }
                 }
             }
 #pragma unroll
@@ -1580,11 +1634,7 @@ static cudaError_t launch_block_t(const HopParams& p, int Q, int threads, cudaSt
         attr[na].val.clusterDim.z = 1;
         ++na;
     }
-    static const bool pdl = [] {  // TVOLAP_PDL=0 disables (A/B: profiles/r01_ab_pdl.txt)
-        const char* v = std::getenv("TVOLAP_PDL");
-        return !(v && v[0] == '0');
-    }();
-    if (pdl) {  // overlap this launch's setup with the previous hop launch's tail
+    if (g_launch_pdl) {  // tuning "pdl" (A/B: profiles/r01_ab_pdl.txt)  // overlap this launch's setup with the previous hop launch's tail
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -1679,22 +1729,14 @@ static cudaError_t launch_partition_warp(int M, long rows, const float* ir, long
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    static const int k4_prefetch = [] {  // TVOLAP_K4_PREFETCH=0 disables the per-slice L2 prefetch (A/B)
-        const char* v = std::getenv("TVOLAP_K4_PREFETCH");
-        return v ? std::atoi(v) : 1;
-    }();
     return cudaLaunchKernelEx(&cfg, partition_warp_kernel<NC>, M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk,
-                              k4_prefetch);
+                              (int)g_launch_k4_prefetch);  // tuning "k4_prefetch": per-slice L2 prefetch
 }
 
 cudaError_t launch_partition(int L, int M, long rows, const float* ir, long ir_stride, long ir_len, float2* pool,
                              long row0, const float2* tw, const float2* pk, cudaStream_t stream, bool pdl) {
-    // one warp per partition for the common transform lengths (TVOLAP_K4_WARP=0: CTA batches)
-    static const bool warp_k4 = [] {
-        const char* v = std::getenv("TVOLAP_K4_WARP");
-        return !(v && v[0] == '0');
-    }();
-    if (warp_k4) {
+    // one warp per partition for the common transform lengths (tuning "k4_warp" = 0: CTA batches)
+    if (g_launch_k4_warp) {
         switch (2 * L) {
             case 64: return launch_partition_warp<64>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);
             case 128: return launch_partition_warp<128>(M, rows, ir, ir_stride, ir_len, pool, row0, tw, pk, stream, pdl);

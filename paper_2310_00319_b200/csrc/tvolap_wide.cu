@@ -574,17 +574,218 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     }
 }
 
+// ============================================================================ bank pass
+// K3 for bank engines with a per-hop schedule (C3, C5: every lane picks a bank entry every hop,
+// so no filter spectrum is reused across the hops of a tile; engine.cpp:85-92 with the set
+// exchanged before every hop, engine.hpp:55). One CTA per (tile, source x 32-float4 column
+// chunk, partition group q). q is the SLOWEST grid axis: all resident CTAs read the same 1/Q
+// slice of the bank, which stays L2-resident while the pass streams every (source, tile)
+// through it, so the bank comes from HBM about once per pass instead of once per wave of CTAs.
+// Thread = (column f, parity g, JO consecutive outputs of that parity) x E ears. Per partition
+// step: one Xe load (L1-cached: the tile's other output groups re-read it a few steps later)
+// and JO x E filter loads (L2 only), all issued KPF steps ahead into registers; the delay-line
+// window slides by register renaming (m unrolled by JO). The partials of group q go to yq[q];
+// bank_k5_kernel sums them in q order (deterministic).
+template <int NC, int E, int JH, int JO, int KPF>
+__global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_mac_kernel(const WideParams p) {
+    constexpr int N = NC, V4 = N / 2, CH = V4 / 32;
+    static_assert(V4 % 32 == 0 && JH % JO == 0 && JO % KPF == 0 && (JO & (JO - 1)) == 0, "bank MAC geometry");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = warp & 1, o = warp >> 1;
+    const int tile = blockIdx.x;
+    const int s = blockIdx.y / CH, f = (blockIdx.y % CH) * 32 + lane;
+    const int q = blockIdx.z;
+    const int M = p.M, S = p.S;
+    const int mq0 = (int)((long)q * M / p.Q), mq1 = (int)((long)(q + 1) * M / p.Q);
+    const int l0r = p.tile0[tile], jt = p.tile0[tile + 1] - l0r;
+    const long l0 = p.hop0 + l0r;
+    const float4* pool4 = reinterpret_cast<const float4*>(p.pool);
+    // filter rows of this thread's outputs (hop l0 + g + 2 (o JO + i)) at partition mq0
+    const float4* hb[JO][E];
+#pragma unroll
+    for (int i = 0; i < JO; ++i) {
+        const int jj = min(g + 2 * (o * JO + i), jt - 1);  // outputs past the tile: any valid entry, never stored
+        const long ent = p.sched[(long)(l0r + jj) * S + s];
+#pragma unroll
+        for (int e = 0; e < E; ++e) hb[i][e] = pool4 + ((ent * E + e) * M + mq0) * V4 + f;
+    }
+    // Xe slot t of output i at step m: tb + i - m
+    const float4* xs = reinterpret_cast<const float4*>(p.xe) + ((long)s * 2 + ((l0 + g) & 1)) * p.T * V4 + f;
+    const long tb = ((l0 + g) >> 1) - p.tbase + o * JO;
+    float4 acc[JO][E];
+    float aux[JO][E];
+    float4 win[JO];
+#pragma unroll
+    for (int i = 0; i < JO; ++i) {
+        win[i] = __ldg(xs + (tb + i - mq0) * V4);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            acc[i][e] = make_float4(0.f, 0.f, 0.f, 0.f);
+            aux[i][e] = 0.f;
+        }
+    }
+    // step m needs X[tb - m - 1] (the window's next entry) and H_i[m]; loads run KPF steps ahead.
+    // Prefetches past mq1 read the next entry's / the pool tail rows and the Xe front slots.
+    const float4* px = xs + (tb - mq0 - 1) * V4;
+    float4 fx[KPF], fh[KPF][JO][E];
+#pragma unroll
+    for (int k = 0; k < KPF; ++k) {
+        fx[k] = __ldg(px - (long)k * V4);
+#pragma unroll
+        for (int i = 0; i < JO; ++i)
+#pragma unroll
+            for (int e = 0; e < E; ++e) fh[k][i][e] = __ldcg(hb[i][e] + (long)k * V4);
+    }
+    auto step = [&](auto u_tag) {
+        constexpr int u = decltype(u_tag)::value, sl = u % KPF;
+        // FMAs on the operands loaded KPF steps ago, then the slot's registers take the loads of
+        // step m + KPF (one register set per slot: no extra live copies)
+#pragma unroll
+        for (int i = 0; i < JO; ++i)
+#pragma unroll
+            for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], fh[sl][i][e], win[(i - u) & (JO - 1)]);
+        win[(JO - 1 - u) & (JO - 1)] = fx[sl];  // replaces the entry output JO - 1 just used
+        fx[sl] = __ldg(px - (long)(u + KPF) * V4);
+#pragma unroll
+        for (int i = 0; i < JO; ++i)
+#pragma unroll
+            for (int e = 0; e < E; ++e) fh[sl][i][e] = __ldcg(hb[i][e] + (long)(u + KPF) * V4);
+    };
+    auto advance = [&](int k) {
+        px -= (long)k * V4;
+#pragma unroll
+        for (int i = 0; i < JO; ++i)
+#pragma unroll
+            for (int e = 0; e < E; ++e) hb[i][e] += (long)k * V4;
+    };
+    int m = mq0;
+    for (; m + JO <= mq1; m += JO) {
+        step(std::integral_constant<int, 0>{});
+        if constexpr (JO > 1) step(std::integral_constant<int, 1>{});
+        if constexpr (JO > 2) {
+            step(std::integral_constant<int, 2>{});
+            step(std::integral_constant<int, 3>{});
+        }
+        if constexpr (JO > 4) {
+            step(std::integral_constant<int, 4>{});
+            step(std::integral_constant<int, 5>{});
+            step(std::integral_constant<int, 6>{});
+            step(std::integral_constant<int, 7>{});
+        }
+        advance(JO);
+    }
+    const int rem = mq1 - m;  // < JO: the same unrolled steps, cut short
+    if constexpr (JO > 1) {
+        if (rem > 0) step(std::integral_constant<int, 0>{});
+        if constexpr (JO > 2) {
+            if (rem > 1) step(std::integral_constant<int, 1>{});
+            if (rem > 2) step(std::integral_constant<int, 2>{});
+        }
+        if constexpr (JO > 4) {
+            if (rem > 3) step(std::integral_constant<int, 3>{});
+            if (rem > 4) step(std::integral_constant<int, 4>{});
+            if (rem > 5) step(std::integral_constant<int, 5>{});
+            if (rem > 6) step(std::integral_constant<int, 6>{});
+        }
+    }
+    float4* yq4 = reinterpret_cast<float4*>(p.yq);
+#pragma unroll
+    for (int i = 0; i < JO; ++i) {
+        const int jj = g + 2 * (o * JO + i);
+        if (jj >= jt) continue;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            float4 a = acc[i][e];
+            if (f == 0) {  // packed bin 0: two real products (Re X_0 H_0, Re X_N H_N)
+                a.x += aux[i][e];
+                a.y = aux[i][e];
+            }
+            __stcg(yq4 + ((((long)q * S + s) * E + e) * p.n + l0r + jj) * V4 + f, a);
+        }
+    }
+}
+
+// K5 of the bank pass (spectral.cpp:127-158, engine.cpp:94-102): one CTA per (tile, output lane
+// s * E + e): Y of the tile's hops = the partition-group partials summed in q order, tangle +
+// inverse FFT (one warp per two frames, warp four-step, in place), then the overlap-add of the
+// tile's outputs from its 4th hop on; the first three need the previous tile's carry
+// (wide_fixup_kernel), exactly as in wide_mac_kernel.
+template <int NC, int JH>
+__global__ void __launch_bounds__(256) bank_k5_kernel(const WideParams p) {
+    constexpr int N = NC, L = NC / 2, J = 2 * JH, V4 = N / 2;
+    static_assert(N >= 64 && N <= 512, "bank K5 covers 64..512-point transforms");
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* s_pk = reinterpret_cast<float2*>(smem);
+    float2* s_y = reinterpret_cast<float2*>(smem + a16((N + 2) * sizeof(float2)));
+    const int tid = threadIdx.x, NT = 256, lane = tid & 31, warp = tid >> 5;
+    const int tile = blockIdx.x;
+    const long le = blockIdx.y;  // output lane s * E + e
+    const long lanes = (long)p.S * p.E;
+    const int l0r = p.tile0[tile], jt = p.tile0[tile + 1] - l0r;
+    for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    const float4* yq4 = reinterpret_cast<const float4*>(p.yq);
+    float4* y4 = reinterpret_cast<float4*>(s_y);
+    for (int i = tid; i < J * V4; i += NT) {
+        const int jj = i / V4, k4 = i - jj * V4;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (jj < jt) {
+            const float4* src = yq4 + (le * p.n + l0r + jj) * V4 + k4;
+            a = __ldcs(src);
+            for (int q = 1; q < p.Q; ++q) a = f4add(a, __ldcs(src + (long)q * lanes * p.n * V4));
+        }
+        y4[i] = a;
+    }
+    __syncthreads();
+    for (int jj = 2 * warp; jj < jt; jj += 2 * (NT >> 5)) {  // rows jj, jj + 1 (J even: both exist)
+        float2* rows = s_y + (size_t)jj * N;
+        auto ld = [&](int t, int n) { return tangle_packed(rows + (size_t)t * N, N, n, s_pk); };
+        fft_warp4<true, N, false, 2, decltype(ld), true>(rows, p.tw + N, lane, ld);
+    }
+    __syncthreads();
+    const float sc = 1.0f / (float)N;
+    float* head = p.thead + (le * p.ntiles + tile) * 6 * L;
+    float* outp = p.out + le * p.out_stride + (long)l0r * L;
+    const float* ytd = reinterpret_cast<const float*>(s_y);
+    for (int u = tid; u < L; u += NT) {
+        float st0 = 0.f, st1 = 0.f, st2 = 0.f;
+        for (int jj = 0; jj < jt; ++jj) {
+            const float* yf = ytd + (size_t)jj * 2 * N + u;
+            const float y0 = yf[0] * sc, y1 = yf[L] * sc, y2 = yf[2 * L] * sc, y3 = yf[3 * L] * sc;
+            const float o = 0.5f * (y0 + st0);
+            st0 = st1 + y1;
+            st1 = st2 + y2;
+            st2 = y3;
+            if (jj >= 3) {
+                outp[(long)jj * L + u] = o;
+            } else if (jj == 0) {
+                head[0 * L + u] = y0;
+                head[1 * L + u] = y1;
+                head[2 * L + u] = y2;
+            } else if (jj == 1) {
+                head[3 * L + u] = y0;
+                head[4 * L + u] = y1;
+            } else {
+                head[5 * L + u] = y0;
+            }
+        }
+        float* stt = p.tstate + (le * p.ntiles + tile) * 3 * L;
+        stt[u] = st0;
+        stt[L + u] = st1;
+        stt[2 * L + u] = st2;
+    }
+}
+
 // First three outputs of every tile: the overlap-add recurrence of engine.cpp:97-102 continued
 // from the carry after the previous tile (tile 0: the engine's carry from the previous call),
 // in the order the sequential kernels evaluate it. Tile 0's threads also hand the last tile's
 // carry and the last input hop (history) to the next call.
 __global__ void wide_fixup_kernel(const WideParams p) {
     const int L = p.L;
-    const long total = (long)p.S * p.ntiles * L;
+    const long total = (long)p.S * p.E * p.ntiles * L;  // output lanes s * E + e
     for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
         const int u = (int)(i % L);
         const int tile = (int)((i / L) % p.ntiles);
-        const long s = i / ((long)L * p.ntiles);
+        const long s = i / ((long)L * p.ntiles);  // output lane
         const float* A = tile == 0 ? p.ola + s * 3 * L : p.tstate + (s * p.ntiles + tile - 1) * 3 * L;
         const float A0 = A[u], A1 = A[L + u], A2 = A[2 * L + u];
         const float* h = p.thead + (s * p.ntiles + tile) * 6 * L;
@@ -604,7 +805,10 @@ __global__ void wide_fixup_kernel(const WideParams p) {
             C[u] = last[u];
             C[L + u] = last[L + u];
             C[2 * L + u] = last[2 * L + u];
-            p.hist[s * L + u] = p.in[s * p.in_stride + (long)(p.n - 1) * L + u];
+            if (s % p.E == 0) {  // the source's last input hop (history), once per source
+                const long src = s / p.E;
+                p.hist[src * L + u] = p.in[src * p.in_stride + (long)(p.n - 1) * L + u];
+            }
         }
     }
 }
@@ -667,10 +871,40 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
         kern<<<dim3((unsigned)p.ntiles, (unsigned)p.S), 256, smem, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
         if (t1) cudaEventRecord(t1, stream);
-        wide_fixup_kernel<<<grid_cap((long)p.S * p.ntiles * p.L, 256), 256, 0, stream>>>(p);
+        wide_fixup_kernel<<<grid_cap((long)p.S * p.E * p.ntiles * p.L, 256), 256, 0, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
     return cudaSuccess;
+}
+
+template <int NC, int E, int JH, int JO>
+cudaError_t launch_bank_mac(const WideParams& p, cudaStream_t stream) {
+    constexpr int KPF = 2;
+    auto kern = bank_mac_kernel<NC, E, JH, JO, KPF>;
+    const dim3 grid((unsigned)p.ntiles, (unsigned)(p.S * (NC / 64)), (unsigned)p.Q);
+    kern<<<grid, 64 * (JH / JO), 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+template <int NC>
+cudaError_t launch_bank_pass_t(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1) {
+    cudaError_t err = launch_wide_t<NC>(p, 8, stream, nullptr, nullptr, 1);  // head copy + K1 into Xe
+    if (err != cudaSuccess) return err;
+    if (t0) cudaEventRecord(t0, stream);
+    if (p.E == 1 && JH == 16) err = launch_bank_mac<NC, 1, 16, 4>(p, stream);
+    else if (p.E == 1 && JH == 8) err = launch_bank_mac<NC, 1, 8, 4>(p, stream);
+    else if (p.E == 2 && JH == 8) err = launch_bank_mac<NC, 2, 8, 2>(p, stream);
+    else return cudaErrorInvalidValue;
+    if (err != cudaSuccess) return err;
+    if (t1) cudaEventRecord(t1, stream);
+    const size_t smem = a16((NC + 2) * sizeof(float2)) + (size_t)2 * JH * NC * sizeof(float2);
+    auto k5 = JH == 16 ? bank_k5_kernel<NC, 16> : bank_k5_kernel<NC, 8>;
+    if ((err = cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return err;
+    k5<<<dim3((unsigned)p.ntiles, (unsigned)(p.S * p.E)), 256, smem, stream>>>(p);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    wide_fixup_kernel<<<grid_cap((long)p.S * p.E * p.ntiles * p.L, 256), 256, 0, stream>>>(p);
+    return cudaGetLastError();
 }
 
 template <int NC>
@@ -722,6 +956,23 @@ cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEv
         case 256: return launch_wide_t<256>(p, JH, stream, t0, t1, parts);
         case 512: return launch_wide_t<512>(p, JH, stream, t0, t1, parts);
         case 1024: return launch_wide_t<1024>(p, JH, stream, t0, t1, parts);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool bank_pass_supported(int L, int E, int JH) {
+    const int N = 2 * L;
+    if (!(N == 64 || N == 128 || N == 256 || N == 512)) return false;
+    return (E == 1 && (JH == 16 || JH == 8)) || (E == 2 && JH == 8);
+}
+
+cudaError_t launch_bank_pass(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1) {
+    if (!bank_pass_supported(p.L, p.E, JH) || !p.warp_fft) return cudaErrorInvalidValue;
+    switch (2 * p.L) {
+        case 64: return launch_bank_pass_t<64>(p, JH, stream, t0, t1);
+        case 128: return launch_bank_pass_t<128>(p, JH, stream, t0, t1);
+        case 256: return launch_bank_pass_t<256>(p, JH, stream, t0, t1);
+        case 512: return launch_bank_pass_t<512>(p, JH, stream, t0, t1);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -19,6 +19,7 @@ device, the call is then asynchronous on the engine stream).
 from __future__ import annotations
 
 import ctypes as C
+from contextlib import contextmanager
 import os
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -112,6 +113,18 @@ def lib() -> C.CDLL:
             "tvolap_kernel_launches": (C.c_uint64, [vp]),
             "tvolap_wide_passes": (C.c_uint64, [vp]),
             "tvolap_set_block_config": (ip, [vp, ip, lg]),
+            "tvolap_set_tuning": (ip, [vp, C.c_char_p, lg]),
+            "tvolap_set_create": (ip, [C.POINTER(vp), ip, lg, lg, lg, fp, lg]),
+            "tvolap_set_release": (ip, [vp]),
+            "tvolap_set_geometry": (ip, [vp, fp, fp, fp, fp]),
+            "tvolap_set_spectra": (ip, [vp, fp]),
+            "tvolap_set_reassemble": (ip, [vp, fp]),
+            "tvolap_create_from_set": (ip, [C.POINTER(vp), vp]),
+            "tvolap_exchange_set": (ip, [vp, vp]),
+            "tvolap_get_tuning": (ip, [vp, C.c_char_p, C.POINTER(lg)]),
+            "tvolap_set_default_tuning": (ip, [C.c_char_p, lg]),
+            "tvolap_reset_default_tuning": (ip, []),
+            "tvolap_tuning_keys": (C.c_char_p, []),
             "tvolap_block_config": (ip, [vp, fp, fp, fp]),
             "tvolap_forward_real": (ip, [ip, lg, lg, fp, fp]),
             "tvolap_inverse_real": (ip, [ip, lg, lg, fp, fp]),
@@ -121,6 +134,10 @@ def lib() -> C.CDLL:
             "tvolap_gen_white_device": (ip, [ip, C.c_uint64, lg, lg, lg, lg, fp, lg]),
             "tvolap_gen_irs_device": (ip, [ip, C.c_uint64, lg, fp, fp, fp, fp, C.c_double, lg, fp]),
             "tvolap_mix_device": (ip, [ip, lg, lg, lg, fp, lg, fp, lg, vp]),
+            "tvolap_mix_allreduce": (ip, [ip, lg, lg, lg, fp, lg, fp, lg, vp, vp]),
+            "tvolap_nccl_unique_id": (ip, [vp]),
+            "tvolap_nccl_comm_init": (ip, [C.POINTER(vp), ip, ip, ip, vp]),
+            "tvolap_nccl_comm_destroy": (ip, [vp]),
             "tvolap_cmp_create": (ip, [C.POINTER(vp), ip, ip, lg, lg, fp, lg, lg, lg, ip]),
             "tvolap_cmp_destroy": (ip, [vp]),
             "tvolap_cmp_process_hops": (ip, [vp, fp, lg, fp, lg, lg]),
@@ -145,8 +162,12 @@ EXPORTED_SYMBOLS = (
     "tvolap_output_channels tvolap_partition_count tvolap_delay_line_depth tvolap_latency "
     "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
     "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_wide_passes tvolap_set_block_config tvolap_block_config "
+    "tvolap_set_create tvolap_set_release tvolap_set_geometry tvolap_set_spectra tvolap_set_reassemble "
+    "tvolap_create_from_set tvolap_exchange_set "
+    "tvolap_set_tuning tvolap_get_tuning tvolap_set_default_tuning tvolap_reset_default_tuning tvolap_tuning_keys "
     "tvolap_forward_real tvolap_inverse_real tvolap_mac tvolap_hann_window tvolap_partition "
-    "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device "
+    "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device tvolap_mix_allreduce tvolap_nccl_unique_id "
+    "tvolap_nccl_comm_init tvolap_nccl_comm_destroy "
     "tvolap_cmp_create tvolap_cmp_destroy tvolap_cmp_process_hops tvolap_cmp_set_filter tvolap_cmp_switch_filter "
     "tvolap_cmp_reset tvolap_cmp_geometry"
 ).split()
@@ -226,7 +247,9 @@ def mac(acc, a, b, device: int = 0) -> np.ndarray:
 # ---------------------------------------------------------------- partition (partition.hpp)
 @dataclass
 class FilterPartitionSet:
-    """partition.hpp:21-32. Holds the time-domain taps; the spectra live on the device."""
+    """partition.hpp:21-32: immutable, shared. Keeps the fp32 taps it was built from; the partition
+    spectra live on the device (tvolap_set_create, one K4 per device on first use) and engines
+    take / exchange to them in O(1) (tvolap_create_from_set / tvolap_exchange_set)."""
 
     hop: int
     partition_count: int
@@ -235,6 +258,7 @@ class FilterPartitionSet:
     taps: np.ndarray = field(repr=False)  # (channels, source_length) fp32
     normalization_gain: float = 0.5
     sample_rate: float = 48000.0
+    _dev: dict = field(default_factory=dict, repr=False, compare=False)  # device -> tvolap_set*
 
     def transform_length(self) -> int:
         return 4 * self.hop
@@ -242,13 +266,27 @@ class FilterPartitionSet:
     def padded_length(self) -> int:
         return 2 * self.hop * self.partition_count
 
+    def device_set(self, device: int = 0):
+        """The set's device-resident spectra on `device` (created once, then shared)."""
+        h = self._dev.get(device)
+        if h is None:
+            h = C.c_void_p()
+            _check(lib().tvolap_set_create(C.byref(h), device, self.hop, self.channels, self.source_length,
+                                           self.taps.ctypes.data, self.partition_count))
+            self._dev[device] = h
+        return h
+
+    def __del__(self):
+        for h in getattr(self, "_dev", {}).values():
+            if h and _lib is not None:
+                _lib.tvolap_set_release(h)
+        self._dev = {}
+
     def spectra(self, device: int = 0) -> np.ndarray:
-        """(channels, M, 2L+1) complex partition spectra computed on the device."""
+        """(channels, M, 2L+1) complex partition spectra (the device set's)."""
         nb = 2 * self.hop + 1
         out = np.empty((self.channels, self.partition_count, nb, 2), dtype=np.float32)
-        m = C.c_long()
-        _check(lib().tvolap_partition(device, self.hop, self.channels, self.source_length, self.taps.ctypes.data,
-                                      self.partition_count, out.ctypes.data, C.byref(m)))
+        _check(lib().tvolap_set_spectra(self.device_set(device), out.ctypes.data))
         return out[..., 0] + 1j * out[..., 1]
 
 
@@ -267,6 +305,14 @@ def partition(ir, hop: int, min_partitions: int = 1, sample_rate: float = 48000.
     return FilterPartitionSet(hop, m, h.shape[1], h.shape[0], taps, sample_rate=sample_rate)
 
 
+def reassemble(s: FilterPartitionSet, device: int = 0) -> np.ndarray:
+    """reassemble(set) (partition.hpp:43, partition.cpp:53-65) from the device spectra:
+    (M * 2L, channels), the response zero-padded to M * 2L taps."""
+    out = np.empty((s.channels, 2 * s.hop * s.partition_count), dtype=np.float32)
+    _check(lib().tvolap_set_reassemble(s.device_set(device), out.ctypes.data))
+    return np.ascontiguousarray(out.T)
+
+
 # ---------------------------------------------------------------- engine (engine.hpp)
 class TvolapEngine:
     """B200 TvolapEngine (engine.hpp:33-94) behind tvolap_create / tvolap_process."""
@@ -275,8 +321,7 @@ class TvolapEngine:
         if filter is None:
             raise InvalidConfigurationError("engine requires a filter partition set")
         h = C.c_void_p()
-        _check(lib().tvolap_create(C.byref(h), device, filter.hop, filter.channels, filter.source_length,
-                                   filter.taps.ctypes.data, filter.partition_count))
+        _check(lib().tvolap_create_from_set(C.byref(h), filter.device_set(device)))  # engine.hpp:35
         self._h = h
         self._filter = filter
         self.device = device
@@ -313,7 +358,8 @@ class TvolapEngine:
         return self._filter
 
     def exchange_filter(self, next: Optional[FilterPartitionSet]) -> None:
-        """engine.cpp:37-48: validate, stage; latched at the next process()."""
+        """engine.hpp:55, engine.cpp:37-48: validate, stage (O(1): the set's device spectra are read in
+        place, no transform); latched at the next process(), last staged wins."""
         if next is None:
             raise IncompatibleFilterError("replacement filter is null")
         if next.hop != self.hop():
@@ -322,7 +368,7 @@ class TvolapEngine:
             raise IncompatibleFilterError("replacement filter partition count differs")
         if next.channels != self.channels():
             raise IncompatibleFilterError("replacement filter channel count differs")
-        _check(lib().tvolap_exchange_filter(self._h, next.taps.ctypes.data, next.source_length, next.channels))
+        _check(lib().tvolap_exchange_set(self._h, next.device_set(self.device)))
         self._filter = next
 
     def exchange_ir(self, ir) -> None:
@@ -367,10 +413,17 @@ class TvolapEngine:
                 out = np.empty((self.channels_out(), total), dtype=np.float32)
         if not hasattr(x, "data_ptr"):
             x = _f32(x)
+        _check_buffer(x, self.channels(), total, "process_hops input")
+        _check_buffer(out, self.channels_out(), total, "process_hops output")
+        if schedule is not None:
+            if not hasattr(schedule, "data_ptr"):
+                schedule = np.ascontiguousarray(schedule, np.int32)
+            _check_buffer(schedule, n, self.channels(), "process_hops schedule", "int32")
+            if n > 1 and _stride(schedule) != self.channels():
+                raise InvalidInputError("process_hops schedule: rows must be dense (n_hops, sources)")
         xp, _k1 = _ptr(x)
         op, _k2 = _ptr(out)
-        sp, _k3 = _ptr(None if schedule is None else
-                       (schedule if hasattr(schedule, "data_ptr") else np.ascontiguousarray(schedule, np.int32)))
+        sp, _k3 = _ptr(schedule)
         _check(lib().tvolap_process_hops(self._h, xp, _stride(x), op, _stride(out), n, sp))
         return out
 
@@ -396,6 +449,8 @@ class TvolapEngine:
                 out = np.empty((self.channels_out(), total), dtype=np.float32)
         if not hasattr(x, "data_ptr"):
             x = _f32(x)
+        _check_buffer(x, self.channels(), total, "process_switching input")
+        _check_buffer(out, self.channels_out(), total, "process_switching output")
         keep, ptrs, taps = [], (C.c_void_p * nsw)(), 0
         for k in range(nsw):
             ir = irs[k]
@@ -469,9 +524,42 @@ class TvolapEngine:
     def kernel_launches(self) -> int:
         return lib().tvolap_kernel_launches(self._h)
 
+    def set_tuning(self, key: str, value: int) -> None:
+        """A/B knob of this engine (tvolap_set_tuning; keys: tuning_keys())."""
+        _check(lib().tvolap_set_tuning(self._h, key.encode(), int(value)))
+
+    def get_tuning(self, key: str) -> int:
+        v = C.c_long()
+        _check(lib().tvolap_get_tuning(self._h, key.encode(), C.byref(v)))
+        return v.value
+
     def wide_passes(self) -> int:
         """Time-parallel passes run (device-resident switching calls, csrc/tvolap_wide.cu)."""
         return lib().tvolap_wide_passes(self._h)
+
+
+def tuning_keys():
+    return lib().tvolap_tuning_keys().decode().split(",")
+
+
+def set_default_tuning(key: str, value: int) -> None:
+    """Value engines created afterwards start with (process-wide launch knobs take effect at once)."""
+    _check(lib().tvolap_set_default_tuning(key.encode(), int(value)))
+
+
+def reset_default_tuning() -> None:
+    _check(lib().tvolap_reset_default_tuning())
+
+
+@contextmanager
+def default_tuning(**knobs):
+    """with default_tuning(wide=0): ... — engines created inside start with these knobs."""
+    for k, v in knobs.items():
+        set_default_tuning(k, v)
+    try:
+        yield
+    finally:
+        reset_default_tuning()
 
 
 @dataclass
@@ -479,6 +567,26 @@ class OpCounts:
     forward_transforms: int
     inverse_transforms: int
     spectral_macs: int
+
+
+def _check_buffer(a, rows: int, total: int, what: str, dtype_name: str = "float32"):
+    """Shape / dtype / layout of a caller buffer before its pointer crosses the C-ABI: a short or
+    mistyped buffer would be read or written out of bounds there (engine.cpp:66-67 raises
+    InvalidInputError on a channel mismatch)."""
+    if a.ndim != 2 or a.shape[0] != rows or a.shape[-1] != total:
+        raise InvalidInputError(f"{what}: expected shape ({rows}, {total}), got {tuple(a.shape)}")
+    if hasattr(a, "data_ptr"):
+        if str(a.dtype) != "torch." + dtype_name:
+            raise InvalidInputError(f"{what}: expected torch.{dtype_name}, got {a.dtype}")
+        if a.shape[-1] > 1 and a.stride(-1) != 1:
+            raise InvalidInputError(f"{what}: the sample axis must be contiguous (unit stride)")
+    else:
+        if a.dtype != np.dtype(dtype_name):
+            raise InvalidInputError(f"{what}: expected {dtype_name}, got {a.dtype}")
+        if a.shape[-1] > 1 and a.strides[-1] != a.itemsize:
+            raise InvalidInputError(f"{what}: the sample axis must be contiguous (unit stride)")
+    if a.shape[0] > 1 and _stride(a) < total:
+        raise InvalidInputError(f"{what}: lane stride shorter than the row")
 
 
 def _stride(a) -> int:
@@ -548,9 +656,13 @@ class TvolapProcessor:
         return self._engine.process(input)
 
     def set_filter(self, ir) -> None:
-        """exchange_filter(partition(ir, L, M)) (reference.cpp:335-338)."""
+        """exchange_filter(partition(ir, L, M)) (reference.cpp:335-338). The reference partitions on
+        the caller's thread (a load spike); here the taps are staged and transformed (K4) on the
+        device on a side stream overlapping the running hops, latched at the next process()."""
         e = self._engine
-        self._engine.exchange_filter(partition(ir, e.hop(), e.partition_count()))
+        s = partition(ir, e.hop(), e.partition_count())  # validation and M, as the reference
+        e.exchange_ir(s.taps)
+        e._filter = s
 
     def reset(self) -> None:
         self._engine.reset()

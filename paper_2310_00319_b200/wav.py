@@ -23,8 +23,11 @@ class WavError(RuntimeError):
 
 def read_wav(path: str):
     """-> (samples (frames, channels) float64, sample_rate)."""
-    with open(path, "rb") as f:
-        data = f.read()
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise WavError(f"cannot open '{path}'", 0) from None  # wav.cpp:69-71
     pos = 0
 
     def need(n, what):
@@ -56,13 +59,16 @@ def read_wav(path: str):
             if fmt is None:
                 raise WavError("data chunk before fmt chunk", pos)
             code, ch, rate, align, bits = fmt
+            if body + size > len(data):  # wav.cpp:118-119: a data chunk shorter than declared
+                raise WavError("truncated data chunk", pos)
             if not 1 <= ch <= 16:
                 raise WavError("channel count must be 1-16", pos)
+            if rate == 0:
+                raise WavError("malformed header, zero sample rate", body)
             if (code, bits) not in ((PCM, 16), (PCM, 24), (IEEE_FLOAT, 32)):
                 raise WavError(f"unsupported sample format {code}/{bits}-bit", pos)
             if align != ch * bits // 8:
                 raise WavError("block align does not match the format", pos)
-            size = min(size, len(data) - body)
             frames = size // align
             raw = data[body: body + frames * align]
             if bits == 16:
@@ -107,5 +113,8 @@ def write_wav(path: str, samples, sample_rate: float = 48000.0, fmt: str = "floa
     if fact:
         head += struct.pack("<H", 0) + b"fact" + struct.pack("<II", 4, x.shape[0])
     head += b"data" + struct.pack("<I", len(payload))
-    with open(path, "wb") as f:
-        f.write(head + payload)
+    try:
+        with open(path, "wb") as f:
+            f.write(head + payload)
+    except OSError:
+        raise WavError(f"cannot open '{path}' for writing", 0) from None

@@ -3,10 +3,10 @@ sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 from paper_2310_00319_b200 import tvolap as T
 for mode in ["0", "1"]:
-    os.environ["TVOLAP_WIDE"] = mode
     g = np.random.default_rng(0)
     S, hop, taps, n = 2, 256, 32768, 5625
     eng = T.TvolapEngine(T.partition(g.standard_normal((taps, S)) * 0.01, hop))
+    eng.set_tuning("wide", int(mode))
     x = torch.from_numpy(g.uniform(-1, 1, (S, n * hop)).astype(np.float32)).cuda()
     out = torch.empty_like(x)
     torch.cuda.synchronize()

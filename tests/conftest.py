@@ -30,3 +30,13 @@ def gpu_available() -> bool:
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(autouse=True)
+def _default_tuning_reset():
+    """Tests that set process-wide default tuning (tvolap_set_default_tuning) leave none behind."""
+    yield
+    import paper_2310_00319_b200.tvolap as T
+
+    if T._lib is not None:
+        T.reset_default_tuning()

@@ -1,7 +1,8 @@
 // Drop-in check of include/tvolap_b200.hpp: the reference's own engine tests
 // (proj/tests/test_engine.cpp:71-77 identity, :159-188 half-cosine crossfade,
-// :203-216 error classes) written against the C++ wrapper exactly as the
-// reference writes them against tvolap::TvolapEngine. Exit 0 = pass,
+// :203-216 error classes, partition/reassemble of test_partition.cpp) written
+// against the C++ wrapper exactly as the reference writes them against
+// tvolap::TvolapEngine; run by tests/test_gpu_engine.py::test_cpp_wrapper. Exit 0 = pass,
 // 77 = no GPU (the wrapper threw CudaError: there is no CPU fallback).
 #include <cmath>
 #include <cstdio>
@@ -75,9 +76,47 @@ int main() {
         try { TvolapEngine bad(std::shared_ptr<const FilterPartitionSet>{}); } catch (const InvalidConfigurationError&) { threw = true; }
         CHECK(threw);
 
+        // pre-partitioned sets (partition.hpp:21-43): exchange is O(1) — no transform is launched, one
+        // set is shared by two engines, reassemble() returns the response zero-padded to M * 2L
+        {
+            const Index L = 64;
+            ImpulseResponse r;
+            r.samples = Frames(700, 2);
+            for (Index n = 0; n < 700; ++n) {
+                r.samples(n, 0) = std::sin(0.1 * n) * std::exp(-n / 200.0);
+                r.samples(n, 1) = std::cos(0.07 * n) * std::exp(-n / 150.0);
+            }
+            auto a = std::make_shared<const FilterPartitionSet>(partition(r, L));
+            auto b = std::make_shared<const FilterPartitionSet>(partition(delta_ir(1.0, 700), L));  // 1 channel
+            auto d = std::make_shared<const FilterPartitionSet>(partition(r, L, 1));
+            TvolapEngine e1(a), e2(a);  // shared
+            Frames xin(L, 2, 0.5);
+            e1.process(xin);
+            const uint64_t before = tvolap_kernel_launches(e1.handle());
+            e1.exchange_filter(d);
+            e1.process(xin);
+            CHECK(tvolap_kernel_launches(e1.handle()) - before == 1);  // the hop kernel only, no K4
+            bool t2 = false;
+            try { e1.exchange_filter(b); } catch (const IncompatibleFilterError&) { t2 = true; }
+            CHECK(t2);
+            Frames y2 = e2.process(xin);
+            CHECK(y2.rows() == L && y2.cols() == 2);
+            ImpulseResponse back = reassemble(*a);
+            CHECK(back.length() == 2 * L * a->partition_count && back.channels() == 2);
+            double re = 0.0;
+            for (Index c = 0; c < 2; ++c)
+                for (Index n = 0; n < back.length(); ++n)
+                    re = std::fmax(re, std::fabs(back.samples(n, c) - (n < 700 ? r.samples(n, c) : 0.0)));
+            CHECK(re < 1e-5);
+        }
+
         TvolapProcessor proc(delta_ir(0.5, 300), 64);
         Frames y = proc.process(Frames(64, 1, 1.0));
         CHECK(proc.name() == "tvolap" && y.rows() == 64);
+        proc.set_filter(delta_ir(2.0, 300));  // reference.cpp:335-338: staged, latched next hop
+        proc.process(Frames(64, 1, 1.0));
+        Frames y3 = proc.process(Frames(64, 1, 1.0));
+        CHECK(std::fabs(y3(63, 0) - 2.0) < 1e-5);
 
         // comparison convolvers through the StreamingProcessor face (reference.hpp:26-226)
         for (const char* name : {"tdc", "cf-tdc", "ola", "ols", "wola", "tvolap"}) {

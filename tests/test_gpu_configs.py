@@ -208,3 +208,38 @@ def test_c1_device_path_matches_oracle():
     assert eng.wide_passes() >= 1
     ref = oracle_config(cfg, n)
     assert rel_err(y.cpu().numpy(), ref) <= TOL
+
+
+def test_c3_mix_allreduce_single_rank_nccl():
+    """tvolap_mix_allreduce through a real (1-rank) NCCL communicator made by the C-ABI helpers:
+    the all-reduce of one partial mix is that mix; NULL comm = the single-GPU mix."""
+    import ctypes
+
+    import torch
+
+    from paper_2310_00319_b200 import tvolap as T
+
+    cfg = W.CONFIGS["C3"]
+    n_hops, S = 24, 64
+    L = cfg.hop
+    eng = drive.make_engine(cfg, sources=S)
+    x = torch.from_numpy(W.white(cfg, 0, S, 0, n_hops * L)).cuda()
+    out = torch.empty((S * cfg.ears, n_hops * L), device="cuda")
+    eng.process_hops(x, out=out, schedule=torch.from_numpy(W.schedule(cfg, 0, n_hops, 0, S)).cuda())
+    eng.synchronize()
+    lib = T.lib()
+    ref = torch.empty((cfg.ears, n_hops * L), device="cuda")
+    T._check(lib.tvolap_mix_allreduce(0, S, cfg.ears, n_hops * L, ctypes.c_void_p(out.data_ptr()), n_hops * L,
+                                      ctypes.c_void_p(ref.data_ptr()), n_hops * L, None, None))
+    uid = (ctypes.c_char * 128)()
+    T._check(lib.tvolap_nccl_unique_id(uid))
+    comm = ctypes.c_void_p()
+    T._check(lib.tvolap_nccl_comm_init(ctypes.byref(comm), 0, 1, 0, uid))
+    got = torch.empty_like(ref)
+    T._check(lib.tvolap_mix_allreduce(0, S, cfg.ears, n_hops * L, ctypes.c_void_p(out.data_ptr()), n_hops * L,
+                                      ctypes.c_void_p(got.data_ptr()), n_hops * L, comm, None))
+    torch.cuda.synchronize()
+    T._check(lib.tvolap_nccl_comm_destroy(comm))
+    assert torch.equal(got, ref)
+    sums = out.double().view(S, cfg.ears, -1).sum(0)
+    assert (ref.double() - sums).abs().max().item() <= 1e-5 * sums.abs().max().item()

@@ -357,6 +357,8 @@ def test_block_kernel_bank_schedule(ears, jb):
     x = np.ascontiguousarray(rnd(hop * n, 6, S).T)
     a = T.TvolapBankEngine(bank, hop, S)
     b = T.TvolapBankEngine(bank, hop, S)
+    a.set_tuning("bank_pass", 0)  # the hop-blocked kernel itself (the bank pass: test_gpu_bank_pass.py)
+    b.set_tuning("bank_pass", 0)
     a.set_block_config(jb, 2)
     b.set_block_config(jb, 1 << 30)  # never block, same partition grouping
     ya = a.process_hops(x, schedule=sched)
@@ -434,3 +436,45 @@ def test_bank_engine_single_hop_select(S):
     assert np.array_equal(ya, yb)
     with pytest.raises(T.InvalidInputError):
         a.select_bank(np.full(S, n_bank, np.int32))
+
+
+def test_cpp_wrapper():
+    """The C++ drop-in (include/tvolap_b200.hpp) runs the reference's engine tests on the GPU:
+    tests/cpp/test_wrapper.cpp, built by _build.build() into lib/test_wrapper; exit 0 = PASS."""
+    import subprocess
+    from pathlib import Path
+
+    exe = Path(T.__file__).resolve().parent / "lib" / "test_wrapper"
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout
+
+
+def test_prebuilt_set_exchange_is_o1_and_shared():
+    """exchange_filter(shared_ptr<const FilterPartitionSet>) (engine.hpp:55) launches no K4: the
+    engine reads the set's device spectra in place; sets are shared between engines; reassemble
+    (partition.cpp:53-65) gives the response back, zero-padded to M*2L taps."""
+    hop = 64
+    g = np.random.default_rng(12)
+    sets = [T.partition(g.standard_normal((1500, 3)) * 0.1, hop) for _ in range(3)]
+    a, b = T.TvolapEngine(sets[0]), T.TvolapEngine(sets[0])
+    x = g.uniform(-1, 1, (hop * 20, 3))
+    a.process(x[:hop])
+    b.process(x[:hop])
+    n0 = a.kernel_launches()
+    a.exchange_filter(sets[1])
+    a.exchange_filter(sets[2])  # last staged wins
+    ya = a.process(x[hop:2 * hop])
+    assert a.kernel_launches() - n0 == 1
+    b.exchange_filter(sets[2])
+    yb = b.process(x[hop:2 * hop])
+    assert np.array_equal(ya, yb)
+    back = T.reassemble(sets[1])
+    assert back.shape == (2 * hop * sets[1].partition_count, 3)
+    assert np.abs(back[:1500] - sets[1].taps.T).max() <= 1e-5 * np.abs(sets[1].taps).max()
+    assert np.abs(back[1500:]).max() <= 1e-6
+    # a set transformed from taps (exchange_ir, side-stream K4) gives the same outputs as the set
+    c = T.TvolapEngine(sets[0])
+    c.process(x[:hop])
+    c.exchange_ir(sets[2].taps)
+    assert np.array_equal(c.process(x[hop:2 * hop]), ya)

@@ -1,8 +1,7 @@
 """K4 variants: the warp-per-partition kernel (default, register four-step FFT) and the partition
-transform fused into the hop kernels (TVOLAP_K4_SIDE=0) run the same warp FFT, so spectra and
-engine outputs are bit-identical; the CTA-batched Stockham kernel (TVOLAP_K4_WARP=0) is a
+transform fused into the hop kernels (tuning k4_side=0) run the same warp FFT, so spectra and
+engine outputs are bit-identical; the CTA-batched Stockham kernel (tuning k4_warp=0) is a
 different factorisation and agrees to fp32 rounding."""
-import os
 import subprocess
 import sys
 from pathlib import Path
@@ -17,12 +16,15 @@ SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
 from paper_2310_00319_b200 import tvolap as T
+for kv in sys.argv[3:]:
+    k, v = kv.split("=")
+    T.set_default_tuning(k, int(v))
 out = {}
 g = np.random.default_rng(5)
 for hop, n_ir, ch in [(32, 2000, 2), (64, 900, 1), (128, 3000, 3), (256, 33000, 2), (512, 9000, 1), (1024, 5000, 1)]:
     ir = g.uniform(-1, 1, (n_ir, ch))
     out[f"p{hop}"] = T.partition(ir, hop).spectra()
-# engine with an exchange every 16 hops (side or fused K4 per the environment)
+# engine with an exchange every 16 hops (side or fused K4 per the tuning)
 hop, S = 256, 4
 sets = [T.partition(g.uniform(-1, 1, (5000, S)), hop, 20) for _ in range(3)]
 x = np.ascontiguousarray(g.uniform(-1, 1, (S, hop * 48)).astype(np.float32))
@@ -30,34 +32,34 @@ e = T.TvolapEngine(sets[0])
 ys = []
 for k in range(3):
     if k:
-        e.exchange_filter(sets[k])
+        e.exchange_ir(sets[k].taps)  # taps: the K4 path under test (a pre-built set would skip it)
     ys.append(e.process_hops(np.ascontiguousarray(x[:, k * 16 * hop:(k + 1) * 16 * hop])))
 out["engine"] = np.concatenate(ys, 1)
-# one-hop kernel path with exchanges (fused K4 in the hop kernel when TVOLAP_K4_SIDE=0)
+# one-hop kernel path with exchanges (fused K4 in the hop kernel when k4_side=0)
 e1 = T.TvolapEngine(sets[0])
 y1 = []
 for h in range(6):
     if h in (2, 4):
-        e1.exchange_filter(sets[h // 2])
+        e1.exchange_ir(sets[h // 2].taps)
     y1.append(e1.process(np.ascontiguousarray(x[:, h * hop:(h + 1) * hop].T)))
 out["hop"] = np.concatenate(y1)
 np.savez(sys.argv[2], **out)
 """
 
 
-def _run(tmp_path, name, env_extra):
-    env = dict(os.environ, **env_extra)
+def _run(tmp_path, name, knobs):
     path = tmp_path / f"{name}.npz"
-    subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), str(path)], check=True, env=env, timeout=600)
+    subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), str(path)] + [f"{k}={v}" for k, v in knobs.items()],
+                   check=True, timeout=600)
     return np.load(path)
 
 
 def test_k4_variants(tmp_path):
-    base = _run(tmp_path, "warp", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "1"})
-    fused = _run(tmp_path, "fused", {"TVOLAP_K4_WARP": "1", "TVOLAP_K4_SIDE": "0"})
+    base = _run(tmp_path, "warp", {"k4_warp": 1, "k4_side": 1})
+    fused = _run(tmp_path, "fused", {"k4_warp": 1, "k4_side": 0})
     for k in base.files:
         assert np.array_equal(base[k], fused[k]), k
-    cta = _run(tmp_path, "cta", {"TVOLAP_K4_WARP": "0", "TVOLAP_K4_SIDE": "1"})
+    cta = _run(tmp_path, "cta", {"k4_warp": 0, "k4_side": 1})
     for k in base.files:
         scale = max(np.abs(cta[k]).max(), 1e-30)
         assert np.abs(base[k] - cta[k]).max() <= 2e-6 * scale, k

@@ -42,7 +42,7 @@ def _loop(eng, x, dirs, period, hop):
     (512, 2, 8192, 48, 8, (0,)),            # N = 1024, no switch at the first hop
 ])
 def test_switching_equals_exchange_loop(monkeypatch, hop, S, taps, n_hops, period, none_at):
-    monkeypatch.setenv("TVOLAP_WIDE", "0")  # the hop-blocked switching launch (the pass: test_gpu_wide.py)
+    T.set_default_tuning("wide", 0)  # the hop-blocked switching launch (the pass: test_gpu_wide.py)
     ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at)
     a = T.TvolapEngine(T.partition(ir0, hop))
     b = T.TvolapEngine(T.partition(ir0, hop))
@@ -109,7 +109,7 @@ def test_switching_pinned_host_pipeline(monkeypatch, n_hops, period, hop):
     device staging for 2048-point transforms), bit-identical to the device call."""
     import torch
 
-    monkeypatch.setenv("TVOLAP_WIDE", "0")  # device reference = the switching launch the pipeline runs
+    T.set_default_tuning("wide", 0)  # device reference = the switching launch the pipeline runs
     S, taps = 4, 4096
     ir0, x, dirs = _case(hop, S, taps, n_hops, period, none_at=(1,))
     xh = x.cpu().pin_memory()

@@ -38,13 +38,11 @@ def _loop(eng, x, dirs, period, hop):
 
 
 def _engines(monkeypatch, ir0, hop, warp_fft=False):
-    monkeypatch.setenv("TVOLAP_WIDE", "2")
-    monkeypatch.setenv("TVOLAP_WIDE_WARPFFT", "1" if warp_fft else "0")
     a = T.TvolapEngine(T.partition(ir0, hop))
-    monkeypatch.setenv("TVOLAP_WIDE", "0")
+    a.set_tuning("wide", 2)
+    a.set_tuning("wide_warp_fft", 1 if warp_fft else 0)
     b = T.TvolapEngine(T.partition(ir0, hop))
-    monkeypatch.delenv("TVOLAP_WIDE")
-    monkeypatch.delenv("TVOLAP_WIDE_WARPFFT")
+    b.set_tuning("wide", 0)
     return a, b
 
 
@@ -118,7 +116,7 @@ def test_wide_chunked_pool(monkeypatch):
     hop, S, taps, n, period = 256, 4, 4096, 16 * 7 + 5, 16
     ir0, x, dirs = _case(hop, S, taps, n, period, none_at=(3,))
     a, b = _engines(monkeypatch, ir0, hop)
-    monkeypatch.setenv("TVOLAP_WIDE_POOL_MB", "1")
+    a.set_tuning("wide_pool_mb", 1)
     ya = a.process_switching(x, dirs, period)
     yb = _loop(b, x, dirs, period, hop)
     a.synchronize()
@@ -133,7 +131,7 @@ def test_wide_chunked_passes(monkeypatch, period, none_at):
     hop, S, taps, n = 256, 4, 4096, period * 9 + 5
     ir0, x, dirs = _case(hop, S, taps, n, period, none_at=none_at)
     a, b = _engines(monkeypatch, ir0, hop)
-    monkeypatch.setenv("TVOLAP_WIDE_XE_MB", "1")
+    a.set_tuning("wide_xe_mb", 1)
     ya = a.process_switching(x, dirs, period)
     yb = _loop(b, x, dirs, period, hop)
     a.synchronize()
@@ -160,8 +158,8 @@ def test_wide_back_to_back_calls(monkeypatch):
 def test_wide_matches_oracle(monkeypatch):
     hop, S, taps, n, period = 128, 2, 4096, 80, 16
     ir0, x, dirs = _case(hop, S, taps, n, period)
-    monkeypatch.setenv("TVOLAP_WIDE", "2")
     eng_g = T.TvolapEngine(T.partition(ir0, hop))
+    eng_g.set_tuning("wide", 2)
     y = eng_g.process_switching(x, dirs, period)
     eng_g.synchronize()
     y = y.cpu().numpy()
@@ -201,11 +199,12 @@ def test_wide_after_staged_exchange(monkeypatch, first_switch):
 
 
 def _bank_engines(monkeypatch, bank, hop, S):
-    monkeypatch.setenv("TVOLAP_WIDE", "2")
+    """a: time-parallel passes forced; b: the hop-blocked launch only (no pass of either kind)."""
     a = T.TvolapBankEngine(bank, hop, S)
-    monkeypatch.setenv("TVOLAP_WIDE", "0")
+    a.set_tuning("wide", 2)
     b = T.TvolapBankEngine(bank, hop, S)
-    monkeypatch.delenv("TVOLAP_WIDE")
+    b.set_tuning("wide", 0)
+    b.set_tuning("bank_pass", 0)
     return a, b
 
 
@@ -270,12 +269,14 @@ def test_wide_bank_pinned_host_pipeline(monkeypatch):
 
 
 def test_wide_bank_random_schedule_stays_blocked(monkeypatch):
-    """A schedule that changes every hop (C3/C5) has no >= 3-hop segments: no pass is taken."""
+    """A schedule that changes every hop (C3/C5) has no >= 3-hop segments: no piecewise pass;
+    with the bank pass switched off the call stays on the hop-blocked kernel."""
     import torch
 
     g = np.random.default_rng(4)
     bank = (g.standard_normal((4, 1, 2048)) * 0.05).astype(np.float32)
     a, _ = _bank_engines(monkeypatch, bank, 128, 2)
+    a.set_tuning("bank_pass", 0)
     x = torch.from_numpy(g.uniform(-1, 1, (2, 64 * 128)).astype(np.float32)).cuda()
     sched = torch.from_numpy(g.integers(0, 4, (64, 2)).astype(np.int32)).cuda()
     a.process_hops(x, schedule=sched)
@@ -291,9 +292,8 @@ def test_wide_set_process_hops_equals_one_hop(monkeypatch, hop, S, taps, n_hops)
 
     g = np.random.default_rng(6)
     ir = g.standard_normal((taps, S)) * 0.05
-    monkeypatch.setenv("TVOLAP_WIDE", "2")
     a = T.TvolapEngine(T.partition(ir, hop))
-    monkeypatch.delenv("TVOLAP_WIDE")
+    a.set_tuning("wide", 2)
     b = T.TvolapEngine(T.partition(ir, hop))
     xs = g.uniform(-1, 1, (S, (n_hops + 5) * hop)).astype(np.float32)
     ya = a.process_hops(torch.from_numpy(np.ascontiguousarray(xs[:, : n_hops * hop])).cuda())

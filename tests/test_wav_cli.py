@@ -75,6 +75,19 @@ def test_parse_failures_carry_offsets(tmp_path):  # test_wav.cpp:160-202
     assert e.value.offset > 0
     with pytest.raises(ValueError):
         wav.write_wav(str(tmp_path / "x.wav"), np.zeros((4, 17)))
+    # test_wav.cpp:172-180: a valid header, the file shortened by 5 bytes (data shorter than declared)
+    p.write_bytes(_craft_pcm16(1, 48000, [1, 2, 3, 4])[:-5])
+    with pytest.raises(wav.WavError) as e:
+        wav.read_wav(str(p))
+    assert e.value.offset > 0
+    # test_wav.cpp:182, 199-201, 208: missing file, zero sample rate, unwritable path
+    with pytest.raises(wav.WavError):
+        wav.read_wav(str(tmp_path / "does_not_exist.wav"))
+    p.write_bytes(_craft_pcm16(1, 0, [0]))
+    with pytest.raises(wav.WavError):
+        wav.read_wav(str(p))
+    with pytest.raises(wav.WavError):
+        wav.write_wav("/nonexistent_dir/x.wav", np.zeros((4, 1)))
 
 
 def _cli(*args, env=None):
