@@ -245,6 +245,7 @@ struct tvolap_engine {
     long bank_pass = 1;              // 0: per-hop schedules stay on the hop-blocked kernel
     long bank_pass_mb = 32768;       // Xe + partials budget per pass
     long bank_pass_hops = 0;         // max hops per pass (0: by the budget)
+    long bank_pass_q = 0;            // partition groups of the bank pass (0: auto, bank slice <= 40 MB)
     uint64_t wide_passes = 0;
     long pipe_merge = 1;             // "pipe_merge": one H2D copy per run of host-contiguous sets
     long wide_warp_fft = 1;          // "wide_warp_fft": 1 warp FFTs for K1/K5 (0: bit-identical Stockham)
@@ -1193,6 +1194,7 @@ bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride,
     const double bank_bytes = (double)e->n_bank * E * M * N * sizeof(float2);
     int Q = 1;
     while (Q < 64 && 2 * Q <= M && bank_bytes / Q > 40e6) Q *= 2;
+    if (e->bank_pass_q > 0) Q = (int)std::min<long>(e->bank_pass_q, M);
     // hops per pass: extended spectra + partials within the budget
     const long per_hop = (long)(S * N * sizeof(float2) + (size_t)Q * S * E * N * sizeof(float2));
     long max_hops = std::max<long>(4 * J, (e->bank_pass_mb << 20) / per_hop);
@@ -1734,6 +1736,7 @@ const Knob kKnobs[] = {
     {"bank_pass", &tvolap_engine::bank_pass, nullptr, 0, 1, 0},
     {"bank_pass_mb", &tvolap_engine::bank_pass_mb, nullptr, 1, 1L << 20, 0},
     {"bank_pass_hops", &tvolap_engine::bank_pass_hops, nullptr, 0, 1L << 30, 0},
+    {"bank_pass_q", &tvolap_engine::bank_pass_q, nullptr, 0, 64, 0},
     {"pipe_merge", &tvolap_engine::pipe_merge, nullptr, 0, 1, 0},
     {"pipe_mb", &tvolap_engine::pipe_mb, nullptr, 1, 1L << 20, 0},
     {"pipe_log2", &tvolap_engine::pipe_log2, nullptr, 10, 34, 0},

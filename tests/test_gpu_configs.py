@@ -37,9 +37,10 @@ def test_c2_all_lanes_fresh_switches():
 
 
 def test_c3_binaural_bank():
-    """C3: 1024 sources x 2 ears on the GPU; per-block bank choice; 16 sources checked over 520 hops."""
+    """C3: 1024 sources x 2 ears on the GPU (bank pass); per-block bank choice; 64 strided sources
+    checked over 520 hops (ring of 255 slots wrapped)."""
     cfg = W.CONFIGS["C3"]
-    subset = list(range(0, 1024, 64))
+    subset = list(range(0, 1024, 16))
     y, ref = check(cfg, 520, subset=subset)
 
 
@@ -56,9 +57,52 @@ def test_c4_full_lane_count_prefix():
 
 
 def test_c5_low_latency_bank():
-    """C5: 4096 lanes, L=32, M=512, per-block choice from 1024 IRs; 1100 hops, 8 lanes checked."""
+    """C5: 4096 lanes, L=32, M=512, per-block choice from 1024 IRs (bank pass); 2100 hops (ring of
+    1023 slots wrapped twice), 64 strided lanes checked."""
     cfg = W.CONFIGS["C5"]
-    check(cfg, 1100, subset=list(range(0, 4096, 512)))
+    check(cfg, 2100, subset=list(range(0, 4096, 64)))
+
+
+def test_c3_stereo_mix_against_reference_mix():
+    """C3's stereo mix (tvolap_mix_allreduce, the bench path) against the fp64 sum of the reference
+    outputs of ALL 1024 sources x 2 ears, over 64 hops."""
+    import ctypes
+
+    import torch
+
+    from paper_2310_00319_b200 import tvolap as T
+
+    cfg = W.CONFIGS["C3"]
+    n, L, S = 64, cfg.hop, cfg.sources
+    eng = drive.make_engine(cfg)
+    x = torch.from_numpy(W.white(cfg, 0, S, 0, n * L)).cuda()
+    out = torch.empty((S * cfg.ears, n * L), device="cuda")
+    eng.process_hops(x, out=out, schedule=torch.from_numpy(W.schedule(cfg, 0, n)).cuda())
+    mix = torch.empty((cfg.ears, n * L), device="cuda")
+    eng.synchronize()
+    T._check(T.lib().tvolap_mix_allreduce(0, S, cfg.ears, n * L, ctypes.c_void_p(out.data_ptr()), n * L,
+                                          ctypes.c_void_p(mix.data_ptr()), n * L, None, None))
+    torch.cuda.synchronize()
+    ref = oracle_config(cfg, n).reshape(S, cfg.ears, -1).sum(0)
+    assert rel_err(mix.cpu().numpy(), ref) <= TOL
+
+
+def test_c2_full_pass_against_reference():
+    """The whole 30-s C2 pass as the bench runs it (one process_switching call on device buffers,
+    5625 hops, 352 fresh-IR switches) against the reference on 4 strided lanes."""
+    import torch
+
+    cfg = W.CONFIGS["C2"]
+    n, L, S = cfg.hops, cfg.hop, cfg.sources
+    eng = drive.make_engine(cfg)
+    x = torch.from_numpy(W.white(cfg, 0, S, 0, n * L)).cuda()
+    irs = [None] + _c2_device_irs(cfg, range(1, -(-n // cfg.period)), S)
+    torch.cuda.synchronize()
+    y = eng.process_switching(x, irs, cfg.period)
+    eng.synchronize()
+    subset = [0, 21, 42, 63]
+    ref = oracle_config(cfg, n, subset=subset)
+    assert rel_err(y.cpu().numpy()[subset], ref) <= TOL
 
 
 def test_c3_mix_kernel_deterministic():

@@ -427,6 +427,7 @@ def test_bank_engine_single_hop_select(S):
     sched = np.random.default_rng(9).integers(0, n_bank, (n, S)).astype(np.int32)
     x = rnd(hop * n, 18, S)
     a, b = T.TvolapBankEngine(bank, hop, S), T.TvolapBankEngine(bank, hop, S)
+    b.set_tuning("bank_pass", 0)  # the hop kernels: bit-identical to process() per hop
     ya = []
     for h in range(n):
         a.select_bank(sched[h])
@@ -434,6 +435,10 @@ def test_bank_engine_single_hop_select(S):
     ya = np.concatenate(ya).T
     yb = b.process_hops(np.ascontiguousarray(x.T), schedule=sched)
     assert np.array_equal(ya, yb)
+    c = T.TvolapBankEngine(bank, hop, S)  # default: the bank pass, equal to fp32 rounding
+    yc = c.process_hops(np.ascontiguousarray(x.T), schedule=sched)
+    assert c.wide_passes() >= 1
+    assert np.abs(yc - ya).max() <= 2e-6 * np.abs(ya).max()
     with pytest.raises(T.InvalidInputError):
         a.select_bank(np.full(S, n_bank, np.int32))
 

@@ -199,9 +199,11 @@ def test_wide_after_staged_exchange(monkeypatch, first_switch):
 
 
 def _bank_engines(monkeypatch, bank, hop, S):
-    """a: time-parallel passes forced; b: the hop-blocked launch only (no pass of either kind)."""
+    """a: piecewise time-parallel passes forced; b: the hop-blocked launch only (no pass of either
+    kind; the per-hop bank pass is tested in test_gpu_bank_pass.py)."""
     a = T.TvolapBankEngine(bank, hop, S)
     a.set_tuning("wide", 2)
+    a.set_tuning("bank_pass", 0)
     b = T.TvolapBankEngine(bank, hop, S)
     b.set_tuning("wide", 0)
     b.set_tuning("bank_pass", 0)
