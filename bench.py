@@ -263,6 +263,8 @@ def roofline_block(cfg, summ_path, kern_ms, kern_n, hops_per_launch, distinct, c
     fpk = fp32_peak_tflops(sms, mhz)
     sides["fp32"] = {"achieved": flops / t / 1e12, "peak": fpk, "unit": "TFLOP/s", "frac": flops / t / 1e12 / fpk,
                      "flops_per_hop": W.flops_per_hop(cfg),
+                     "flops_model": "cost.cpp:34-38 (MAC 8 B M per lane + the hop's forward / inverse transforms) "
+                                    "+ for fresh-IR configs the K4 transforms of the switches (M per lane / period)",
                      "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x {mhz:.0f} MHz (median SM clock under load)"}
     bound = max(sides, key=lambda k: sides[k]["frac"])
     b = sides[bound]
@@ -311,6 +313,8 @@ def main():
     ap.add_argument("--cpu-hops", type=int, default=0, help="CPU sample hops (default >= 2(2M-1))")
     ap.add_argument("--latency-hops", type=int, default=300,
                     help="single-hop process() calls timed for the p50/p99 per-hop latency (0: skip)")
+    ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
+                    help="engine tuning knob for an A/B run (tvolap_set_default_tuning; DESIGN.md §10)")
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -329,6 +333,9 @@ def main():
     from paper_2310_00319_b200.tvolap import TvolapBankEngine, TvolapEngine, partition
 
     _build.build()
+    for kv in args.tune:
+        k, v = kv.split("=")
+        T.set_default_tuning(k, int(v))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -352,12 +359,15 @@ def main():
     T._check(lib.tvolap_gen_white_device(local, cfg.seed, lane0, S, 0, H * L, ctypes.c_void_p(x.data_ptr()), H * L))
     out = torch.empty((lanes, H * L), dtype=torch.float32, device=dev)
 
-    def gen_irs(items, dst):
-        la = np.array([i[0] for i in items], np.int64)
-        ea = np.array([i[1] for i in items], np.int64)
-        ka = np.array([i[2] for i in items], np.int64)
-        ta = np.array([W.t60_of(cfg, int(l), int(k)) for l, _, k in items], np.float64)
-        T._check(lib.tvolap_gen_irs_device(local, cfg.seed, len(items), la.ctypes.data, ea.ctypes.data,
+    def gen_irs(items, dst, arrays=None):
+        if arrays is None:
+            la = np.array([i[0] for i in items], np.int64)
+            ea = np.array([i[1] for i in items], np.int64)
+            ka = np.array([i[2] for i in items], np.int64)
+            ta = np.array([W.t60_of(cfg, int(l), int(k)) for l, _, k in items], np.float64)
+        else:
+            la, ea, ka, ta = arrays
+        T._check(lib.tvolap_gen_irs_device(local, cfg.seed, len(la), la.ctypes.data, ea.ctypes.data,
                                            ka.ctypes.data, ta.ctypes.data, W.FS, cfg.ir_length,
                                            ctypes.c_void_p(dst.data_ptr())))
 
@@ -368,13 +378,28 @@ def main():
             e.set_block_config(max(2, 1 << (cfg.period.bit_length() - 1)))
 
     sched = mix = irs = None
-    n_pool = n_sw
+    stream = torch.cuda.Stream(device=dev)
+    chunk = n_sw
     if cfg.mode == "fresh":
-        # C4's 704 switches x 256 channels x 131072 taps would not fit: cycle through a pool of
-        # distinct seeded sets (<= 24 GB); every switch still uploads + transforms a whole set
-        n_pool = int(max(2, min(n_sw, 24e9 // (S * cfg.ir_length * 4))))
-        irs = torch.empty((n_pool, S, cfg.ir_length), dtype=torch.float32, device=dev)
-        gen_irs([(lane0 + s, 0, k) for k in range(n_pool) for s in range(S)], irs)
+        # a fresh seeded IR per (channel, switch), generated on the device. C4's 704 switches x 256
+        # channels x 262144 taps (180 GB) do not fit: the step runs in chunks of periods whose sets
+        # (<= 16 GB) are generated between the chunks' process_switching calls, outside the timed
+        # intervals (the reference times process + partition, experiment.cpp:42-52)
+        set_bytes = S * cfg.ir_length * 4
+        chunk = int(max(1, min(n_sw, 16e9 // set_bytes)))
+        irs = torch.empty((chunk, S, cfg.ir_length), dtype=torch.float32, device=dev)
+        items = [(lane0 + s, 0, k) for k in range(n_sw) for s in range(S)]
+        ir_arrays = (np.array([i[0] for i in items], np.int64), np.array([i[1] for i in items], np.int64),
+                     np.array([i[2] for i in items], np.int64),
+                     np.array([W.t60_of(cfg, int(l), int(k)) for l, _, k in items], np.float64))
+
+        def gen_chunk(c0):
+            stream.synchronize()  # the previous chunk's calls are done reading the sets
+            c1 = min(n_sw, c0 + chunk)
+            gen_irs(None, irs, tuple(a[c0 * S: c1 * S] for a in ir_arrays))
+
+        if chunk >= n_sw:
+            gen_chunk(0)
         ir0 = W.fresh_irs(cfg, 0, lane0, S)[:, 0, :]
         eng = TvolapEngine(partition(ir0.T, L, M), device=local)
         fit_block(eng)
@@ -391,17 +416,45 @@ def main():
     torch.cuda.synchronize()
     log(f"[rank {rank}] {cfg.name}: channels {lane0}..{lane0 + S - 1}, generated {x.numel() * 4 / 1e6:.0f} MB input"
         f"{'' if irs is None else f' + {irs.numel() * 4 / 1e9:.2f} GB IRs'} in {time.time() - t0:.1f} s")
-    stream = torch.cuda.Stream(device=dev)
     eng.set_stream(stream.cuda_stream)
     comm = None
     if mix is not None and world > 1:  # C3: the partial mixes are summed with NCCL through the C-ABI
         comm = NcclComm(lib, rank, world, local)
 
-    def step(e, xs, outs, ir_set, sch, mx=None):
+    class ChunkTimer:
+        """Sum of CUDA-event intervals (engine stream) around the chunks' process_switching calls."""
+
+        def __init__(self):
+            self.pairs = []
+
+        def begin(self):
+            self.pairs.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+            self.pairs[-1][0].record(stream)
+
+        def end(self):
+            self.pairs[-1][1].record(stream)
+
+        def total(self):
+            return sum(a.elapsed_time(b) for a, b in self.pairs)
+
+    def step(e, xs, outs, ir_set, sch, mx=None, timer=None):
         e.reset()
-        if cfg.mode == "fresh":
-            # the drive() loop (exchange before every period's hops) as one call
-            e.process_switching(xs, [ir_set[k % n_pool] for k in range(n_sw)], cfg.period, out=outs)
+        if cfg.mode == "fresh" and ir_set is not None and ir_set.is_cuda:
+            # the drive() loop (exchange before every period's hops), one call per chunk of periods
+            for c0 in range(0, n_sw, chunk):
+                c1 = min(n_sw, c0 + chunk)
+                if chunk < n_sw:
+                    gen_chunk(c0)  # this chunk's fresh IRs, outside the timed interval
+                h0, h1 = c0 * cfg.period, min(H, c1 * cfg.period)
+                if timer:
+                    timer.begin()
+                e.process_switching(xs[:, h0 * L: h1 * L], [ir_set[k - c0] for k in range(c0, c1)], cfg.period,
+                                    out=outs[:, h0 * L: h1 * L])
+                if timer:
+                    timer.end()
+        elif cfg.mode == "fresh":
+            # e2e: host-pinned sets, every switch uploads a whole set (cycled when they do not all fit)
+            e.process_switching(xs, [ir_set[k % ir_set.shape[0]] for k in range(n_sw)], cfg.period, out=outs)
         else:
             e.process_hops(xs, out=outs, schedule=sch)
             if mx is not None and outs.is_cuda:
@@ -422,16 +475,18 @@ def main():
     barrier()
     launches0 = eng.kernel_launches()
     wide0 = eng.wide_passes()
+    chunked = cfg.mode == "fresh" and chunk < n_sw
+    timer = ChunkTimer() if chunked else None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
-        step(eng, x, out, irs, sched, mix)
+        step(eng, x, out, irs, sched, mix, timer)
     ev1.record(stream)
     barrier()
     t_end = time.time()
     clk = clocks.stop(t_start, t_end)
-    elapsed = ev0.elapsed_time(ev1)
+    elapsed = timer.total() if timer else ev0.elapsed_time(ev1)
     gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
     passes = eng.wide_passes() - wide0
     # Per-launch kernel durations: a separate pass of the same steps with CUDA events around the
@@ -439,14 +494,15 @@ def main():
     prof_steps = max(1, min(args.steps, 2))
     eng.set_profiling(True)
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ptimer = ChunkTimer() if chunked else None
     ev2.record(stream)
     for _ in range(prof_steps):
-        step(eng, x, out, irs, sched, mix)
+        step(eng, x, out, irs, sched, mix, ptimer)
     ev3.record(stream)
     barrier()
     kern_ms, kern_n = eng.kernel_time()
     eng.set_profiling(False)
-    prof_elapsed = ev2.elapsed_time(ev3)
+    prof_elapsed = ptimer.total() if ptimer else ev2.elapsed_time(ev3)
     elapsed = shard.max_over_ranks(elapsed, dev)
     ms_per_step = elapsed / args.steps
     total_sources = cfg.sources * (world if args.scaling == "weak" else 1)
@@ -475,8 +531,13 @@ def main():
         oh = torch.empty(tuple(out.shape), dtype=torch.float32, pin_memory=True)
         h2d = xh.numel() * 4
         if cfg.mode == "fresh":
-            irh = torch.empty(irs.shape, dtype=torch.float32, pin_memory=True)
-            irh.copy_(irs)
+            # pinned host sets (<= 8 GB): the device's first chunk of fresh sets; every switch
+            # uploads a whole set (C4: 704 uploads cycle through 31 sets)
+            n_e2e = int(max(1, min(n_sw, 8e9 // (S * cfg.ir_length * 4), chunk)))
+            if chunk < n_sw:
+                gen_chunk(0)
+            irh = torch.empty((n_e2e,) + tuple(irs.shape[1:]), dtype=torch.float32, pin_memory=True)
+            irh.copy_(irs[:n_e2e])
             eng2 = TvolapEngine(partition(ir0.T, L, M), device=local)
             fit_block(eng2)
             h2d += n_sw * S * cfg.ir_length * 4  # one whole set uploaded per switch
@@ -497,7 +558,7 @@ def main():
         barrier()
         e2e_s = (time.perf_counter() - tw) / args.steps
         e2e_s = shard.max_over_ranks(e2e_s, dev)
-        same = bool(torch.equal(oh, out.cpu()))
+        same = bool(torch.equal(oh, out.cpu())) if (cfg.mode != "fresh" or n_e2e >= n_sw) else None
         e2e = {"value": samples_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_s * 1e3,
                "timing": "host wall clock around each full pass incl. final synchronize",
@@ -549,13 +610,21 @@ def main():
         "config": config_block(cfg, H, world, S, args.scaling), "clocks": clk, "gpu_launches": int(gpu_launches),
         "roofline": roofline, "e2e": e2e, "latency": latency,
         "realtime_factor": (H * L / W.FS) / (ms_per_step / 1e3),
+        "tuning": dict(kv.split("=") for kv in args.tune) or "defaults",
         "path": {"passes_per_step": passes / args.steps,
                  "kind": "bank pass" if (cfg.mode == "bank" and cfg.period == 1 and passes) else
                          ("time-parallel pass" if passes else "hop-blocked launches")},
     }
-    if cfg.mode == "fresh" and n_pool < n_sw:
-        line["config"]["ir_sets"] = (f"{n_sw} switches per step cycle through {n_pool} distinct seeded IR sets "
-                                     "held in HBM (every switch uploads and transforms a whole set)")
+    if chunked:
+        line["config"]["ir_sets"] = (f"a fresh seeded IR per (channel, switch): {n_sw} switches per step in chunks of "
+                                     f"{chunk} periods whose sets are generated on the device between the chunks' "
+                                     "process_switching calls")
+        line["timing"] = ("sum of CUDA-event intervals (engine stream) around each chunk's process_switching call; "
+                          "the IR generation between them is outside the timed region (experiment.cpp:42-52 times "
+                          "process + partition)")
+    if e2e and cfg.mode == "fresh" and e2e["matches_device_path"] is None:
+        e2e["ir_sets"] = (f"{n_e2e} pinned host sets cycled over the {n_sw} switches (each switch uploads a whole "
+                          "set); outputs not comparable to the device path's fresh sets")
 
     # ---- CPU baseline + in-line parity (rank 0, N=1 only): the reference on a bounded sample
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -255,6 +255,7 @@ struct tvolap_engine {
     long wide_pool_mb = 8192;        // unfused wide pass: filter-set pool budget
     long wide_fuse = 1;              // fused K4 in the wide MAC tiles
     long wide_xe_mb = 4096;          // wide pass: extended-spectra budget
+    long wide_period = 1;            // fused K4 in shared-memory partition groups (wide_period_kernel)
     long k4_gap_mult = 1;            // switching launch: K4 units per barrier gap (x warps x CTAs)
     long sw_1024 = 0;                // switching launch also for 1024-point transforms
     long pipe_mb = 64;               // pinned switching pipeline chunk
@@ -890,12 +891,20 @@ int sm_count_of(int device) {
     return sms;
 }
 
-bool wide_eligible(const tvolap_engine* e, long n_hops, long period) {
+// The period tiles of wide_period_kernel apply: every period one tile of <= 8 hops with its set
+// transformed in shared-memory partition groups (C4).
+bool period_tiles(const tvolap_engine* e, long period, long ir_length) {
+    return e->wide_period != 0 && e->wide_fuse != 0 && e->wide_warp_fft != 0 && period >= 3 && period <= 8 &&
+           tvb::period_kernel_supported((int)e->L, (int)e->M, 4, ir_length);
+}
+
+bool wide_eligible(const tvolap_engine* e, long n_hops, long period, long ir_length) {
     if (e->wide_mode == 0 || e->bank || e->E != 1 || !tvb::wide_supported((int)e->L)) return false;
     if (period < 3 || n_hops < period || n_hops < 16) return false;
-    // auto: only where the hop-blocked kernel leaves most of the GPU idle (lanes x cluster CTAs
-    // below two per SM, e.g. C1/C2); there the hop axis is the parallelism
-    if (e->wide_mode == 1 && e->S * e->PB > 2 * e->sms) return false;
+    // auto: where the hop-blocked kernel leaves most of the GPU idle (lanes x cluster CTAs below
+    // two per SM, e.g. C1/C2; there the hop axis is the parallelism), or where the period tiles
+    // keep every set's spectra on chip (C4)
+    if (e->wide_mode == 1 && e->S * e->PB > 2 * e->sms && !period_tiles(e, period, ir_length)) return false;
     return true;
 }
 
@@ -926,7 +935,8 @@ void ensure_dev(T*& p, size_t& cap, size_t count) {
 // (base of [M][2L]); tirs (optional): per tile the IR set the tile transforms itself (fused K4).
 void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, float* out, long out_stride, long nh,
                const std::vector<int>& t0, const std::vector<const float2*>& fs, bool per_lane,
-               const std::vector<const float*>* tirs, long ir_length, int JH, int nslots, int warp_fft) {
+               const std::vector<const float*>* tirs, long ir_length, int JH, int nslots, int warp_fft,
+               int period_smem = 0) {
     const long S = e->S, M = e->M, N = e->N, L = e->L;
     const long ntiles = (long)t0.size() - 1;
     ensure_dev(e->d_wide_fset, e->wide_fset_cap, fs.size());
@@ -980,6 +990,7 @@ void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, flo
     p.nslots = nslots;
     p.warp_fft = warp_fft;
     p.stage_ir = (int)e->wide_stage;
+    p.period_smem = period_smem;
     cudaEvent_t ev0, ev1;
     prof_pair(e, &ev0, &ev1);
     CK(tvb::launch_wide(p, JH, e->stream, ev0, ev1, 3));
@@ -1023,8 +1034,12 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
     // Fused K4: when every period is one tile, each tile transforms its own set into an
     // L2-resident scratch slot (no set spectra through HBM); TVOLAP_WIDE_FUSE=0 disables.
     const bool fuse = e->wide_fuse != 0 && period <= Jmax && period >= 3;
+    // period tiles: the set of each tile transformed group by group into shared memory (the IR
+    // slices arrive by bulk copies: 16-byte aligned sets)
+    bool ptiles = fuse && JH == 4 && period_tiles(e, period, ir_length);
+    for (long k = 0; ptiles && k < nsw; ++k) ptiles = !irs[k] || (reinterpret_cast<uintptr_t>(irs[k]) & 15) == 0;
     int nslots = 0;
-    if (fuse) {
+    if (fuse && !ptiles) {
         const int q_launch = e->wide_q > 0 ? (int)e->wide_q : (e->wide_warp_fft ? 1 : e->QM);  // as wide_pass sets it
         nslots = tvb::wide_mac_ctas_per_sm((int)L, JH, (int)M, q_launch) * sm_count_of(e->device);
         if (nslots <= 0) throw ApiError{TVOLAP_ERR_CUDA, "wide pass: no resident CTA for the MAC kernel"};
@@ -1081,7 +1096,7 @@ void run_wide(tvolap_engine* e, const float* in, long in_stride, float* out, lon
         if (fuse && tirs.size() != fs.size())
             throw ApiError{TVOLAP_ERR_CUDA, "wide pass: fused K4 needs one tile per period"};
         wide_pass(e, e->hops, in + h0 * L, in_stride, out + h0 * L, out_stride, nh, t0, fs, false,
-                  fuse ? &tirs : nullptr, ir_length, JH, nslots, e->wide_warp_fft);
+                  fuse ? &tirs : nullptr, ir_length, JH, nslots, e->wide_warp_fft, ptiles ? 1 : 0);
         e->hops += nh;
         if (fuse && last_ir) {  // the pass's last set becomes the engine's active set (K4 into a pool slot)
             const int slot = (e->active + 1) % kSlots;
@@ -1311,7 +1326,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
     return guarded([&] {
         CK(cudaSetDevice(e->device));
         {  // device-resident call with enough hops: the time-parallel pass
-            bool wide = classify(in) == Mem::Device && classify(out) == Mem::Device && wide_eligible(e, n_hops, period);
+            bool wide = classify(in) == Mem::Device && classify(out) == Mem::Device && wide_eligible(e, n_hops, period, ir_length);
             for (long k = 0; wide && k < nsw; ++k) wide = !irs[k] || classify(irs[k]) == Mem::Device;
             if (wide) {
                 run_wide(e, in, in_lane_stride, out, out_lane_stride, n_hops, period, irs, ir_length);
@@ -1733,6 +1748,7 @@ const Knob kKnobs[] = {
     {"wide_pool_mb", &tvolap_engine::wide_pool_mb, nullptr, 1, 1L << 20, 0},
     {"wide_fuse", &tvolap_engine::wide_fuse, nullptr, 0, 1, 0},
     {"wide_xe_mb", &tvolap_engine::wide_xe_mb, nullptr, 1, 1L << 20, 0},
+    {"wide_period", &tvolap_engine::wide_period, nullptr, 0, 1, 0},
     {"bank_pass", &tvolap_engine::bank_pass, nullptr, 0, 1, 0},
     {"bank_pass_mb", &tvolap_engine::bank_pass_mb, nullptr, 1, 1L << 20, 0},
     {"bank_pass_hops", &tvolap_engine::bank_pass_hops, nullptr, 0, 1L << 30, 0},

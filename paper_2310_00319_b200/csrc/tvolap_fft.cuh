@@ -534,6 +534,26 @@ __device__ __forceinline__ void untangle_pairs_warp(const float2* Z, int N, cons
     }
 }
 
+// untangle_pairs_warp over the warp's own buffer (Z == dst): a lane reads both bins of its pair
+// (k, N - k) before writing them, and pairs are disjoint across lanes. Same operations.
+__device__ __forceinline__ void untangle_pairs_inplace_warp(float2* Z, int N, const float2* __restrict__ pk,
+                                                            int lane) {
+    for (int k = lane; k <= N / 2; k += 32) {
+        if (k == 0) {
+            const float2 z0 = Z[0];
+            Z[0] = make_float2(z0.x + z0.y, z0.x - z0.y);
+            continue;
+        }
+        const float2 zk = Z[k], zm = Z[N - k];
+        const float2 even = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+        const float2 odd = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+        const float2 po = cmul(pk[k], odd);
+        Z[k] = cadd(even, po);
+        if (k != N / 2) Z[N - k] = make_float2(even.x - po.x, -(even.y - po.y));
+    }
+    __syncwarp();
+}
+
 // Tangle bin k < N for the inverse (spectral.cpp:142-148), from a packed
 // spectrum Y:  z_k = E + i O,  E = (X_k + conj X_{N-k})/2,
 // O = (X_k - conj X_{N-k})/2 * conj(pack_k).

@@ -83,6 +83,7 @@ struct WideParams {
     unsigned* slot_lock;
     int nslots;
     int stage_ir;               // fused K4: IR slices through a cp.async double buffer in shared memory
+    int period_smem = 0;        // fused K4 in partition groups into shared memory (wide_period_kernel)
     int warp_fft;               // K1 / K5 with one warp per frame (warp four-step FFT) instead of the
                                 // hop kernels' CTA Stockham (equal to fp32 rounding, not bit-identical)
     // bank pass (per-hop bank schedules, tvolap_wide.cu bank_mac_kernel / bank_k5_kernel)
@@ -93,6 +94,8 @@ struct WideParams {
 };
 int wide_mac_ctas_per_sm(int L, int JH, int M, int Q);
 bool wide_supported(int L);
+// wide_period_kernel (fused K4 in shared-memory partition groups) covers this geometry
+bool period_kernel_supported(int L, int M, int JH, long ir_len);
 size_t wide_mac_smem_bytes(int L, int JH, int M, int Q);
 constexpr int kWideFront = 8;   // Xe front padding slots per parity (tbase = (hop0 >> 1) - M - kWideFront)
 constexpr int kWideTail = 8;    // spectra rows readable past the end of every filter set (prefetch)

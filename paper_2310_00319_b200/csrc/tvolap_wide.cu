@@ -574,6 +574,284 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
     }
 }
 
+// ============================================================================ period tiles
+// K4 + K3 + K5 of one (lane, filter period) tile with the period's set transformed in partition
+// groups into SHARED memory (C4: 2L = 1024 bins, M = 256, a fresh IR every 8 hops). A whole set
+// (M x 2L complex = 2 MB for C4) per resident CTA does not stay in L2 (wide_mac_kernel's scratch
+// slots: 148 x 2 MB), so here the tile walks its partitions in groups of G = NT / 32 (one warp per
+// partition, 16 for C4): the group's IR taps (G x 2L contiguous floats, 64 KB) arrive by one
+// cp.async.bulk (TMA) into a staging buffer signalled by an mbarrier — issued a whole group ahead,
+// so the copy overlaps the previous group's MAC — each warp transforms its partition from the
+// staging buffer into its spectra row (the warp four-step FFT + in-place untangle: the same
+// operations as partition_warp_kernel), and the MAC reads the filter from shared memory:
+//   Y_l += sum_{m in group} H[m] X_{l-2m}   (engine.cpp:85-92)
+// A thread owns bins (t, t + NT) x both parities x JH outputs; the delay-line window slides by
+// register renaming, X comes from Xe (L2) KPF steps ahead. The set's spectra never leave the SM.
+// Then Y -> shared memory, tangle + inverse warp FFT one frame per warp, hop-2 overlap-add
+// (engine.cpp:94-102), carries for wide_fixup_kernel — as in wide_mac_kernel.
+// Partition sums run in m order inside each group and across groups (deterministic).
+template <int NC>
+struct PeriodLayout {
+    static constexpr int N = NC, NT = NC / 2, G = NT / 32;
+    static constexpr size_t pk = 0;
+    static constexpr size_t spec = (((size_t)(N + 2) * 8) + 15) & ~size_t(15);  // G spectra rows (Y, K5 buffers later)
+    static constexpr size_t stage = spec + (size_t)G * N * 8;                   // G x 2L IR taps
+    static constexpr size_t auxx = stage + (size_t)G * N * 4;                   // [2][G + 8] Im X[.][0]
+    static constexpr size_t auxr = auxx + 2 * (G + 8) * 4;                      // [16] running Nyquist sums
+    static constexpr size_t bar = (auxr + 16 * 4 + 15) & ~size_t(15);
+    static constexpr size_t total = bar + 16;
+};
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// one thread: bytes (multiple of 16, 16-byte aligned both ends) global -> shared, completion on bar
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic reads of dst are done
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <int NC, int JH>
+__global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams p) {
+    using Lay = PeriodLayout<NC>;
+    constexpr int N = NC, L = NC / 2, NT = Lay::NT, G = Lay::G, J = 2 * JH, KPF = 2;
+    static_assert(J <= G && JH % KPF == 0 && G % JH == 0, "period tile geometry");
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* s_pk = reinterpret_cast<float2*>(smem + Lay::pk);
+    float2* s_spec = reinterpret_cast<float2*>(smem + Lay::spec);
+    float* s_stage = reinterpret_cast<float*>(smem + Lay::stage);
+    float* s_auxx = reinterpret_cast<float*>(smem + Lay::auxx);
+    float* s_auxr = reinterpret_cast<float*>(smem + Lay::auxr);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(smem + Lay::bar);
+    const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(s_stage);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tile = blockIdx.x;
+    const long s = blockIdx.y;
+    const int l0r = p.tile0[tile], jt = p.tile0[tile + 1] - l0r;
+    const long l0 = p.hop0 + l0r;
+    const int M = p.M;
+    const int groups = M / G;
+    // tiles before the call's first switch use the engine's active set in place (global memory)
+    const float* tir = p.tile_ir[tile];
+    const float* h = tir ? tir + s * p.ir_len : nullptr;
+    const float2* hset = tir ? nullptr : (p.fset_per_lane ? p.fset[(long)tile * p.S + s] : p.fset[tile] + s * M * N);
+    // taps of group q: [q G N, (q + 1) G N) clipped to the IR; the rest of the staging row is zero
+    auto group_bytes = [&](int q) -> unsigned {
+        const long a = (long)q * G * N, b = min((long)(q + 1) * G * N, p.ir_len);
+        return b > a ? (unsigned)((b - a) * 4) : 0u;
+    };
+    for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    if (tid < 16) s_auxr[tid] = 0.f;
+    if (tid == 0 && h) {
+        mbar_init(bar, 1);
+        const unsigned b0 = group_bytes(0);
+        if (b0) bulk_g2s(stage_sa, h, b0, bar);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+    }
+    __syncthreads();
+
+    const float2* X[2];
+    long bse[2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        X[g] = p.xe + (s * 2 + ((l0 + g) & 1)) * p.T * N;
+        bse[g] = ((l0 + g) >> 1) - p.tbase;  // slot of output i at partition m: bse + i - m
+    }
+    float2 acc[2][2][JH];  // [bin b][parity g][output i]
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int i = 0; i < JH; ++i) acc[b][g][i] = make_float2(0.f, 0.f);
+
+    for (int q = 0; q < groups; ++q) {
+        const int mu0 = q * G;
+        // ---- K4 of partitions mu0 .. mu0 + G - 1 (partition.cpp:20-51): warp w, partition mu0 + w
+        const float2* hg = h ? s_spec : hset + (size_t)mu0 * N;  // the group's spectra rows
+        if (h) {
+            mbar_wait(bar, (unsigned)(q & 1));
+            const unsigned nb = group_bytes(q);
+            const float* src = s_stage + (size_t)warp * N;
+            const long valid = (long)nb / 4 - (long)warp * N;  // taps of this partition present in staging
+            float2* row = s_spec + (size_t)warp * N;
+            fft_warp4<false, N, true>(row, p.tw + N, lane, [&](int, int n) -> float2 {
+                const long i0 = 2 * n;
+                return make_float2(i0 < valid ? src[i0] : 0.f, i0 + 1 < valid ? src[i0 + 1] : 0.f);
+            });
+            untangle_pairs_inplace_warp(row, N, s_pk, lane);
+        }
+        __syncthreads();  // spectra of the group ready; staging consumed
+        if (h && tid == 0 && q + 1 < groups) {
+            const unsigned b1 = group_bytes(q + 1);
+            if (b1) bulk_g2s(stage_sa, h + (long)(q + 1) * G * N, b1, bar);
+            else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+        }
+        // Nyquist terms of packed bin 0 (warp 0): Im X[g][t][0] of the group's window into shared memory
+        if (warp == 0) {
+            for (int j = lane; j < 2 * (G + JH - 1); j += 32) {
+                const int g = j >= G + JH - 1, jj = j - g * (G + JH - 1);  // slot bse - mu0 - (G - 1) + jj
+                s_auxx[g * (G + 8) + jj] = __ldcg(X[g] + (bse[g] - mu0 - (G - 1) + jj) * N).y;
+            }
+        }
+        // ---- K3 over the group: bins k_b = tid + b NT
+        {
+            float2 win[2][2][JH], fx[KPF][2][2];
+            const float2* px[2];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                px[g] = X[g] + (bse[g] - mu0 - 1) * N + tid;
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int i = 0; i < JH; ++i) win[b][g][i] = __ldcg(X[g] + (bse[g] + i - mu0) * N + tid + b * NT);
+            }
+#pragma unroll
+            for (int u = 0; u < KPF; ++u)
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) fx[u][g][b] = __ldcg(px[g] - (long)u * N + b * NT);
+            const float2* hrow = hg + tid;
+            auto step = [&](auto u_tag, int mm) {
+                constexpr int u = decltype(u_tag)::value, sl = u % KPF;
+                const float2 hv[2] = {hrow[(size_t)mm * N], hrow[(size_t)mm * N + NT]};
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int g = 0; g < 2; ++g)
+#pragma unroll
+                        for (int i = 0; i < JH; ++i) {
+                            float2& a = acc[b][g][i];
+                            const float2 x = win[b][g][(i - u) & (JH - 1)];
+                            a.x = fmaf(hv[b].x, x.x, a.x);
+                            a.x = fmaf(-hv[b].y, x.y, a.x);
+                            a.y = fmaf(hv[b].x, x.y, a.y);
+                            a.y = fmaf(hv[b].y, x.x, a.y);
+                        }
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) win[b][g][(JH - 1 - u) & (JH - 1)] = fx[sl][g][b];
+                // slot bse - mu0 - 1 - (mm + KPF): past the group it reads the next slots down
+                // (Xe front padding at the last group), never used
+#pragma unroll
+                for (int g = 0; g < 2; ++g)
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) fx[sl][g][b] = __ldcg(px[g] - (long)(mm + KPF) * N + b * NT);
+            };
+            for (int mm = 0; mm < G; mm += JH) {
+                step(std::integral_constant<int, 0>{}, mm);
+                step(std::integral_constant<int, 1>{}, mm + 1);
+                step(std::integral_constant<int, 2>{}, mm + 2);
+                step(std::integral_constant<int, 3>{}, mm + 3);
+                if constexpr (JH == 8) {
+                    step(std::integral_constant<int, 4>{}, mm + 4);
+                    step(std::integral_constant<int, 5>{}, mm + 5);
+                    step(std::integral_constant<int, 6>{}, mm + 6);
+                    step(std::integral_constant<int, 7>{}, mm + 7);
+                }
+            }
+        }
+        if (warp == 0) {
+            __syncwarp();
+            if (lane < J) {  // output (g, i): sum_m Im H[m][0] Im X[g][bse + i - m][0], m in order
+                const int g = lane / JH, i = lane % JH;
+                float a = s_auxr[lane];
+                for (int mm = 0; mm < G; ++mm)
+                    a = fmaf(hg[(size_t)mm * N].y, s_auxx[g * (G + 8) + (G - 1) + i - mm], a);
+                s_auxr[lane] = a;
+            }
+        }
+        __syncthreads();  // every read of the group's spectra done
+    }
+
+    // ---- Y rows jj = g + 2 i into shared memory (rows 0 .. J - 1), packed bin 0 fixed up
+    float2* s_y = s_spec;
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int i = 0; i < JH; ++i) {
+            const int jj = g + 2 * i;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                float2 a = acc[b][g][i];
+                if (b == 0 && tid == 0) {
+                    const float x = s_auxr[g * JH + i];
+                    a.x += x;
+                    a.y = x;
+                }
+                s_y[(size_t)jj * N + tid + b * NT] = a;
+            }
+        }
+    __syncthreads();
+    // ---- K5: tangle + inverse warp FFT over the Y rows
+    if constexpr (2 * J <= G) {  // one frame per warp, tangled into a warp buffer (rows J .. 2J - 1)
+        for (int jj = warp; jj < jt; jj += NT / 32) {
+            float2* yrow = s_y + (size_t)jj * N;
+            float2* wb = s_y + (size_t)(J + (jj % J)) * N;
+            for (int kk = lane; kk < N; kk += 32) wb[kk] = tangle_packed(yrow, N, kk, s_pk);
+            __syncwarp();
+            fft_warp4<true, N, false>(yrow, p.tw + N, lane, [&](int, int n) { return wb[n]; });
+            __syncwarp();
+        }
+    } else {  // no room for buffers: two frames per warp, tangled in the transform's loads, in place
+        for (int jj = 2 * warp; jj < jt; jj += 2 * (NT / 32)) {  // rows jj, jj + 1 < J (J even)
+            float2* rows = s_y + (size_t)jj * N;
+            auto ld = [&](int t, int n) { return tangle_packed(rows + (size_t)t * N, N, n, s_pk); };
+            fft_warp4<true, N, false, 2, decltype(ld), true>(rows, p.tw + N, lane, ld);
+        }
+    }
+    __syncthreads();
+    const float sc = 1.0f / (float)N;
+    float* head = p.thead + (s * p.ntiles + tile) * 6 * L;
+    float* outp = p.out + s * p.out_stride + (long)l0r * L;
+    const float* ytd = reinterpret_cast<const float*>(s_y);
+    if (tid < L) {
+        const int u = tid;
+        float st0 = 0.f, st1 = 0.f, st2 = 0.f;
+        for (int jj = 0; jj < jt; ++jj) {
+            const float* yf = ytd + (size_t)jj * 2 * N + u;
+            const float y0 = yf[0] * sc, y1 = yf[L] * sc, y2 = yf[2 * L] * sc, y3 = yf[3 * L] * sc;
+            const float o = 0.5f * (y0 + st0);
+            st0 = st1 + y1;
+            st1 = st2 + y2;
+            st2 = y3;
+            if (jj >= 3) {
+                outp[(long)jj * L + u] = o;
+            } else if (jj == 0) {
+                head[0 * L + u] = y0;
+                head[1 * L + u] = y1;
+                head[2 * L + u] = y2;
+            } else if (jj == 1) {
+                head[3 * L + u] = y0;
+                head[4 * L + u] = y1;
+            } else {
+                head[5 * L + u] = y0;
+            }
+        }
+        float* stt = p.tstate + (s * p.ntiles + tile) * 3 * L;
+        stt[u] = st0;
+        stt[L + u] = st1;
+        stt[2 * L + u] = st2;
+    }
+}
+
 // ============================================================================ bank pass
 // K3 for bank engines with a per-hop schedule (C3, C5: every lane picks a bank entry every hop,
 // so no filter spectrum is reused across the hops of a tile; engine.cpp:85-92 with the set
@@ -862,6 +1140,24 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
         wide_forward_kernel<NC><<<(unsigned)grid, 256, smem, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
+    if ((parts & 2) && p.period_smem) {
+        if constexpr (NC == 512 || NC == 1024) {
+            if (JH != 4 || !p.tile_ir) return cudaErrorInvalidValue;
+            auto kern = wide_period_kernel<NC, 4>;
+            constexpr size_t smem = PeriodLayout<NC>::total;
+            if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+                cudaSuccess)
+                return err;
+            if (t0) cudaEventRecord(t0, stream);
+            kern<<<dim3((unsigned)p.ntiles, (unsigned)p.S), NC / 2, smem, stream>>>(p);
+            if ((err = cudaGetLastError()) != cudaSuccess) return err;
+            if (t1) cudaEventRecord(t1, stream);
+            wide_fixup_kernel<<<grid_cap((long)p.S * p.E * p.ntiles * p.L, 256), 256, 0, stream>>>(p);
+            return cudaGetLastError();
+        } else {
+            return cudaErrorInvalidValue;
+        }
+    }
     if (parts & 2) {
         auto kern = JH == 8 ? wide_mac_kernel<NC, 8> : wide_mac_kernel<NC, 4>;
         const size_t smem = WideLayout(NC, 2 * JH, p.M, p.Q).total;
@@ -940,6 +1236,11 @@ int wide_mac_ctas_per_sm(int L, int JH, int M, int Q) {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess) return 0;
     return per_sm;
+}
+
+bool period_kernel_supported(int L, int M, int JH, long ir_len) {
+    const int N = 2 * L;
+    return (N == 512 || N == 1024) && JH == 4 && M % (N / 64) == 0 && ir_len % 4 == 0;
 }
 
 bool wide_supported(int L) {

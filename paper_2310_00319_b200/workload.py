@@ -169,12 +169,17 @@ def bytes_per_hop(cfg: Config, distinct_filters: Optional[float] = None, mix_out
     return 8 * B * M * S + 8 * B * M * E * F + 8 * B * S + 4 * L * S + 4 * L * O + 48 * L * cfg.lanes
 
 
-def flops_per_hop(cfg: Config) -> float:
-    """MAC + forward/inverse FFT flops per hop (reference cost model, cost.cpp:34-38)."""
+def flops_per_hop(cfg: Config, with_switches: bool = True) -> float:
+    """MAC + forward/inverse FFT flops per hop (reference cost model, cost.cpp:34-38), plus — for
+    the fresh-IR configs — the filter partition transforms of the switches (partition.cpp:20-51:
+    M transforms of the same size per lane and switch, spread over the period)."""
     L, M = cfg.hop, cfg.partitions
     B = 2 * L + 1
     fft = (5 * np.log2(2 * L) + 14) * 2 * L
-    return cfg.lanes * 8 * B * M + (cfg.sources + cfg.lanes) * fft
+    f = cfg.lanes * 8 * B * M + (cfg.sources + cfg.lanes) * fft
+    if with_switches and cfg.mode == "fresh":
+        f += cfg.lanes * M * fft / cfg.period
+    return f
 
 
 def gen_pink(seed: int, n: int) -> np.ndarray:
