@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
 
 #include "tvolap_fft.cuh"
 #include "tvolap_internal.cuh"
@@ -593,12 +594,14 @@ __global__ void __launch_bounds__(256, 2) wide_mac_kernel(const WideParams p) {
 template <int NC>
 struct PeriodLayout {
     static constexpr int N = NC, NT = NC / 2, G = NT / 32;
-    static constexpr size_t pk = 0;
-    static constexpr size_t spec = (((size_t)(N + 2) * 8) + 15) & ~size_t(15);  // G spectra rows (Y, K5 buffers later)
-    static constexpr size_t stage = spec + (size_t)G * N * 8;                   // G x 2L IR taps
-    static constexpr size_t auxx = stage + (size_t)G * N * 4;                   // [2][G + 8] Im X[.][0]
-    static constexpr size_t auxr = auxx + 2 * (G + 8) * 4;                      // [16] running Nyquist sums
-    static constexpr size_t bar = (auxr + 16 * 4 + 15) & ~size_t(15);
+    static constexpr size_t a16c(size_t x) { return (x + 15) & ~size_t(15); }
+    static constexpr size_t pk = 0;                                  // N + 2 pack phasors
+    static constexpr size_t tw4 = a16c((size_t)(N + 2) * 8);        // N + 32 four-step twiddles
+    static constexpr size_t spec = a16c(tw4 + (size_t)(N + 32) * 8);  // G spectra rows (Y, K5 buffers later)
+    static constexpr size_t stage = spec + (size_t)G * N * 8;       // G x 2L IR taps
+    static constexpr size_t auxx = stage + (size_t)G * N * 4;       // [2][G + 8] Im X[.][0]
+    static constexpr size_t auxr = auxx + 2 * (G + 8) * 4;          // [16] running Nyquist sums
+    static constexpr size_t bar = a16c(auxr + 16 * 4);
     static constexpr size_t total = bar + 16;
 };
 
@@ -617,13 +620,26 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
 // one thread: bytes (multiple of 16, 16-byte aligned both ends) global -> shared, completion on bar
 __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic reads of dst are done
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic accesses of dst are done
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+
+#ifndef TVOLAP_PERIOD_KP
+#define TVOLAP_PERIOD_KP 12  // period-tile MAC: X rows in flight per thread (JH + KP divides the group)
+#endif
+
+// f(integral_constant<int, u>) for u = 0 .. n - 1, fully unrolled
+template <class F, int... us>
+__device__ __forceinline__ void unroll_steps(F&& f, std::integer_sequence<int, us...>) {
+    (f(std::integral_constant<int, us>{}), ...);
 }
 
 template <int NC, int JH>
@@ -633,12 +649,14 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
     static_assert(J <= G && JH % KPF == 0 && G % JH == 0, "period tile geometry");
     extern __shared__ __align__(16) unsigned char smem[];
     float2* s_pk = reinterpret_cast<float2*>(smem + Lay::pk);
+    float2* s_tw4 = reinterpret_cast<float2*>(smem + Lay::tw4);
     float2* s_spec = reinterpret_cast<float2*>(smem + Lay::spec);
     float* s_stage = reinterpret_cast<float*>(smem + Lay::stage);
     float* s_auxx = reinterpret_cast<float*>(smem + Lay::auxx);
     float* s_auxr = reinterpret_cast<float*>(smem + Lay::auxr);
     const unsigned bar = (unsigned)__cvta_generic_to_shared(smem + Lay::bar);
     const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(s_stage);
+    const unsigned spec_sa = (unsigned)__cvta_generic_to_shared(s_spec);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tile = blockIdx.x;
     const long s = blockIdx.y;
@@ -646,22 +664,31 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
     const long l0 = p.hop0 + l0r;
     const int M = p.M;
     const int groups = M / G;
-    // tiles before the call's first switch use the engine's active set in place (global memory)
+    // Tiles before the call's first switch use the engine's active set: its group spectra are
+    // bulk-copied into the spectra rows instead of being transformed.
     const float* tir = p.tile_ir[tile];
     const float* h = tir ? tir + s * p.ir_len : nullptr;
     const float2* hset = tir ? nullptr : (p.fset_per_lane ? p.fset[(long)tile * p.S + s] : p.fset[tile] + s * M * N);
-    // taps of group q: [q G N, (q + 1) G N) clipped to the IR; the rest of the staging row is zero
+    // IR taps of group q: [q G N, (q + 1) G N) clipped to the IR; the rest of the staging row is zero
     auto group_bytes = [&](int q) -> unsigned {
         const long a = (long)q * G * N, b = min((long)(q + 1) * G * N, p.ir_len);
         return b > a ? (unsigned)((b - a) * 4) : 0u;
     };
+    auto fetch = [&](int q) {  // one thread: the bytes group q needs, completion on bar
+        if (h) {
+            const unsigned nb = group_bytes(q);
+            if (nb) bulk_g2s(stage_sa, h + (long)q * G * N, nb, bar);
+            else mbar_arrive(bar);
+        } else {
+            bulk_g2s(spec_sa, hset + (size_t)q * G * N, (unsigned)(G * N * sizeof(float2)), bar);
+        }
+    };
     for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    for (int i = tid; i < N + 32; i += NT) s_tw4[i] = p.tw[N + i];
     if (tid < 16) s_auxr[tid] = 0.f;
-    if (tid == 0 && h) {
+    if (tid == 0) {
         mbar_init(bar, 1);
-        const unsigned b0 = group_bytes(0);
-        if (b0) bulk_g2s(stage_sa, h, b0, bar);
-        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+        fetch(0);
     }
     __syncthreads();
 
@@ -672,35 +699,34 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
         X[g] = p.xe + (s * 2 + ((l0 + g) & 1)) * p.T * N;
         bse[g] = ((l0 + g) >> 1) - p.tbase;  // slot of output i at partition m: bse + i - m
     }
-    float2 acc[2][2][JH];  // [bin b][parity g][output i]
+    float4 acc[2][JH];  // [parity g][output i]: bins 2 tid, 2 tid + 1
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int g = 0; g < 2; ++g)
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-            for (int i = 0; i < JH; ++i) acc[b][g][i] = make_float2(0.f, 0.f);
+        for (int i = 0; i < JH; ++i) acc[g][i] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     for (int q = 0; q < groups; ++q) {
         const int mu0 = q * G;
-        // ---- K4 of partitions mu0 .. mu0 + G - 1 (partition.cpp:20-51): warp w, partition mu0 + w
-        const float2* hg = h ? s_spec : hset + (size_t)mu0 * N;  // the group's spectra rows
+        mbar_wait(bar, (unsigned)(q & 1));
         if (h) {
-            mbar_wait(bar, (unsigned)(q & 1));
-            const unsigned nb = group_bytes(q);
+            // ---- K4 of partitions mu0 .. mu0 + G - 1 (partition.cpp:20-51): warp w, partition
+            // mu0 + w, from the staged taps; the warp four-step FFT + in-place untangle
             const float* src = s_stage + (size_t)warp * N;
-            const long valid = (long)nb / 4 - (long)warp * N;  // taps of this partition present in staging
+            const long valid = (long)group_bytes(q) / 4 - (long)warp * N;  // taps of this partition staged
             float2* row = s_spec + (size_t)warp * N;
-            fft_warp4<false, N, true>(row, p.tw + N, lane, [&](int, int n) -> float2 {
-                const long i0 = 2 * n;
-                return make_float2(i0 < valid ? src[i0] : 0.f, i0 + 1 < valid ? src[i0 + 1] : 0.f);
-            });
+            if (valid >= N) {
+                fft_warp4<false, N, true>(row, s_tw4, lane, [&](int, int n) -> float2 {
+                    return *reinterpret_cast<const float2*>(src + 2 * n);
+                });
+            } else {
+                fft_warp4<false, N, true>(row, s_tw4, lane, [&](int, int n) -> float2 {
+                    const long i0 = 2 * n;
+                    return make_float2(i0 < valid ? src[i0] : 0.f, i0 + 1 < valid ? src[i0 + 1] : 0.f);
+                });
+            }
             untangle_pairs_inplace_warp(row, N, s_pk, lane);
-        }
-        __syncthreads();  // spectra of the group ready; staging consumed
-        if (h && tid == 0 && q + 1 < groups) {
-            const unsigned b1 = group_bytes(q + 1);
-            if (b1) bulk_g2s(stage_sa, h + (long)(q + 1) * G * N, b1, bar);
-            else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+            __syncthreads();  // spectra of the group ready; staging consumed
+            if (tid == 0 && q + 1 < groups) fetch(q + 1);  // overlaps this group's MAC
         }
         // Nyquist terms of packed bin 0 (warp 0): Im X[g][t][0] of the group's window into shared memory
         if (warp == 0) {
@@ -709,64 +735,51 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
                 s_auxx[g * (G + 8) + jj] = __ldcg(X[g] + (bse[g] - mu0 - (G - 1) + jj) * N).y;
             }
         }
-        // ---- K3 over the group: bins k_b = tid + b NT
+        // ---- K3 over the group (engine.cpp:85-92), filter rows from shared memory; a thread owns the
+        // bin pair (2 tid, 2 tid + 1): one 16-byte load per operand row. The two parities run one
+        // after the other (the filter rows are read twice from shared memory), so the window (JH
+        // rows) and the loads in flight (KPF rows ahead) of one parity fit the register budget; the
+        // m loop is unrolled by JH + KPF, one full turn of the window + prefetch registers, so the
+        // rotation costs no moves.
         {
-            float2 win[2][2][JH], fx[KPF][2][2];
-            const float2* px[2];
+            constexpr int V = N / 2, KP = TVOLAP_PERIOD_KP < G - JH ? TVOLAP_PERIOD_KP : G - JH, U = JH + KP;  // float4 per row; prefetch depth; unroll
+            static_assert(G % U == 0, "period tile: the group must hold whole unrolled turns");
+            const float4* hrow = reinterpret_cast<const float4*>(s_spec) + tid;
+            auto parity = [&](auto g_tag) {
+                constexpr int g = decltype(g_tag)::value;
+                const float4* xg = reinterpret_cast<const float4*>(X[g]) + tid;
+                float4 win[JH], fx[KP];
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                px[g] = X[g] + (bse[g] - mu0 - 1) * N + tid;
+                for (int i = 0; i < JH; ++i) win[i] = __ldcg(xg + (bse[g] + i - mu0) * V);
+                // step m needs slot bse - m - 1 (the window's next entry); loads run KP steps ahead and
+                // past the group read the next slots down (Xe front padding at the last group), unused
+                const float4* px = xg + (bse[g] - mu0 - 1) * V;
 #pragma unroll
-                for (int b = 0; b < 2; ++b)
+                for (int k = 0; k < KP; ++k) fx[k] = __ldcg(px - (long)k * V);
+                auto step = [&](auto u_tag, int mm) {
+                    constexpr int u = decltype(u_tag)::value, sl = u % KP;
+                    const float4 hv = hrow[(size_t)(mm + u) * V];
 #pragma unroll
-                    for (int i = 0; i < JH; ++i) win[b][g][i] = __ldcg(X[g] + (bse[g] + i - mu0) * N + tid + b * NT);
-            }
-#pragma unroll
-            for (int u = 0; u < KPF; ++u)
-#pragma unroll
-                for (int g = 0; g < 2; ++g)
-#pragma unroll
-                    for (int b = 0; b < 2; ++b) fx[u][g][b] = __ldcg(px[g] - (long)u * N + b * NT);
-            const float2* hrow = hg + tid;
-            auto step = [&](auto u_tag, int mm) {
-                constexpr int u = decltype(u_tag)::value, sl = u % KPF;
-                const float2 hv[2] = {hrow[(size_t)mm * N], hrow[(size_t)mm * N + NT]};
-#pragma unroll
-                for (int b = 0; b < 2; ++b)
-#pragma unroll
-                    for (int g = 0; g < 2; ++g)
-#pragma unroll
-                        for (int i = 0; i < JH; ++i) {
-                            float2& a = acc[b][g][i];
-                            const float2 x = win[b][g][(i - u) & (JH - 1)];
-                            a.x = fmaf(hv[b].x, x.x, a.x);
-                            a.x = fmaf(-hv[b].y, x.y, a.x);
-                            a.y = fmaf(hv[b].x, x.y, a.y);
-                            a.y = fmaf(hv[b].y, x.x, a.y);
-                        }
-#pragma unroll
-                for (int b = 0; b < 2; ++b)
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) win[b][g][(JH - 1 - u) & (JH - 1)] = fx[sl][g][b];
-                // slot bse - mu0 - 1 - (mm + KPF): past the group it reads the next slots down
-                // (Xe front padding at the last group), never used
-#pragma unroll
-                for (int g = 0; g < 2; ++g)
-#pragma unroll
-                    for (int b = 0; b < 2; ++b) fx[sl][g][b] = __ldcg(px[g] - (long)(mm + KPF) * N + b * NT);
+                    for (int i = 0; i < JH; ++i) {
+                        float4& a = acc[g][i];
+                        const float4 x = win[(i - u) & (JH - 1)];
+                        a.x = fmaf(hv.x, x.x, a.x);
+                        a.x = fmaf(-hv.y, x.y, a.x);
+                        a.y = fmaf(hv.x, x.y, a.y);
+                        a.y = fmaf(hv.y, x.x, a.y);
+                        a.z = fmaf(hv.z, x.z, a.z);
+                        a.z = fmaf(-hv.w, x.w, a.z);
+                        a.w = fmaf(hv.z, x.w, a.w);
+                        a.w = fmaf(hv.w, x.z, a.w);
+                    }
+                    win[(JH - 1 - u) & (JH - 1)] = fx[sl];
+                    fx[sl] = __ldcg(px - (long)(mm + u + KP) * V);
+                };
+                for (int mm = 0; mm < G; mm += U)
+                    unroll_steps([&](auto u_tag) { step(u_tag, mm); }, std::make_integer_sequence<int, U>{});
             };
-            for (int mm = 0; mm < G; mm += JH) {
-                step(std::integral_constant<int, 0>{}, mm);
-                step(std::integral_constant<int, 1>{}, mm + 1);
-                step(std::integral_constant<int, 2>{}, mm + 2);
-                step(std::integral_constant<int, 3>{}, mm + 3);
-                if constexpr (JH == 8) {
-                    step(std::integral_constant<int, 4>{}, mm + 4);
-                    step(std::integral_constant<int, 5>{}, mm + 5);
-                    step(std::integral_constant<int, 6>{}, mm + 6);
-                    step(std::integral_constant<int, 7>{}, mm + 7);
-                }
-            }
+            parity(std::integral_constant<int, 0>{});
+            parity(std::integral_constant<int, 1>{});
         }
         if (warp == 0) {
             __syncwarp();
@@ -774,11 +787,12 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
                 const int g = lane / JH, i = lane % JH;
                 float a = s_auxr[lane];
                 for (int mm = 0; mm < G; ++mm)
-                    a = fmaf(hg[(size_t)mm * N].y, s_auxx[g * (G + 8) + (G - 1) + i - mm], a);
+                    a = fmaf(s_spec[(size_t)mm * N].y, s_auxx[g * (G + 8) + (G - 1) + i - mm], a);
                 s_auxr[lane] = a;
             }
         }
         __syncthreads();  // every read of the group's spectra done
+        if (!h && tid == 0 && q + 1 < groups) fetch(q + 1);  // copied spectra: the rows are free only now
     }
 
     // ---- Y rows jj = g + 2 i into shared memory (rows 0 .. J - 1), packed bin 0 fixed up
@@ -788,16 +802,13 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
 #pragma unroll
         for (int i = 0; i < JH; ++i) {
             const int jj = g + 2 * i;
-#pragma unroll
-            for (int b = 0; b < 2; ++b) {
-                float2 a = acc[b][g][i];
-                if (b == 0 && tid == 0) {
-                    const float x = s_auxr[g * JH + i];
-                    a.x += x;
-                    a.y = x;
-                }
-                s_y[(size_t)jj * N + tid + b * NT] = a;
+            float4 a = acc[g][i];
+            if (tid == 0) {
+                const float x = s_auxr[g * JH + i];
+                a.x += x;
+                a.y = x;
             }
+            reinterpret_cast<float4*>(s_y + (size_t)jj * N)[tid] = a;
         }
     __syncthreads();
     // ---- K5: tangle + inverse warp FFT over the Y rows
@@ -807,14 +818,14 @@ __global__ void __launch_bounds__(NC / 2, 1) wide_period_kernel(const WideParams
             float2* wb = s_y + (size_t)(J + (jj % J)) * N;
             for (int kk = lane; kk < N; kk += 32) wb[kk] = tangle_packed(yrow, N, kk, s_pk);
             __syncwarp();
-            fft_warp4<true, N, false>(yrow, p.tw + N, lane, [&](int, int n) { return wb[n]; });
+            fft_warp4<true, N, false>(yrow, s_tw4, lane, [&](int, int n) { return wb[n]; });
             __syncwarp();
         }
     } else {  // no room for buffers: two frames per warp, tangled in the transform's loads, in place
         for (int jj = 2 * warp; jj < jt; jj += 2 * (NT / 32)) {  // rows jj, jj + 1 < J (J even)
             float2* rows = s_y + (size_t)jj * N;
             auto ld = [&](int t, int n) { return tangle_packed(rows + (size_t)t * N, N, n, s_pk); };
-            fft_warp4<true, N, false, 2, decltype(ld), true>(rows, p.tw + N, lane, ld);
+            fft_warp4<true, N, false, 2, decltype(ld), true>(rows, s_tw4, lane, ld);
         }
     }
     __syncthreads();
