@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_wide.py tests/test_gpu_period.py tests/test_gpu_configs.py tests/test_gpu_switching.py -x -q > gpurun_out/wide_test.log 2>&1; echo "pytest rc=$?" >> gpurun_out/wide_test.log
+tail -3 gpurun_out/wide_test.log
+timeout 900 python bench.py --config C2 --steps 5 --warmup 3 --latency-hops 0 --no-cpu --no-e2e > gpurun_out/bench_C2_persist.json 2> gpurun_out/bench_C2_persist.err; echo "bench rc=$?"
+python -c "
+import json;d=json.load(open('gpurun_out/bench_C2_persist.json'));r=d['roofline'];print('C2 %.4g'%d['value'], 'avg launch %.3f ms'%r['avg_launch_ms'], r['launches'], d['clocks'])"
