@@ -39,6 +39,8 @@ def _rel(a, b):
     (512, 3, 128 * 1024, 6 * 7, 6, (3,), 2),            # 6-hop periods
     (256, 3, 64 * 512, 8 * 6, 8, (), 1),                # 512-point transforms (G = 8)
     (512, 2, 32 * 1024, 3 * 12, 3, (), 0),              # shortest tile (3 hops)
+    (256, 3, 64 * 512, 16 * 5 + 7, 16, (2,), 1),        # C2 geometry (16-hop periods: wide_mac_kernel's L2 slots)
+    (256, 2, 32 * 512 - 256, 12 * 4, 12, (0,), 2),      # 12-hop periods (wide_mac_kernel)
 ])
 def test_period_tiles_equal_exchange_loop(hop, S, taps, n_hops, period, none_at, pre):
     g = np.random.default_rng(hop + S + taps + period)
@@ -91,6 +93,25 @@ def test_c4_device_path_vs_reference():
     1100 hops (ring of 264 slots wrapped, 138 switches) against the reference engine."""
     cfg = W.CONFIGS["C4"]
     S, n, L = 8, 1100, cfg.hop
+    x = torch.from_numpy(W.white(cfg, 0, S, 0, n * L)).cuda()
+    nsw = -(-n // cfg.period)
+    irs = [None] + [torch.from_numpy(np.ascontiguousarray(W.fresh_irs(cfg, k, 0, S)[:, 0, :])).cuda()
+                    for k in range(1, nsw)]
+    eng = T.TvolapEngine(T.partition(W.fresh_irs(cfg, 0, 0, S)[:, 0, :].T, L, cfg.partitions))
+    y = eng.process_switching(x, irs, cfg.period)
+    eng.synchronize()
+    assert eng.wide_passes() >= 1
+    ref = oracle_config(cfg, n, sources=S)
+    err = rel_err(y.cpu().numpy(), ref)
+    assert err <= TOL, err
+
+
+def test_c2_device_path_vs_reference():
+    """C2 as the bench runs it (process_switching on device buffers: the time-parallel pass with K4
+    fused into L2 scratch slots), 6 lanes
+    over 400 hops (25 switches, ring wrapped) against the reference engine."""
+    cfg = W.CONFIGS["C2"]
+    S, n, L = 6, 400, cfg.hop
     x = torch.from_numpy(W.white(cfg, 0, S, 0, n * L)).cuda()
     nsw = -(-n // cfg.period)
     irs = [None] + [torch.from_numpy(np.ascontiguousarray(W.fresh_irs(cfg, k, 0, S)[:, 0, :])).cuda()
