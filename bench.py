@@ -269,8 +269,15 @@ def roofline_block(cfg, summ_path, kern_ms, kern_n, hops_per_launch, distinct, c
     bound = max(sides, key=lambda k: sides[k]["frac"])
     b = sides[bound]
     alg = W.bytes_per_hop(cfg, distinct_filters=distinct)
+    k4 = None
+    if cfg.mode == "fresh":  # the IR-switch path's bytes, reported beside the MAC's
+        B = 2 * cfg.hop + 1
+        k4 = {"bytes_per_hop": cfg.lanes * cfg.partitions * (2 * cfg.hop * 4 + 8 * B) / cfg.period,
+              "note": "lanes x M x (2L taps x 4 B + B bins x 8 B) / period: IR slices read + partition spectra "
+                      "written once per switch (the period tiles keep the spectra on chip, so only the taps move)"}
     return {
         "bound": bound, "achieved": b["achieved"], "peak": b["peak"], "unit": b["unit"], "frac": b["frac"],
+        "switch_k4": k4,
         "traffic": (sides["hbm"]["bytes_per_hop"] * hops_per_launch) if "hbm" in sides else None,
         "sides": sides,
         "kernel": wide,
