@@ -123,3 +123,33 @@ def test_c2_device_path_vs_reference():
     ref = oracle_config(cfg, n, sources=S)
     err = rel_err(y.cpu().numpy(), ref)
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("case", ["taps_not_multiple_of_4", "ir_not_16B_aligned", "bit_identical_mode"])
+def test_period_tiles_fall_back(case):
+    """Where the bulk copies cannot take the IR slices (tap count not a multiple of 4, a set not
+    16-byte aligned) or the caller asked for the hop kernels' transforms (wide_warp_fft = 0), C4
+    geometry runs on wide_mac_kernel instead — same results to fp32 rounding."""
+    hop, S, n, period = 512, 2, 40, 8
+    taps = 64 * 1024 - (2 if case == "taps_not_multiple_of_4" else 0)
+    g = np.random.default_rng(3)
+    irs = []
+    for _ in range(n // period):
+        h = torch.from_numpy(g.standard_normal((S, taps + 1)).astype(np.float32) * 0.02).cuda()
+        irs.append(h[:, 1:] if case == "ir_not_16B_aligned" else h[:, :taps].contiguous())
+    if case == "ir_not_16B_aligned":  # a dense (lanes, taps) view starting one float in
+        flat = torch.from_numpy(g.standard_normal(S * taps + 1).astype(np.float32) * 0.02).cuda()
+        irs = [flat[1:].view(S, taps) for _ in irs]
+    ir0 = g.standard_normal((taps, S)) * 0.02
+    x = torch.from_numpy(g.uniform(-1, 1, (S, n * hop)).astype(np.float32)).cuda()
+    a = T.TvolapEngine(T.partition(ir0, hop))
+    b = T.TvolapEngine(T.partition(ir0, hop))
+    b.set_tuning("wide", 0)
+    if case == "bit_identical_mode":
+        a.set_tuning("wide_warp_fft", 0)
+    ya = a.process_switching(x, irs, period)
+    yb = _loop(b, x, irs, period, hop)
+    a.synchronize()
+    b.synchronize()
+    assert a.wide_passes() >= 1
+    assert _rel(ya, yb) <= 1e-5
