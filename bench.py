@@ -84,7 +84,7 @@ def config_block(cfg, n_hops, world, lanes_per_rank, scaling):
         "l2": f"inputs larger than L2: {total * n_hops * cfg.hop * 4 / 1e6:.0f} MB input + "
               f"{total * cfg.ears * n_hops * cfg.hop * 4 / 1e6:.0f} MB output per step",
         "parallelism": f"{scaling} channel sharding over {world} GPU(s), "
-                       + ("NCCL all-reduce of the stereo mix" if cfg.mix and world > 1 else "no collective"),
+                       + ("cross-GPU stereo mix (see mix_path)" if cfg.mix and world > 1 else "no collective"),
     }
 
 
@@ -320,6 +320,8 @@ def main():
     ap.add_argument("--cpu-hops", type=int, default=0, help="CPU sample hops (default >= 2(2M-1))")
     ap.add_argument("--latency-hops", type=int, default=300,
                     help="single-hop process() calls timed for the p50/p99 per-hop latency (0: skip)")
+    ap.add_argument("--mix", default="p2p", choices=["p2p", "nccl"],
+                    help="C3 cross-GPU mix: fused peer-memory kernels (default) or NCCL all-reduce")
     ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
                     help="engine tuning knob for an A/B run (tvolap_set_default_tuning; DESIGN.md §10)")
     args = ap.parse_args()
@@ -424,9 +426,27 @@ def main():
     log(f"[rank {rank}] {cfg.name}: channels {lane0}..{lane0 + S - 1}, generated {x.numel() * 4 / 1e6:.0f} MB input"
         f"{'' if irs is None else f' + {irs.numel() * 4 / 1e9:.2f} GB IRs'} in {time.time() - t0:.1f} s")
     eng.set_stream(stream.cuda_stream)
-    comm = None
-    if mix is not None and world > 1:  # C3: the partial mixes are summed with NCCL through the C-ABI
-        comm = NcclComm(lib, rank, world, local)
+    comm = grp = None
+    mix_path = None
+    if mix is not None and world > 1:
+        # C3: the fused peer-memory mix (one kernel per rank stores its partial into every rank's
+        # gather buffer over NVLink, rank-ordered sums); NCCL through the C-ABI if IPC is unavailable
+        if args.mix == "p2p":
+            try:
+                grp = shard.MixGroup(local, cfg.ears, H * L)
+            except Exception as ex:  # noqa: BLE001
+                log(f"[rank {rank}] peer-memory mix unavailable ({ex}); using NCCL")
+            ok = torch.tensor([1 if grp is not None else 0], device=dev)
+            torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)  # every rank takes the same path
+            if ok.item() == 1:
+                mix_path = ("peer memory: tvolap_mix_scatter (per-GPU source sum + P2P stores into every rank's "
+                            "gather slot) + rank-ordered tvolap_mix_gather")
+            elif grp is not None:
+                grp.close()
+                grp = None
+        if grp is None:
+            comm = NcclComm(lib, rank, world, local)
+            mix_path = "per-GPU mix kernel + ncclAllReduce (tvolap_mix_allreduce)"
 
     class ChunkTimer:
         """Sum of CUDA-event intervals (engine stream) around the chunks' process_switching calls."""
@@ -464,7 +484,9 @@ def main():
             e.process_switching(xs, [ir_set[k % ir_set.shape[0]] for k in range(n_sw)], cfg.period, out=outs)
         else:
             e.process_hops(xs, out=outs, schedule=sch)
-            if mx is not None and outs.is_cuda:
+            if mx is not None and outs.is_cuda and grp is not None:
+                grp.allreduce(outs, S, H * L, mx, stream.cuda_stream)
+            elif mx is not None and outs.is_cuda:
                 T._check(lib.tvolap_mix_allreduce(local, S, cfg.ears, H * L, ctypes.c_void_p(outs.data_ptr()), H * L,
                                                   ctypes.c_void_p(mx.data_ptr()), H * L,
                                                   ctypes.c_void_p(comm.handle if comm else None),
@@ -628,6 +650,7 @@ def main():
         "roofline": roofline, "e2e": e2e, "latency": latency,
         "realtime_factor": (H * L / W.FS) / (ms_per_step / 1e3),
         "warmup_clock_fill_steps": fill,
+        "mix_path": mix_path,
         "tuning": dict(kv.split("=") for kv in args.tune) or "defaults",
         "path": {"passes_per_step": passes / args.steps,
                  "kind": "bank pass" if (cfg.mode == "bank" and cfg.period == 1 and passes) else
@@ -668,6 +691,8 @@ def main():
         print(json.dumps(line), flush=True)
     if comm:
         comm.close()
+    if grp:
+        grp.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -303,6 +303,26 @@ int tvolap_nccl_comm_init(void** comm_out, int device, int nranks, int rank, con
 int tvolap_nccl_comm_destroy(void* comm);
 
 
+/*
+ * Multi-GPU C3 mix over peer memory (the fused alternative to tvolap_mix_allreduce): one kernel per
+ * rank sums the GPU's sources and stores the partial mix straight into slot `rank` of every rank's
+ * gather buffer (NVLink P2P stores into cudaIpc-mapped peer buffers); a second kernel sums the
+ * slots in rank order, so every rank ends with the bit-identical mix. Setup: every rank creates its
+ * group (its gather buffer + a 64-byte IPC handle), the host distributes the handles (any
+ * transport), every rank opens them. Per pass: tvolap_mix_scatter on every rank; all ranks'
+ * scatters complete (stream sync + a host barrier); tvolap_mix_gather; a host barrier before the
+ * next scatter overwrites the slots. world == 1 needs no handles. Replaces the per-GPU sum +
+ * ncclAllReduce of the reference's single-process mix (audio_buffer.hpp:60-67 summed per GPU).
+ */
+typedef struct tvolap_mix_group tvolap_mix_group;
+int tvolap_mix_group_create(tvolap_mix_group** out, int device, int world, int rank, long ears, long capacity,
+                            char ipc_handle_out[64]);
+int tvolap_mix_group_open(tvolap_mix_group* g, const char* handles /* world x 64 bytes, rank order */);
+int tvolap_mix_scatter(tvolap_mix_group* g, long sources, long samples, const float* out, long out_stride,
+                       void* stream);
+int tvolap_mix_gather(tvolap_mix_group* g, long samples, float* mix, long mix_stride, void* stream);
+int tvolap_mix_group_destroy(tvolap_mix_group* g);
+
 /* ------------------------------------------------------ comparison convolvers
  * The reference's other streaming convolvers (reference.hpp:53-200, reference.cpp:34-320) on the
  * GPU, for switching comparisons against TVOLAP:

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -2292,6 +2293,104 @@ int tvolap_nccl_comm_init(void** comm_out, int device, int nranks, int rank, con
 int tvolap_nccl_comm_destroy(void* comm) {
     if (!comm) return TVOLAP_OK;
     return guarded([&] { nccl_check(nccl().comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy"); });
+}
+
+// ======================================================================= peer-memory mix (C3)
+struct tvolap_mix_group {
+    int device = 0, world = 1, rank = 0;
+    long ears = 0, cap = 0;
+    float* gather = nullptr;               // this rank's [world][ears][cap] slots
+    std::vector<float*> peer;              // every rank's gather buffer in this process's address space
+    std::vector<bool> opened;              // peer[r] came from cudaIpcOpenMemHandle
+    float** d_slots = nullptr;             // device copy of peer[]
+    bool ready = false;
+};
+
+int tvolap_mix_group_create(tvolap_mix_group** out, int device, int world, int rank, long ears, long capacity,
+                            char ipc_handle_out[64]) {
+    if (!out || world < 1 || rank < 0 || rank >= world || ears < 1 || capacity < 1)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "mix group: bad arguments");
+    *out = nullptr;
+    return guarded([&] {
+        require_device(device);
+        auto g = std::make_unique<tvolap_mix_group>();
+        g->device = device;
+        g->world = world;
+        g->rank = rank;
+        g->ears = ears;
+        g->cap = capacity;
+        g->gather = dalloc<float>((size_t)world * ears * capacity);
+        g->peer.assign(world, nullptr);
+        g->opened.assign(world, false);
+        g->peer[rank] = g->gather;
+        g->d_slots = dalloc<float*>((size_t)world);
+        if (ipc_handle_out) {
+            static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+            cudaIpcMemHandle_t hnd;
+            CK(cudaIpcGetMemHandle(&hnd, g->gather));
+            std::memcpy(ipc_handle_out, &hnd, sizeof hnd);
+        }
+        if (world == 1) {
+            CK(cudaMemcpy(g->d_slots, g->peer.data(), sizeof(float*), cudaMemcpyHostToDevice));
+            g->ready = true;
+        }
+        *out = g.release();
+    });
+}
+
+int tvolap_mix_group_open(tvolap_mix_group* g, const char* handles) {
+    if (!g || (!handles && g->world > 1)) return set_err(TVOLAP_ERR_INVALID_INPUT, "mix group: null handles");
+    return guarded([&] {
+        CK(cudaSetDevice(g->device));
+        for (int r = 0; r < g->world; ++r) {
+            if (r == g->rank || g->opened[r]) continue;
+            cudaIpcMemHandle_t hnd;
+            std::memcpy(&hnd, handles + 64 * (size_t)r, sizeof hnd);
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, hnd, cudaIpcMemLazyEnablePeerAccess));  // NVLink P2P when on another GPU
+            g->peer[r] = static_cast<float*>(p);
+            g->opened[r] = true;
+        }
+        CK(cudaMemcpy(g->d_slots, g->peer.data(), sizeof(float*) * g->world, cudaMemcpyHostToDevice));
+        g->ready = true;
+    });
+}
+
+int tvolap_mix_scatter(tvolap_mix_group* g, long sources, long samples, const float* out, long out_stride,
+                       void* stream) {
+    if (!g || !out || sources < 1 || samples < 1 || out_stride < samples)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "mix scatter: bad buffers or sizes");
+    if (samples > g->cap) return set_err(TVOLAP_ERR_INVALID_SIZE, "mix scatter: more samples than the group holds");
+    if (!g->ready) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "mix scatter: peer handles not opened");
+    return guarded([&] {
+        CK(cudaSetDevice(g->device));
+        CK(tvb::launch_mix_scatter(sources, g->ears, samples, out, out_stride, g->d_slots, g->world, g->rank, g->cap,
+                                   (cudaStream_t)stream));
+    });
+}
+
+int tvolap_mix_gather(tvolap_mix_group* g, long samples, float* mix, long mix_stride, void* stream) {
+    if (!g || !mix || samples < 1 || mix_stride < samples)
+        return set_err(TVOLAP_ERR_INVALID_INPUT, "mix gather: bad buffers or sizes");
+    if (samples > g->cap) return set_err(TVOLAP_ERR_INVALID_SIZE, "mix gather: more samples than the group holds");
+    return guarded([&] {
+        CK(cudaSetDevice(g->device));
+        CK(tvb::launch_mix_gather(g->ears, samples, g->gather, g->world, g->cap, mix, mix_stride,
+                                  (cudaStream_t)stream));
+    });
+}
+
+int tvolap_mix_group_destroy(tvolap_mix_group* g) {
+    if (!g) return TVOLAP_OK;
+    return guarded([&] {
+        std::unique_ptr<tvolap_mix_group> own(g);
+        CK(cudaSetDevice(g->device));
+        CK(cudaDeviceSynchronize());
+        for (int r = 0; r < g->world; ++r)
+            if (g->opened[r]) CK(cudaIpcCloseMemHandle(g->peer[r]));
+        CK(cudaFree(g->d_slots));
+        CK(cudaFree(g->gather));
+    });
 }
 
 // ======================================================================= comparison convolvers

@@ -138,6 +138,12 @@ cudaError_t launch_gen_irs(uint64_t seed, long count, const long* lanes, const l
                            const double* t60, double fs, long len, float* out, cudaStream_t stream);
 cudaError_t launch_mix(long sources, long ears, long samples, const float* out, long out_stride, float* mix,
                        long mix_stride, cudaStream_t stream);
+// peer-memory mix: per-GPU source sums stored into slot `rank` of every rank's gather buffer
+// (slots[r] = rank r's buffer [world][ears][cap]), then the rank-ordered sum of the slots
+cudaError_t launch_mix_scatter(long sources, long ears, long samples, const float* out, long out_stride,
+                               float* const* slots, int world, int rank, long cap, cudaStream_t stream);
+cudaError_t launch_mix_gather(long ears, long samples, const float* gather, int world, long cap, float* mix,
+                              long mix_stride, cudaStream_t stream);
 
 // comparison convolvers: OLA / OLS / WOLA block FFT convolution (kind 2/3/4)
 // and the direct-form FIR of "tdc" / "cf-tdc"

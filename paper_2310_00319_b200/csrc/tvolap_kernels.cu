@@ -1424,6 +1424,37 @@ __global__ void mix_kernel(long sources, long ears, long samples, const float* _
     }
 }
 
+// Multi-GPU stereo mix over peer memory (C3), fused: each thread sums this GPU's
+// sources for one (ear, sample) in source order (the mix_kernel order) and stores the partial
+// straight into slot `rank` of every rank's gather buffer — its own and, over NVLink, the peers'
+// (cudaIpc-mapped) — so the reduction's transfer is the kernel's own store stream.
+__global__ void mix_scatter_kernel(long sources, long ears, long samples, const float* __restrict__ out,
+                                   long out_stride, float* const* __restrict__ slots, int world, int rank,
+                                   long cap) {
+    const long total = ears * samples;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const long e = i / samples, t = i % samples;
+        float acc = 0.f;
+        for (long s = 0; s < sources; ++s) acc += out[(s * ears + e) * out_stride + t];
+        const long off = ((long)rank * ears + e) * cap + t;
+        for (int r = 0; r < world; ++r) slots[r][off] = acc;
+    }
+}
+
+// mix[e][t] = sum over ranks, in rank order, of the gathered partials: every rank computes the
+// same sums in the same order, so the mix is bit-identical on all of them (deterministic, unlike
+// a ring all-reduce whose summation order depends on the rank).
+__global__ void mix_gather_kernel(long ears, long samples, const float* __restrict__ gather, int world, long cap,
+                                  float* __restrict__ mix, long mix_stride) {
+    const long total = ears * samples;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const long e = i / samples, t = i % samples;
+        float acc = gather[e * cap + t];
+        for (int r = 1; r < world; ++r) acc += gather[((long)r * ears + e) * cap + t];
+        mix[e * mix_stride + t] = acc;
+    }
+}
+
 int grid_for(long work, int threads) {
     long b = (work + threads - 1) / threads;
     return (int)std::max<long>(1, std::min<long>(b, 148L * 16));
@@ -1816,6 +1847,20 @@ cudaError_t launch_mix(long sources, long ears, long samples, const float* out, 
                        long mix_stride, cudaStream_t stream) {
     mix_kernel<<<grid_for(ears * samples, 256), 256, 0, stream>>>(sources, ears, samples, out, out_stride, mix,
                                                                  mix_stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mix_scatter(long sources, long ears, long samples, const float* out, long out_stride,
+                               float* const* slots, int world, int rank, long cap, cudaStream_t stream) {
+    mix_scatter_kernel<<<grid_for(ears * samples, 256), 256, 0, stream>>>(sources, ears, samples, out, out_stride,
+                                                                         slots, world, rank, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mix_gather(long ears, long samples, const float* gather, int world, long cap, float* mix,
+                              long mix_stride, cudaStream_t stream) {
+    mix_gather_kernel<<<grid_for(ears * samples, 256), 256, 0, stream>>>(ears, samples, gather, world, cap, mix,
+                                                                        mix_stride);
     return cudaGetLastError();
 }
 

@@ -138,6 +138,11 @@ def lib() -> C.CDLL:
             "tvolap_nccl_unique_id": (ip, [vp]),
             "tvolap_nccl_comm_init": (ip, [C.POINTER(vp), ip, ip, ip, vp]),
             "tvolap_nccl_comm_destroy": (ip, [vp]),
+            "tvolap_mix_group_create": (ip, [C.POINTER(vp), ip, ip, ip, lg, lg, vp]),
+            "tvolap_mix_group_open": (ip, [vp, vp]),
+            "tvolap_mix_scatter": (ip, [vp, lg, lg, fp, lg, vp]),
+            "tvolap_mix_gather": (ip, [vp, lg, fp, lg, vp]),
+            "tvolap_mix_group_destroy": (ip, [vp]),
             "tvolap_cmp_create": (ip, [C.POINTER(vp), ip, ip, lg, lg, fp, lg, lg, lg, ip]),
             "tvolap_cmp_destroy": (ip, [vp]),
             "tvolap_cmp_process_hops": (ip, [vp, fp, lg, fp, lg, lg]),
@@ -168,6 +173,7 @@ EXPORTED_SYMBOLS = (
     "tvolap_forward_real tvolap_inverse_real tvolap_mac tvolap_hann_window tvolap_partition "
     "tvolap_gen_white_device tvolap_gen_irs_device tvolap_mix_device tvolap_mix_allreduce tvolap_nccl_unique_id "
     "tvolap_nccl_comm_init tvolap_nccl_comm_destroy "
+    "tvolap_mix_group_create tvolap_mix_group_open tvolap_mix_scatter tvolap_mix_gather tvolap_mix_group_destroy "
     "tvolap_cmp_create tvolap_cmp_destroy tvolap_cmp_process_hops tvolap_cmp_set_filter tvolap_cmp_switch_filter "
     "tvolap_cmp_reset tvolap_cmp_geometry"
 ).split()

@@ -483,3 +483,29 @@ def test_prebuilt_set_exchange_is_o1_and_shared():
     c.process(x[:hop])
     c.exchange_ir(sets[2].taps)
     assert np.array_equal(c.process(x[hop:2 * hop]), ya)
+
+
+def test_mix_group_single_rank_equals_device_mix():
+    """tvolap_mix_group_* with world = 1 (no handles): scatter + rank-ordered gather = tvolap_mix_device,
+    bit for bit (same source order), with a strided output buffer."""
+    import ctypes
+
+    import torch
+
+    from paper_2310_00319_b200 import shard
+
+    g = np.random.default_rng(5)
+    S, E, n = 7, 2, 3000
+    out = torch.from_numpy(g.standard_normal((S * E, n + 16)).astype(np.float32)).cuda()
+    ref = torch.empty((E, n), device="cuda")
+    T._check(T.lib().tvolap_mix_device(0, S, E, n, ctypes.c_void_p(out.data_ptr()), n + 16,
+                                       ctypes.c_void_p(ref.data_ptr()), n, None))
+    grp = shard.MixGroup(0, E, 4096)
+    got = torch.empty((E, n), device="cuda")
+    grp.allreduce(out, S, n, got)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    big = torch.zeros((S * E, 5000), device="cuda")
+    with pytest.raises(T.InvalidSizeError):
+        grp.allreduce(big, S, 5000, torch.empty((E, 5000), device="cuda"))  # more samples than the group holds
+    grp.close()

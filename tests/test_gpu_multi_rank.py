@@ -50,6 +50,13 @@ def _worker(rank, world, port, out_dir):
             shard.mix_allreduce(m)  # gloo here; NCCL (tvolap_mix_allreduce's comm) across GPUs
             if rank == 0:
                 np.save(os.path.join(out_dir, f"{name}_mix.npy"), m.numpy())
+            # the fused peer-memory mix: each rank's kernel stores its partial into both ranks'
+            # gather buffers (cudaIpc-mapped; P2P over NVLink across GPUs), rank-ordered sums
+            grp = shard.MixGroup(0, cfg.ears, N_HOPS * L)
+            pm = torch.empty((cfg.ears, N_HOPS * L), device="cuda")
+            grp.allreduce(y, S, N_HOPS * L, pm)
+            np.save(os.path.join(out_dir, f"{name}_pmix_{rank}.npy"), pm.cpu().numpy())
+            grp.close()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -75,3 +82,16 @@ def test_two_ranks_strong_split_matches_reference(tmp_path):
         if cfg.mix:
             mref = ref.reshape(total, cfg.ears, -1).sum(0)
             assert rel_err(np.load(tmp_path / f"{name}_mix.npy"), mref) <= TOL
+            # peer-memory mix: the same bits on both ranks, = the rank-ordered fp32 sum of the
+            # per-rank source-ordered partials, and within the north-star bound of the reference mix
+            pm = [np.load(tmp_path / f"{name}_pmix_{r}.npy") for r in range(2)]
+            assert np.array_equal(pm[0], pm[1])
+            want = None
+            for r in range(2):
+                lane0, S = (0, total // 2) if r == 0 else (total // 2, total - total // 2)
+                part = np.zeros((cfg.ears, y.shape[1]), np.float32)
+                for s_ in range(lane0, lane0 + S):
+                    part += y[s_ * cfg.ears: (s_ + 1) * cfg.ears]
+                want = part if want is None else want + part
+            assert np.array_equal(pm[0], want)
+            assert rel_err(pm[0], mref) <= TOL
