@@ -368,6 +368,32 @@ private:
     TvolapEngine engine_;
 };
 
+// C3's cross-GPU stereo mix over peer memory (tvolap_mix_group_*): construct on every rank,
+// all-gather handle() (64 bytes per rank, any transport), open(all); per pass scatter() on every
+// rank, a host barrier, gather(), a host barrier. world == 1 needs no open().
+class MixGroup {
+public:
+    MixGroup(int device, int world, int rank, long ears, long capacity) {
+        check(tvolap_mix_group_create(&g_, device, world, rank, ears, capacity, handle_));
+        if (world == 1) check(tvolap_mix_group_open(g_, nullptr));
+    }
+    ~MixGroup() { tvolap_mix_group_destroy(g_); }
+    MixGroup(const MixGroup&) = delete;
+    MixGroup& operator=(const MixGroup&) = delete;
+    const char* handle() const { return handle_; }
+    void open(const char* all_handles) { check(tvolap_mix_group_open(g_, all_handles)); }
+    void scatter(long sources, long samples, const float* out, long out_stride, void* stream = nullptr) {
+        check(tvolap_mix_scatter(g_, sources, samples, out, out_stride, stream));
+    }
+    void gather(long samples, float* mix, long mix_stride, void* stream = nullptr) {
+        check(tvolap_mix_gather(g_, samples, mix, mix_stride, stream));
+    }
+
+private:
+    tvolap_mix_group* g_ = nullptr;
+    char handle_[64] = {};
+};
+
 // reference.cpp:345-363
 inline std::unique_ptr<StreamingProcessor> make_processor(const std::string& name, const ImpulseResponse& ir,
                                                           Index hop, int device = 0) {
