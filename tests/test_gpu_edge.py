@@ -138,3 +138,20 @@ def test_identity_through_switch_storm_matches_oracle():
         y = eng.process(seg)
         yo = oe.process(seg.astype(np.float32))
         assert np.abs(y - yo).max() <= 1e-4 * max(np.abs(yo).max(), 1.0)
+
+
+@pytest.mark.parametrize("bad", [-1, 3, 2**31 - 1])
+def test_host_schedule_range_checked(bad):
+    """A host schedule with a bank index outside [0, n_bank) is rejected before anything runs
+    (InvalidInputError, the engine state untouched), for small and multi-threaded (>= 4M entry)
+    checks alike."""
+    g = np.random.default_rng(4)
+    bank = g.standard_normal((3, 1, 256)).astype(np.float32)
+    for S, n in ((2, 10), (4096, 1100)):
+        e = T.TvolapBankEngine(bank, 32, S)
+        x = np.zeros((S, n * 32), np.float32)
+        sched = g.integers(0, 3, (n, S)).astype(np.int32)
+        sched[n // 2, S - 1] = bad
+        with pytest.raises(T.InvalidInputError):
+            e.process_hops(x, schedule=sched)
+        assert e.hops_processed() == 0
