@@ -665,15 +665,15 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
                             sizeof(float) * pend[b].kc * L);
             pend[b].h0 = -1;
         };
-        // chunk sizes: full chunks of Kc hops between a ramp up (Kc/64, Kc/16, Kc/4) and a ramp down
-        // (Kc/4, Kc/16, Kc/64), so the first H2D and the last D2H — the only copies no kernel hides —
-        // move small chunks; every other copy overlaps the neighbouring chunk's kernels (a 4x step
-        // keeps that true while a hop's kernels take >= 4x its copies: C5 ~7x, C3 ~5x). Results do
-        // not depend on the split (the passes are split-invariant).
+        // chunk sizes: full chunks of Kc hops between a ramp up (Kc/32 .. Kc/2, doubling) and the
+        // same ramp down, so the first H2D and the last D2H — the only copies no kernel hides — move
+        // small chunks; every other copy overlaps the neighbouring chunk's kernels (a 2x step keeps
+        // that true while a hop's kernels take >= 2x its copies: C5 ~7x, C3 ~2.3x). Results do not
+        // depend on the split (the passes are split-invariant).
         std::vector<long> sizes;
         {
             std::vector<long> ramp;
-            for (long k = Kc / 64; k >= 1 && k < Kc; k *= 4)
+            for (long k = Kc / 32; k >= 1 && k < Kc; k *= 2)
                 if (k >= 16) ramp.push_back(k);
             long rs = 0;
             for (long k : ramp) rs += k;
