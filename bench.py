@@ -618,6 +618,7 @@ def main():
         xsrc = x[:, : nl * L].cpu()
         sch_np = sched.cpu().numpy() if sched is not None else None
         gpu_ms, host_ms = [], []
+        lat_eng.set_profiling(True)  # events around the one-hop kernel launches (engine stream)
         for h in range(nl):
             xin.copy_(xsrc[:, h * L:(h + 1) * L])
             if sch_np is not None:
@@ -632,8 +633,26 @@ def main():
             if h >= 8:
                 host_ms.append((time.perf_counter() - t0h) * 1e3)
                 gpu_ms.append(a.elapsed_time(b))
+        kms, kn = lat_eng.kernel_time()
+        lat_eng.set_profiling(False)
         q = lambda v, p: float(np.percentile(v, p))  # noqa: E731
+        # roofline of the streaming kernel: it reads every channel's M delay-line spectra and M filter
+        # rows each hop (no reuse across hops), HBM-bound; ncu's DRAM bytes per launch over ncu's
+        # (cold) duration, against MEASURED_PEAKS hbm_gbs (profiles/ncu_summary_<cfg>_hop.json)
+        hop_rf = None
+        hs = ROOT / "profiles" / f"ncu_summary_{cfg.name}_hop.json"
+        if hs.exists():
+            hj = json.loads(hs.read_text())
+            ph = hj.get("per_hop", {})
+            if ph.get("dram_bytes") and ph.get("duration_us"):
+                hbm = peaks().get("hbm_gbs") or 6650.0
+                a = ph["dram_bytes"] / (ph["duration_us"] * 1e-6) / 1e9
+                hop_rf = {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm,
+                          "dram_bytes_per_hop": ph["dram_bytes"], "kernel_us_ncu_cold": ph["duration_us"],
+                          "kernel_us_live": 1e3 * kms / kn if kn else None,
+                          "kernel": hj.get("kernel"), "file": f"profiles/{hs.name}"}
         latency = {"hops": len(gpu_ms), "gpu_ms_p50": q(gpu_ms, 50), "gpu_ms_p99": q(gpu_ms, 99),
+                   "kernel_roofline": hop_rf,
                    "host_ms_p50": q(host_ms, 50), "host_ms_p99": q(host_ms, 99),
                    "hop_period_ms": 1e3 * L / W.FS,
                    "streaming_value": S * cfg.ears * L / (statistics.median(host_ms) / 1e3),
