@@ -1245,10 +1245,11 @@ bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride,
     const long J = 2 * JH;
     // (any call of >= 3 hops: the same per-output sums whatever the call / chunk boundaries)
     if (!tvb::bank_pass_supported((int)L, (int)E, JH) || n < 3) return false;
-    // partition groups: the bank slice a group reads stays well inside L2 (<= 40 MB)
+    // partition groups: the fewest whose bank slice stays well inside L2 (<= 40 MB); fewer groups
+    // = fewer partial sums through HBM (C5: Q = 7, 38 MB slices, 1.89e9 vs 1.86e9 with Q = 8 and
+    // 1.77e9 with Q = 4, profiles/r02_ab_bank_q.txt)
     const double bank_bytes = (double)e->n_bank * E * M * N * sizeof(float2);
-    int Q = 1;
-    while (Q < 64 && 2 * Q <= M && bank_bytes / Q > 40e6) Q *= 2;
+    int Q = (int)std::min<long>(std::min<long>(64, M), std::max<long>(1, (long)std::ceil(bank_bytes / 40e6)));
     if (e->bank_pass_q > 0) Q = (int)std::min<long>(e->bank_pass_q, M);
     // hops per pass: extended spectra + partials within the budget
     const long per_hop = (long)(S * N * sizeof(float2) + (size_t)Q * S * E * N * sizeof(float2));
