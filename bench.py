@@ -322,6 +322,9 @@ def main():
                     help="single-hop process() calls timed for the p50/p99 per-hop latency (0: skip)")
     ap.add_argument("--mix", default="p2p", choices=["p2p", "nccl"],
                     help="C3 cross-GPU mix: fused peer-memory kernels (default) or NCCL all-reduce")
+    ap.add_argument("--one-gpu", action="store_true",
+                    help="test harness: every rank on cuda:0 over gloo (the launcher, sharding and mix logic on one GPU)")
+    ap.add_argument("--dump", default="", help="test harness: save each rank's outputs (and mix) as .npy here")
     ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
                     help="engine tuning knob for an A/B run (tvolap_set_default_tuning; DESIGN.md §10)")
     args = ap.parse_args()
@@ -345,12 +348,19 @@ def main():
     for kv in args.tune:
         k, v = kv.split("=")
         T.set_default_tuning(k, int(v))
+    if args.one_gpu:  # test harness: every rank on cuda:0, gloo (NCCL needs a GPU per rank)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev  # device of the tensors the process group reduces
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.one_gpu:
+            dist.init_process_group("gloo")
+            cdev = torch.device("cpu")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     L, M = cfg.hop, cfg.partitions
     H = args.hops or cfg.hops
     n_sw = -(-H // cfg.period)
@@ -436,7 +446,7 @@ def main():
                 grp = shard.MixGroup(local, cfg.ears, H * L)
             except Exception as ex:  # noqa: BLE001
                 log(f"[rank {rank}] peer-memory mix unavailable ({ex}); using NCCL")
-            ok = torch.tensor([1 if grp is not None else 0], device=dev)
+            ok = torch.tensor([1 if grp is not None else 0], device=cdev)
             torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)  # every rank takes the same path
             if ok.item() == 1:
                 mix_path = ("peer memory: tvolap_mix_scatter (per-GPU source sum + P2P stores into every rank's "
@@ -528,6 +538,13 @@ def main():
     elapsed = timer.total() if timer else ev0.elapsed_time(ev1)
     gpu_launches = eng.kernel_launches() - launches0 + (args.steps if mix is not None else 0)
     passes = eng.wide_passes() - wide0
+    if args.dump:  # test harness: this rank's outputs of the timed steps (and the mix)
+        os.makedirs(args.dump, exist_ok=True)
+        np.save(os.path.join(args.dump, f"out_{rank}.npy"), out.cpu().numpy())
+        if mix is not None:
+            np.save(os.path.join(args.dump, f"mix_{rank}.npy"), mix.cpu().numpy())
+        with open(os.path.join(args.dump, f"shard_{rank}.json"), "w") as f:
+            json.dump({"lane0": lane0, "sources": S, "hops": H, "mix_path": mix_path}, f)
     # Per-launch kernel durations: a separate pass of the same steps with CUDA events around the
     # dominant launch on the engine stream (kept out of the timed region above).
     prof_steps = max(1, min(args.steps, 2))
@@ -542,7 +559,7 @@ def main():
     kern_ms, kern_n = eng.kernel_time()
     eng.set_profiling(False)
     prof_elapsed = ptimer.total() if ptimer else ev2.elapsed_time(ev3)
-    elapsed = shard.max_over_ranks(elapsed, dev)
+    elapsed = shard.max_over_ranks(elapsed, cdev)
     ms_per_step = elapsed / args.steps
     total_sources = cfg.sources * (world if args.scaling == "weak" else 1)
     samples_per_step = total_sources * cfg.ears * H * L
@@ -596,7 +613,7 @@ def main():
             eng2.synchronize()
         barrier()
         e2e_s = (time.perf_counter() - tw) / args.steps
-        e2e_s = shard.max_over_ranks(e2e_s, dev)
+        e2e_s = shard.max_over_ranks(e2e_s, cdev)
         same = bool(torch.equal(oh, out.cpu())) if (cfg.mode != "fresh" or n_e2e >= n_sw) else None
         e2e = {"value": samples_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_s * 1e3,
