@@ -193,8 +193,15 @@ struct tvolap_engine {
     const tvolap_set* active_ext = nullptr;
     const tvolap_set* pending_ext = nullptr;
     float *win = nullptr, *hist = nullptr, *ola = nullptr;
-    int* d_sel = nullptr;
+    int* d_sel = nullptr;            // [S] latched selection | [S] sources sorted by it (d_sel + S)
     std::vector<int> sel, staged;
+    int* h_sel[2] = {};              // pinned host staging of d_sel's two halves (alternating;
+    cudaEvent_t ev_sel[2] = {};      // a pageable 32 KB upload costs ~25 us per hop, pinned ~7)
+    int sel_next = 0;
+    bool sel_dirty = false;          // `sel` not yet uploaded: done right before the next hop launch,
+                                     // after the call's input copy is queued (host sort off the path)
+    bool order_valid = false;        // d_sel + S holds the order of the current selection
+    long entry_order = 1;            // "entry_order": one-hop kernel visits sources grouped by entry
     bool sel_staged = false;
     int active = 0;
     bool pending = false;
@@ -303,9 +310,11 @@ struct tvolap_engine {
             if (p) cudaFree(p);
         for (float* p : {h_in[0], h_in[1], h_out[0], h_out[1]})
             if (p) cudaFreeHost(p);
+        for (int* p : {h_sel[0], h_sel[1]})
+            if (p) cudaFreeHost(p);
         for (cudaEvent_t ev : {ev_side, ev_main, ev_start, ev_in[0], ev_in[1], ev_k[0], ev_k[1], ev_o[0], ev_o[1],
                                 ev_slot[0], ev_slot[1], ev_slot[2], ev_up[0], ev_up[1], ev_up[2], ev_up[3],
-                                ev_used[0], ev_used[1], ev_used[2], ev_used[3]})
+                                ev_used[0], ev_used[1], ev_used[2], ev_used[3], ev_sel[0], ev_sel[1]})
             if (ev) cudaEventDestroy(ev);
         for (auto& pr : prof_events) {
             cudaEventDestroy(pr.first);
@@ -421,7 +430,8 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     for (cudaEvent_t* ev : {&e->ev_side, &e->ev_main, &e->ev_start, &e->ev_in[0], &e->ev_in[1], &e->ev_k[0],
                             &e->ev_k[1], &e->ev_o[0], &e->ev_o[1], &e->ev_slot[0], &e->ev_slot[1],
                             &e->ev_slot[2], &e->ev_up[0], &e->ev_up[1], &e->ev_up[2], &e->ev_up[3],
-                            &e->ev_used[0], &e->ev_used[1], &e->ev_used[2], &e->ev_used[3]})
+                            &e->ev_used[0], &e->ev_used[1], &e->ev_used[2], &e->ev_used[3], &e->ev_sel[0],
+                            &e->ev_sel[1]})
         CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     Tables t(e->N);
     std::vector<float> w = hann(hop);
@@ -440,8 +450,9 @@ void init_common(tvolap_engine* e, int device, long hop, long sources, long ears
     CK(cudaMemsetAsync(e->ola, 0, (size_t)e->S * e->E * 3 * e->L * sizeof(float), e->stream));
     e->sel.assign(e->S, 0);
     e->staged.assign(e->S, 0);
-    e->d_sel = dalloc<int>(e->S);
+    e->d_sel = dalloc<int>(2 * e->S);
     CK(cudaMemsetAsync(e->d_sel, 0, sizeof(int) * e->S, e->stream));
+    for (int b = 0; b < 2; ++b) CK(cudaMallocHost(&e->h_sel[b], sizeof(int) * 2 * e->S));
     apply_default_tuning(e);
     pick_launch_config(e);
     validate_launch(e, e->P, e->NT);
@@ -459,6 +470,38 @@ const float* stage_ir(tvolap_engine* e, const float* ir, size_t count, cudaStrea
     }
     CK(cudaMemcpyAsync(e->d_irstage, ir, count * sizeof(float), cudaMemcpyHostToDevice, s));
     return e->d_irstage;
+}
+
+// Upload a host selection with the sources sorted by it (a stable counting sort over the bank
+// entries): the one-hop kernel runs the sources that share an entry in adjacent clusters, so each
+// selected filter is read from HBM about once per hop instead of once per source using it.
+// Row-pitched copy; one contiguous copy when neither side has gaps between rows (one-hop calls on
+// dense [lanes][L] buffers: 4096 rows of 128 B as one 512 KB DMA instead of 4096 descriptors).
+cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                      cudaMemcpyKind kind, cudaStream_t st) {
+    if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, st);
+    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, st);
+}
+
+void upload_selection(tvolap_engine* e, const int* sel) {
+    const long S = e->S;
+    e->sel_dirty = false;
+    const int hb = e->sel_next;
+    e->sel_next ^= 1;
+    CK(cudaEventSynchronize(e->ev_sel[hb]));  // the upload that last read this buffer is done
+    int* buf = e->h_sel[hb];
+    std::memcpy(buf, sel, sizeof(int) * S);
+    e->order_valid = e->entry_order != 0;
+    if (e->order_valid) {
+        std::vector<int> start(e->n_bank + 1, 0);
+        for (long s = 0; s < S; ++s) ++start[sel[s] + 1];
+        for (long b = 0; b < e->n_bank; ++b) start[b + 1] += start[b];
+        int* order = buf + S;
+        for (long s = 0; s < S; ++s) order[start[sel[s]]++] = (int)s;
+    }
+    CK(cudaMemcpyAsync(e->d_sel, buf, sizeof(int) * (e->order_valid ? 2 : 1) * S, cudaMemcpyHostToDevice,
+                       e->stream));
+    CK(cudaEventRecord(e->ev_sel[hb], e->stream));
 }
 
 void latch(tvolap_engine* e) {  // engine.cpp:54-58
@@ -490,8 +533,8 @@ void latch(tvolap_engine* e) {  // engine.cpp:54-58
         e->pending = false;
     }
     if (e->sel_staged) {
-        CK(cudaMemcpyAsync(e->d_sel, e->staged.data(), sizeof(int) * e->S, cudaMemcpyHostToDevice, e->stream));
         e->sel = e->staged;
+        e->sel_dirty = true;
         e->sel_staged = false;
     }
 }
@@ -535,11 +578,14 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     p.ring = e->ring;
     p.pool = e->active_ext ? e->active_ext->spec : e->pool;
     if (e->bank && !sched) {  // bank engines without a per-hop schedule: the latched selection
+        if (e->sel_dirty) upload_selection(e, e->sel.data());
         sched = e->d_sel;
         sched_stride = 0;
     }
     p.sched = sched;
     p.sched_stride = sched_stride;
+    if (!blocked && e->bank && e->entry_order && e->order_valid && sched == e->d_sel && sched_stride == 0)
+        p.order = e->d_sel + e->S;
     p.entry_base = (e->bank || e->active_ext) ? 0 : e->active * (int)e->S;
     p.hist = e->hist;
     p.ola = e->ola;
@@ -651,9 +697,13 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
         const long kc_max = std::max<long>(1, std::min<long>(n, kc_want));
         ensure_pipeline(e, kc_max, sched && msch != Mem::Device, min == Mem::Pageable || mout == Mem::Pageable);
         const long Kc = e->chunk_hops;
+        // one chunk (one-hop process() calls): nothing to overlap, so the copies go on the engine
+        // stream itself — no cross-stream event hand-offs on the latency path
+        const bool single = n <= Kc;
+        cudaStream_t sh = single ? e->stream : e->h2d, sd = single ? e->stream : e->d2h;
         CK(cudaEventRecord(e->ev_start, e->stream));
-        CK(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
-        CK(cudaStreamWaitEvent(e->d2h, e->ev_start, 0));
+        CK(cudaStreamWaitEvent(sh, e->ev_start, 0));
+        CK(cudaStreamWaitEvent(sd, e->ev_start, 0));
         struct Pend {
             long h0 = -1, kc = 0;
         } pend[2];
@@ -696,29 +746,29 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
                 in_ptr = in + h0 * L;
                 in_s = in_stride;
             } else {
-                CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
+                CK(cudaStreamWaitEvent(sh, e->ev_k[b], 0));
                 if (min == Mem::Pinned) {
-                    CK(cudaMemcpy2DAsync(e->d_in[b], Kc * L * sizeof(float), in + h0 * L, in_stride * sizeof(float),
-                                         kc * L * sizeof(float), S, cudaMemcpyHostToDevice, e->h2d));
+                    CK(copy_rows(e->d_in[b], Kc * L * sizeof(float), in + h0 * L, in_stride * sizeof(float),
+                                         kc * L * sizeof(float), S, cudaMemcpyHostToDevice, sh));
                 } else {
                     CK(cudaEventSynchronize(e->ev_in[b]));
                     for (long r = 0; r < S; ++r)
                         std::memcpy(e->h_in[b] + r * Kc * L, in + r * in_stride + h0 * L, sizeof(float) * kc * L);
                     CK(cudaMemcpyAsync(e->d_in[b], e->h_in[b], sizeof(float) * S * Kc * L, cudaMemcpyHostToDevice,
-                                       e->h2d));
+                                       sh));
                 }
                 in_ptr = e->d_in[b];
                 in_s = Kc * L;
                 copied_in = true;
             }
             if (sched && msch != Mem::Device) {
-                if (!copied_in) CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
-                CK(cudaMemcpyAsync(e->d_sch[b], sched + h0 * S, sizeof(int) * S * kc, cudaMemcpyHostToDevice, e->h2d));
+                if (!copied_in) CK(cudaStreamWaitEvent(sh, e->ev_k[b], 0));
+                CK(cudaMemcpyAsync(e->d_sch[b], sched + h0 * S, sizeof(int) * S * kc, cudaMemcpyHostToDevice, sh));
                 sch_ptr = e->d_sch[b];
                 copied_in = true;
             }
             if (copied_in) {
-                CK(cudaEventRecord(e->ev_in[b], e->h2d));
+                CK(cudaEventRecord(e->ev_in[b], sh));
                 CK(cudaStreamWaitEvent(e->stream, e->ev_in[b], 0));
             }
             float* out_ptr;
@@ -734,37 +784,36 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
             hops_launch(e->hops + h0, kc, in_ptr, in_s, out_ptr, out_s, sch_ptr, sched ? sched + h0 * S : nullptr);
             CK(cudaEventRecord(e->ev_k[b], e->stream));
             if (mout != Mem::Device) {
-                CK(cudaStreamWaitEvent(e->d2h, e->ev_k[b], 0));
+                CK(cudaStreamWaitEvent(sd, e->ev_k[b], 0));
                 if (mout == Mem::Pinned) {
-                    CK(cudaMemcpy2DAsync(out + h0 * L, out_stride * sizeof(float), e->d_out[b], Kc * L * sizeof(float),
-                                         kc * L * sizeof(float), S * E, cudaMemcpyDeviceToHost, e->d2h));
+                    CK(copy_rows(out + h0 * L, out_stride * sizeof(float), e->d_out[b], Kc * L * sizeof(float),
+                                         kc * L * sizeof(float), S * E, cudaMemcpyDeviceToHost, sd));
                 } else {
                     flush_out(b);
                     CK(cudaMemcpyAsync(e->h_out[b], e->d_out[b], sizeof(float) * S * E * Kc * L,
-                                       cudaMemcpyDeviceToHost, e->d2h));
+                                       cudaMemcpyDeviceToHost, sd));
                     pend[b].h0 = h0;
                     pend[b].kc = kc;
                 }
-                CK(cudaEventRecord(e->ev_o[b], e->d2h));
+                CK(cudaEventRecord(e->ev_o[b], sd));
             }
         }
         flush_out(0);
         flush_out(1);
         // later work on the engine stream sees the outputs
-        CK(cudaEventRecord(e->ev_start, e->d2h));
+        CK(cudaEventRecord(e->ev_start, sd));
         CK(cudaStreamWaitEvent(e->stream, e->ev_start, 0));
     }
     if (sched) {  // the last row becomes the current selection
         std::vector<int> last(S);
         if (msch == Mem::Device) {
-            CK(cudaMemcpyAsync(e->d_sel, sched + (n - 1) * S, sizeof(int) * S, cudaMemcpyDeviceToDevice, e->stream));
             CK(cudaMemcpyAsync(last.data(), sched + (n - 1) * S, sizeof(int) * S, cudaMemcpyDeviceToHost, e->stream));
             CK(cudaStreamSynchronize(e->stream));
         } else {
             std::memcpy(last.data(), sched + (n - 1) * S, sizeof(int) * S);
-            CK(cudaMemcpyAsync(e->d_sel, last.data(), sizeof(int) * S, cudaMemcpyHostToDevice, e->stream));
         }
         e->sel = last;
+        e->sel_dirty = true;
     }
     CK(cudaEventRecord(e->ev_main, e->stream));
     e->hops += n;
@@ -1498,7 +1547,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
                 const long hops = std::min(nk * period, n_hops - h0), w = Kp * period * L;
                 // H2D: the chunk's hops and sets, after the launch that last read buffer b
                 if (c >= 2) CK(cudaStreamWaitEvent(e->h2d, e->ev_k[b], 0));
-                CK(cudaMemcpy2DAsync(e->swh_x[b], w * sizeof(float), in + h0 * L, in_lane_stride * sizeof(float),
+                CK(copy_rows(e->swh_x[b], w * sizeof(float), in + h0 * L, in_lane_stride * sizeof(float),
                                      hops * L * sizeof(float), S, cudaMemcpyHostToDevice, e->h2d));
                 // the chunk's sets; runs of sets that are consecutive in host memory (and so in the
                 // staging buffer) go as one copy when they lie in one pinned allocation (the
@@ -1539,7 +1588,7 @@ int tvolap_process_switching(tvolap_engine* e, const float* in, long in_lane_str
                 }
                 CK(cudaEventRecord(e->ev_k[b], e->stream));
                 CK(cudaStreamWaitEvent(e->d2h, e->ev_k[b], 0));
-                CK(cudaMemcpy2DAsync(out + h0 * L, out_lane_stride * sizeof(float), e->swh_y[b], w * sizeof(float),
+                CK(copy_rows(out + h0 * L, out_lane_stride * sizeof(float), e->swh_y[b], w * sizeof(float),
                                      hops * L * sizeof(float), S, cudaMemcpyDeviceToHost, e->d2h));
                 CK(cudaEventRecord(e->ev_o[b], e->d2h));
             }
@@ -1794,6 +1843,7 @@ const Knob kKnobs[] = {
     {"bank_pass_mb", &tvolap_engine::bank_pass_mb, nullptr, 1, 1L << 20, 0},
     {"bank_pass_hops", &tvolap_engine::bank_pass_hops, nullptr, 0, 1L << 30, 0},
     {"bank_pass_q", &tvolap_engine::bank_pass_q, nullptr, 0, 64, 0},
+    {"entry_order", &tvolap_engine::entry_order, nullptr, 0, 1, 0},
     {"pipe_merge", &tvolap_engine::pipe_merge, nullptr, 0, 1, 0},
     {"pipe_mb", &tvolap_engine::pipe_mb, nullptr, 1, 1L << 20, 0},
     {"pipe_log2", &tvolap_engine::pipe_log2, nullptr, 10, 34, 0},

@@ -36,6 +36,10 @@ struct HopParams {
     float2* pool_w;        // writable view of pool
     int new_entry_base;    // pool entry of source 0 for the staged set
     int qm;                // one-hop kernel: partition groups (== the blocked kernel's, for bit-identical sums)
+    // one-hop kernel, bank engines: the source of CTA cluster i is order[i] — sources sorted by
+    // their selected bank entry, so the sources sharing an entry run side by side and its filter
+    // rows come from HBM once per hop (L2 hits for the others); null = source i
+    const int* order = nullptr;
     // switching mode (tvolap_process_switching, hop-blocked set engines): a filter switch may
     // happen every sw_period hops of this launch; switch k (k < sw_count) installs the set
     // sw_irs[k] into pool entry sw_entry[k] (entry of source 0; -1: no switch at k).

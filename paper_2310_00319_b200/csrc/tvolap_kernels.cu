@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int L = NC ? NC / 2 : p.L, N = 2 * L, M = p.M, D = p.D, P = p.P;
     const int tid = threadIdx.x, NT = blockDim.x;
-    const int s = blockIdx.x / P;
+    const int s = p.order ? p.order[blockIdx.x / P] : blockIdx.x / P;
     const int r = blockIdx.x % P;  // == cluster rank (1-D clusters of P consecutive CTAs)
     const SmemLayout lay(L, P, E, p.qm);
     float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);

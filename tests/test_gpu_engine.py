@@ -443,6 +443,29 @@ def test_bank_engine_single_hop_select(S):
         a.select_bank(np.full(S, n_bank, np.int32))
 
 
+@pytest.mark.parametrize("hop,ears,S,n_bank", [(32, 1, 300, 7), (128, 2, 96, 5)])
+def test_bank_engine_entry_order(hop, ears, S, n_bank):
+    """The one-hop kernel visits the sources grouped by their bank entry (tuning entry_order=1,
+    default): only the CTA order changes, so the outputs equal the source-order launch bit for bit,
+    after select_bank and after a schedule call whose last row becomes the selection."""
+    n = 10
+    bank = rnd(n_bank * ears * 900, 27).reshape(n_bank, ears, 900)
+    sched = np.random.default_rng(29).integers(0, n_bank, (2 * n, S)).astype(np.int32)
+    x = rnd(hop * 2 * n, 28, S)
+    ys = []
+    for order in (1, 0):
+        e = T.TvolapBankEngine(bank, hop, S)
+        e.set_tuning("entry_order", order)
+        y = []
+        for h in range(n):
+            e.select_bank(sched[h])
+            y.append(e.process(x[h * hop:(h + 1) * hop]))
+        y.append(e.process_hops(np.ascontiguousarray(x[n * hop:(2 * n - 1) * hop].T), schedule=sched[n:2 * n - 1]).T)
+        y.append(e.process(x[(2 * n - 1) * hop:]))  # the schedule's last row is the latched selection
+        ys.append(np.concatenate(y))
+    assert np.array_equal(ys[0], ys[1])
+
+
 def test_cpp_wrapper():
     """The C++ drop-in (include/tvolap_b200.hpp) runs the reference's engine tests on the GPU:
     tests/cpp/test_wrapper.cpp, built by _build.build() into lib/test_wrapper; exit 0 = PASS."""
