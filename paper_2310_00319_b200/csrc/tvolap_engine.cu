@@ -254,6 +254,9 @@ struct tvolap_engine {
     long bank_pass = 1;              // 0: per-hop schedules stay on the hop-blocked kernel
     long bank_pass_mb = 32768;       // Xe + partials budget per pass
     long bank_pass_hops = 0;         // max hops per pass (0: by the budget)
+    long bank_pass_tpc = 0;          // bank MAC tiles per CTA (0: all tiles of the pass)
+    long k1_small = 1;               // 64-point K1 of the passes with 8 lanes per frame
+    long bank_pass_jh = 0;           // half the hops of a bank-pass tile (0: auto; 8, 16 or 32)
     long bank_pass_q = 0;            // partition groups of the bank pass (0: auto, bank slice <= 40 MB)
     uint64_t wide_passes = 0;
     long pipe_merge = 1;             // "pipe_merge": one H2D copy per run of host-contiguous sets
@@ -1078,6 +1081,7 @@ void wide_pass(tvolap_engine* e, long hop0, const float* in, long in_stride, flo
     p.slot_lock = e->wide_lock;
     p.nslots = nslots;
     p.warp_fft = warp_fft;
+    p.k1_small = (int)e->k1_small;
     p.stage_ir = (int)e->wide_stage;
     p.period_smem = period_smem;
     cudaEvent_t ev0, ev1;
@@ -1290,7 +1294,11 @@ bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride,
                    const int* dsched) {
     const long S = e->S, M = e->M, N = e->N, L = e->L, E = e->E;
     if (!e->bank_pass || !dsched || classify(dsched) != Mem::Device) return false;
-    const int JH = (N <= 128 && E == 1) ? 16 : 8;
+    // tiles of 64 hops (one CTA of 512 threads per SM) where the register budget allows: fewer Xe
+    // window rows per output than 32-hop tiles (C5 1.94e9 -> 1.97e9; -> 2.02e9 with every CTA
+    // walking all tiles of its (source, group), so the window stays in L1: profiles/r02_ab_bank_tpc.txt)
+    int JH = (N <= 128 && E == 1) ? 32 : 8;
+    if (e->bank_pass_jh > 0 && tvb::bank_pass_supported((int)L, (int)E, (int)e->bank_pass_jh)) JH = (int)e->bank_pass_jh;
     const long J = 2 * JH;
     // (any call of >= 3 hops: the same per-output sums whatever the call / chunk boundaries)
     if (!tvb::bank_pass_supported((int)L, (int)E, JH) || n < 3) return false;
@@ -1349,6 +1357,8 @@ bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride,
         p.tstate = e->wide_state;
         p.thead = e->wide_head;
         p.warp_fft = 1;
+        p.k1_small = (int)e->k1_small;
+        p.tpc = e->bank_pass_tpc > 0 ? (int)std::min<long>(e->bank_pass_tpc, ntiles) : (int)ntiles;
         p.pool = e->pool;
         p.sched = dsched + h0 * S;
         p.yq = e->bank_yq;
@@ -1843,6 +1853,9 @@ const Knob kKnobs[] = {
     {"bank_pass_mb", &tvolap_engine::bank_pass_mb, nullptr, 1, 1L << 20, 0},
     {"bank_pass_hops", &tvolap_engine::bank_pass_hops, nullptr, 0, 1L << 30, 0},
     {"bank_pass_q", &tvolap_engine::bank_pass_q, nullptr, 0, 64, 0},
+    {"bank_pass_jh", &tvolap_engine::bank_pass_jh, nullptr, 0, 32, 0},
+    {"k1_small", &tvolap_engine::k1_small, nullptr, 0, 1, 0},
+    {"bank_pass_tpc", &tvolap_engine::bank_pass_tpc, nullptr, 0, 1L << 20, 0},
     {"entry_order", &tvolap_engine::entry_order, nullptr, 0, 1, 0},
     {"pipe_merge", &tvolap_engine::pipe_merge, nullptr, 0, 1, 0},
     {"pipe_mb", &tvolap_engine::pipe_mb, nullptr, 1, 1L << 20, 0},

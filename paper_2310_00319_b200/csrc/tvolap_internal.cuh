@@ -95,6 +95,8 @@ struct WideParams {
     const float2* pool = nullptr;  // bank spectra [n_bank][E][M][2L]
     const int* sched = nullptr;    // bank entry of (pass hop h, source s): sched[h * S + s]
     float2* yq = nullptr;          // MAC partials per partition group [Q][S * E][n][2L]
+    int tpc = 1;                   // bank MAC: consecutive tiles per CTA (L1 reuse of the Xe window)
+    int k1_small = 1;              // 64-point K1 with 8 lanes per frame (wide_forward_small_kernel)
 };
 int wide_mac_ctas_per_sm(int L, int JH, int M, int Q);
 bool wide_supported(int L);

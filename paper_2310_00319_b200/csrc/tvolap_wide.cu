@@ -188,6 +188,99 @@ __global__ void __launch_bounds__(256) wide_forward_warp_kernel(const WideParams
     }
 }
 
+// K1 for 64-point transforms (L = 32: C5), where one warp per frame leaves two points per lane
+// and the transform is all shuffles and index arithmetic (2.4 us per C5 hop against 0.4 us of
+// memory time). Here 8 lanes own a frame (4 frames per warp, 32 consecutive hops of one source
+// per CTA iteration): lane t holds z[8 n1 + t], an 8-point DFT in registers (upper half zero),
+// twiddles W_64^(t k1), an 8 x 8 transpose through shared memory (row stride 9, frame stride 72
+// float2: conflict-free), a second 8-point DFT, the spectrum left in natural order, then every
+// lane untangles 8 bins and stores them as four float4 (spectral.cpp:105-124). Window, twiddles
+// and pack phasors are per-lane constants held in registers.
+__global__ void __launch_bounds__(256) wide_forward_small_kernel(const WideParams p) {
+    constexpr int N = 64, L = 32, FS = 72;
+    __shared__ __align__(16) float2 s_buf[8][4 * FS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, t = lane & 7, fr = lane >> 3;
+    float2* buf = s_buf[warp] + fr * FS;
+    float2 wn[4], twr[8], pkr[8];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) wn[n1] = make_float2(p.win[2 * (8 * n1 + t)], p.win[2 * (8 * n1 + t) + 1]);
+    twr[0] = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int k1 = 1; k1 < 8; ++k1) {  // W_64^(t k1) from the four-step table (W_64^j, j < 32)
+        const int j = t * k1;
+        const float2 w = p.tw[N + 32 + (j & 31)];
+        twr[k1] = (j & 32) ? make_float2(-w.x, -w.y) : w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        pkr[2 * i] = p.pk[2 * (t + 8 * i)];
+        pkr[2 * i + 1] = p.pk[2 * (t + 8 * i) + 1];
+    }
+    const long ring_from = p.hop0 + p.n - 2L * p.D;
+    const int chunks = (p.n + 31) / 32;
+    const long items = (long)p.S * chunks;
+    for (long it = blockIdx.x; it < items; it += gridDim.x) {
+        const long s = it / chunks;
+        const int r = (int)(it - s * chunks) * 32 + warp * 4 + fr;
+        const bool valid = r < p.n;
+        const int rc = min(r, p.n - 1);
+        const float* cur = p.in + s * p.in_stride + (long)rc * L;
+        const float* prev = rc == 0 ? p.hist + s * L : cur - L;
+        float2 v[8];
+#pragma unroll
+        for (int n1 = 0; n1 < 4; ++n1) {  // z_n = (x[2n] w[2n], x[2n+1] w[2n+1]), n = 8 n1 + t < L
+            const float* src = (n1 < 2 ? prev : cur - L) + 2 * (8 * n1 + t);
+            v[n1] = make_float2(src[0] * wn[n1].x, src[1] * wn[n1].y);
+            v[n1 + 4] = make_float2(0.f, 0.f);
+        }
+        dft_reg<false, 8, true>(v);
+#pragma unroll
+        for (int k1 = 1; k1 < 8; ++k1) v[k1] = twmul<false>(v[k1], twr[k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < 8; ++k1) buf[k1 * 9 + t] = v[k1];
+        __syncwarp();
+#pragma unroll
+        for (int n2 = 0; n2 < 8; ++n2) v[n2] = buf[t * 9 + n2];
+        dft_reg<false, 8>(v);
+        __syncwarp();
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) buf[t + 8 * k2] = v[k2];  // Z[k1 + 8 k2], natural order
+        __syncwarp();
+        const long j = p.hop0 + rc;
+        const int par = (int)(j & 1);
+        float4* dst = reinterpret_cast<float4*>(p.xe + ((s * 2 + par) * p.T + ((j >> 1) - p.tbase)) * N);
+        float4* rdst = j >= ring_from ? reinterpret_cast<float4*>(p.ring + ((s * 2 + par) * p.D + (j >> 1) % p.D) * N)
+                                      : nullptr;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j4 = t + 8 * i, k = 2 * j4;
+            float2 a, b;
+            {
+                const float2 zk = buf[k], zm = buf[(N - k) & (N - 1)];
+                if (k == 0) {
+                    a = make_float2(zk.x + zk.y, zk.x - zk.y);
+                } else {
+                    const float2 even = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+                    const float2 odd = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+                    a = cadd(even, cmul(pkr[2 * i], odd));
+                }
+            }
+            {
+                const float2 zk = buf[k + 1], zm = buf[N - k - 1];
+                const float2 even = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+                const float2 odd = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+                b = cadd(even, cmul(pkr[2 * i + 1], odd));
+            }
+            if (valid) {
+                const float4 o = make_float4(a.x, a.y, b.x, b.y);
+                dst[j4] = o;
+                if (rdst) rdst[j4] = o;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // K4 for the sets a call installs: row r = k * S + s transforms irs[k] + s * ir_len into
 // pool[(r * M + m) * N] (partition.cpp:20-51). Same warp transform as partition_warp_kernel.
 template <int NC>
@@ -886,11 +979,14 @@ __global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_m
     static_assert(V4 % 32 == 0 && JH % JO == 0 && JO % KPF == 0 && (JO & (JO - 1)) == 0, "bank MAC geometry");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = warp & 1, o = warp >> 1;
-    const int tile = blockIdx.x;
     const int s = blockIdx.y / CH, f = (blockIdx.y % CH) * 32 + lane;
     const int q = blockIdx.z;
     const int M = p.M, S = p.S;
     const int mq0 = (int)((long)q * M / p.Q), mq1 = (int)((long)(q + 1) * M / p.Q);
+    // a CTA walks `tpc` consecutive tiles of its (source, partition group): the next tile's Xe
+    // window is the previous one's shifted by JH slots, so most of its rows are still in L1
+    const int tile_end = min(p.ntiles, ((int)blockIdx.x + 1) * p.tpc);
+    for (int tile = (int)blockIdx.x * p.tpc; tile < tile_end; ++tile) {
     const int l0r = p.tile0[tile], jt = p.tile0[tile + 1] - l0r;
     const long l0 = p.hop0 + l0r;
     const float4* pool4 = reinterpret_cast<const float4*>(p.pool);
@@ -997,6 +1093,7 @@ __global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_m
             __stcg(yq4 + ((((long)q * S + s) * E + e) * p.n + l0r + jj) * V4 + f, a);
         }
     }
+    }  // tiles of this CTA
 }
 
 // K5 of the bank pass (spectral.cpp:127-158, engine.cpp:94-102): one CTA per (tile, output lane
@@ -1024,8 +1121,15 @@ __global__ void __launch_bounds__(256) bank_k5_kernel(const WideParams p) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
         if (jj < jt) {
             const float4* src = yq4 + (le * p.n + l0r + jj) * V4 + k4;
+            const long qs = lanes * p.n * V4;
             a = __ldcs(src);
-            for (int q = 1; q < p.Q; ++q) a = f4add(a, __ldcs(src + (long)q * lanes * p.n * V4));
+            int q = 1;
+            for (; q + 3 <= p.Q; q += 3) {  // three partials in flight, summed in q order
+                const float4 b0 = __ldcs(src + (long)q * qs), b1 = __ldcs(src + (long)(q + 1) * qs),
+                             b2 = __ldcs(src + (long)(q + 2) * qs);
+                a = f4add(f4add(f4add(a, b0), b1), b2);
+            }
+            for (; q < p.Q; ++q) a = f4add(a, __ldcs(src + (long)q * qs));
         }
         y4[i] = a;
     }
@@ -1040,28 +1144,32 @@ __global__ void __launch_bounds__(256) bank_k5_kernel(const WideParams p) {
     float* head = p.thead + (le * p.ntiles + tile) * 6 * L;
     float* outp = p.out + le * p.out_stride + (long)l0r * L;
     const float* ytd = reinterpret_cast<const float*>(s_y);
-    for (int u = tid; u < L; u += NT) {
-        float st0 = 0.f, st1 = 0.f, st2 = 0.f;
-        for (int jj = 0; jj < jt; ++jj) {
-            const float* yf = ytd + (size_t)jj * 2 * N + u;
-            const float y0 = yf[0] * sc, y1 = yf[L] * sc, y2 = yf[2 * L] * sc, y3 = yf[3 * L] * sc;
-            const float o = 0.5f * (y0 + st0);
-            st0 = st1 + y1;
-            st1 = st2 + y2;
-            st2 = y3;
-            if (jj >= 3) {
-                outp[(long)jj * L + u] = o;
-            } else if (jj == 0) {
-                head[0 * L + u] = y0;
-                head[1 * L + u] = y1;
-                head[2 * L + u] = y2;
-            } else if (jj == 1) {
-                head[3 * L + u] = y0;
-                head[4 * L + u] = y1;
-            } else {
-                head[5 * L + u] = y0;
-            }
+    // hop-2 overlap-add (engine.cpp:94-102) without the serial carry: output jj needs only the
+    // frames jj - 3 .. jj, summed in the carry's order ((y3 + y2) + y1, then y0) — the same
+    // values the running carry gives (a tile has >= 3 hops)
+    for (int idx = tid; idx < jt * L; idx += NT) {
+        const int jj = idx / L, u = idx - jj * L;
+        const float* yf = ytd + (size_t)jj * 2 * N + u;
+        const float y0 = yf[0] * sc;
+        if (jj >= 3) {
+            const float y1 = yf[L - 2 * N] * sc, y2 = yf[2 * L - 4 * N] * sc, y3 = yf[3 * L - 6 * N] * sc;
+            outp[(long)jj * L + u] = 0.5f * (y0 + ((y3 + y2) + y1));
+        } else if (jj == 0) {
+            head[0 * L + u] = y0;
+            head[1 * L + u] = yf[L] * sc;
+            head[2 * L + u] = yf[2 * L] * sc;
+        } else if (jj == 1) {
+            head[3 * L + u] = y0;
+            head[4 * L + u] = yf[L] * sc;
+        } else {
+            head[5 * L + u] = y0;
         }
+    }
+    for (int u = tid; u < L; u += NT) {  // the carry after the tile's last hop
+        const float* yl = ytd + (size_t)(jt - 1) * 2 * N + u;
+        const float st2 = yl[3 * L] * sc;
+        const float st1 = yl[3 * L - 2 * N] * sc + yl[2 * L] * sc;
+        const float st0 = (yl[3 * L - 4 * N] * sc + yl[2 * L - 2 * N] * sc) + yl[L] * sc;
         float* stt = p.tstate + (le * p.ntiles + tile) * 3 * L;
         stt[u] = st0;
         stt[L + u] = st1;
@@ -1126,6 +1234,17 @@ cudaError_t launch_wide_t(const WideParams& p, int JH, cudaStream_t stream, cuda
     if (parts & 1) {
         wide_head_kernel<<<grid_cap((long)p.S * 2 * (p.M + 2) * (NC / 2), 256), 256, 0, stream>>>(p);
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
+        if (p.warp_fft && NC == 64 && p.k1_small) {
+            int per_sm = 0;
+            if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_forward_small_kernel, 256, 0)) !=
+                cudaSuccess)
+                return err;
+            const long items = (long)p.S * ((p.n + 31) / 32);
+            const long grid = std::max<long>(1, std::min<long>(items, (long)sm_count() * std::max(1, per_sm)));
+            wide_forward_small_kernel<<<(unsigned)grid, 256, 0, stream>>>(p);
+            if ((err = cudaGetLastError()) != cudaSuccess) return err;
+            return launch_wide_t<NC>(p, JH, stream, t0, t1, parts & ~1);
+        }
         if (p.warp_fft && NC >= 64 && NC <= 1024) {
             const size_t smem = a16((NC + 2) * sizeof(float2)) + a16(NC * sizeof(float)) + 16 * (size_t)NC * sizeof(float2);
             if ((err = cudaFuncSetAttribute(wide_forward_warp_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1193,7 +1312,7 @@ template <int NC, int E, int JH, int JO>
 cudaError_t launch_bank_mac(const WideParams& p, cudaStream_t stream) {
     constexpr int KPF = 2;
     auto kern = bank_mac_kernel<NC, E, JH, JO, KPF>;
-    const dim3 grid((unsigned)p.ntiles, (unsigned)(p.S * (NC / 64)), (unsigned)p.Q);
+    const dim3 grid((unsigned)((p.ntiles + p.tpc - 1) / p.tpc), (unsigned)(p.S * (NC / 64)), (unsigned)p.Q);
     kern<<<grid, 64 * (JH / JO), 0, stream>>>(p);
     return cudaGetLastError();
 }
@@ -1203,7 +1322,8 @@ cudaError_t launch_bank_pass_t(const WideParams& p, int JH, cudaStream_t stream,
     cudaError_t err = launch_wide_t<NC>(p, 8, stream, nullptr, nullptr, 1);  // head copy + K1 into Xe
     if (err != cudaSuccess) return err;
     if (t0) cudaEventRecord(t0, stream);
-    if (p.E == 1 && JH == 16) err = launch_bank_mac<NC, 1, 16, 4>(p, stream);
+    if (p.E == 1 && JH == 32 && NC <= 128) err = launch_bank_mac<NC, 1, 32, 4>(p, stream);
+    else if (p.E == 1 && JH == 16) err = launch_bank_mac<NC, 1, 16, 4>(p, stream);
     else if (p.E == 1 && JH == 8) err = launch_bank_mac<NC, 1, 8, 4>(p, stream);
     else if (p.E == 2 && JH == 8) err = launch_bank_mac<NC, 2, 8, 2>(p, stream);
     else return cudaErrorInvalidValue;
@@ -1211,6 +1331,8 @@ cudaError_t launch_bank_pass_t(const WideParams& p, int JH, cudaStream_t stream,
     if (t1) cudaEventRecord(t1, stream);
     const size_t smem = a16((NC + 2) * sizeof(float2)) + (size_t)2 * JH * NC * sizeof(float2);
     auto k5 = JH == 16 ? bank_k5_kernel<NC, 16> : bank_k5_kernel<NC, 8>;
+    if constexpr (NC <= 128)
+        if (JH == 32) k5 = bank_k5_kernel<NC, 32>;
     if ((err = cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return err;
     k5<<<dim3((unsigned)p.ntiles, (unsigned)(p.S * p.E)), 256, smem, stream>>>(p);
@@ -1280,7 +1402,7 @@ cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEv
 bool bank_pass_supported(int L, int E, int JH) {
     const int N = 2 * L;
     if (!(N == 64 || N == 128 || N == 256 || N == 512)) return false;
-    return (E == 1 && (JH == 16 || JH == 8)) || (E == 2 && JH == 8);
+    return (E == 1 && (JH == 16 || JH == 8 || (JH == 32 && N <= 128))) || (E == 2 && JH == 8);
 }
 
 cudaError_t launch_bank_pass(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1) {

@@ -37,7 +37,7 @@ def _dev(a):
 
 
 @pytest.mark.parametrize("hop,S,ears,n_bank,taps,n,pre", [
-    (32, 6, 1, 9, 4096, 300, 0),     # C5 shape (N = 64, 16-hop tiles x 2), ring wrapped (M = 64)
+    (32, 6, 1, 9, 4096, 300, 0),     # C5 shape (N = 64, tiles of <= 64 hops), ring wrapped (M = 64)
     (32, 3, 1, 5, 1500, 97, 5),      # ragged tiles, odd start hop after a short call
     (128, 4, 2, 6, 4096, 120, 3),    # C3 shape (N = 256, two ears share the source spectrum)
     (64, 2, 1, 4, 2048, 70, 0),      # N = 128
@@ -130,3 +130,36 @@ def test_bank_pass_tuning_switch():
         e.set_tuning("bank_pass", 7)
     with pytest.raises(T.InvalidInputError):
         e.set_tuning("no_such_knob", 1)
+
+
+def test_bank_pass_tile_geometry_knobs():
+    """Tile size (bank_pass_jh: 16 / 32 / 64-hop tiles) and tiles per MAC CTA (bank_pass_tpc: how
+    many consecutive tiles a CTA walks so its Xe window stays in L1) only regroup the work: the
+    tpc variants are bit-identical, every tile size matches the reference."""
+    hop, S, n_bank, taps, n = 32, 5, 7, 4096, 333
+    bank, x, sched = _case(hop, S, 1, n_bank, taps, n, 51)
+    ref = None
+    outs = {}
+    for jh in (8, 16, 32):
+        for tpc in (1, 2, 0):
+            e = T.TvolapBankEngine(bank, hop, S)
+            e.set_tuning("bank_pass_jh", jh)
+            e.set_tuning("bank_pass_tpc", tpc)
+            assert e.get_tuning("bank_pass_jh") == jh and e.get_tuning("bank_pass_tpc") == tpc
+            y = e.process_hops(_dev(x), schedule=_dev(sched)).cpu().numpy()
+            assert e.wide_passes() >= 1
+            outs[jh, tpc] = y
+            if ref is None:
+                ref = _oracle(bank, x, sched, hop, e.partition_count())
+        assert np.array_equal(outs[jh, 1], outs[jh, 2]) and np.array_equal(outs[jh, 1], outs[jh, 0])
+        err = np.abs(outs[jh, 0] - ref).max() / np.abs(ref).max()
+        assert err <= TOL, (jh, err)
+    assert np.abs(outs[8, 0] - outs[32, 0]).max() <= 2e-6 * np.abs(ref).max()
+    # two-ear engines (C3 geometry) keep 16-hop tiles; the tiles-per-CTA walk applies to them too
+    bank2, x2, sched2 = _case(128, 3, 2, 5, 3000, 90, 52)
+    ys = []
+    for tpc in (1, 0):
+        e = T.TvolapBankEngine(bank2, 128, 3)
+        e.set_tuning("bank_pass_tpc", tpc)
+        ys.append(e.process_hops(_dev(x2), schedule=_dev(sched2)).cpu().numpy())
+    assert np.array_equal(ys[0], ys[1])
