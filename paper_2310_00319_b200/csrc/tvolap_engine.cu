@@ -1311,18 +1311,22 @@ bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride,
     // hops per pass: extended spectra + partials within the budget
     const long per_hop = (long)(S * N * sizeof(float2) + (size_t)Q * S * E * N * sizeof(float2));
     long max_hops = std::max<long>(4 * J, (e->bank_pass_mb << 20) / per_hop);
+    max_hops -= max_hops % J;  // whole tiles per pass
     if (e->bank_pass_hops > 0) max_hops = std::max<long>(2 * J, e->bank_pass_hops);
     for (long h0 = 0; h0 < n;) {
         long nh = std::min(max_hops, n - h0);
         if (n - h0 - nh > 0 && n - h0 - nh < 3) nh -= 3;  // no 1-2 hop pass at the end
-        const long tp = (nh + J - 1) / J, base = nh / tp, rem = nh % tp;  // tiles of 3 .. J hops
+        // full J-hop tiles and one shorter last tile (whose idle MAC warps exit at once); a 1-2 hop
+        // remainder borrows from the tile before it, so every tile has 3 .. J hops
         std::vector<int> t0;
-        for (long w = 0, st = 0; w < tp; ++w) {
+        for (long st = 0; st < nh;) {
             t0.push_back((int)st);
-            st += base + (w < rem ? 1 : 0);
+            long len = std::min<long>(J, nh - st);
+            if (nh - st - len > 0 && nh - st - len < 3) len -= 3 - (nh - st - len);
+            st += len;
         }
         t0.push_back((int)nh);
-        const long ntiles = tp;
+        const long ntiles = (long)t0.size() - 1;
         ensure_dev(e->d_wide_tile0, e->wide_tile_cap, (size_t)ntiles + 1);
         CK(cudaMemcpyAsync(e->d_wide_tile0, t0.data(), sizeof(int) * (ntiles + 1), cudaMemcpyHostToDevice, e->stream));
         ensure_dev(e->wide_state, e->wide_state_cap, (size_t)S * E * ntiles * 3 * L);

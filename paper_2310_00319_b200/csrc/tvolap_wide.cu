@@ -988,6 +988,7 @@ __global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_m
     const int tile_end = min(p.ntiles, ((int)blockIdx.x + 1) * p.tpc);
     for (int tile = (int)blockIdx.x * p.tpc; tile < tile_end; ++tile) {
     const int l0r = p.tile0[tile], jt = p.tile0[tile + 1] - l0r;
+    if (g + 2 * o * JO >= jt) continue;  // a short tile: none of this warp's outputs exist (no barriers here)
     const long l0 = p.hop0 + l0r;
     const float4* pool4 = reinterpret_cast<const float4*>(p.pool);
     // filter rows of this thread's outputs (hop l0 + g + 2 (o JO + i)) at partition mq0
@@ -1026,8 +1027,10 @@ __global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_m
 #pragma unroll
             for (int e = 0; e < E; ++e) fh[k][i][e] = __ldcg(hb[i][e] + (long)k * V4);
     }
-    auto step = [&](auto u_tag) {
+    int m = mq0;
+    auto step = [&](auto u_tag, auto guard_tag) {
         constexpr int u = decltype(u_tag)::value, sl = u % KPF;
+        constexpr bool GUARD = decltype(guard_tag)::value;  // the group's last steps: no loads past mq1
         // FMAs on the operands loaded KPF steps ago, then the slot's registers take the loads of
         // step m + KPF (one register set per slot: no extra live copies)
 #pragma unroll
@@ -1035,11 +1038,13 @@ __global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_m
 #pragma unroll
             for (int e = 0; e < E; ++e) cmac4(acc[i][e], aux[i][e], fh[sl][i][e], win[(i - u) & (JO - 1)]);
         win[(JO - 1 - u) & (JO - 1)] = fx[sl];  // replaces the entry output JO - 1 just used
-        fx[sl] = __ldg(px - (long)(u + KPF) * V4);
+        if (!GUARD || m + u + KPF < mq1) {
+            fx[sl] = __ldg(px - (long)(u + KPF) * V4);
 #pragma unroll
-        for (int i = 0; i < JO; ++i)
+            for (int i = 0; i < JO; ++i)
 #pragma unroll
-            for (int e = 0; e < E; ++e) fh[sl][i][e] = __ldcg(hb[i][e] + (long)(u + KPF) * V4);
+                for (int e = 0; e < E; ++e) fh[sl][i][e] = __ldcg(hb[i][e] + (long)(u + KPF) * V4);
+        }
     };
     auto advance = [&](int k) {
         px -= (long)k * V4;
@@ -1048,34 +1053,44 @@ __global__ void __launch_bounds__(64 * (JH / JO), 512 / (64 * (JH / JO))) bank_m
 #pragma unroll
             for (int e = 0; e < E; ++e) hb[i][e] += (long)k * V4;
     };
-    int m = mq0;
-    for (; m + JO <= mq1; m += JO) {
-        step(std::integral_constant<int, 0>{});
-        if constexpr (JO > 1) step(std::integral_constant<int, 1>{});
+    using IC0 = std::integral_constant<int, 0>;
+    using IC1 = std::integral_constant<int, 1>;
+    using IC2 = std::integral_constant<int, 2>;
+    using IC3 = std::integral_constant<int, 3>;
+    using IC4 = std::integral_constant<int, 4>;
+    using IC5 = std::integral_constant<int, 5>;
+    using IC6 = std::integral_constant<int, 6>;
+    using IC7 = std::integral_constant<int, 7>;
+    auto turn = [&](auto guard) {  // JO steps: one full turn of the register window
+        step(IC0{}, guard);
+        if constexpr (JO > 1) step(IC1{}, guard);
         if constexpr (JO > 2) {
-            step(std::integral_constant<int, 2>{});
-            step(std::integral_constant<int, 3>{});
+            step(IC2{}, guard);
+            step(IC3{}, guard);
         }
         if constexpr (JO > 4) {
-            step(std::integral_constant<int, 4>{});
-            step(std::integral_constant<int, 5>{});
-            step(std::integral_constant<int, 6>{});
-            step(std::integral_constant<int, 7>{});
+            step(IC4{}, guard);
+            step(IC5{}, guard);
+            step(IC6{}, guard);
+            step(IC7{}, guard);
         }
         advance(JO);
-    }
+    };
+    for (; m + JO + KPF <= mq1; m += JO) turn(std::false_type{});
+    for (; m + JO <= mq1; m += JO) turn(std::true_type{});  // (the loads of the group's last KPF steps are skipped)
     const int rem = mq1 - m;  // < JO: the same unrolled steps, cut short
     if constexpr (JO > 1) {
-        if (rem > 0) step(std::integral_constant<int, 0>{});
+        constexpr std::true_type G{};
+        if (rem > 0) step(IC0{}, G);
         if constexpr (JO > 2) {
-            if (rem > 1) step(std::integral_constant<int, 1>{});
-            if (rem > 2) step(std::integral_constant<int, 2>{});
+            if (rem > 1) step(IC1{}, G);
+            if (rem > 2) step(IC2{}, G);
         }
         if constexpr (JO > 4) {
-            if (rem > 3) step(std::integral_constant<int, 3>{});
-            if (rem > 4) step(std::integral_constant<int, 4>{});
-            if (rem > 5) step(std::integral_constant<int, 5>{});
-            if (rem > 6) step(std::integral_constant<int, 6>{});
+            if (rem > 3) step(IC3{}, G);
+            if (rem > 4) step(IC4{}, G);
+            if (rem > 5) step(IC5{}, G);
+            if (rem > 6) step(IC6{}, G);
         }
     }
     float4* yq4 = reinterpret_cast<float4*>(p.yq);
