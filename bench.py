@@ -673,9 +673,11 @@ def main():
                    "host_ms_p50": q(host_ms, 50), "host_ms_p99": q(host_ms, 99),
                    "hop_period_ms": 1e3 * L / W.FS,
                    "streaming_value": S * cfg.ears * L / (statistics.median(host_ms) / 1e3),
-                   "what": "one tvolap_process() call per hop (the reference's process() API): pinned H2D of the "
-                           "hop, one-hop kernel, D2H of the outputs; CUDA events on the engine stream (gpu) and "
-                           "host wall clock (host); streaming_value = channel-samples/s at the median host time"}
+                   "what": "one tvolap_process() call per hop (the reference's process() API) on pinned host "
+                           "buffers: the one-hop kernel reads the hop and writes the outputs through their device "
+                           "mapping (PCIe traffic inside the kernel; tuning zero_copy = 0: H2D copy, kernel, D2H "
+                           "copy); CUDA events on the engine stream (gpu) and host wall clock (host); "
+                           "streaming_value = channel-samples/s at the median host time"}
         del lat_eng
 
     line = {

@@ -255,6 +255,7 @@ struct tvolap_engine {
     long bank_pass_mb = 32768;       // Xe + partials budget per pass
     long bank_pass_hops = 0;         // max hops per pass (0: by the budget)
     long bank_pass_tpc = 0;          // bank MAC tiles per CTA (0: all tiles of the pass)
+    long zero_copy = 1;              // one-hop calls on pinned host buffers: the kernel reads / writes them in place
     long k1_small = 1;               // 64-point K1 of the passes with 8 lanes per frame
     long bank_pass_jh = 0;           // half the hops of a bank-pass tile (0: auto; 8, 16 or 32)
     long bank_pass_q = 0;            // partition groups of the bank pass (0: auto, bank slice <= 40 MB)
@@ -690,8 +691,28 @@ void process_hops_impl(tvolap_engine* e, const float* in, long in_stride, float*
         if (!sched && !e->bank && run_wide_set(e, hop0, ip, is, op, os, kc)) return;
         launch_hops(e, hop0, kc, ip, is, op, os, sch_launch, sched ? S : 0);
     };
-    if (min == Mem::Device && mout == Mem::Device && msch == Mem::Device) {
-        hops_launch(e->hops, n, in, in_stride, out, out_stride, sched, sched);
+    // one hop between pinned host buffers (the reference's process() call from a host that keeps
+    // its audio in page-locked memory): the hop kernel reads the hop and writes its outputs through
+    // the buffers' device mapping — L floats per source over PCIe while other CTAs multiply —
+    // instead of two stream-ordered copies around it
+    bool direct = min == Mem::Device && mout == Mem::Device && msch == Mem::Device;
+    const float* din = in;
+    float* dout = out;
+    if (!direct && n == 1 && !sched && e->zero_copy && min != Mem::Pageable && mout != Mem::Pageable) {
+        bool ok = true;
+        if (min == Mem::Pinned)
+            ok = cudaHostGetDevicePointer((void**)&din, const_cast<float*>(in), 0) == cudaSuccess;
+        if (ok && mout == Mem::Pinned) ok = cudaHostGetDevicePointer((void**)&dout, out, 0) == cudaSuccess;
+        if (ok) {
+            direct = true;
+        } else {
+            cudaGetLastError();
+            din = in;
+            dout = out;
+        }
+    }
+    if (direct) {
+        hops_launch(e->hops, n, din, in_stride, dout, out_stride, sched, sched);
     } else {
         const long per_hop = S * L * (1 + E);
         long kc_want = (1L << e->pipe_log2) / per_hop;
@@ -1859,6 +1880,7 @@ const Knob kKnobs[] = {
     {"bank_pass_q", &tvolap_engine::bank_pass_q, nullptr, 0, 64, 0},
     {"bank_pass_jh", &tvolap_engine::bank_pass_jh, nullptr, 0, 32, 0},
     {"k1_small", &tvolap_engine::k1_small, nullptr, 0, 1, 0},
+    {"zero_copy", &tvolap_engine::zero_copy, nullptr, 0, 1, 0},
     {"bank_pass_tpc", &tvolap_engine::bank_pass_tpc, nullptr, 0, 1L << 20, 0},
     {"entry_order", &tvolap_engine::entry_order, nullptr, 0, 1, 0},
     {"pipe_merge", &tvolap_engine::pipe_merge, nullptr, 0, 1, 0},

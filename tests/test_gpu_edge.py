@@ -155,3 +155,44 @@ def test_host_schedule_range_checked(bad):
         with pytest.raises(T.InvalidInputError):
             e.process_hops(x, schedule=sched)
         assert e.hops_processed() == 0
+
+
+def test_one_hop_calls_on_pinned_buffers_in_place():
+    """process() on page-locked host buffers: the hop kernel reads the hop and writes its outputs
+    through the buffers' device mapping (no copies). Same outputs, bit for bit, as the copying path
+    (tuning zero_copy = 0) and as pageable buffers, for set engines and bank engines, with a
+    strided input view."""
+    import torch
+
+    hop, S, n = 64, 5, 12
+    s = T.partition(rnd(900, 11, S), hop)
+    xs = np.ascontiguousarray(rnd(hop * n, 12, S).T).astype(np.float32)
+    xh = torch.from_numpy(xs).pin_memory()
+    outs = []
+    for zc in (1, 0):
+        e = T.TvolapEngine(s)
+        e.set_tuning("zero_copy", zc)
+        y = torch.zeros((S, hop * n), dtype=torch.float32).pin_memory()
+        for h in range(n):  # the hop as a strided view of the whole pinned signal
+            T._check(T.lib().tvolap_process(e._h, xh.data_ptr() + 4 * h * hop, hop * n, hop, S,
+                                            y.data_ptr() + 4 * h * hop, hop * n))
+        e.synchronize()
+        outs.append(y.numpy().copy())
+    ref = T.TvolapEngine(s).process_hops(xs)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], ref)
+    # bank engine (two ears), selection changing every hop
+    g = np.random.default_rng(13)
+    bank = (g.standard_normal((4, 2, 700)) * np.exp(-np.arange(700) / 200)).astype(np.float32)
+    sel = g.integers(0, 4, (n, S)).astype(np.int32)
+    got = []
+    for zc in (1, 0):
+        e = T.TvolapBankEngine(bank, hop, S)
+        e.set_tuning("zero_copy", zc)
+        y = torch.zeros((2 * S, hop * n), dtype=torch.float32).pin_memory()
+        for h in range(n):
+            e.select_bank(sel[h])
+            T._check(T.lib().tvolap_process(e._h, xh.data_ptr() + 4 * h * hop, hop * n, hop, S,
+                                            y.data_ptr() + 4 * h * hop, hop * n))
+        e.synchronize()
+        got.append(y.numpy().copy())
+    assert np.array_equal(got[0], got[1])
