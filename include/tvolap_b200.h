@@ -231,6 +231,11 @@ uint64_t tvolap_kernel_launches(const tvolap_engine* e);
    schedules (a diagnostic of which path a call took; tuning "wide" / "bank_pass" select). */
 uint64_t tvolap_wide_passes(const tvolap_engine* e);
 
+/* One-hop launches of bank engines that ran on the persistent bulk-copy ring kernel (delay-line
+   and filter rows staged into shared memory by cp.async.bulk + mbarrier across sources; tuning
+   "hop_ring"); the others ran on the cluster hop kernel. A diagnostic like tvolap_wide_passes. */
+uint64_t tvolap_ring_launches(const tvolap_engine* e);
+
 /*
  * Tuning knobs: every A/B switch of the kernel, geometry and pipeline choices, by name (the
  * library reads no environment variables). Defaults are the measured-best choices; DESIGN.md §10

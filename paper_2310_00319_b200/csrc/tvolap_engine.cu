@@ -256,10 +256,13 @@ struct tvolap_engine {
     long bank_pass_hops = 0;         // max hops per pass (0: by the budget)
     long bank_pass_tpc = 0;          // bank MAC tiles per CTA (0: all tiles of the pass)
     long zero_copy = 1;              // one-hop calls on pinned host buffers: the kernel reads / writes them in place
+    long hop_ring = 0;               // one-hop calls of bank engines on the persistent bulk-copy ring kernel
+                                     // (geometry variant 1..4; measured no faster: profiles/r02_ab_hop_ring.txt)
     long k1_small = 1;               // 64-point K1 of the passes with 8 lanes per frame
     long bank_pass_jh = 0;           // half the hops of a bank-pass tile (0: auto; 8, 16 or 32)
     long bank_pass_q = 0;            // partition groups of the bank pass (0: auto, bank slice <= 40 MB)
     uint64_t wide_passes = 0;
+    uint64_t ring_launches = 0;   // one-hop launches on the bulk-copy ring kernel
     long pipe_merge = 1;             // "pipe_merge": one H2D copy per run of host-contiguous sets
     long wide_warp_fft = 1;          // "wide_warp_fft": 1 warp FFTs for K1/K5 (0: bit-identical Stockham)
     // further tuning knobs (tvolap_set_tuning; defaults = the measured-best choices)
@@ -623,6 +626,10 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     }
     if (blocked)
         CK(tvb::launch_block_kernel(p, (int)e->E, e->JH, e->QB, e->NTB, e->stream));
+    else if (e->bank && e->hop_ring && (p.ring_var = (int)e->hop_ring, tvb::hop_ring_supported(p, (int)e->E, hop_threads(e)))) {
+        CK(tvb::launch_hop_ring_kernel(p, (int)e->E, hop_threads(e), e->stream));
+        ++e->ring_launches;
+    }
     else
         CK(tvb::launch_hop_kernel(p, (int)e->E, hop_threads(e), e->stream));
     if (t1) CK(cudaEventRecord(t1, e->stream));
@@ -1848,6 +1855,7 @@ int tvolap_block_config(const tvolap_engine* e, int* hops_per_block, long* block
 uint64_t tvolap_kernel_launches(const tvolap_engine* e) { return e ? e->launches : 0; }
 
 uint64_t tvolap_wide_passes(const tvolap_engine* e) { return e ? e->wide_passes : 0; }
+uint64_t tvolap_ring_launches(const tvolap_engine* e) { return e ? e->ring_launches : 0; }
 
 // ------------------------------------------------------------------ tuning knobs
 // Every A/B switch of the kernel, geometry and pipeline choices is a named knob; the defaults are
@@ -1880,6 +1888,7 @@ const Knob kKnobs[] = {
     {"bank_pass_q", &tvolap_engine::bank_pass_q, nullptr, 0, 64, 0},
     {"bank_pass_jh", &tvolap_engine::bank_pass_jh, nullptr, 0, 32, 0},
     {"k1_small", &tvolap_engine::k1_small, nullptr, 0, 1, 0},
+    {"hop_ring", &tvolap_engine::hop_ring, nullptr, 0, 4, 0},
     {"zero_copy", &tvolap_engine::zero_copy, nullptr, 0, 1, 0},
     {"bank_pass_tpc", &tvolap_engine::bank_pass_tpc, nullptr, 0, 1L << 20, 0},
     {"entry_order", &tvolap_engine::entry_order, nullptr, 0, 1, 0},

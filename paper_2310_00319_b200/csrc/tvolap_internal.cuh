@@ -40,6 +40,7 @@ struct HopParams {
     // their selected bank entry, so the sources sharing an entry run side by side and its filter
     // rows come from HBM once per hop (L2 hits for the others); null = source i
     const int* order = nullptr;
+    int ring_var = 0;      // one-hop bank launches on the bulk-copy ring kernel: geometry variant 1..4 (0: cluster hop kernel)
     // switching mode (tvolap_process_switching, hop-blocked set engines): a filter switch may
     // happen every sw_period hops of this launch; switch k (k < sw_count) installs the set
     // sw_irs[k] into pool entry sw_entry[k] (entry of source 0; -1: no switch at k).
@@ -118,6 +119,9 @@ cudaError_t launch_partition_multi(int L, int M, int S, long rows, const float* 
 
 size_t hop_kernel_smem_bytes(int L, int P, int E, int qm);
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
+// persistent one-hop kernel with a cp.async.bulk ring (bank engines, P = 1): tvolap_kernels.cu
+bool hop_ring_supported(const HopParams& p, int E, int threads);
+cudaError_t launch_hop_ring_kernel(const HopParams& p, int E, int threads, cudaStream_t stream);
 
 // Hop-blocked variant (2*JH hops per block, Q partition groups; threads == Q * (2L/P) when 2L/P < threads).
 size_t block_kernel_smem_bytes(int L, int P, int E, int JH, bool bank, int threads);

@@ -389,6 +389,251 @@ __global__ void __launch_bounds__(1024) tvolap_hop_kernel(const HopParams p) {
 }
 
 // ============================================================================
+// Streaming kernel with a bulk-copy ring (bank engines, one hop per call, P = 1): persistent CTAs
+// (one per SM) walk the sources in the launch order, and the delay-line rows and filter rows of
+// the MAC arrive in shared memory by cp.async.bulk (TMA) signalled on mbarriers — a ring of ST
+// stages, each R partition steps of every partition group, refilled by one thread as soon as a
+// stage is consumed and running ahead ACROSS sources, so the HBM stream does not stop while a
+// source's transforms (K1, K5) run and bytes in flight are not tied to registers or to resident
+// warps. The hop's own spectrum (partition 0) never travels through memory: K2 writes it into
+// the stage's row next to the global delay-line store. Same partition groups and summation order
+// as tvolap_hop_kernel: bit-identical outputs (spectral.cpp:160-166, engine.cpp:60-106).
+constexpr int kRingSources = 64;  // sources per CTA whose (index, bank entry) the kernel tabulates up front
+struct RingLayout {
+    size_t tw, pk, win, x0, x1, fa, fb, red, yb, bar, tab, ring, stage, total;
+    int G, R, ST;
+    __host__ __device__ RingLayout(int L, int E, int G_, int R_, int ST_) : G(G_), R(R_), ST(ST_) {
+        const size_t N = 2 * (size_t)L;
+        tw = 0;
+        pk = align16(tw + N * sizeof(float2));
+        win = align16(pk + (N + 2) * sizeof(float2));
+        x0 = align16(win + N * sizeof(float));
+        x1 = align16(x0 + L * sizeof(float));
+        fa = align16(x1 + L * sizeof(float));
+        fb = align16(fa + N * sizeof(float2));
+        red = align16(fb + N * sizeof(float2));
+        yb = align16(red + (size_t)G * L * E * sizeof(float4));
+        bar = align16(yb + (size_t)E * N * sizeof(float2));
+        tab = align16(bar + 8 * 8);
+        ring = (tab + 2 * kRingSources * sizeof(int) + 127) / 128 * 128;
+        stage = (size_t)G * (1 + E) * R * N * sizeof(float2);
+        total = ring + (size_t)ST * stage;
+    }
+};
+
+__device__ __forceinline__ void ring_bar_init(unsigned bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void ring_bar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "RWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra RWAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void ring_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ring_copy(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <int E, int NC, int R, int ST>
+__global__ void __launch_bounds__(1024) tvolap_hop_ring_kernel(const HopParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int N = NC, L = NC / 2, V = L;
+    const int M = p.M, D = p.D, G = p.qm;
+    const int tid = threadIdx.x, NT = blockDim.x;  // NT == G * V: one float4 column of one group per thread
+    const RingLayout lay(L, E, G, R, ST);
+    float2* s_tw = reinterpret_cast<float2*>(smem + lay.tw);
+    float2* s_pk = reinterpret_cast<float2*>(smem + lay.pk);
+    float* s_win = reinterpret_cast<float*>(smem + lay.win);
+    float* xprev = reinterpret_cast<float*>(smem + lay.x0);
+    float* xcur = reinterpret_cast<float*>(smem + lay.x1);
+    float2* s_fa = reinterpret_cast<float2*>(smem + lay.fa);
+    float2* s_fb = reinterpret_cast<float2*>(smem + lay.fb);
+    float4* s_red = reinterpret_cast<float4*>(smem + lay.red);
+    float2* s_yb = reinterpret_cast<float2*>(smem + lay.yb);
+    unsigned char* s_ring = smem + lay.ring;
+    const unsigned bar0 = (unsigned)__cvta_generic_to_shared(smem + lay.bar);
+    const unsigned ring0 = (unsigned)__cvta_generic_to_shared(s_ring);
+    const unsigned rowB = N * sizeof(float2);              // one spectrum
+    const unsigned blkB = R * rowB;                          // R rows of one kind
+    const unsigned grpB = (1 + E) * blkB;                    // one group's X block + E filter blocks
+    const unsigned stageB = (unsigned)lay.stage;
+    const int MG = M / G, SPS = MG / R;                      // steps per group, stages per source (host-checked)
+    const int f0 = tid % V, g = tid / V;
+    const long hop = p.hop0;
+    const int par = (int)(hop & 1), sl = (int)((hop >> 1) % D);
+    const int nsrc = (p.S - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // sources of this CTA
+
+    for (int i = tid; i < N; i += NT) {
+        s_tw[i] = p.tw[i];
+        s_win[i] = p.win[i];
+    }
+    for (int i = tid; i <= N; i += NT) s_pk[i] = p.pk[i];
+    // this CTA's sources and their bank entries (the issuing thread must not chase them through
+    // global memory in front of every stage)
+    int* s_src = reinterpret_cast<int*>(smem + lay.tab);
+    int* s_ent = s_src + kRingSources;
+    for (int k = tid; k < nsrc; k += NT) {
+        const int idx = (int)blockIdx.x + k * (int)gridDim.x;
+        const int s = p.order ? p.order[idx] : idx;
+        s_src[k] = s;
+        s_ent[k] = p.sched[s];
+    }
+    if (tid == 0) {
+        for (int b = 0; b < ST; ++b) ring_bar_init(bar0 + 8 * b);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    // stage j of this CTA's stream: source iteration j / SPS, steps t R .. t R + R - 1 of every group.
+    // Issued by warp 0: lane 0 arms the stage's barrier with the byte count, then every lane issues
+    // one of the stage's bulk copies (per group: the X block in up to two pieces around the
+    // delay line's wrap, and E filter blocks).
+    auto issue = [&](int j) {
+        const int k = j / SPS, t = j - k * SPS;
+        if (k >= nsrc) return;
+        const int s = s_src[k], entry = s_ent[k];
+        const int b = j % ST;
+        const unsigned bar = bar0 + 8 * b, dst0 = ring0 + b * stageB;
+        const int lane = tid & 31;
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the stage's generic reads are done
+            ring_expect(bar, G * grpB - (t == 0 ? rowB : 0));
+        }
+        __syncwarp();
+        const float2* xbase = p.ring + (((long)s * 2 + par) * D) * N;
+        for (int c = lane; c < G * (2 + E); c += 32) {
+            const int gg = c / (2 + E), kind = c - gg * (2 + E);
+            const int m = gg * MG + t * R;
+            const unsigned dg = dst0 + gg * grpB;
+            if (kind < 2) {
+                // X rows: position q of the block holds slot (sl - m - (R - 1) + q) mod D, i.e. step r = R - 1 - q;
+                // the hop's own spectrum (m = 0: q = R - 1 of group 0) comes from K2, not from memory
+                const int cnt = R - ((gg == 0 && t == 0) ? 1 : 0);
+                int lo = (sl - m - (R - 1)) % D;
+                if (lo < 0) lo += D;
+                const int first = min(cnt, D - lo);
+                if (kind == 0) {
+                    if (first > 0) ring_copy(dg, xbase + (long)lo * N, first * rowB, bar);
+                } else if (first < cnt) {
+                    ring_copy(dg + first * rowB, xbase, (cnt - first) * rowB, bar);
+                }
+            } else {
+                const int e = kind - 2;
+                ring_copy(dg + (1 + e) * blkB, p.pool + (((long)entry * E + e) * M + m) * N, blkB, bar);
+            }
+        }
+    };
+    if (tid < 32)
+        for (int j = 0; j < ST; ++j) issue(j);
+
+    for (int k = 0; k < nsrc; ++k) {
+        const int s = s_src[k];
+        const int jbase = k * SPS;
+
+        // ---- K1: frame (previous hop | this hop) x Hann, zero-pad to 4L, FFT.
+        const float* inp = p.in + (long)s * p.in_stride;
+        for (int i = tid; i < L; i += NT) {
+            xprev[i] = p.hist[(long)s * L + i];
+            xcur[i] = inp[i];
+        }
+        __syncthreads();
+        for (int j = tid; j < L; j += NT) {
+            const int i0 = 2 * j, i1 = 2 * j + 1;
+            const float a = (i0 < L ? xprev[i0] : xcur[i0 - L]) * s_win[i0];
+            const float b = (i1 < L ? xprev[i1] : xcur[i1 - L]) * s_win[i1];
+            s_fa[j] = make_float2(a, b);
+        }
+        for (int i = tid; i < L; i += NT) p.hist[(long)s * L + i] = xcur[i];
+        __syncthreads();
+        const float2* Z = fft_stockham<false, NC>(s_fa, s_fb, N, s_tw, true, tid, NT);
+
+        // ---- K2: X_hop into the delay line and into the ring stage that holds step 0.
+        {
+            float2* ringw = p.ring + (((long)s * 2 + par) * D + sl) * N;
+            float2* fresh = reinterpret_cast<float2*>(s_ring + (size_t)(jbase % ST) * stageB + (size_t)(R - 1) * rowB);
+            for (int kk = tid; kk < N; kk += NT) {
+                const float2 x = untangle_packed(Z, N, kk, s_pk);
+                ringw[kk] = x;
+                fresh[kk] = x;
+            }
+        }
+        __syncthreads();
+
+        // ---- K3: Y = sum_m H[m] X_{hop-2m}; thread (g, f0) walks its group's steps in order.
+        float4 acc[E];
+        float aux[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+            aux[e] = 0.f;
+        }
+        for (int t = 0; t < SPS; ++t) {
+            const int j = jbase + t, b = j % ST;
+            ring_bar_wait(bar0 + 8 * b, (unsigned)((j / ST) & 1));
+            const float4* xb = reinterpret_cast<const float4*>(s_ring + (size_t)b * stageB + (size_t)g * grpB) + f0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float4 x = xb[(R - 1 - r) * V];
+#pragma unroll
+                for (int e = 0; e < E; ++e) cmac4(acc[e], aux[e], xb[((1 + e) * R + r) * V], x);
+            }
+            __syncthreads();
+            if (tid < 32) issue(j + ST);
+        }
+        if (f0 == 0) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {  // packed bin 0: (H_0 X_0, H_N X_N) as two real products
+                acc[e].x += aux[e];
+                acc[e].y = aux[e];
+            }
+        }
+        if (G == 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) reinterpret_cast<float4*>(s_yb + (size_t)e * N)[f0] = acc[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) s_red[((size_t)g * V + f0) * E + e] = acc[e];
+            __syncthreads();
+            for (int i = tid; i < V * E; i += NT) {
+                const int f = i / E, e = i % E;
+                float4 sum = s_red[(size_t)f * E + e];
+                for (int gg = 1; gg < G; ++gg) sum = f4add(sum, s_red[((size_t)gg * V + f) * E + e]);
+                reinterpret_cast<float4*>(s_yb + (size_t)e * N)[f] = sum;
+            }
+        }
+        __syncthreads();
+
+        // ---- K5: inverse real FFT, hop-2 overlap-add.
+        for (int e = 0; e < E; ++e) {
+            for (int i = tid; i < N; i += NT) s_fb[i] = tangle_packed(s_yb + (size_t)e * N, N, i, s_pk);
+            __syncthreads();
+            const float* yf = reinterpret_cast<const float*>(fft_stockham<true, NC>(s_fb, s_fa, N, s_tw, false, tid, NT));
+            const float sc = 1.0f / (float)N;
+            float* A = p.ola + ((long)s * E + e) * 3 * L;
+            float* o = p.out + ((long)s * E + e) * p.out_stride;
+            for (int u = tid; u < L; u += NT) {
+                const float y0 = yf[u] * sc, y1 = yf[L + u] * sc, y2 = yf[2 * L + u] * sc, y3 = yf[3 * L + u] * sc;
+                o[u] = 0.5f * (y0 + A[u]);
+                A[u] = y1 + A[L + u];
+                A[L + u] = y2 + A[2 * L + u];
+                A[2 * L + u] = y3;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ============================================================================
 // Hop-blocked kernel: the same per-hop semantics, processed J = 2*JH hops at a
 // time when a call carries several hops (tvolap_process_hops). Within a block
 // all J forward FFTs run first (spread over the cluster), then the MAC for the
@@ -1698,6 +1943,64 @@ cudaError_t launch_block_kernel(const HopParams& p, int E, int JH, int Q, int th
         case 4: return launch_block_t<1, 4, true>(p, Q, threads, stream);
         default: return launch_block_t<1, 8, true>(p, Q, threads, stream);
     }
+}
+
+namespace {
+// ring geometry (steps per stage R, stages ST) by variant v = HopParams::ring_var: sized so that
+// several CTAs share an SM (their transforms overlap each other's MACs) with ~100 KB of rows in
+// flight per SM
+__host__ __device__ constexpr int ring_r(int N, int v) {
+    return N == 64 ? (v == 2 ? 8 : v == 4 ? 2 : 4) : (v >= 3 ? 4 : 2);
+}
+__host__ __device__ constexpr int ring_st(int N, int v) {
+    return N == 64 ? (v >= 3 ? 4 : 3) : (v == 1 || v == 4 ? 3 : 2);
+}
+
+template <int E, int NC, int VAR>
+cudaError_t launch_hop_ring_t(const HopParams& p, int threads, cudaStream_t stream) {
+    constexpr int R = ring_r(NC, VAR), ST = ring_st(NC, VAR);
+    auto fn = tvolap_hop_ring_kernel<E, NC, R, ST>;
+    const size_t smem = RingLayout(p.L, E, p.qm, R, ST).total;
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem)) != cudaSuccess) return err;
+    fn<<<(unsigned)std::min<long>(p.S, (long)sms * std::max(1, per_sm)), threads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+template <int E, int NC>
+cudaError_t launch_hop_ring_v(const HopParams& p, int threads, cudaStream_t stream) {
+    switch (p.ring_var) {
+        case 2: return launch_hop_ring_t<E, NC, 2>(p, threads, stream);
+        case 3: return launch_hop_ring_t<E, NC, 3>(p, threads, stream);
+        case 4: return launch_hop_ring_t<E, NC, 4>(p, threads, stream);
+        default: return launch_hop_ring_t<E, NC, 1>(p, threads, stream);
+    }
+}
+}  // namespace
+
+// The ring kernel covers: bank engines (a latched selection), one hop, P = 1, 64- or 256-point
+// spectra, one float4 column of one partition group per thread, whole stages per group.
+bool hop_ring_supported(const HopParams& p, int E, int threads) {
+    const int N = 2 * p.L, G = p.qm;
+    if (!(N == 64 || N == 256) || p.P != 1 || p.n_hops != 1 || !p.sched || p.new_ir || G < 1) return false;
+    if (threads != G * p.L || p.M % G || p.ring_var < 1 || p.ring_var > 4) return false;
+    const int R = ring_r(N, p.ring_var), ST = ring_st(N, p.ring_var);
+    const int MG = p.M / G;
+    if (MG % R || MG / R < ST || p.D < R) return false;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (p.S > (long)kRingSources * sms) return false;  // the per-CTA source table
+    return RingLayout(p.L, E, G, R, ST).total <= 227 * 1024;
+}
+
+cudaError_t launch_hop_ring_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {
+    if (!hop_ring_supported(p, E, threads)) return cudaErrorInvalidValue;
+    if (2 * p.L == 64) return E == 2 ? launch_hop_ring_v<2, 64>(p, threads, stream) : launch_hop_ring_v<1, 64>(p, threads, stream);
+    return E == 2 ? launch_hop_ring_v<2, 256>(p, threads, stream) : launch_hop_ring_v<1, 256>(p, threads, stream);
 }
 
 cudaError_t launch_hop_kernel(const HopParams& p, int E, int threads, cudaStream_t stream) {

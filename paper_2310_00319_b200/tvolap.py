@@ -112,6 +112,7 @@ def lib() -> C.CDLL:
             "tvolap_set_launch_config": (ip, [vp, ip, ip]),
             "tvolap_kernel_launches": (C.c_uint64, [vp]),
             "tvolap_wide_passes": (C.c_uint64, [vp]),
+            "tvolap_ring_launches": (C.c_uint64, [vp]),
             "tvolap_set_block_config": (ip, [vp, ip, lg]),
             "tvolap_set_tuning": (ip, [vp, C.c_char_p, lg]),
             "tvolap_set_create": (ip, [C.POINTER(vp), ip, lg, lg, lg, fp, lg]),
@@ -166,7 +167,7 @@ EXPORTED_SYMBOLS = (
     "tvolap_process_hops tvolap_process_switching tvolap_exchange_filter tvolap_select_bank tvolap_reset tvolap_hop tvolap_channels "
     "tvolap_output_channels tvolap_partition_count tvolap_delay_line_depth tvolap_latency "
     "tvolap_switching_latency tvolap_stream_delay tvolap_hops_processed tvolap_op_counts tvolap_set_stream "
-    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_wide_passes tvolap_set_block_config tvolap_block_config "
+    "tvolap_synchronize tvolap_set_host_async tvolap_set_profiling tvolap_kernel_time tvolap_launch_config tvolap_set_launch_config tvolap_kernel_launches tvolap_wide_passes tvolap_ring_launches tvolap_set_block_config tvolap_block_config "
     "tvolap_set_create tvolap_set_release tvolap_set_geometry tvolap_set_spectra tvolap_set_reassemble "
     "tvolap_create_from_set tvolap_exchange_set "
     "tvolap_set_tuning tvolap_get_tuning tvolap_set_default_tuning tvolap_reset_default_tuning tvolap_tuning_keys "
@@ -542,6 +543,10 @@ class TvolapEngine:
     def wide_passes(self) -> int:
         """Time-parallel passes run (device-resident switching calls, csrc/tvolap_wide.cu)."""
         return lib().tvolap_wide_passes(self._h)
+
+    def ring_launches(self) -> int:
+        """One-hop launches that ran on the persistent bulk-copy ring kernel (bank engines)."""
+        return lib().tvolap_ring_launches(self._h)
 
 
 def tuning_keys():

@@ -532,3 +532,52 @@ def test_mix_group_single_rank_equals_device_mix():
     with pytest.raises(T.InvalidSizeError):
         grp.allreduce(big, S, 5000, torch.empty((E, 5000), device="cuda"))  # more samples than the group holds
     grp.close()
+
+
+@pytest.mark.parametrize("hop,ears,taps,S", [(32, 1, 4096, 256), (128, 2, 4096, 160), (32, 2, 8192, 160),
+                                             (128, 1, 4096, 256)])
+def test_one_hop_ring_kernel_is_bit_identical(hop, ears, taps, S):
+    """Bank engines' process() on the persistent bulk-copy ring kernel (cp.async.bulk + mbarrier
+    stages running ahead across sources; opt-in, tuning hop_ring = 1..4) against the default hop kernel:
+    same partition groups and summation order, so every output bit agrees — over enough hops to
+    wrap the delay line, with the selection changing every hop, and vs the reference."""
+    import oracle as O
+    from parity import TOL, best_oracle
+
+    g = np.random.default_rng(hop + ears)
+    n_bank = 6
+    bank = (g.standard_normal((n_bank, ears, taps)) * np.exp(-np.arange(taps) / (taps / 5))).astype(np.float32)
+    a = T.TvolapBankEngine(bank, hop, S)
+    a.set_tuning("hop_ring", 1 + (hop + ears) % 4)  # one of the four ring geometries (opt-in: default 0)
+    b = T.TvolapBankEngine(bank, hop, S)
+    assert b.get_tuning("hop_ring") == 0
+    M = a.partition_count()
+    n = 2 * M + 21  # the 2M-1 deep delay line wraps
+    x = g.uniform(-1, 1, (S, n * hop)).astype(np.float32)
+    sel = g.integers(0, n_bank, (n, S)).astype(np.int32)
+    ya, yb = [], []
+    for h in range(n):
+        blk = np.ascontiguousarray(x[:, h * hop:(h + 1) * hop].T)
+        a.select_bank(sel[h])
+        b.select_bank(sel[h])
+        ya.append(a.process(blk).T)
+        yb.append(b.process(blk).T)
+    assert a.ring_launches() == n and b.ring_launches() == 0
+    ya, yb = np.concatenate(ya, 1), np.concatenate(yb, 1)
+    assert np.array_equal(ya, yb)
+    with O.using(best_oracle()):
+        _, ref = O.run_workload(hop, M, S, ears, n, x.astype(np.float64), 1, bank_ir=bank.astype(np.float64),
+                                schedule=sel, threads=8)
+    assert np.abs(ya - ref).max() <= TOL * np.abs(ref).max()
+    # mixed with multi-hop calls (bank pass / hop-blocked kernel) the stream continues seamlessly
+    c = T.TvolapBankEngine(bank, hop, S)
+    c.set_tuning("hop_ring", 1)
+    half = n // 2
+    y1 = c.process_hops(x[:, : half * hop], schedule=sel[:half])
+    tail = []
+    for h in range(half, n):
+        c.select_bank(sel[h])
+        tail.append(c.process(np.ascontiguousarray(x[:, h * hop:(h + 1) * hop].T)).T)
+    yc = np.concatenate([y1] + tail, 1)
+    assert c.ring_launches() == n - half
+    assert np.abs(yc - ref).max() <= TOL * np.abs(ref).max()
