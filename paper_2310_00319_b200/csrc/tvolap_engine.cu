@@ -1325,7 +1325,8 @@ bool run_bank_pass(tvolap_engine* e, long hop0, const float* in, long in_stride,
     // tiles of 64 hops (one CTA of 512 threads per SM) where the register budget allows: fewer Xe
     // window rows per output than 32-hop tiles (C5 1.94e9 -> 1.97e9; -> 2.02e9 with every CTA
     // walking all tiles of its (source, group), so the window stays in L1: profiles/r02_ab_bank_tpc.txt)
-    int JH = (N <= 128 && E == 1) ? 32 : 8;
+    // two ears: 32-hop tiles where the K5 tile fits (C3 7.13e9 -> 7.18e9)
+    int JH = (N <= 128 && E == 1) ? 32 : (E == 2 && N <= 256) ? 16 : 8;
     if (e->bank_pass_jh > 0 && tvb::bank_pass_supported((int)L, (int)E, (int)e->bank_pass_jh)) JH = (int)e->bank_pass_jh;
     const long J = 2 * JH;
     // (any call of >= 3 hops: the same per-output sums whatever the call / chunk boundaries)

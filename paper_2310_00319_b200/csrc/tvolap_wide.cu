@@ -1341,6 +1341,7 @@ cudaError_t launch_bank_pass_t(const WideParams& p, int JH, cudaStream_t stream,
     else if (p.E == 1 && JH == 16) err = launch_bank_mac<NC, 1, 16, 4>(p, stream);
     else if (p.E == 1 && JH == 8) err = launch_bank_mac<NC, 1, 8, 4>(p, stream);
     else if (p.E == 2 && JH == 8) err = launch_bank_mac<NC, 2, 8, 2>(p, stream);
+    else if (p.E == 2 && JH == 16 && NC <= 256) err = launch_bank_mac<NC, 2, 16, 2>(p, stream);
     else return cudaErrorInvalidValue;
     if (err != cudaSuccess) return err;
     if (t1) cudaEventRecord(t1, stream);
@@ -1417,7 +1418,7 @@ cudaError_t launch_wide(const WideParams& p, int JH, cudaStream_t stream, cudaEv
 bool bank_pass_supported(int L, int E, int JH) {
     const int N = 2 * L;
     if (!(N == 64 || N == 128 || N == 256 || N == 512)) return false;
-    return (E == 1 && (JH == 16 || JH == 8 || (JH == 32 && N <= 128))) || (E == 2 && JH == 8);
+    return (E == 1 && (JH == 16 || JH == 8 || (JH == 32 && N <= 128))) || (E == 2 && (JH == 8 || (JH == 16 && N <= 256)));
 }
 
 cudaError_t launch_bank_pass(const WideParams& p, int JH, cudaStream_t stream, cudaEvent_t t0, cudaEvent_t t1) {

@@ -155,11 +155,17 @@ def test_bank_pass_tile_geometry_knobs():
         err = np.abs(outs[jh, 0] - ref).max() / np.abs(ref).max()
         assert err <= TOL, (jh, err)
     assert np.abs(outs[8, 0] - outs[32, 0]).max() <= 2e-6 * np.abs(ref).max()
-    # two-ear engines (C3 geometry) keep 16-hop tiles; the tiles-per-CTA walk applies to them too
+    # two-ear engines (C3 geometry): 16- or 32-hop tiles; the tiles-per-CTA walk applies to them too
     bank2, x2, sched2 = _case(128, 3, 2, 5, 3000, 90, 52)
-    ys = []
-    for tpc in (1, 0):
-        e = T.TvolapBankEngine(bank2, 128, 3)
-        e.set_tuning("bank_pass_tpc", tpc)
-        ys.append(e.process_hops(_dev(x2), schedule=_dev(sched2)).cpu().numpy())
-    assert np.array_equal(ys[0], ys[1])
+    ys = {}
+    for jh in (8, 16):
+        for tpc in (1, 0):
+            e = T.TvolapBankEngine(bank2, 128, 3)
+            e.set_tuning("bank_pass_jh", jh)
+            e.set_tuning("bank_pass_tpc", tpc)
+            ys[jh, tpc] = e.process_hops(_dev(x2), schedule=_dev(sched2)).cpu().numpy()
+        assert np.array_equal(ys[jh, 0], ys[jh, 1])
+    ref2 = _oracle(bank2, x2, sched2, 128, e.partition_count())
+    for jh in (8, 16):
+        assert np.abs(ys[jh, 0] - ref2).max() <= TOL * np.abs(ref2).max()
+    assert np.abs(ys[8, 0] - ys[16, 0]).max() <= 2e-6 * np.abs(ref2).max()
