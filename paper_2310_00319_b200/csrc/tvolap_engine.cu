@@ -393,11 +393,24 @@ void pick_block_geometry(tvolap_engine* e) {
     e->QM = items < e->NTB ? (int)(e->NTB / items) : 1;
 }
 
+// Threads of the opt-in ring variant: one per (partition group, float4 column), as its stages assume.
+int hop_ring_threads(const tvolap_engine* e) {
+    const long t = std::min<long>(1024, e->QM * (e->N / (2 * e->P)));
+    return (int)std::max<long>(32, (t + 31) / 32 * 32);
+}
+
 // Threads of the one-hop kernel: QM partition groups x the slice's float4 columns.
 int hop_threads(const tvolap_engine* e) {
+    // tuning nt: fewer threads than QM x V make each MAC thread stride over several columns of its
+    // group (same groups, same summation order: bit-identical), trading warps for resident CTAs
+    if (e->fix_nt >= 32) return (int)e->fix_nt;
     const long V = e->N / (2 * e->P);
     long t = std::min<long>(1024, e->QM * V);
     t = std::max<long>(32, (t + 31) / 32 * 32);
+    // bank engines with a slice one warp wide (C5: V = 32, 8 groups): two-warp CTAs, each MAC
+    // thread walking 4 columns — 16 resident CTAs per SM instead of 4, cheaper barriers around
+    // the 64-point transforms (C5 hop kernel 246.5 -> 240.5 us, profiles/r02_ab_hop_threads.txt)
+    if (e->bank && e->P == 1 && V <= 32 && t > 64) t = 64;
     return (int)t;
 }
 
@@ -626,8 +639,8 @@ void launch_hops(tvolap_engine* e, long hop0, long n, const float* in, long in_s
     }
     if (blocked)
         CK(tvb::launch_block_kernel(p, (int)e->E, e->JH, e->QB, e->NTB, e->stream));
-    else if (e->bank && e->hop_ring && (p.ring_var = (int)e->hop_ring, tvb::hop_ring_supported(p, (int)e->E, hop_threads(e)))) {
-        CK(tvb::launch_hop_ring_kernel(p, (int)e->E, hop_threads(e), e->stream));
+    else if (e->bank && e->hop_ring && (p.ring_var = (int)e->hop_ring, tvb::hop_ring_supported(p, (int)e->E, hop_ring_threads(e)))) {
+        CK(tvb::launch_hop_ring_kernel(p, (int)e->E, hop_ring_threads(e), e->stream));
         ++e->ring_launches;
     }
     else
