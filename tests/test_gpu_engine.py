@@ -466,6 +466,32 @@ def test_bank_engine_entry_order(hop, ears, S, n_bank):
     assert np.array_equal(ys[0], ys[1])
 
 
+@pytest.mark.parametrize("hop,ears,S,taps", [(32, 1, 300, 32 * 64), (128, 2, 96, 128 * 16), (32, 2, 40, 900)])
+def test_one_hop_kernel_threads_per_cta(hop, ears, S, taps):
+    """Threads per CTA of the one-hop kernel (tuning nt; automatic rule: one thread per (partition
+    group, float4 column), two-warp CTAs for bank engines whose slice is one warp wide, like C5):
+    fewer threads make each MAC thread walk several columns of its group, more leave threads idle
+    in the MAC — the partition groups and the summation order do not change, so every geometry
+    gives the same bits as the automatic one (engine.cpp:85-92 sums over m in one fixed order)."""
+    n, n_bank = 12, 5
+    bank = rnd(n_bank * ears * taps, 31).reshape(n_bank, ears, taps)
+    sched = np.random.default_rng(33).integers(0, n_bank, (n, S)).astype(np.int32)
+    x = rnd(hop * n, 32, S)
+    ys = []
+    for nt in (0, 32, 64, 128, 256, 512):
+        e = T.TvolapBankEngine(bank, hop, S)
+        e.set_tuning("bank_pass", 0)
+        if nt:
+            e.set_tuning("nt", nt)
+        y = []
+        for h in range(n):
+            e.select_bank(sched[h])
+            y.append(e.process(x[h * hop:(h + 1) * hop]))
+        ys.append(np.concatenate(y))
+    for y in ys[1:]:
+        assert np.array_equal(ys[0], y)
+
+
 def test_cpp_wrapper():
     """The C++ drop-in (include/tvolap_b200.hpp) runs the reference's engine tests on the GPU:
     tests/cpp/test_wrapper.cpp, built by _build.build() into lib/test_wrapper; exit 0 = PASS."""
