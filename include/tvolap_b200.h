@@ -207,7 +207,8 @@ int tvolap_set_profiling(tvolap_engine* e, int enable);
 int tvolap_kernel_time(tvolap_engine* e, double* total_ms, long* launches);
 
 /* Launch configuration: CTAs per source (thread-block cluster size) of the multi-hop (blocked)
- * kernel and threads per CTA of the one-hop kernel. */
+ * kernel and threads per CTA the one-hop kernel is launched with (the automatic rule, or the
+ * override below / tuning "nt"; every value gives the same output bits). */
 int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* threads_per_cta);
 /* Override the cluster size P (1, 2, 4 or 8; both kernels) and the one-hop kernel's threads per CTA
  * (32..1024); 0 keeps the current value. */

@@ -1821,7 +1821,7 @@ int tvolap_synchronize(tvolap_engine* e) {
 int tvolap_launch_config(const tvolap_engine* e, int* ctas_per_source, int* threads_per_cta) {
     if (!e) return set_err(TVOLAP_ERR_INVALID_CONFIGURATION, "null engine");
     if (ctas_per_source) *ctas_per_source = e->PB;
-    if (threads_per_cta) *threads_per_cta = e->NT;
+    if (threads_per_cta) *threads_per_cta = hop_threads(e);  // what the one-hop launch really uses
     return TVOLAP_OK;
 }
 
@@ -1833,6 +1833,7 @@ int tvolap_set_launch_config(tvolap_engine* e, int ctas_per_source, int threads_
         validate_launch(e, P, NT);
         e->P = P;
         e->NT = NT;
+        if (threads_per_cta > 0) e->fix_nt = NT;  // the one-hop launch honours it (hop_threads)
         if (ctas_per_source > 0) {
             e->PB = P;
             e->geometry_fixed = true;

@@ -490,6 +490,14 @@ def test_one_hop_kernel_threads_per_cta(hop, ears, S, taps):
         ys.append(np.concatenate(y))
     for y in ys[1:]:
         assert np.array_equal(ys[0], y)
+    # the launch-config call reports what the one-hop launch uses, and an override is honoured
+    e = T.TvolapBankEngine(bank, hop, S)
+    auto = e.launch_config()[1]
+    assert (auto <= 64) if hop == 32 else (auto == 256)
+    e.set_launch_config(0, 128)
+    assert e.launch_config()[1] == 128
+    e.select_bank(sched[0])
+    assert np.array_equal(e.process(x[:hop]), ys[0][:hop])
 
 
 def test_cpp_wrapper():
